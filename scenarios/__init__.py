@@ -1,0 +1,421 @@
+"""Seeded synthetic inputs shared by the oracle tests and the CUDA path.
+
+This module is the ONLY code both sides use.  It holds none of the method's
+arithmetic (no forces, no cells, no integration, no quantisation): it only
+builds initial states -- lattices, jitter, Maxwell-Boltzmann draws, random
+orientations -- with the shapes and state points of BASELINE.json's configs
+(restated concretely in SURVEY.md §8(d) and DESIGN.md §3).  Every random
+number comes from ``numpy.random.default_rng(20140819 + k)`` for config k.
+
+A *system* is a plain dict:
+
+    name, box (3,), rc, dt, steps, eps_rf, lj_shift, T (target temperature),
+    components: list of component dicts (see ``component``),
+    id (N,) int64, comp (N,) int32, r (N,3) f64, v (N,3) f64 (on-step, t=0),
+    q (N,4) f64 unit quaternions (w,x,y,z), j (N,3) f64 world-frame angular
+    momentum (on-step, t=0).
+
+A *component* (rigid molecule species) is a dict with
+``mass``, ``inertia`` (principal moments, body axes = principal axes) and
+site lists ``lj`` [(pos, sigma, eps)], ``charges`` [(pos, q)],
+``dipoles`` [(pos, axis, mu)], ``quadrupoles`` [(pos, axis, Q)], positions
+in the body frame relative to the centre of mass.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+SEED = 20140819
+
+# ----------------------------------------------------------------------------
+# Table 1 units with the typo readings of DESIGN.md (A16):
+# E0 = one Hartree, t0 = 3.26585e-14 s, T0 = 315775 K.
+BOHR_M = 5.29177e-11          # l0
+E0_J = 4.359745e-18           # P:107 misprint 4.35946e-18 (reading A16)
+T0_K = 315775.0
+T0_S = 3.26585e-14            # t0
+AVOGADRO = 6.02214076e23
+ANGSTROM = 1e-10 / BOHR_M     # 1 Angstrom in Bohr
+M0_U = 1000.0                 # unit mass = 1000 u = 1 kg/mol
+
+
+def component(mass, inertia=(0.0, 0.0, 0.0), lj=(), charges=(), dipoles=(),
+              quadrupoles=(), name="comp"):
+    return {
+        "name": name,
+        "mass": float(mass),
+        "inertia": tuple(float(x) for x in inertia),
+        "lj": [(tuple(map(float, p)), float(s), float(e)) for p, s, e in lj],
+        "charges": [(tuple(map(float, p)), float(q)) for p, q in charges],
+        "dipoles": [(tuple(map(float, p)), tuple(map(float, a)), float(m))
+                    for p, a, m in dipoles],
+        "quadrupoles": [(tuple(map(float, p)), tuple(map(float, a)), float(m))
+                        for p, a, m in quadrupoles],
+    }
+
+
+def lj1_component(sigma=1.0, eps=1.0, mass=1.0):
+    """Single LJ site at the centre of mass (configs 0, 1, 4)."""
+    return component(mass, (0, 0, 0), lj=[((0, 0, 0), sigma, eps)], name="LJ")
+
+
+def c2_component():
+    """2CLJQ (config 2): two LJ sites (sigma=eps=1) at +-0.25 sigma on body z,
+    mass 0.5 each, linear point quadrupole Q at the COM along z with
+    Q^2/(eps sigma^5) = 2.  I = diag(0.0625, 0.0625, 0)."""
+    Q = math.sqrt(2.0)
+    return component(1.0, (2 * 0.5 * 0.25 ** 2, 2 * 0.5 * 0.25 ** 2, 0.0),
+                     lj=[((0, 0, 0.25), 1.0, 1.0), ((0, 0, -0.25), 1.0, 1.0)],
+                     quadrupoles=[((0, 0, 0), (0, 0, 1), Q)], name="2CLJQ")
+
+
+def c3_component():
+    """TIP4P-like water (config 3) in Table 1 units (Bohr, Hartree, 1000 u).
+
+    Geometry from BASELINE.json (O-H 0.9572 A, H-O-H 104.52 deg, M 0.15 A
+    from O on the bisector); charges +q,+q,-2q with q = 0.52 e and the O LJ
+    site sigma = 3.15365 A, eps = 0.6480 kJ/mol (reading A17: published
+    TIP4P values, not in the container).  Body axes: x in-plane
+    perpendicular to the bisector, y normal to the plane, z along the
+    bisector (principal axes by symmetry)."""
+    mO, mH = 15.9994 / M0_U, 1.008 / M0_U
+    half = math.radians(104.52) / 2.0
+    hx = 0.9572 * math.sin(half) * ANGSTROM
+    hz = 0.9572 * math.cos(half) * ANGSTROM
+    mz = 0.15 * ANGSTROM
+    zc = (2 * mH * hz) / (mO + 2 * mH)
+    pos = {"O": (0.0, 0.0, -zc), "H1": (hx, 0.0, hz - zc),
+           "H2": (-hx, 0.0, hz - zc), "M": (0.0, 0.0, mz - zc)}
+    masses = [(mO, pos["O"]), (mH, pos["H1"]), (mH, pos["H2"])]
+    Ixx = sum(m * (p[1] ** 2 + p[2] ** 2) for m, p in masses)
+    Iyy = sum(m * (p[0] ** 2 + p[2] ** 2) for m, p in masses)
+    Izz = sum(m * (p[0] ** 2 + p[1] ** 2) for m, p in masses)
+    sigma = 3.15365 * ANGSTROM
+    eps = 648.0 / AVOGADRO / E0_J
+    qH = 0.52
+    return component(mO + 2 * mH, (Ixx, Iyy, Izz),
+                     lj=[(pos["O"], sigma, eps)],
+                     charges=[(pos["H1"], qH), (pos["H2"], qH), (pos["M"], -2 * qH)],
+                     name="TIP4P")
+
+
+def c3_units():
+    """Config-3 state point in Table 1 units."""
+    return {
+        "T": 298.0 / T0_K,
+        "rc": 10.0 * ANGSTROM,           # 1 nm
+        "dt": 1e-15 / T0_S,              # 1 fs
+        "number_density": 997.0 / 0.01801528 * AVOGADRO * BOHR_M ** 3,
+    }
+
+
+# ----------------------------------------------------------------------------
+# building blocks
+
+def fcc(n_cells, a, n_cells_z=None):
+    """FCC lattice, cells enumerated with meshgrid(indexing='ij') (i_x slowest),
+    basis fastest in the order (0,0,0), (1/2,1/2,0), (1/2,0,1/2), (0,1/2,1/2)."""
+    nz = n_cells if n_cells_z is None else n_cells_z
+    ix, iy, iz = np.meshgrid(np.arange(n_cells), np.arange(n_cells), np.arange(nz),
+                             indexing="ij")
+    cells = np.stack([ix.ravel(), iy.ravel(), iz.ravel()], axis=1).astype(np.float64)
+    basis = np.array([[0, 0, 0], [0.5, 0.5, 0], [0.5, 0, 0.5], [0, 0.5, 0.5]])
+    return ((cells[:, None, :] + basis[None, :, :]) * a).reshape(-1, 3)
+
+
+def simple_cubic(n, a):
+    ix, iy, iz = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    return np.stack([ix.ravel(), iy.ravel(), iz.ravel()], axis=1).astype(np.float64) * a
+
+
+def maxwell_boltzmann(rng, n, mass, T):
+    """On-step velocities at exactly T (3N translational dof), zero momentum."""
+    v = rng.normal(0.0, 1.0, size=(n, 3)) * math.sqrt(T / mass)
+    v -= v.mean(axis=0)
+    v *= math.sqrt(3 * n * T / (mass * np.sum(v * v)))
+    return v
+
+
+def random_quaternions(rng, n):
+    """Uniform on SO(3): normalised 4-Gaussian quaternions (w,x,y,z)."""
+    q = rng.normal(size=(n, 4))
+    return q / np.linalg.norm(q, axis=1, keepdims=True)
+
+
+def _body_to_world(q, vb):
+    """Rotate body-frame vectors to the world frame (initial-state preparation)."""
+    w, x, y, z = q[:, 0], q[:, 1], q[:, 2], q[:, 3]
+    R = np.empty((len(q), 3, 3))
+    R[:, 0, 0] = 1 - 2 * (y * y + z * z); R[:, 0, 1] = 2 * (x * y - w * z); R[:, 0, 2] = 2 * (x * z + w * y)
+    R[:, 1, 0] = 2 * (x * y + w * z); R[:, 1, 1] = 1 - 2 * (x * x + z * z); R[:, 1, 2] = 2 * (y * z - w * x)
+    R[:, 2, 0] = 2 * (x * z - w * y); R[:, 2, 1] = 2 * (y * z + w * x); R[:, 2, 2] = 1 - 2 * (x * x + y * y)
+    return np.einsum("nij,nj->ni", R, vb)
+
+
+def angular_momenta(rng, q, inertia, T):
+    """Body-frame j_k ~ N(0, sqrt(I_k T)) on every axis with I_k > 0 (axial
+    axis of a linear molecule gets 0), rescaled so that the rotational
+    temperature is exactly T, then rotated to the world frame (reading A21)."""
+    n = len(q)
+    I = np.asarray(inertia, dtype=np.float64)
+    active = I > 0
+    jb = np.zeros((n, 3))
+    jb[:, active] = rng.normal(size=(n, int(active.sum()))) * np.sqrt(I[active] * T)
+    ke = 0.5 * np.sum(jb[:, active] ** 2 / I[active])
+    dof = int(active.sum()) * n
+    jb *= math.sqrt(0.5 * dof * T / ke)
+    return _body_to_world(q, jb)
+
+
+def _system(name, box, rc, dt, steps, T, components, r, v, q=None, j=None,
+            comp=None, eps_rf=math.inf, lj_shift=1):
+    n = len(r)
+    return {
+        "name": name, "box": np.asarray(box, dtype=np.float64), "rc": float(rc),
+        "dt": float(dt), "steps": int(steps), "T": float(T), "eps_rf": float(eps_rf),
+        "lj_shift": int(lj_shift), "components": components,
+        "id": np.arange(n, dtype=np.int64),
+        "comp": np.zeros(n, np.int32) if comp is None else np.asarray(comp, np.int32),
+        "r": np.ascontiguousarray(r, dtype=np.float64),
+        "v": np.ascontiguousarray(v, dtype=np.float64),
+        "q": np.tile([1.0, 0.0, 0.0, 0.0], (n, 1)) if q is None else np.ascontiguousarray(q),
+        "j": np.zeros((n, 3)) if j is None else np.ascontiguousarray(j),
+    }
+
+
+# ----------------------------------------------------------------------------
+# the five BASELINE.json configs (and their scaled-down parity variants)
+
+def lj_fcc(n_cells, rho, T, seed_k, name, steps, jitter=0.05, rc=2.5, dt=0.002):
+    """Configs 0 and 1: single-site LJTS on a jittered FCC lattice."""
+    rng = np.random.default_rng(SEED + seed_k)
+    N = 4 * n_cells ** 3
+    L = (N / rho) ** (1.0 / 3.0)
+    X = fcc(n_cells, L / n_cells)
+    if jitter:
+        X += rng.uniform(-jitter, jitter, size=(N, 3))
+    X %= L
+    V = maxwell_boltzmann(rng, N, 1.0, T)
+    return _system(name, (L, L, L), rc, dt, steps, T, [lj1_component()], X, V)
+
+
+def config0():
+    """BJ configs[0]: 4000 LJ particles, FCC 10^3, rho=0.6, T=0.7, 10 steps."""
+    return lj_fcc(10, 0.6, 0.7, 0, "c0", 10)
+
+
+def config1(n_cells=64):
+    """BJ configs[1]: 1,048,576 LJ particles (FCC 64^3), rho=0.75, T=0.95, 100 steps."""
+    return lj_fcc(n_cells, 0.75, 0.95, 1, "c1" if n_cells == 64 else f"c1[{n_cells}]", 100)
+
+
+def config2(n=100):
+    """BJ configs[2]: 2CLJQ, simple cubic n^3 at rho=0.45, T=1, rc=4, dt=0.001."""
+    rng = np.random.default_rng(SEED + 2)
+    N = n ** 3
+    L = (N / 0.45) ** (1.0 / 3.0)
+    X = simple_cubic(n, L / n)
+    comp = c2_component()
+    V = maxwell_boltzmann(rng, N, comp["mass"], 1.0)
+    q = random_quaternions(rng, N)
+    j = angular_momenta(rng, q, comp["inertia"], 1.0)
+    return _system("c2" if n == 100 else f"c2[{n}]", (L, L, L), 4.0, 0.001, 100, 1.0,
+                   [comp], X, V, q, j)
+
+
+def config3(n_cells=50):
+    """BJ configs[3]: TIP4P-like water, FCC n^3 molecules, 0.997 g/cm^3, 298 K,
+    reaction field eps_RF = inf at rc = 1 nm, dt = 1 fs (Table 1 units)."""
+    rng = np.random.default_rng(SEED + 3)
+    u = c3_units()
+    N = 4 * n_cells ** 3
+    L = (N / u["number_density"]) ** (1.0 / 3.0)
+    X = fcc(n_cells, L / n_cells)
+    comp = c3_component()
+    V = maxwell_boltzmann(rng, N, comp["mass"], u["T"])
+    q = random_quaternions(rng, N)
+    j = angular_momenta(rng, q, comp["inertia"], u["T"])
+    return _system("c3" if n_cells == 50 else f"c3[{n_cells}]", (L, L, L), u["rc"], u["dt"],
+                   100, u["T"], [comp], X, V, q, j, eps_rf=math.inf)
+
+
+def _neighbours_within(points, L, cand, dmin):
+    """Boolean mask: candidate within dmin (minimum image) of any point.
+    Plain grid lookup; generator-side rejection test only."""
+    if len(points) == 0 or len(cand) == 0:
+        return np.zeros(len(cand), dtype=bool)
+    ng = np.maximum((L // dmin).astype(np.int64), 1)
+    cell_of = lambda X: np.minimum((X / L * ng).astype(np.int64), ng - 1)
+    cp = cell_of(points)
+    key = (cp[:, 0] * ng[1] + cp[:, 1]) * ng[2] + cp[:, 2]
+    order = np.argsort(key, kind="stable")
+    skey = key[order]
+    spts = points[order]
+    cc = cell_of(cand)
+    hit = np.zeros(len(cand), dtype=bool)
+    for ox in (-1, 0, 1):
+        for oy in (-1, 0, 1):
+            for oz in (-1, 0, 1):
+                nc = (cc + np.array([ox, oy, oz])) % ng
+                k = (nc[:, 0] * ng[1] + nc[:, 1]) * ng[2] + nc[:, 2]
+                lo = np.searchsorted(skey, k, "left")
+                hi = np.searchsorted(skey, k, "right")
+                cnt = hi - lo
+                m = 0
+                while True:
+                    sel = np.nonzero(cnt > m)[0]
+                    if len(sel) == 0:
+                        break
+                    d = spts[lo[sel] + m] - cand[sel]
+                    d -= L * np.round(d / L)
+                    close = np.einsum("ij,ij->i", d, d) < dmin * dmin
+                    hit[sel[close]] = True
+                    m += 1
+    return hit
+
+
+def config4(n_xy=158, T=0.8, steps=200):
+    """BJ configs[4]: vapour-liquid slab, N = 4 n_xy^2 (n_xy+1) + N_v.
+
+    Full size (n_xy = 158): N = 2^24 = 16,777,216.  L from N = 0.73 L^3 +
+    0.02 * 2 L^3; box (L, L, 3L).  Liquid: FCC n_xy x n_xy x (n_xy+1) unit
+    cells with a = L/n_xy, centred in z.  Vapour: uniform candidates in the
+    two vapour slabs (1 sigma clear of the liquid), accepted in draw order iff
+    no accepted vapour particle lies within 1 sigma (sequential rejection,
+    reading A22); stop at N_v = N_total - N_liq."""
+    rng = np.random.default_rng(SEED + 4)
+    N_liq = 4 * n_xy * n_xy * (n_xy + 1)
+    if n_xy == 158:
+        N_tot = 2 ** 24
+    else:  # scaled-down variant: same liquid/vapour density ratio
+        N_tot = int(round(N_liq * (1 + 0.02 * 2 / 0.73)))
+    L = (N_tot / (0.73 + 0.04)) ** (1.0 / 3.0)
+    Lz = 3 * L
+    a = L / n_xy
+    X = fcc(n_xy, a, n_xy + 1)
+    z0 = (Lz - (n_xy + 1) * a) / 2
+    X[:, 2] += z0
+    z_top = X[:, 2].max()
+    N_v = N_tot - N_liq
+    lo_len = z0 - 1.0
+    hi_start = z_top + 1.0
+    hi_len = Lz - hi_start
+    box = np.array([L, L, Lz])
+    acc = np.zeros((0, 3))
+    while len(acc) < N_v:
+        c = rng.uniform(size=(2 ** 20, 3))
+        zz = c[:, 2] * (lo_len + hi_len)
+        z = np.where(zz < lo_len, zz, hi_start + (zz - lo_len))
+        cand = np.stack([c[:, 0] * L, c[:, 1] * L, z], axis=1)
+        # exact sequential semantics, processed in chunks
+        for s in range(0, len(cand), 8192):
+            ch = cand[s:s + 8192]
+            ok = ~_neighbours_within(acc, box, ch, 1.0)
+            ch = ch[ok]
+            # resolve conflicts inside the chunk in draw order
+            keep = np.ones(len(ch), dtype=bool)
+            inner = _pairs_within(ch, box, 1.0)
+            for i_, j_ in inner:          # i_ < j_, sorted by j_
+                if keep[i_]:
+                    keep[j_] = False
+            ch = ch[keep]
+            need = N_v - len(acc)
+            acc = np.concatenate([acc, ch[:need]])
+            if len(acc) >= N_v:
+                break
+    X = np.concatenate([X, acc]) % box
+    V = maxwell_boltzmann(rng, len(X), 1.0, T)
+    return _system("c4" if n_xy == 158 else f"c4[{n_xy}]", box, 2.5, 0.002, steps, T,
+                   [lj1_component()], X, V)
+
+
+def _pairs_within(P, L, dmin):
+    """All index pairs (i<j) of P closer than dmin (minimum image), sorted by
+    (j, i).  Grid-based; generator-side only."""
+    n = len(P)
+    if n < 2:
+        return []
+    ng = np.maximum((L // dmin).astype(np.int64), 1)
+    c = np.minimum((P / L * ng).astype(np.int64), ng - 1)
+    key = (c[:, 0] * ng[1] + c[:, 1]) * ng[2] + c[:, 2]
+    buckets = {}
+    for idx, k in enumerate(key.tolist()):
+        buckets.setdefault(k, []).append(idx)
+    out = []
+    for idx in range(n):
+        cx, cy, cz = c[idx]
+        for ox in (-1, 0, 1):
+            for oy in (-1, 0, 1):
+                for oz in (-1, 0, 1):
+                    k = ((((cx + ox) % ng[0]) * ng[1] + (cy + oy) % ng[1]) * ng[2]
+                         + (cz + oz) % ng[2])
+                    for jdx in buckets.get(int(k), ()):
+                        if jdx < idx:
+                            d = P[idx] - P[jdx]
+                            d -= L * np.round(d / L)
+                            if d @ d < dmin * dmin:
+                                out.append((jdx, idx))
+    out = sorted(set(out), key=lambda t: (t[1], t[0]))
+    return out
+
+
+def config(name):
+    """Config by name: 'c0'..'c4' at full size, or scaled parity variants
+    'c1s', 'c2s', 'c3s', 'c4s'."""
+    table = {
+        "c0": config0,
+        "c1": config1, "c1s": lambda: config1(10),
+        "c2": config2, "c2s": lambda: config2(16),
+        "c3": config3, "c3s": lambda: config3(7),
+        "c4": config4, "c4s": lambda: config4(16),
+    }
+    return table[name]()
+
+
+# ----------------------------------------------------------------------------
+# small random systems for unit / parity tests (mixtures, dipoles, ...)
+
+def random_polar_components():
+    """Two test species covering every site kind: a Stockmayer-like LJ +
+    dipole + charge pair species and a 2-LJ + quadrupole + dipole species."""
+    a = component(1.3, (0.05, 0.08, 0.11),
+                  lj=[((0.0, 0.0, 0.1), 1.0, 1.0)],
+                  charges=[((0.3, 0.0, 0.0), 0.6), ((-0.3, 0.0, 0.0), -0.6)],
+                  dipoles=[((0.0, 0.1, -0.1), (0.0, 0.6, 0.8), 0.9)], name="A")
+    b = component(1.0, (0.0625, 0.0625, 0.0),
+                  lj=[((0, 0, 0.25), 0.9, 1.2), ((0, 0, -0.25), 0.9, 1.2)],
+                  dipoles=[((0, 0, 0.1), (0, 0, 1), 0.7)],
+                  quadrupoles=[((0, 0, 0), (0, 0, -1), 1.1)], name="B")
+    return [a, b]
+
+
+def random_system(n, box, components, T=1.0, seed_k=100, rc=2.5, dmin=0.9,
+                  eps_rf=math.inf, lj_shift=1, dt=0.001, name="random"):
+    """n molecules at random positions with COM separations >= dmin, random
+    components, orientations, velocities and angular momenta."""
+    rng = np.random.default_rng(SEED + seed_k)
+    box = np.asarray(box, dtype=np.float64)
+    pts = np.zeros((0, 3))
+    while len(pts) < n:
+        c = rng.uniform(size=(4 * n, 3)) * box
+        for p in c:
+            if len(pts) >= n:
+                break
+            if len(pts):
+                d = pts - p
+                d -= box * np.round(d / box)
+                if np.min(np.einsum("ij,ij->i", d, d)) < dmin * dmin:
+                    continue
+            pts = np.vstack([pts, p])
+    comp = rng.integers(0, len(components), size=n).astype(np.int32)
+    v = rng.normal(size=(n, 3)) * math.sqrt(T)
+    q = random_quaternions(rng, n)
+    j = np.zeros((n, 3))
+    for c_idx, cd in enumerate(components):
+        sel = comp == c_idx
+        if sel.any() and any(x > 0 for x in cd["inertia"]):
+            j[sel] = angular_momenta(rng, q[sel], cd["inertia"], T)
+    return _system(name, box, rc, dt, 10, T, components, pts, v, q, j, comp=comp,
+                   eps_rf=eps_rf, lj_shift=lj_shift)
