@@ -289,11 +289,15 @@ def config4(n_xy=158, T=0.8, steps=200):
     N_liq = 4 * n_xy * n_xy * (n_xy + 1)
     if n_xy == 158:
         N_tot = 2 ** 24
-    else:  # scaled-down variant: same liquid/vapour density ratio
-        N_tot = int(round(N_liq * (1 + 0.02 * 2 / 0.73)))
-    L = (N_tot / (0.73 + 0.04)) ** (1.0 / 3.0)
+        L = (N_tot / (0.73 + 0.04)) ** (1.0 / 3.0)
+        a = L / n_xy
+    else:  # scaled-down variant: the full-size liquid lattice constant and
+        # vapour density (rho_l = 0.7241, rho_v ~ 0.0207)
+        a = (2 ** 24 / 0.77) ** (1.0 / 3.0) / 158
+        L = n_xy * a
+        vap_len = 3 * L - (n_xy + 1) * a - 2.0
+        N_tot = N_liq + int(round(0.0207 * L * L * vap_len))
     Lz = 3 * L
-    a = L / n_xy
     X = fcc(n_xy, a, n_xy + 1)
     z0 = (Lz - (n_xy + 1) * a) / 2
     X[:, 2] += z0
