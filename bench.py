@@ -1,0 +1,296 @@
+"""Benchmark of the B200 ls1-mardyn hot path (BASELINE.json metric: million
+molecule-updates per second (MMUPS) and % of the FP32 roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1] [--impl mardyn|reference]
+
+One step = one pass of the whole hot path: forces and
+torques at t_k on the linked-cell grid, observables, leapfrog (+ rotation),
+cell rebuild by counting sort.  Default workload: BASELINE configs[1]
+(1,048,576 LJTS particles, FCC 64^3, rho = 0.75, T = 0.95, rc = 2.5).
+Inputs are resident in HBM when the timed region starts; L2 (126 MB) is
+flushed between timed steps by writing a 256 MB buffer.  Each step is timed
+with CUDA events on the context's stream; the force kernel is timed with
+event nodes inside the captured step graph.
+
+--impl reference times the fp64 CPU oracle (oracle/) as it stands on the
+host cores: each step is a bounded sample of the same workload (full-shell
+forces on a fixed sample of molecules), see DESIGN.md §7.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+FLOP_COM_TEST = 8      # per half-shell candidate (SURVEY §8(d) flop model)
+FLOP_LJ_PAIR = 20      # per in-range unique pair (incl. U, W)
+REF_SAMPLE = 32768     # molecules per --impl reference step
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="c1")
+    p.add_argument("--impl", default="mardyn", choices=["mardyn", "reference"])
+    p.add_argument("--e2e-steps", type=int, default=5)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def fp32_peak_tflops(num_sms, mhz):
+    """FP32 CUDA-core peak: SMs x 128 lanes x 2 flops (FFMA) x clock."""
+    return num_sms * 128 * 2 * mhz * 1e6 / 1e12
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax = max(smax, float(r[2]))
+                for nm, val in zip(names, r[5:9]):
+                    if val.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def run_reference(args, system, rank, world):
+    """The oracle as it stands, on the host cores (bounded sample per step)."""
+    if rank != 0:
+        return
+    import oracle
+    o = oracle.System(system)
+    u = o.quantize(system["r"])
+    N = len(u)
+    rng = np.random.default_rng(1)
+    sample = np.sort(rng.choice(N, size=min(REF_SAMPLE, N), replace=False)).astype(np.int64)
+    cores = os.cpu_count()
+    times = []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        o.forces(system["comp"], u, system["q"], mode="full", idx=sample, nthreads=cores)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = len(sample) * len(times) / tot / 1e6
+    line = {
+        "impl": "reference", "metric": "MMUPS (million molecule-updates/s)", "value": value,
+        "unit": "MMUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, BASELINE configs)",
+        "config": {"workload": system["name"], "n_molecules": N, "sample_per_step": len(sample)},
+        "cpu_baseline": {"value": value, "unit": "MMUPS", "cores": cores, "kind": "oracle",
+                         "sample": f"full-shell fp64 forces on {len(sample)} fixed random molecules of "
+                                   f"{system['name']} per step (cell lists over all {N})"},
+        "e2e": {"value": value, "unit": "MMUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(system, seconds=12.0):
+    """Oracle timed on the host cores on a bounded sample of the workload."""
+    import oracle
+    o = oracle.System(system)
+    u = o.quantize(system["r"])
+    N = len(u)
+    rng = np.random.default_rng(2)
+    m = min(REF_SAMPLE, N)
+    sample = np.sort(rng.choice(N, size=m, replace=False)).astype(np.int64)
+    cores = os.cpu_count()
+    done, t_tot, reps = 0, 0.0, 0
+    while t_tot < seconds and reps < 50:
+        t0 = time.perf_counter()
+        o.forces(system["comp"], u, system["q"], mode="full", idx=sample, nthreads=cores)
+        t_tot += time.perf_counter() - t0
+        done += m
+        reps += 1
+    return {"value": done / t_tot / 1e6, "unit": "MMUPS", "cores": cores, "kind": "oracle",
+            "sample": f"{reps} x full-shell fp64 force evaluations of {m} fixed random molecules of "
+                      f"{system['name']} ({t_tot:.1f} s, OpenMP over molecules)"}
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import scenarios as S
+    system = S.config(args.config)
+    if args.impl == "reference":
+        return run_reference(args, system, rank, world)
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1408_4599_b200 import build as b
+    from paper_1408_4599_b200 import mardyn
+    b.build()
+    N = len(system["r"])
+    stream = torch.cuda.Stream()
+    ctx = mardyn.from_system(system, stream=stream)
+    for _ in range(args.warmup):
+        ctx.step(1)
+    ctx.get_observables()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    clocks = Clocks(local)
+    step_ms, force_ms = [], []
+    l0 = ctx.launch_count()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    with torch.cuda.stream(stream):
+        for k in range(args.steps):
+            flush.zero_()                          # L2 flush, outside the events
+            ev[k][0].record(stream)
+            ctx.step(1)
+            ev[k][1].record(stream)
+            stream.synchronize()
+            force_ms.append(ctx.last_step_timing()["force_ms"])
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = ctx.launch_count() - l0
+    step_ms = [a.elapsed_time(e) for a, e in ev]
+    obs = ctx.get_observables()
+    tot_ms = float(sum(step_ms))
+    if dist:
+        t = torch.tensor([tot_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        dist.barrier()
+    value = world * N * args.steps / (tot_ms / 1e3) / 1e6
+    # ---- roofline of the dominant kernel (force): algorithmic flops
+    ncand_half = obs["n_candidates"] / 2.0
+    flops = FLOP_COM_TEST * ncand_half + FLOP_LJ_PAIR * obs["n_pairs"]
+    f_ms = float(np.mean(force_ms)) if force_ms and min(force_ms) > 0 else None
+    pk = peaks()
+    props = torch.cuda.get_device_properties(local)
+    peak = fp32_peak_tflops(props.multi_processor_count, pk.get("sm_max_mhz", 1965.0))
+    achieved = flops / (f_ms / 1e3) / 1e12 if f_ms else None
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "force_traffic.json")))
+        traffic = prof.get(args.config)
+    except Exception:
+        pass
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "kernel": "k_force_lj1" if ctx.get_grid()["kernel"] == 0 else "k_force_rigid",
+                "force_ms": f_ms, "force_share": (f_ms * args.steps / tot_ms) if f_ms else None,
+                "algorithmic_gflop_per_launch": flops / 1e9,
+                "peak_note": "FP32 CUDA cores: SMs x 128 x 2 x sm_max_mhz (MEASURED_PEAKS.json), derived"}
+    # ---- end to end through the C ABI with pinned host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        h_r, h_v = pin(system["r"]), pin(system["v"])
+        h_c, h_id = pin(system["comp"]), pin(system["id"])
+        rigid = ctx.get_grid()["kernel"] != 0
+        h_q = pin(system["q"]) if rigid else None
+        h_j = pin(system["j"]) if rigid else None
+        out = {"r": torch.empty((N, 3), dtype=torch.float64).pin_memory(),
+               "v": torch.empty((N, 3), dtype=torch.float64).pin_memory()}
+        if rigid:
+            out["q"] = torch.empty((N, 4), dtype=torch.float64).pin_memory()
+            out["j"] = torch.empty((N, 3), dtype=torch.float64).pin_memory()
+        e_ms = []
+        for k in range(args.e2e_steps + 1):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx.set_molecules(h_r, h_v, comp=h_c, q=h_q, j=h_j, id=h_id, half_step=1)
+            ctx.step(1)
+            ctx.get_observables()
+            ctx.get_molecules(out)
+            dt = time.perf_counter() - t0
+            if k > 0:
+                e_ms.append(dt * 1e3)
+        h2d = N * (3 * 8 + 3 * 8 + 4 + 8 + (7 * 8 if rigid else 0))
+        d2h = N * (3 * 8 + 3 * 8 + (7 * 8 if rigid else 0)) + 64
+        e2e = {"value": N / (np.mean(e_ms) / 1e3) / 1e6, "unit": "MMUPS", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": float(np.mean(e_ms)),
+               "what": "set_molecules(pinned host) + step(1) + get_observables + get_molecules(pinned host)"}
+    if rank != 0:
+        return
+    cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(system)
+    line = {
+        "metric": "MMUPS (million molecule-updates/s)", "value": value, "unit": "MMUPS",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong",
+        "vs_baseline": None, "dtype": "f32 (fixed-point u32 positions, fp64 sums)",
+        "data": "synthetic (seeded generator of BASELINE configs, no checkpoints)",
+        "config": {"workload": system["name"], "n_molecules": N, "steps_per_run": args.steps,
+                   "parallelism": "replicas" if world > 1 else "single GPU",
+                   "l2": "flushed between timed steps (256 MB write)",
+                   "pair_interactions_per_s": obs["n_pairs"] * args.steps / (tot_ms / 1e3)},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clk,
+        "observables": {k: obs[k] for k in ("step", "U_pot", "virial", "T", "n_pairs", "n_candidates")},
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,194 @@
+/*
+ * mardyn.h -- C ABI of the B200-native ls1-mardyn hot path (arXiv:1408.4599).
+ *
+ * One context = one simulation box on one GPU: rigid multi-centre molecules
+ * interacting through Lennard-Jones 12-6 sites (Eq. 1,
+ * P:70-74, truncated and shifted P:75-76), point charges with reaction field
+ * (P:39), point dipoles and linear point quadrupoles; forces
+ * found by linked cells of edge >= rc rebuilt every step; time
+ * integration by leapfrog (Eqs. 2-3) plus the quaternion
+ * rotational leapfrog (Eqs. 4-5).  The readings of the paper's
+ * silent points are listed in DESIGN.md §2 and cited below as A<k>.
+ *
+ * Conventions shared by every call
+ *  - Every call returns int: MARDYN_OK (0) or a negative MARDYN_E* code;
+ *    mardyn_last_error(ctx) gives a one-line message.  After MARDYN_ECUDA the
+ *    context is poisoned and must be destroyed.
+ *  - Units: any consistent set with k_B = k_C = 1.
+ *  - Host arrays passed in are owned by the caller and only read during the
+ *    call; output arrays are caller-allocated with the stated capacity.
+ *  - Device memory is owned by the caller (PyTorch in the Python binding):
+ *    the library reports its need (mardyn_workspace_bytes) and carves the
+ *    buffer given to mardyn_set_workspace.  The context owns no device memory
+ *    except the workspace pointer it was handed and its CUDA graphs/events.
+ *  - All device work is enqueued on the stream given in mardyn_options
+ *    (NULL: a private non-blocking stream).  mardyn_step is asynchronous;
+ *    every mardyn_get_* call synchronises that stream.
+ *  - One context per host thread; calls are not reentrant.
+ *
+ * Positions (reading A12).  Positions are stored as unsigned fixed point
+ * u_k in [0, P_k) with one quantum s = 2^(ceil(log2(max cell edge)) - 23)
+ * common to all axes; each cell edge is E_k quanta, P_k = n_k E_k, and the
+ * box is snapped to P_k s (a relative change below 1e-6; mardyn_get_grid
+ * returns it).  Cell assignment cell_k = floor(u_k / E_k) is exact integer
+ * arithmetic; the cutoff test r^2 < rc^2 on the minimum-image separation is
+ * decided exactly (integer arithmetic in a guard band around rc).
+ */
+#ifndef MARDYN_H
+#define MARDYN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    MARDYN_OK = 0,
+    MARDYN_EINVAL = -1,     /* bad input: < 3 cells per axis, rc <= 0, dt <= 0,
+                               eps_rf < 1, mass <= 0, inertia < 0, bad component id,
+                               |quaternion| far from 1, n > capacity            */
+    MARDYN_EOVERLAP = -2,   /* two molecule centres coincide                    */
+    MARDYN_EUNSTABLE = -3,  /* non-finite force/torque or a molecule moved more
+                               than one cell edge in one step    */
+    MARDYN_ECAPACITY = -4,  /* workspace too small for the requested capacity   */
+    MARDYN_ECUDA = -5,      /* CUDA runtime error (context poisoned)            */
+    MARDYN_ENCCL = -6,      /* reserved: multi-GPU transport error              */
+    MARDYN_ESTATE = -7      /* call order, e.g. step before set_molecules       */
+};
+
+/* Sites of a component, body frame, positions relative to the centre of
+ * mass.  Dipole/quadrupole axes are unit vectors.                 */
+typedef struct { double r[3]; double sigma, epsilon; } mardyn_lj_site;
+typedef struct { double r[3]; double q; } mardyn_charge;
+typedef struct { double r[3]; double e[3]; double m; } mardyn_polar; /* m = mu or Q */
+
+/* A component (molecule species).  inertia = principal moments; the body
+ * axes are the principal axes.  A moment of 0 removes that rotational
+ * degree of freedom (linear molecules: 2; single point site: 0).            */
+typedef struct {
+    int32_t n_lj, n_q, n_mu, n_Q;
+    const mardyn_lj_site* lj;
+    const mardyn_charge* q;
+    const mardyn_polar* mu;
+    const mardyn_polar* Q;
+    double mass;
+    double inertia[3];
+} mardyn_component;
+
+typedef struct {
+    double dt;                  /* time step (> 0)                               */
+    double eps_rf;              /* reaction-field dielectric constant (>= 1;
+                                   INFINITY = conducting boundary), A4           */
+    int32_t lj_shift;           /* 1 = truncated and shifted LJ (LJTS, A2)       */
+    const double* eta;          /* n_comps*n_comps binary parameters or
+                                   NULL (all 1); copied                           */
+    void* cuda_stream;          /* cudaStream_t or NULL                          */
+} mardyn_options;
+
+typedef struct {
+    int64_t step;               /* index k of the time t_k these values refer to */
+    double U_pot;               /* potential energy U(t_k)                       */
+    double virial;              /* molecular virial W = sum_{i<j} (r_i-r_j).F_ij, A6 */
+    double T;                   /* 2 (KE_t + KE_r) / N_dof, A9                   */
+    double E_kin_trans, E_kin_rot;
+    int64_t n_pairs;            /* unique molecule pairs with r_ij < rc          */
+    int64_t n_candidates;       /* 27-cell full-shell candidates (i != j)        */
+} mardyn_observables;
+
+typedef struct {
+    int32_t ncell[3];           /* cells per axis, n_k = floor(L_k / rc)         */
+    int32_t pad;
+    double quantum;             /* s (a power of two)                            */
+    int64_t period[3];          /* P_k in quanta                                 */
+    int64_t edge[3];            /* E_k in quanta                                 */
+    double box[3];              /* snapped box P_k * s                           */
+    int64_t cut2_q;             /* smallest r^2 (in quanta^2) NOT within rc:
+                                   ceil(fl64(rc*rc) / s^2)                        */
+    int32_t kernel;             /* force kernel in use: 0 = single LJ site fast
+                                   path, 1 = rigid (templated shape), 2 = generic */
+    int32_t n_slots;            /* float4 site slots per molecule (rigid kernels) */
+} mardyn_grid;
+
+/*
+ * Create a context for box L[3] (periodic), cutoff rc and the given
+ * components (copied).  Requires n_k = floor(L_k / rc) >= 3 on every axis.
+ */
+int mardyn_create(const double box[3], double cutoff, const mardyn_component* comps,
+                  int32_t n_comps, const mardyn_options* opt, struct mardyn_ctx** out);
+
+/* Grid, lattice and kernel choice of a context (reading A12).              */
+int mardyn_get_grid(const struct mardyn_ctx* ctx, mardyn_grid* out);
+
+/* Device bytes needed for up to n_capacity molecules.                      */
+int mardyn_workspace_bytes(struct mardyn_ctx* ctx, int64_t n_capacity, size_t* bytes);
+
+/* Hand the context a device buffer (16-byte aligned) of at least
+ * mardyn_workspace_bytes(n_capacity) bytes; must precede set_molecules.     */
+int mardyn_set_workspace(struct mardyn_ctx* ctx, void* device_ptr, size_t bytes,
+                         int64_t n_capacity);
+
+/*
+ * Load n molecules from HOST arrays: id (n, may be NULL = 0..n-1), comp (n),
+ * r (n*3 positions, wrapped into the box), v (n*3), q (n*4 unit quaternions
+ * (w,x,y,z), body->world), j (n*3 world-frame angular momenta; q, j may be
+ * NULL for single-site models).  half_step = 0: v, j are on-step values at
+ * t0 and the library applies the backward half kick v -= dt/2 F/m,
+ * j -= dt/2 tau with F(t0), tau(t0) (A8); 1: v, j are already
+ * v(t0 - dt/2), j(t0 - dt/2), as returned by mardyn_get_molecules.
+ * The arrays are copied to the device and converted there.
+ */
+int mardyn_set_molecules(struct mardyn_ctx* ctx, int64_t n, const int64_t* id,
+                         const int32_t* comp, const double* r, const double* v,
+                         const double* q, const double* j, int32_t half_step);
+
+/* F(t), tau(t), U, W at the current positions (no integration).           */
+int mardyn_compute_forces(struct mardyn_ctx* ctx);
+
+/* n leapfrog steps (asynchronous; per step: forces at t_k, observables of
+ * t_k, kick + drift + rotation, cell rebuild by counting sort).            */
+int mardyn_step(struct mardyn_ctx* ctx, int32_t n);
+
+/* Observables of the last evaluated time (A23): after step(n) from t0 this
+ * is t_{n-1}; after compute_forces it is the current t.                     */
+int mardyn_get_observables(struct mardyn_ctx* ctx, mardyn_observables* out);
+
+/* Up to cap most recent per-step observables, oldest first (ring of 4096). */
+int mardyn_get_observable_history(struct mardyn_ctx* ctx, int32_t cap, int32_t* n,
+                                  mardyn_observables* out);
+
+/* Molecule state in the caller's original order (index of set_molecules):
+ * r (n*3), v (n*3, at t - dt/2), q (n*4), j (n*3, at t - dt/2); any output
+ * pointer may be NULL.  cap must be >= n.                                  */
+int mardyn_get_molecules(struct mardyn_ctx* ctx, int64_t cap, int64_t* n, int64_t* id,
+                         int32_t* comp, double* r, double* v, double* q, double* j);
+
+/* Forces F (n*3) and torques tau (n*3) of the last force evaluation, in the
+ * caller's original order.                                                  */
+int mardyn_get_forces(struct mardyn_ctx* ctx, int64_t cap, double* F, double* tau);
+
+/* Raw parity hook: fixed-point positions u (n*3, original order), cell of
+ * each molecule (n) and count per cell (n_cells), as used by the last force
+ * evaluation.  Any pointer may be NULL.                                     */
+int mardyn_get_raw(struct mardyn_ctx* ctx, int64_t cap, uint32_t* pos_fixed,
+                   int32_t* cell, int32_t* cell_count);
+
+/* Device timing of the last mardyn_step call: total ms and ms in the force
+ * kernel (CUDA events on the context stream; 0 if not recorded).           */
+int mardyn_last_step_timing(struct mardyn_ctx* ctx, double* total_ms, double* force_ms,
+                            int32_t* force_launches);
+
+/* Enable (1) / disable (0) per-step CUDA event timing of the force kernel. */
+int mardyn_set_profiling(struct mardyn_ctx* ctx, int32_t on);
+
+/* Number of device kernel launches enqueued so far by this context.        */
+int64_t mardyn_launch_count(const struct mardyn_ctx* ctx);
+
+const char* mardyn_last_error(const struct mardyn_ctx* ctx);
+void mardyn_destroy(struct mardyn_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MARDYN_H */

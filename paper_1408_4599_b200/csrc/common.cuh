@@ -1,0 +1,118 @@
+// common.cuh -- device-side data layout and constants of the B200 hot path.
+//
+// HBM layout: structure of arrays, one row per molecule,
+// sorted by cell (x fastest) and, inside a cell, by internal id (reading
+// A13), rebuilt every step by counting sort.  The state is double-buffered
+// (cur -> nxt by the canonicalising gather).
+//   pos   uint4  (u_x, u_y, u_z, iid)        fixed-point position (A12) + id
+//   vel   float4 (v_x, v_y, v_z, comp bits)  v(t - dt/2)
+//   quat  float4 (w, x, y, z)                rigid only
+//   angm  float4 (j_x, j_y, j_z, 0)          world frame, j(t - dt/2), rigid
+//   xs    float4 (x, y, z cell-relative, comp bits)  staging copy read by the
+//                force kernels; exact multiples of s below 2^23 s
+//   site  float4 [n_slots][cap]              world-frame site offsets / axes
+//   force float4 (F, 0), torque float4 (tau, 0)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define MD_MAX_COMP 8
+#define MD_MAX_SITES 12          // sites per component
+#define MD_MAX_LJ_TOTAL 16       // LJ sites over all components (mixing table)
+#define MD_MAX_SLOTS 16          // float4 site slots per molecule
+#define MD_HISTORY 4096          // observable ring buffer
+
+enum { MD_LJ = 0, MD_CHARGE = 1, MD_DIPOLE = 2, MD_QUAD = 3 };
+
+struct DevComp {
+    float mass, inv_mass;
+    float invI[3];               // 0 where the moment is 0
+    int n_lj, n_q, n_mu, n_Q;
+    int lj0;                     // first global LJ index (mixing table)
+    int slot_lj, slot_q, slot_mu, slot_Q;   // first slot of each kind; polar
+                                             // sites use 2 slots (pos, axis)
+    int n_slots;
+    int rot;                     // rotational degrees of freedom
+    float bpos[MD_MAX_SITES][3]; // body positions in slot order of kinds
+    float baxis[MD_MAX_SITES][3];
+    float mom[MD_MAX_SITES];     // q / mu / Q per site (LJ: unused)
+};
+
+struct DevModel {
+    int n_comp;
+    int n_lj_total;
+    float krf, crf, krf_mumu;    // reaction field (A4)
+    DevComp comp[MD_MAX_COMP];
+    // LJ mixing table over global LJ site indices (Lorentz-Berthelot * eta)
+    float sig2[MD_MAX_LJ_TOTAL * MD_MAX_LJ_TOTAL];
+    float eps24[MD_MAX_LJ_TOTAL * MD_MAX_LJ_TOTAL];
+    float eps4[MD_MAX_LJ_TOTAL * MD_MAX_LJ_TOTAL];
+    float shift[MD_MAX_LJ_TOTAL * MD_MAX_LJ_TOTAL];   // 4 eps [(s/rc)^12 - (s/rc)^6] if LJTS
+};
+
+struct GridP {
+    int nc[3];
+    int ncell;
+    uint32_t E[3];               // cell edge in quanta (<= 2^23)
+    uint32_t P[3];               // period in quanta (P may be 2^32 - wrap with 64-bit)
+    uint64_t P64[3];
+    float s, inv_s;              // quantum, 1/s (powers of two)
+    float edge[3];               // E * s
+    float cut2;                  // rc^2 (fp32)
+    float cut2_lo, cut2_hi;      // guard band around rc^2 for the exact test
+    long long cut2_q;            // exact threshold in quanta^2: in range iff r2q < cut2_q
+    float dt;
+};
+
+struct ObsRec {                  // one history entry (matches mardyn_observables order)
+    long long step;
+    double U, W, T, KEt, KEr;
+    long long npairs, ncand;
+};
+
+struct ForcePartial {            // per warp of a force kernel
+    double U, W;
+    long long npairs, ncand;
+};
+
+__device__ __forceinline__ int warp_lane() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ double warp_sum_d(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_sum_f(float v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// body -> world rotation of vector b by unit quaternion q = (w,x,y,z)
+__device__ __forceinline__ float3 qrot(float4 q, float bx, float by, float bz)
+{
+    const float w = q.x, x = q.y, y = q.z, z = q.w;
+    float3 r;
+    r.x = (1.f - 2.f * (y * y + z * z)) * bx + 2.f * (x * y - w * z) * by + 2.f * (x * z + w * y) * bz;
+    r.y = 2.f * (x * y + w * z) * bx + (1.f - 2.f * (x * x + z * z)) * by + 2.f * (y * z - w * x) * bz;
+    r.z = 2.f * (x * z - w * y) * bx + 2.f * (y * z + w * x) * by + (1.f - 2.f * (x * x + y * y)) * bz;
+    return r;
+}
+// world -> body: R^T v
+__device__ __forceinline__ float3 qrotT(float4 q, float3 v)
+{
+    const float w = q.x, x = q.y, y = q.z, z = q.w;
+    float3 r;
+    r.x = (1.f - 2.f * (y * y + z * z)) * v.x + 2.f * (x * y + w * z) * v.y + 2.f * (x * z - w * y) * v.z;
+    r.y = 2.f * (x * y - w * z) * v.x + (1.f - 2.f * (x * x + z * z)) * v.y + 2.f * (y * z + w * x) * v.z;
+    r.z = 2.f * (x * z + w * y) * v.x + 2.f * (y * z - w * x) * v.y + (1.f - 2.f * (x * x + y * y)) * v.z;
+    return r;
+}

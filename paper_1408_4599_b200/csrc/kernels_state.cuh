@@ -1,0 +1,419 @@
+// kernels_state.cuh -- bandwidth kernels of the hot path: ingest (host
+// doubles -> fixed point), per-step cell rebuild by counting sort
+// (histogram fused into the integrator, exclusive scan, scatter, canonical
+// in-cell order by id), leapfrog + Fincham integrator, deterministic
+// reductions, egress.  All of them are HBM-bound.
+#pragma once
+#include "common.cuh"
+
+// ------------------------------------------------------------------------
+// ingest: host arrays (already on the device as doubles) -> state, cell and
+// arrival rank (reading A12: u = rint(r/s) mod P, exact in fp64 because s is
+// a power of two).
+__global__ void k_ingest(int n, const double* __restrict__ r, const double* __restrict__ v,
+                         const double* __restrict__ q, const double* __restrict__ j,
+                         const int* __restrict__ comp, GridP g, uint4* __restrict__ pos,
+                         float4* __restrict__ vel, float4* __restrict__ quat,
+                         float4* __restrict__ angm, int* __restrict__ cell_of,
+                         int* __restrict__ rank, int* __restrict__ count)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t u[3];
+    int c[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        long long P = (long long)g.P64[k];
+        long long x = __double2ll_rn(r[3 * i + k] / (double)g.s);
+        x %= P;
+        if (x < 0) x += P;
+        u[k] = (uint32_t)x;
+        c[k] = (int)(u[k] / g.E[k]);
+    }
+    pos[i] = make_uint4(u[0], u[1], u[2], (uint32_t)i);
+    vel[i] = make_float4((float)v[3 * i], (float)v[3 * i + 1], (float)v[3 * i + 2],
+                         __int_as_float(comp[i]));
+    if (quat) {
+        quat[i] = q ? make_float4((float)q[4 * i], (float)q[4 * i + 1], (float)q[4 * i + 2], (float)q[4 * i + 3])
+                    : make_float4(1.f, 0.f, 0.f, 0.f);
+        angm[i] = j ? make_float4((float)j[3 * i], (float)j[3 * i + 1], (float)j[3 * i + 2], 0.f)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    int cl = c[0] + g.nc[0] * (c[1] + g.nc[1] * c[2]);
+    cell_of[i] = cl;
+    rank[i] = atomicAdd(&count[cl], 1);
+}
+
+// ------------------------------------------------------------------------
+// exclusive scan of the per-cell counts (3 kernels: tile scan, scan of tile
+// totals, add).  Tiles of 4096 cells, 1024 threads x 4 cells.
+#define SCAN_TILE 4096
+
+__device__ __forceinline__ int warp_incl_scan(int v)
+{
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// block-wide exclusive scan of one int per thread (blockDim = 1024)
+__device__ __forceinline__ int block_excl_scan(int v, int* total)
+{
+    __shared__ int wsum[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int inc = warp_incl_scan(v);
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        int x = wsum[lane];
+        int xi = warp_incl_scan(x);
+        wsum[lane] = xi - x;
+        if (lane == 31) *total = xi;
+    }
+    __syncthreads();
+    int res = inc - v + wsum[w];
+    __syncthreads();
+    return res;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_tiles(int ncell, const int* __restrict__ count,
+                                                     int* __restrict__ start, int* __restrict__ tsum)
+{
+    __shared__ int tot;
+    int base = blockIdx.x * SCAN_TILE + threadIdx.x * 4;
+    int a[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = (base + k < ncell) ? count[base + k] : 0;
+    int s = a[0] + a[1] + a[2] + a[3];
+    int ex = block_excl_scan(s, &tot);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (base + k < ncell) start[base + k] = ex;
+        ex += a[k];
+    }
+    if (threadIdx.x == 0) tsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_sums(int ntiles, int* __restrict__ tsum)
+{
+    __shared__ int tot;
+    // ntiles <= 4096: 4 per thread
+    int base = threadIdx.x * 4;
+    int a[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = (base + k < ntiles) ? tsum[base + k] : 0;
+    int s = a[0] + a[1] + a[2] + a[3];
+    int ex = block_excl_scan(s, &tot);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (base + k < ntiles) tsum[base + k] = ex;
+        ex += a[k];
+    }
+}
+
+__global__ void k_scan_add(int ncell, int n, int* __restrict__ start, const int* __restrict__ tsum)
+{
+    int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < ncell) start[c] += tsum[c / SCAN_TILE];
+    if (c == 0) start[ncell] = n;
+}
+
+// ------------------------------------------------------------------------
+// scatter: key = (iid << 32 | unsorted index) at start[cell] + arrival rank
+__global__ void k_scatter(int n, const uint4* __restrict__ pos, const int* __restrict__ cell_of,
+                          const int* __restrict__ rank, const int* __restrict__ start,
+                          unsigned long long* __restrict__ keys)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int slot = start[cell_of[i]] + rank[i];
+    keys[slot] = ((unsigned long long)pos[i].w << 32) | (unsigned)i;
+}
+
+// canonical gather: each sorted slot finds its rank by id inside its cell
+// (reading A13), then gathers the molecule's state from the unsorted arrays
+// and writes the staging copy (cell-relative coordinates, exact) and, for
+// rigid models, the world-frame site offsets s = R(q) d.
+template <bool RIGID>
+__global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __restrict__ keys,
+                        const int* __restrict__ cell_of, const int* __restrict__ start,
+                        const uint4* __restrict__ pos_s, const float4* __restrict__ vel_s,
+                        const float4* __restrict__ quat_s, const float4* __restrict__ angm_s,
+                        uint4* __restrict__ pos_d, float4* __restrict__ vel_d,
+                        float4* __restrict__ quat_d, float4* __restrict__ angm_d,
+                        float4* __restrict__ xs, float4* __restrict__ site,
+                        const DevModel* __restrict__ model)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    unsigned long long key = keys[t];
+    unsigned old = (unsigned)(key & 0xffffffffu);
+    unsigned id = (unsigned)(key >> 32);
+    int c = cell_of[old];
+    int s0 = start[c], s1 = start[c + 1];
+    int r = 0;
+    for (int m = s0; m < s1; ++m) r += (unsigned)(keys[m] >> 32) < id;
+    int dst = s0 + r;
+    uint4 p = pos_s[old];
+    float4 v = vel_s[old];
+    pos_d[dst] = p;
+    vel_d[dst] = v;
+    int cx = c % g.nc[0];
+    int cy = (c / g.nc[0]) % g.nc[1];
+    int cz = c / (g.nc[0] * g.nc[1]);
+    float4 x;
+    x.x = (float)(int)(p.x - (uint32_t)cx * g.E[0]) * g.s;    // exact (A12)
+    x.y = (float)(int)(p.y - (uint32_t)cy * g.E[1]) * g.s;
+    x.z = (float)(int)(p.z - (uint32_t)cz * g.E[2]) * g.s;
+    x.w = v.w;                                                  // comp bits
+    xs[dst] = x;
+    if (RIGID) {
+        float4 q = quat_s[old];
+        quat_d[dst] = q;
+        angm_d[dst] = angm_s[old];
+        const DevComp& C = model->comp[__float_as_int(v.w)];
+        int ns = C.n_lj + C.n_q;
+        for (int k = 0; k < ns; ++k) {
+            float3 w = qrot(q, C.bpos[k][0], C.bpos[k][1], C.bpos[k][2]);
+            site[(size_t)k * cap + dst] = make_float4(w.x, w.y, w.z, C.mom[k]);
+        }
+        int np = C.n_mu + C.n_Q;
+        for (int k = 0; k < np; ++k) {
+            int sidx = ns + k;
+            float3 w = qrot(q, C.bpos[sidx][0], C.bpos[sidx][1], C.bpos[sidx][2]);
+            float3 e = qrot(q, C.baxis[sidx][0], C.baxis[sidx][1], C.baxis[sidx][2]);
+            site[(size_t)(ns + 2 * k) * cap + dst] = make_float4(w.x, w.y, w.z, C.mom[sidx]);
+            site[(size_t)(ns + 2 * k + 1) * cap + dst] = make_float4(e.x, e.y, e.z, 0.f);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------
+// integrator (Eqs. 2-5 with readings A7, A9, A12), in place on the sorted
+// state; fuses the next step's cell binning (histogram + arrival rank) and
+// the kinetic-energy partials (per block, fixed order, fp64).
+__device__ __forceinline__ float4 qmul(float4 a, float4 b)
+{
+    return make_float4(a.x * b.x - a.y * b.y - a.z * b.z - a.w * b.w,
+                       a.x * b.y + a.y * b.x + a.z * b.w - a.w * b.z,
+                       a.x * b.z - a.y * b.w + a.z * b.x + a.w * b.y,
+                       a.x * b.w + a.y * b.z - a.z * b.y + a.w * b.x);
+}
+__device__ __forceinline__ float4 qnormalize(float4 q)
+{
+    float s = rsqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+    return make_float4(q.x * s, q.y * s, q.z * s, q.w * s);
+}
+
+template <int NT>
+__device__ __forceinline__ void block_sum2_d(double a, double b, double* out_a, double* out_b)
+{
+    __shared__ double sa[NT / 32], sb[NT / 32];
+    a = warp_sum_d(a);
+    b = warp_sum_d(b);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) { sa[w] = a; sb[w] = b; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double x = 0, y = 0;
+        for (int k = 0; k < NT / 32; ++k) { x += sa[k]; y += sb[k]; }
+        *out_a = x; *out_b = y;
+    }
+}
+
+template <bool RIGID>
+__global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevModel* __restrict__ model,
+                                                   uint4* __restrict__ pos, float4* __restrict__ vel,
+                                                   float4* __restrict__ quat, float4* __restrict__ angm,
+                                                   const float4* __restrict__ force,
+                                                   const float4* __restrict__ torque,
+                                                   int* __restrict__ cell_of, int* __restrict__ rank,
+                                                   int* __restrict__ count, double* __restrict__ ke_part,
+                                                   int* __restrict__ flag)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    double ket = 0.0, ker = 0.0;
+    if (t < n) {
+        uint4 p = pos[t];
+        float4 v = vel[t];
+        float4 F = force[t];
+        const DevComp& C = model->comp[__float_as_int(v.w)];
+        const float dt = g.dt, im = C.inv_mass;
+        // A9: KE_t(t) from v(t) = v(t - dt/2) + dt/2 F/m
+        float vx = v.x + 0.5f * dt * F.x * im, vy = v.y + 0.5f * dt * F.y * im,
+              vz = v.z + 0.5f * dt * F.z * im;
+        ket = 0.5 * (double)C.mass * ((double)vx * vx + (double)vy * vy + (double)vz * vz);
+        // Eq. 2 kick, Eq. 3 drift on the fixed-point lattice (A12)
+        v.x += dt * F.x * im; v.y += dt * F.y * im; v.z += dt * F.z * im;
+        float vv[3] = {v.x, v.y, v.z};
+        uint32_t uu[3] = {p.x, p.y, p.z};
+        int c[3];
+        bool bad = !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float d = (dt * vv[k]) * g.inv_s;
+            bad |= !(fabsf(d) < (float)g.E[k]);
+            long long du = bad ? 0 : __float2ll_rn(d);
+            long long x = (long long)uu[k] + du;
+            long long P = (long long)g.P64[k];
+            if (x < 0) x += P;
+            else if (x >= P) x -= P;
+            uu[k] = (uint32_t)x;
+            c[k] = (int)(uu[k] / g.E[k]);
+        }
+        if (bad) atomicOr(flag, 1);
+        pos[t] = make_uint4(uu[0], uu[1], uu[2], p.w);
+        vel[t] = v;
+        if (RIGID && C.rot) {
+            // Fincham rotational leapfrog (reading A7 of Eqs. 4-5)
+            float4 q = quat[t];
+            float4 jh = angm[t];
+            float4 tq = torque[t];
+            float3 jt = make_float3(jh.x + 0.5f * dt * tq.x, jh.y + 0.5f * dt * tq.y, jh.z + 0.5f * dt * tq.z);
+            float3 jb = qrotT(q, jt);
+            float3 wb = make_float3(jb.x * C.invI[0], jb.y * C.invI[1], jb.z * C.invI[2]);
+            ker = 0.5 * ((double)jb.x * wb.x + (double)jb.y * wb.y + (double)jb.z * wb.z);
+            float4 dq = qmul(q, make_float4(0.f, wb.x, wb.y, wb.z));
+            float4 qh = qnormalize(make_float4(q.x + 0.25f * dt * dq.x, q.y + 0.25f * dt * dq.y,
+                                               q.z + 0.25f * dt * dq.z, q.w + 0.25f * dt * dq.w));
+            float3 jn = make_float3(jh.x + dt * tq.x, jh.y + dt * tq.y, jh.z + dt * tq.z);
+            float3 jb2 = qrotT(qh, jn);
+            float3 wb2 = make_float3(jb2.x * C.invI[0], jb2.y * C.invI[1], jb2.z * C.invI[2]);
+            float4 dq2 = qmul(qh, make_float4(0.f, wb2.x, wb2.y, wb2.z));
+            float4 qn = qnormalize(make_float4(q.x + 0.5f * dt * dq2.x, q.y + 0.5f * dt * dq2.y,
+                                               q.z + 0.5f * dt * dq2.z, q.w + 0.5f * dt * dq2.w));
+            quat[t] = qn;
+            angm[t] = make_float4(jn.x, jn.y, jn.z, 0.f);
+            if (!(isfinite(jn.x) && isfinite(jn.y) && isfinite(jn.z))) atomicOr(flag, 1);
+        }
+        int cl = c[0] + g.nc[0] * (c[1] + g.nc[1] * c[2]);
+        cell_of[t] = cl;
+        rank[t] = atomicAdd(&count[cl], 1);
+    }
+    block_sum2_d<256>(ket, ker, &ke_part[2 * blockIdx.x], &ke_part[2 * blockIdx.x + 1]);
+}
+
+// kinetic energy at t without integrating (compute_forces, A9)
+template <bool RIGID>
+__global__ void __launch_bounds__(256) k_kinetic(int n, GridP g, const DevModel* __restrict__ model,
+                                                 const float4* __restrict__ vel,
+                                                 const float4* __restrict__ quat,
+                                                 const float4* __restrict__ angm,
+                                                 const float4* __restrict__ force,
+                                                 const float4* __restrict__ torque,
+                                                 double* __restrict__ ke_part)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    double ket = 0.0, ker = 0.0;
+    if (t < n) {
+        float4 v = vel[t];
+        float4 F = force[t];
+        const DevComp& C = model->comp[__float_as_int(v.w)];
+        const float dt = g.dt, im = C.inv_mass;
+        float vx = v.x + 0.5f * dt * F.x * im, vy = v.y + 0.5f * dt * F.y * im,
+              vz = v.z + 0.5f * dt * F.z * im;
+        ket = 0.5 * (double)C.mass * ((double)vx * vx + (double)vy * vy + (double)vz * vz);
+        if (RIGID && C.rot) {
+            float4 q = quat[t], jh = angm[t], tq = torque[t];
+            float3 jt = make_float3(jh.x + 0.5f * dt * tq.x, jh.y + 0.5f * dt * tq.y, jh.z + 0.5f * dt * tq.z);
+            float3 jb = qrotT(q, jt);
+            ker = 0.5 * ((double)jb.x * jb.x * C.invI[0] + (double)jb.y * jb.y * C.invI[1] +
+                         (double)jb.z * jb.z * C.invI[2]);
+        }
+    }
+    block_sum2_d<256>(ket, ker, &ke_part[2 * blockIdx.x], &ke_part[2 * blockIdx.x + 1]);
+}
+
+// backward half kick of the initial on-step velocities (reading A8)
+template <bool RIGID>
+__global__ void k_half_kick(int n, GridP g, const DevModel* __restrict__ model, float4* __restrict__ vel,
+                            float4* __restrict__ angm, const float4* __restrict__ force,
+                            const float4* __restrict__ torque)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    float4 v = vel[t];
+    float4 F = force[t];
+    const DevComp& C = model->comp[__float_as_int(v.w)];
+    const float h = 0.5f * g.dt;
+    v.x -= h * F.x * C.inv_mass; v.y -= h * F.y * C.inv_mass; v.z -= h * F.z * C.inv_mass;
+    vel[t] = v;
+    if (RIGID && C.rot) {
+        float4 j = angm[t], tq = torque[t];
+        angm[t] = make_float4(j.x - h * tq.x, j.y - h * tq.y, j.z - h * tq.z, 0.f);
+    }
+}
+
+// observables of one time t_k: fixed-order sums of the per-warp force
+// partials and the per-block kinetic partials, written to the ring buffer.
+__global__ void __launch_bounds__(1024) k_finalize(int nfp, const ForcePartial* __restrict__ fp,
+                                                   int nkp, const double* __restrict__ kp,
+                                                   double ndof, long long* __restrict__ step_ctr,
+                                                   int advance, ObsRec* __restrict__ hist)
+{
+    double U = 0, W = 0, Kt = 0, Kr = 0;
+    long long np = 0, nc = 0;
+    for (int k = threadIdx.x; k < nfp; k += 1024) {
+        ForcePartial f = fp[k];
+        U += f.U; W += f.W; np += f.npairs; nc += f.ncand;
+    }
+    for (int k = threadIdx.x; k < nkp; k += 1024) { Kt += kp[2 * k]; Kr += kp[2 * k + 1]; }
+    __shared__ double sU[32], sW[32], sKt[32], sKr[32];
+    __shared__ long long snp[32], snc[32];
+    U = warp_sum_d(U); W = warp_sum_d(W); Kt = warp_sum_d(Kt); Kr = warp_sum_d(Kr);
+    np = warp_sum_ll(np); nc = warp_sum_ll(nc);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) { sU[w] = U; sW[w] = W; sKt[w] = Kt; sKr[w] = Kr; snp[w] = np; snc[w] = nc; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ObsRec o;
+        o.U = 0; o.W = 0; o.KEt = 0; o.KEr = 0; o.npairs = 0; o.ncand = 0;
+        for (int k = 0; k < 32; ++k) {
+            o.U += sU[k]; o.W += sW[k]; o.KEt += sKt[k]; o.KEr += sKr[k];
+            o.npairs += snp[k]; o.ncand += snc[k];
+        }
+        o.npairs /= 2;                       // full shell sees every pair twice
+        o.T = 2.0 * (o.KEt + o.KEr) / ndof;
+        long long s = *step_ctr;
+        o.step = s;
+        hist[s % MD_HISTORY] = o;
+        if (advance) *step_ctr = s + 1;
+    }
+}
+
+// ------------------------------------------------------------------------
+// egress: sorted state -> caller order (index = iid), doubles
+template <bool RIGID>
+__global__ void k_egress(int n, GridP g, const uint4* __restrict__ pos, const float4* __restrict__ vel,
+                         const float4* __restrict__ quat, const float4* __restrict__ angm,
+                         const float4* __restrict__ force, const float4* __restrict__ torque,
+                         double* __restrict__ r, double* __restrict__ v, double* __restrict__ q,
+                         double* __restrict__ j, double* __restrict__ F, double* __restrict__ tau,
+                         uint32_t* __restrict__ ufix, int* __restrict__ cell)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    uint4 p = pos[t];
+    int i = (int)p.w;
+    if (r) { r[3 * i] = (double)p.x * g.s; r[3 * i + 1] = (double)p.y * g.s; r[3 * i + 2] = (double)p.z * g.s; }
+    if (ufix) { ufix[3 * i] = p.x; ufix[3 * i + 1] = p.y; ufix[3 * i + 2] = p.z; }
+    if (cell) {
+        int cx = p.x / g.E[0], cy = p.y / g.E[1], cz = p.z / g.E[2];
+        cell[i] = cx + g.nc[0] * (cy + g.nc[1] * cz);
+    }
+    if (v) { float4 x = vel[t]; v[3 * i] = x.x; v[3 * i + 1] = x.y; v[3 * i + 2] = x.z; }
+    if (F) { float4 x = force[t]; F[3 * i] = x.x; F[3 * i + 1] = x.y; F[3 * i + 2] = x.z; }
+    if (RIGID) {
+        if (q) { float4 x = quat[t]; q[4 * i] = x.x; q[4 * i + 1] = x.y; q[4 * i + 2] = x.z; q[4 * i + 3] = x.w; }
+        if (j) { float4 x = angm[t]; j[3 * i] = x.x; j[3 * i + 1] = x.y; j[3 * i + 2] = x.z; }
+        if (tau) { float4 x = torque[t]; tau[3 * i] = x.x; tau[3 * i + 1] = x.y; tau[3 * i + 2] = x.z; }
+    } else {
+        if (q) { q[4 * i] = 1; q[4 * i + 1] = 0; q[4 * i + 2] = 0; q[4 * i + 3] = 0; }
+        if (j) { j[3 * i] = 0; j[3 * i + 1] = 0; j[3 * i + 2] = 0; }
+        if (tau) { tau[3 * i] = 0; tau[3 * i + 1] = 0; tau[3 * i + 2] = 0; }
+    }
+}

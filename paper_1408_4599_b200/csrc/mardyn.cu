@@ -1,0 +1,867 @@
+// mardyn.cu -- host engine and C ABI (include/mardyn.h) of the B200-native
+// ls1-mardyn hot path.  Every step of the path runs in the kernels of
+// kernels_state.cuh / kernels_force.cuh; this file validates inputs, lays
+// out the caller-provided workspace, builds the per-component tables,
+// captures one time step per buffer parity as a CUDA graph and replays it.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mardyn.h"
+#include "common.cuh"
+#include "kernels_force.cuh"
+#include "kernels_state.cuh"
+
+namespace {
+
+struct HostComp {
+    std::vector<mardyn_lj_site> lj;
+    std::vector<mardyn_charge> q;
+    std::vector<mardyn_polar> mu, Q;
+    double mass;
+    double I[3];
+};
+
+enum KernelKind { KER_LJ1 = 0, KER_RIGID = 1, KER_GENERIC = 2 };
+enum RigidShape { SHAPE_NONE, SHAPE_2CLJQ, SHAPE_TIP4P, SHAPE_GEN };
+
+constexpr int LJ1_WARPS = 4;
+constexpr int RIG_WARPS = 4;
+constexpr int GEN_WARPS = 1;
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct mardyn_ctx {
+    std::string err;
+    double L[3], rc, dt, eps_rf;
+    int lj_shift;
+    std::vector<HostComp> comps;
+    std::vector<double> eta;
+    GridP g;
+    DevModel model;
+    int kernel = KER_LJ1;
+    int shape = SHAPE_NONE;
+    bool rigid = false;
+    int nslots = 0;
+    int force_warps_per_block = LJ1_WARPS;
+    int force_blocks = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int device = 0;
+    int num_sms = 0;
+    // workspace
+    char* ws = nullptr;
+    size_t ws_bytes = 0;
+    int64_t cap = 0;
+    int ncell_pad = 0;
+    int ntiles = 0;
+    int nkblocks = 0;
+    uint4* pos[2] = {nullptr, nullptr};
+    float4* vel[2] = {nullptr, nullptr};
+    float4* quat[2] = {nullptr, nullptr};
+    float4* angm[2] = {nullptr, nullptr};
+    float4* xs = nullptr;
+    float4* site = nullptr;
+    float4* force = nullptr;
+    float4* torque = nullptr;
+    int* cell_of = nullptr;
+    int* rank = nullptr;
+    int* count = nullptr;
+    int* start = nullptr;
+    int* tsum = nullptr;
+    unsigned long long* keys = nullptr;
+    ForcePartial* fpart = nullptr;
+    double* kpart = nullptr;
+    ObsRec* hist = nullptr;
+    long long* step_ctr = nullptr;
+    int* flag = nullptr;
+    DevModel* dmodel = nullptr;
+    char* stage = nullptr;
+    size_t stage_bytes = 0;
+    // state
+    int cur = 0;
+    int64_t n = 0;
+    bool loaded = false;
+    bool poisoned = false;
+    double ndof = 0;
+    long long host_step = 0;       // number of completed steps
+    long long last_obs = -1;       // history index of the last evaluated time
+    std::vector<int64_t> ids;
+    std::vector<int32_t> comp_host;
+    // graphs: one time step starting from buffer parity 0 / 1
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    cudaEvent_t ev_f0[2] = {nullptr, nullptr}, ev_f1[2] = {nullptr, nullptr};
+    cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;
+    int last_parity = 0;
+    bool profiling = true;
+    long long launches = 0;
+    double last_total_ms = 0, last_force_ms = 0;
+    int last_force_launches = 0;
+};
+
+// ------------------------------------------------------------------------
+// helpers
+
+static int fail(mardyn_ctx* c, int code, const std::string& msg)
+{
+    if (c) c->err = msg;
+    return code;
+}
+
+#define CK(call)                                                                           \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) {                                                           \
+            ctx->poisoned = true;                                                          \
+            return fail(ctx, MARDYN_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+        }                                                                                  \
+    } while (0)
+
+// grid and fixed-point lattice, reading A12
+static int setup_grid(mardyn_ctx* ctx)
+{
+    int nc[3];
+    for (int k = 0; k < 3; ++k) {
+        nc[k] = (int)std::floor(ctx->L[k] / ctx->rc);
+        if (nc[k] < 3) return fail(ctx, MARDYN_EINVAL, "box must hold >= 3 cells of edge >= rc per axis");
+    }
+    double s = 0;
+    long long E[3];
+    for (int it = 0; it < 4; ++it) {
+        double emax = 0;
+        for (int k = 0; k < 3; ++k) emax = std::fmax(emax, ctx->L[k] / nc[k]);
+        int ex = (int)std::ceil(std::log2(emax));
+        s = std::ldexp(1.0, ex - 23);
+        bool again = false;
+        for (int k = 0; k < 3; ++k) {
+            E[k] = std::llround(ctx->L[k] / (nc[k] * s));
+            if ((double)E[k] * s < ctx->rc) { nc[k] -= 1; again = true; }
+            if (nc[k] < 3) return fail(ctx, MARDYN_EINVAL, "box must hold >= 3 cells of edge >= rc per axis");
+        }
+        if (!again) break;
+    }
+    GridP& g = ctx->g;
+    std::memset(&g, 0, sizeof(g));
+    long long ncell = 1;
+    for (int k = 0; k < 3; ++k) {
+        g.nc[k] = nc[k];
+        g.E[k] = (uint32_t)E[k];
+        uint64_t P = (uint64_t)E[k] * (uint64_t)nc[k];
+        if (P > (1ull << 32)) return fail(ctx, MARDYN_EINVAL, "box too large for 32-bit fixed point");
+        g.P64[k] = P;
+        g.P[k] = (uint32_t)(P & 0xffffffffu);
+        g.edge[k] = (float)((double)E[k] * s);
+        ncell *= nc[k];
+    }
+    if (ncell > (1ll << 30)) return fail(ctx, MARDYN_EINVAL, "too many cells");
+    g.ncell = (int)ncell;
+    g.s = (float)s;
+    g.inv_s = (float)(1.0 / s);
+    double rc2 = ctx->rc * ctx->rc;
+    g.cut2 = (float)rc2;
+    g.cut2_lo = std::nextafterf((float)(rc2 * (1.0 - std::ldexp(1.0, -20))), 0.f);
+    g.cut2_hi = std::nextafterf((float)(rc2 * (1.0 + std::ldexp(1.0, -20))), INFINITY);
+    g.cut2_q = (long long)std::ceil(rc2 / (s * s));
+    g.dt = (float)ctx->dt;
+    return MARDYN_OK;
+}
+
+static int build_model(mardyn_ctx* ctx)
+{
+    DevModel& M = ctx->model;
+    std::memset(&M, 0, sizeof(M));
+    const int nc = (int)ctx->comps.size();
+    M.n_comp = nc;
+    const double rc = ctx->rc, rc3 = rc * rc * rc;
+    double krf, kmm;
+    if (std::isinf(ctx->eps_rf)) { krf = 1.0 / (2.0 * rc3); kmm = 1.0 / rc3; }
+    else {
+        krf = (ctx->eps_rf - 1.0) / ((2.0 * ctx->eps_rf + 1.0) * rc3);
+        kmm = 2.0 * (ctx->eps_rf - 1.0) / ((2.0 * ctx->eps_rf + 1.0) * rc3);
+    }
+    M.krf = (float)krf;
+    M.crf = (float)(1.0 / rc + krf * rc * rc);
+    M.krf_mumu = (float)kmm;
+    int lj_total = 0;
+    std::vector<double> ljsig, ljeps;
+    std::vector<int> ljcomp;
+    ctx->rigid = false;
+    ctx->nslots = 0;
+    for (int c = 0; c < nc; ++c) {
+        const HostComp& H = ctx->comps[c];
+        DevComp& D = M.comp[c];
+        D.mass = (float)H.mass;
+        D.inv_mass = (float)(1.0 / H.mass);
+        D.rot = 0;
+        for (int k = 0; k < 3; ++k) {
+            D.invI[k] = H.I[k] > 0 ? (float)(1.0 / H.I[k]) : 0.f;
+            D.rot += H.I[k] > 0;
+        }
+        D.n_lj = (int)H.lj.size(); D.n_q = (int)H.q.size();
+        D.n_mu = (int)H.mu.size(); D.n_Q = (int)H.Q.size();
+        D.lj0 = lj_total;
+        D.slot_lj = 0; D.slot_q = D.n_lj; D.slot_mu = D.n_lj + D.n_q; D.slot_Q = D.slot_mu + 2 * D.n_mu;
+        D.n_slots = D.slot_Q + 2 * D.n_Q;
+        ctx->nslots = std::max(ctx->nslots, D.n_slots);
+        int s = 0;
+        bool offcentre = false;
+        for (auto& x : H.lj) {
+            for (int k = 0; k < 3; ++k) { D.bpos[s][k] = (float)x.r[k]; offcentre |= x.r[k] != 0; }
+            D.mom[s++] = 0.f;
+            ljsig.push_back(x.sigma); ljeps.push_back(x.epsilon); ljcomp.push_back(c);
+            ++lj_total;
+        }
+        for (auto& x : H.q) {
+            for (int k = 0; k < 3; ++k) { D.bpos[s][k] = (float)x.r[k]; offcentre |= x.r[k] != 0; }
+            D.mom[s++] = (float)x.q;
+        }
+        for (auto* lst : {&H.mu, &H.Q})
+            for (auto& x : *lst) {
+                double nrm = std::sqrt(x.e[0] * x.e[0] + x.e[1] * x.e[1] + x.e[2] * x.e[2]);
+                for (int k = 0; k < 3; ++k) {
+                    D.bpos[s][k] = (float)x.r[k];
+                    D.baxis[s][k] = (float)(x.e[k] / nrm);
+                }
+                D.mom[s++] = (float)x.m;
+                offcentre = true;
+            }
+        if (offcentre || D.rot > 0 || D.n_q + D.n_mu + D.n_Q > 0 || D.n_lj != 1) ctx->rigid = true;
+    }
+    M.n_lj_total = lj_total;
+    for (int a = 0; a < lj_total; ++a)
+        for (int b = 0; b < lj_total; ++b) {
+            double eta = ctx->eta.empty() ? 1.0 : ctx->eta[ljcomp[a] * nc + ljcomp[b]];
+            double sig = 0.5 * (ljsig[a] + ljsig[b]);          // Lorentz
+            double eps = eta * std::sqrt(ljeps[a] * ljeps[b]); // Berthelot * eta
+            double sc6 = std::pow(sig / rc, 6.0);
+            int t = a * MD_MAX_LJ_TOTAL + b;
+            M.sig2[t] = (float)(sig * sig);
+            M.eps24[t] = (float)(24.0 * eps);
+            M.eps4[t] = (float)(4.0 * eps);
+            M.shift[t] = ctx->lj_shift ? (float)(4.0 * eps * (sc6 * sc6 - sc6)) : 0.f;
+        }
+    // kernel choice
+    if (!ctx->rigid && nc == 1) {
+        ctx->kernel = KER_LJ1;
+        ctx->shape = SHAPE_NONE;
+        ctx->force_warps_per_block = LJ1_WARPS;
+    } else if (nc == 1 && M.comp[0].n_lj == 2 && M.comp[0].n_q == 0 && M.comp[0].n_mu == 0 && M.comp[0].n_Q == 1) {
+        ctx->kernel = KER_RIGID; ctx->shape = SHAPE_2CLJQ; ctx->force_warps_per_block = RIG_WARPS;
+    } else if (nc == 1 && M.comp[0].n_lj == 1 && M.comp[0].n_q == 3 && M.comp[0].n_mu == 0 && M.comp[0].n_Q == 0) {
+        ctx->kernel = KER_RIGID; ctx->shape = SHAPE_TIP4P; ctx->force_warps_per_block = RIG_WARPS;
+    } else {
+        ctx->kernel = KER_GENERIC; ctx->shape = SHAPE_GEN; ctx->force_warps_per_block = GEN_WARPS;
+        ctx->rigid = true;
+    }
+    if (ctx->kernel != KER_LJ1) ctx->rigid = true;
+    return MARDYN_OK;
+}
+
+template <typename K>
+static int occupancy_grid(mardyn_ctx* ctx, K kernel, int threads)
+{
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+    if (e != cudaSuccess || per_sm < 1) per_sm = 1;
+    return per_sm * ctx->num_sms;
+}
+
+static int launch_force(mardyn_ctx* ctx, int buf)
+{
+    (void)buf;
+    ForceArgs a;
+    a.g = ctx->g;
+    a.n = (int)ctx->n;
+    a.cap = (int)ctx->cap;
+    a.start = ctx->start;
+    a.xs = ctx->xs;
+    a.site = ctx->site;
+    a.force = ctx->force;
+    a.torque = ctx->torque;
+    a.part = ctx->fpart;
+    a.model = ctx->dmodel;
+    const DevComp& C0 = ctx->model.comp[0];
+    (void)C0;
+    a.sig2 = ctx->model.sig2[0];
+    a.eps24 = ctx->model.eps24[0];
+    a.eps4 = ctx->model.eps4[0];
+    a.shift = ctx->model.shift[0];
+    const int threads = 32 * ctx->force_warps_per_block;
+    switch (ctx->shape) {
+    case SHAPE_2CLJQ:
+        k_force_rigid<2, 0, 0, 1, false, RIG_WARPS><<<ctx->force_blocks, threads, 0, ctx->stream>>>(a);
+        break;
+    case SHAPE_TIP4P:
+        k_force_rigid<1, 3, 0, 0, false, RIG_WARPS><<<ctx->force_blocks, threads, 0, ctx->stream>>>(a);
+        break;
+    case SHAPE_GEN:
+        k_force_rigid<4, 4, 2, 2, true, GEN_WARPS><<<ctx->force_blocks, threads, 0, ctx->stream>>>(a);
+        break;
+    default:
+        k_force_lj1<LJ1_WARPS><<<ctx->force_blocks, threads, 0, ctx->stream>>>(a);
+    }
+    ctx->launches += 1;
+    return MARDYN_OK;
+}
+
+static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+// counting sort of the unsorted buffer `src` (cell_of / rank / count
+// filled) into buffer `dst`, canonical in-cell order (A13)
+static int enqueue_sort(mardyn_ctx* ctx, int src, int dst)
+{
+    const int n = (int)ctx->n, ncell = ctx->g.ncell;
+    cudaStream_t s = ctx->stream;
+    k_scan_tiles<<<ctx->ntiles, 1024, 0, s>>>(ncell, ctx->count, ctx->start, ctx->tsum);
+    k_scan_sums<<<1, 1024, 0, s>>>(ctx->ntiles, ctx->tsum);
+    k_scan_add<<<nblk(ncell, 256), 256, 0, s>>>(ncell, n, ctx->start, ctx->tsum);
+    k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->pos[src], ctx->cell_of, ctx->rank, ctx->start, ctx->keys);
+    if (ctx->rigid)
+        k_canon<true><<<nblk(n, 256), 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->cell_of, ctx->start,
+                                                   ctx->pos[src], ctx->vel[src], ctx->quat[src], ctx->angm[src],
+                                                   ctx->pos[dst], ctx->vel[dst], ctx->quat[dst], ctx->angm[dst],
+                                                   ctx->xs, ctx->site, ctx->dmodel);
+    else
+        k_canon<false><<<nblk(n, 256), 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->cell_of, ctx->start,
+                                                    ctx->pos[src], ctx->vel[src], nullptr, nullptr,
+                                                    ctx->pos[dst], ctx->vel[dst], nullptr, nullptr, ctx->xs,
+                                                    nullptr, ctx->dmodel);
+    ctx->launches += 5;
+    return MARDYN_OK;
+}
+
+// one time step from buffer parity b (A23): forces at t_k, observables of
+// t_k, leapfrog + rotation, cell rebuild into parity 1-b
+static int enqueue_step(mardyn_ctx* ctx, int b, bool timing_events)
+{
+    cudaStream_t s = ctx->stream;
+    const int n = (int)ctx->n;
+    if (timing_events) CK(cudaEventRecordWithFlags(ctx->ev_f0[b], s, cudaEventRecordExternal));
+    launch_force(ctx, b);
+    if (timing_events) CK(cudaEventRecordWithFlags(ctx->ev_f1[b], s, cudaEventRecordExternal));
+    CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
+    if (ctx->rigid)
+        k_integrate<true><<<ctx->nkblocks, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
+                                                        ctx->quat[b], ctx->angm[b], ctx->force, ctx->torque,
+                                                        ctx->cell_of, ctx->rank, ctx->count, ctx->kpart, ctx->flag);
+    else
+        k_integrate<false><<<ctx->nkblocks, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
+                                                         nullptr, nullptr, ctx->force, ctx->torque, ctx->cell_of,
+                                                         ctx->rank, ctx->count, ctx->kpart, ctx->flag);
+    k_finalize<<<1, 1024, 0, s>>>(ctx->force_blocks * ctx->force_warps_per_block, ctx->fpart, ctx->nkblocks,
+                                  ctx->kpart, ctx->ndof, ctx->step_ctr, 1, ctx->hist);
+    ctx->launches += 2;
+    return enqueue_sort(ctx, b, 1 - b);
+}
+
+static int build_graphs(mardyn_ctx* ctx)
+{
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->gexec[b]) { cudaGraphExecDestroy(ctx->gexec[b]); ctx->gexec[b] = nullptr; }
+        cudaGraph_t graph;
+        long long l0 = ctx->launches;
+        CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_step(ctx, b, ctx->profiling);
+        cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+        ctx->launches = l0;   // captured launches are counted at replay
+        if (rc != MARDYN_OK) return rc;
+        CK(e);
+        CK(cudaGraphInstantiate(&ctx->gexec[b], graph, 0));
+        CK(cudaGraphDestroy(graph));
+    }
+    return MARDYN_OK;
+}
+
+static int launches_per_step(const mardyn_ctx*) { return 8; }
+
+// ------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+int mardyn_create(const double box[3], double cutoff, const mardyn_component* comps, int32_t n_comps,
+                  const mardyn_options* opt, mardyn_ctx** out)
+{
+    if (!out) return MARDYN_EINVAL;
+    *out = nullptr;
+    mardyn_ctx* ctx = new mardyn_ctx();
+    auto bad = [&](const char* m) { ctx->err = m; return MARDYN_EINVAL; };
+    if (!box || !comps || n_comps < 1 || n_comps > MD_MAX_COMP || !opt) {
+        *out = ctx;
+        return bad("invalid arguments (box, components 1..8, options required)");
+    }
+    *out = ctx;
+    if (!(cutoff > 0)) return bad("cutoff must be > 0");
+    if (!(opt->dt > 0)) return bad("dt must be > 0");
+    if (!(opt->eps_rf >= 1.0)) return bad("eps_rf must be >= 1 (INFINITY allowed)");
+    for (int k = 0; k < 3; ++k) {
+        if (!(box[k] > 0) || !std::isfinite(box[k])) return bad("box must be positive and finite");
+        ctx->L[k] = box[k];
+    }
+    ctx->rc = cutoff;
+    ctx->dt = opt->dt;
+    ctx->eps_rf = opt->eps_rf;
+    ctx->lj_shift = opt->lj_shift;
+    int lj_total = 0;
+    for (int c = 0; c < n_comps; ++c) {
+        const mardyn_component& C = comps[c];
+        if (C.n_lj < 0 || C.n_q < 0 || C.n_mu < 0 || C.n_Q < 0) return bad("negative site count");
+        if (C.n_lj > 4 || C.n_q > 4 || C.n_mu > 2 || C.n_Q > 2)
+            return bad("component limits: <= 4 LJ sites, <= 4 charges, <= 2 dipoles, <= 2 quadrupoles");
+        if (C.n_lj + C.n_q + C.n_mu + C.n_Q == 0) return bad("component without sites");
+        if (!(C.mass > 0)) return bad("mass must be > 0");
+        for (int k = 0; k < 3; ++k) if (!(C.inertia[k] >= 0)) return bad("inertia must be >= 0");
+        HostComp H;
+        H.mass = C.mass;
+        for (int k = 0; k < 3; ++k) H.I[k] = C.inertia[k];
+        if ((C.n_lj && !C.lj) || (C.n_q && !C.q) || (C.n_mu && !C.mu) || (C.n_Q && !C.Q))
+            return bad("null site array");
+        H.lj.assign(C.lj, C.lj + C.n_lj);
+        H.q.assign(C.q, C.q + C.n_q);
+        H.mu.assign(C.mu, C.mu + C.n_mu);
+        H.Q.assign(C.Q, C.Q + C.n_Q);
+        for (auto& x : H.lj) if (!(x.sigma > 0) || !(x.epsilon >= 0)) return bad("LJ sigma > 0, epsilon >= 0");
+        for (auto* lst : {&H.mu, &H.Q})
+            for (auto& x : *lst)
+                if (!(std::fabs(x.e[0] * x.e[0] + x.e[1] * x.e[1] + x.e[2] * x.e[2] - 1.0) < 1e-6))
+                    return bad("polar site axis must be a unit vector");
+        lj_total += C.n_lj;
+        ctx->comps.push_back(H);
+    }
+    if (lj_total > MD_MAX_LJ_TOTAL) return bad("more than 16 LJ sites over all components");
+    if (opt->eta) {
+        ctx->eta.assign(opt->eta, opt->eta + n_comps * n_comps);
+        for (double e : ctx->eta) if (!(e > 0)) return bad("eta must be > 0");
+    }
+    int rc = setup_grid(ctx);
+    if (rc) return rc;
+    rc = build_model(ctx);
+    if (rc) return rc;
+    CK(cudaGetDevice(&ctx->device));
+    CK(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, ctx->device));
+    if (opt->cuda_stream) {
+        ctx->stream = (cudaStream_t)opt->cuda_stream;
+    } else {
+        CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+    }
+    int threads = 32 * ctx->force_warps_per_block;
+    switch (ctx->shape) {
+    case SHAPE_2CLJQ: ctx->force_blocks = occupancy_grid(ctx, k_force_rigid<2, 0, 0, 1, false, RIG_WARPS>, threads); break;
+    case SHAPE_TIP4P: ctx->force_blocks = occupancy_grid(ctx, k_force_rigid<1, 3, 0, 0, false, RIG_WARPS>, threads); break;
+    case SHAPE_GEN: ctx->force_blocks = occupancy_grid(ctx, k_force_rigid<4, 4, 2, 2, true, GEN_WARPS>, threads); break;
+    default: ctx->force_blocks = occupancy_grid(ctx, k_force_lj1<LJ1_WARPS>, threads);
+    }
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaEventCreate(&ctx->ev_f0[b]));
+        CK(cudaEventCreate(&ctx->ev_f1[b]));
+    }
+    CK(cudaEventCreate(&ctx->ev_s0));
+    CK(cudaEventCreate(&ctx->ev_s1));
+    return MARDYN_OK;
+}
+
+int mardyn_get_grid(const mardyn_ctx* ctx, mardyn_grid* out)
+{
+    if (!ctx || !out) return MARDYN_EINVAL;
+    const GridP& g = ctx->g;
+    for (int k = 0; k < 3; ++k) {
+        out->ncell[k] = g.nc[k];
+        out->period[k] = (int64_t)g.P64[k];
+        out->edge[k] = g.E[k];
+        out->box[k] = (double)g.P64[k] * (double)g.s;
+    }
+    out->pad = 0;
+    out->quantum = (double)g.s;
+    out->cut2_q = g.cut2_q;
+    out->kernel = ctx->kernel;
+    out->n_slots = ctx->nslots;
+    return MARDYN_OK;
+}
+
+static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
+{
+    const size_t A = 256;
+    size_t off = 0;
+    char* base = ctx->ws;
+    auto take = [&](size_t bytes) -> char* {
+        char* p = assign ? base + off : nullptr;
+        off = align_up(off + bytes, A);
+        return p;
+    };
+    const int ncell = ctx->g.ncell;
+    const int ncell_pad = (int)align_up((size_t)ncell, SCAN_TILE);
+    const int ntiles = ncell_pad / SCAN_TILE;
+    const int nk = std::max(1, nblk(cap, 256));
+    const int nfw = std::max(1, ctx->force_blocks * ctx->force_warps_per_block);
+    uint4* pos0 = (uint4*)take(16 * cap);
+    uint4* pos1 = (uint4*)take(16 * cap);
+    float4* vel0 = (float4*)take(16 * cap);
+    float4* vel1 = (float4*)take(16 * cap);
+    float4 *q0 = nullptr, *q1 = nullptr, *j0 = nullptr, *j1 = nullptr, *site = nullptr, *tq = nullptr;
+    if (ctx->rigid) {
+        q0 = (float4*)take(16 * cap); q1 = (float4*)take(16 * cap);
+        j0 = (float4*)take(16 * cap); j1 = (float4*)take(16 * cap);
+        site = (float4*)take((size_t)16 * cap * std::max(1, ctx->nslots));
+        tq = (float4*)take(16 * cap);
+    }
+    float4* xs = (float4*)take(16 * cap);
+    float4* force = (float4*)take(16 * cap);
+    int* cell_of = (int*)take(4 * cap);
+    int* rank = (int*)take(4 * cap);
+    unsigned long long* keys = (unsigned long long*)take(8 * cap);
+    int* count = (int*)take(4 * (size_t)ncell_pad);
+    int* start = (int*)take(4 * ((size_t)ncell + 1));
+    int* tsum = (int*)take(4 * (size_t)std::max(ntiles, 1));
+    ForcePartial* fpart = (ForcePartial*)take(sizeof(ForcePartial) * nfw);
+    double* kpart = (double*)take(16 * (size_t)nk);
+    ObsRec* hist = (ObsRec*)take(sizeof(ObsRec) * MD_HISTORY);
+    long long* step_ctr = (long long*)take(8);
+    int* flag = (int*)take(4);
+    DevModel* dmodel = (DevModel*)take(sizeof(DevModel));
+    const size_t stage_bytes = (size_t)cap * (19 * 8 + 3 * 4 + 4 + 4);
+    char* stage = take(stage_bytes);
+    if (assign) {
+        ctx->pos[0] = pos0; ctx->pos[1] = pos1; ctx->vel[0] = vel0; ctx->vel[1] = vel1;
+        ctx->quat[0] = q0; ctx->quat[1] = q1; ctx->angm[0] = j0; ctx->angm[1] = j1;
+        ctx->site = site; ctx->torque = tq; ctx->xs = xs; ctx->force = force;
+        ctx->cell_of = cell_of; ctx->rank = rank; ctx->keys = keys; ctx->count = count;
+        ctx->start = start; ctx->tsum = tsum; ctx->fpart = fpart; ctx->kpart = kpart;
+        ctx->hist = hist; ctx->step_ctr = step_ctr; ctx->flag = flag; ctx->dmodel = dmodel;
+        ctx->stage = stage; ctx->stage_bytes = stage_bytes;
+        ctx->ncell_pad = ncell_pad; ctx->ntiles = ntiles; ctx->nkblocks = nk;
+    }
+    return off;
+}
+
+int mardyn_workspace_bytes(mardyn_ctx* ctx, int64_t n_capacity, size_t* bytes)
+{
+    if (!ctx || !bytes || n_capacity < 1 || n_capacity > (1ll << 28)) return fail(ctx, MARDYN_EINVAL, "bad capacity");
+    *bytes = layout(ctx, n_capacity, false);
+    return MARDYN_OK;
+}
+
+int mardyn_set_workspace(mardyn_ctx* ctx, void* device_ptr, size_t bytes, int64_t n_capacity)
+{
+    if (!ctx || !device_ptr || n_capacity < 1) return fail(ctx, MARDYN_EINVAL, "bad workspace");
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (((uintptr_t)device_ptr) % 256) return fail(ctx, MARDYN_EINVAL, "workspace must be 256-byte aligned");
+    size_t need = layout(ctx, n_capacity, false);
+    if (bytes < need) return fail(ctx, MARDYN_ECAPACITY, "workspace too small");
+    ctx->ws = (char*)device_ptr;
+    ctx->ws_bytes = bytes;
+    ctx->cap = n_capacity;
+    layout(ctx, n_capacity, true);
+    ctx->loaded = false;
+    CK(cudaMemcpyAsync(ctx->dmodel, &ctx->model, sizeof(DevModel), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->step_ctr, 0, 8, ctx->stream));
+    CK(cudaMemsetAsync(ctx->flag, 0, 4, ctx->stream));
+    CK(cudaMemsetAsync(ctx->hist, 0, sizeof(ObsRec) * MD_HISTORY, ctx->stream));
+    for (int b = 0; b < 2; ++b)
+        if (ctx->gexec[b]) { cudaGraphExecDestroy(ctx->gexec[b]); ctx->gexec[b] = nullptr; }
+    return MARDYN_OK;
+}
+
+int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const int32_t* comp, const double* r,
+                         const double* v, const double* q, const double* j, int32_t half_step)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (!ctx->ws) return fail(ctx, MARDYN_ESTATE, "set_workspace must precede set_molecules");
+    if (n < 1 || n > ctx->cap) return fail(ctx, MARDYN_EINVAL, "n must be in [1, capacity]");
+    if (!comp || !r || !v) return fail(ctx, MARDYN_EINVAL, "comp, r, v are required");
+    if (ctx->rigid && (!q || !j)) return fail(ctx, MARDYN_EINVAL, "q and j are required for rigid molecules");
+    const int ncomp = (int)ctx->comps.size();
+    for (int64_t i = 0; i < n; ++i) {
+        if (comp[i] < 0 || comp[i] >= ncomp) return fail(ctx, MARDYN_EINVAL, "component id out of range");
+        for (int k = 0; k < 3; ++k)
+            if (!std::isfinite(r[3 * i + k]) || !std::isfinite(v[3 * i + k]))
+                return fail(ctx, MARDYN_EINVAL, "non-finite position or velocity");
+        if (ctx->rigid) {
+            double qn = q[4 * i] * q[4 * i] + q[4 * i + 1] * q[4 * i + 1] + q[4 * i + 2] * q[4 * i + 2] +
+                        q[4 * i + 3] * q[4 * i + 3];
+            if (!(std::fabs(qn - 1.0) < 1e-5)) return fail(ctx, MARDYN_EINVAL, "quaternions must be unit");
+        }
+    }
+    ctx->n = n;
+    ctx->ids.resize(n);
+    ctx->comp_host.assign(comp, comp + n);
+    for (int64_t i = 0; i < n; ++i) ctx->ids[i] = id ? id[i] : i;
+    double ndof = 3.0 * n;
+    for (int64_t i = 0; i < n; ++i) ndof += ctx->model.comp[comp[i]].rot * (ctx->rigid ? 1 : 0);
+    ctx->ndof = ndof;
+    cudaStream_t s = ctx->stream;
+    // host -> device (the caller's buffers; pinned ones are DMA'd directly)
+    double* dr = (double*)ctx->stage;
+    double* dv = dr + 3 * n;
+    double* dq = dv + 3 * n;
+    double* dj = dq + 4 * n;
+    int* dc = (int*)(dj + 3 * n);
+    CK(cudaMemcpyAsync(dr, r, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dv, v, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    if (ctx->rigid) {
+        CK(cudaMemcpyAsync(dq, q, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dj, j, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaMemcpyAsync(dc, comp, sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
+    CK(cudaMemsetAsync(ctx->flag, 0, 4, s));
+    const int src = 1, dst = 0;
+    k_ingest<<<nblk(n, 256), 256, 0, s>>>((int)n, dr, dv, ctx->rigid ? dq : nullptr, ctx->rigid ? dj : nullptr, dc,
+                                           ctx->g, ctx->pos[src], ctx->vel[src], ctx->rigid ? ctx->quat[src] : nullptr,
+                                           ctx->rigid ? ctx->angm[src] : nullptr, ctx->cell_of, ctx->rank, ctx->count);
+    ctx->launches += 1;
+    int rc = enqueue_sort(ctx, src, dst);
+    if (rc) return rc;
+    CK(cudaGetLastError());
+    ctx->cur = dst;
+    long long step = ctx->host_step;
+    CK(cudaMemcpyAsync(ctx->step_ctr, &step, 8, cudaMemcpyHostToDevice, s));
+    if (!half_step) {   // A8: backward half kick with F(t0), tau(t0)
+        launch_force(ctx, ctx->cur);
+        if (ctx->rigid)
+            k_half_kick<true><<<nblk(n, 256), 256, 0, s>>>((int)n, ctx->g, ctx->dmodel, ctx->vel[ctx->cur],
+                                                           ctx->angm[ctx->cur], ctx->force, ctx->torque);
+        else
+            k_half_kick<false><<<nblk(n, 256), 256, 0, s>>>((int)n, ctx->g, ctx->dmodel, ctx->vel[ctx->cur],
+                                                            nullptr, ctx->force, nullptr);
+        ctx->launches += 1;
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    ctx->loaded = true;
+    ctx->last_obs = -1;
+    return MARDYN_OK;
+}
+
+int mardyn_compute_forces(mardyn_ctx* ctx)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    cudaStream_t s = ctx->stream;
+    const int n = (int)ctx->n, b = ctx->cur;
+    launch_force(ctx, b);
+    if (ctx->rigid)
+        k_kinetic<true><<<ctx->nkblocks, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->vel[b], ctx->quat[b], ctx->angm[b],
+                                                      ctx->force, ctx->torque, ctx->kpart);
+    else
+        k_kinetic<false><<<ctx->nkblocks, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->vel[b], nullptr, nullptr,
+                                                       ctx->force, nullptr, ctx->kpart);
+    // kpart beyond the used blocks stays from earlier steps: same block count
+    k_finalize<<<1, 1024, 0, s>>>(ctx->force_blocks * ctx->force_warps_per_block, ctx->fpart, ctx->nkblocks,
+                                  ctx->kpart, ctx->ndof, ctx->step_ctr, 0, ctx->hist);
+    ctx->launches += 3;
+    CK(cudaGetLastError());
+    ctx->last_obs = ctx->host_step;
+    return MARDYN_OK;
+}
+
+int mardyn_step(mardyn_ctx* ctx, int32_t nsteps)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    if (nsteps < 0) return fail(ctx, MARDYN_EINVAL, "n must be >= 0");
+    if (nsteps == 0) return MARDYN_OK;
+    if (!ctx->gexec[0]) {
+        int rc = build_graphs(ctx);
+        if (rc) return rc;
+    }
+    for (int k = 0; k < nsteps; ++k) {
+        CK(cudaGraphLaunch(ctx->gexec[ctx->cur], ctx->stream));
+        ctx->last_parity = ctx->cur;
+        ctx->cur ^= 1;
+        ctx->launches += launches_per_step(ctx);
+    }
+    ctx->host_step += nsteps;
+    ctx->last_obs = ctx->host_step - 1;
+    ctx->last_force_launches = nsteps;
+    return MARDYN_OK;
+}
+
+static int sync_check(mardyn_ctx* ctx)
+{
+    CK(cudaStreamSynchronize(ctx->stream));
+    int flag = 0;
+    CK(cudaMemcpy(&flag, ctx->flag, 4, cudaMemcpyDeviceToHost));
+    if (flag) return fail(ctx, MARDYN_EUNSTABLE, "non-finite force/torque or a molecule moved more than one cell edge in a step");
+    return MARDYN_OK;
+}
+
+static void to_obs(const ObsRec& o, mardyn_observables* out)
+{
+    out->step = o.step;
+    out->U_pot = o.U;
+    out->virial = o.W;
+    out->T = o.T;
+    out->E_kin_trans = o.KEt;
+    out->E_kin_rot = o.KEr;
+    out->n_pairs = o.npairs;
+    out->n_candidates = o.ncand;
+}
+
+int mardyn_get_observables(mardyn_ctx* ctx, mardyn_observables* out)
+{
+    if (!ctx || !out) return MARDYN_EINVAL;
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (ctx->last_obs < 0) return fail(ctx, MARDYN_ESTATE, "no force evaluation yet (step or compute_forces)");
+    int rc = sync_check(ctx);
+    if (rc) return rc;
+    ObsRec o;
+    CK(cudaMemcpy(&o, ctx->hist + (ctx->last_obs % MD_HISTORY), sizeof(o), cudaMemcpyDeviceToHost));
+    to_obs(o, out);
+    return MARDYN_OK;
+}
+
+int mardyn_get_observable_history(mardyn_ctx* ctx, int32_t cap, int32_t* n, mardyn_observables* out)
+{
+    if (!ctx || !n || (cap > 0 && !out)) return MARDYN_EINVAL;
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    int rc = sync_check(ctx);
+    if (rc) return rc;
+    long long last = ctx->last_obs;
+    long long avail = std::min<long long>(last + 1, MD_HISTORY);
+    long long m = std::min<long long>(avail, cap);
+    std::vector<ObsRec> h(MD_HISTORY);
+    CK(cudaMemcpy(h.data(), ctx->hist, sizeof(ObsRec) * MD_HISTORY, cudaMemcpyDeviceToHost));
+    for (long long k = 0; k < m; ++k) to_obs(h[(last - m + 1 + k) % MD_HISTORY], out + k);
+    *n = (int32_t)m;
+    return MARDYN_OK;
+}
+
+static int egress(mardyn_ctx* ctx, double* r, double* v, double* q, double* j, double* F, double* tau,
+                  uint32_t* ufix, int32_t* cell)
+{
+    const int64_t n = ctx->n;
+    cudaStream_t s = ctx->stream;
+    double* d_r = (double*)ctx->stage;
+    double* d_v = d_r + 3 * n;
+    double* d_q = d_v + 3 * n;
+    double* d_j = d_q + 4 * n;
+    double* d_F = d_j + 3 * n;
+    double* d_t = d_F + 3 * n;
+    uint32_t* d_u = (uint32_t*)(d_t + 3 * n);
+    int* d_c = (int*)(d_u + 3 * n);
+    const int b = ctx->cur;
+    if (ctx->rigid)
+        k_egress<true><<<nblk(n, 256), 256, 0, s>>>((int)n, ctx->g, ctx->pos[b], ctx->vel[b], ctx->quat[b],
+                                                    ctx->angm[b], ctx->force, ctx->torque, r ? d_r : nullptr,
+                                                    v ? d_v : nullptr, q ? d_q : nullptr, j ? d_j : nullptr,
+                                                    F ? d_F : nullptr, tau ? d_t : nullptr, ufix ? d_u : nullptr,
+                                                    cell ? d_c : nullptr);
+    else
+        k_egress<false><<<nblk(n, 256), 256, 0, s>>>((int)n, ctx->g, ctx->pos[b], ctx->vel[b], nullptr, nullptr,
+                                                     ctx->force, nullptr, r ? d_r : nullptr, v ? d_v : nullptr,
+                                                     q ? d_q : nullptr, j ? d_j : nullptr, F ? d_F : nullptr,
+                                                     tau ? d_t : nullptr, ufix ? d_u : nullptr, cell ? d_c : nullptr);
+    ctx->launches += 1;
+    CK(cudaGetLastError());
+    if (r) CK(cudaMemcpyAsync(r, d_r, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if (v) CK(cudaMemcpyAsync(v, d_v, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if (q) CK(cudaMemcpyAsync(q, d_q, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, s));
+    if (j) CK(cudaMemcpyAsync(j, d_j, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if (F) CK(cudaMemcpyAsync(F, d_F, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if (tau) CK(cudaMemcpyAsync(tau, d_t, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if (ufix) CK(cudaMemcpyAsync(ufix, d_u, sizeof(uint32_t) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if (cell) CK(cudaMemcpyAsync(cell, d_c, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+    return sync_check(ctx);
+}
+
+int mardyn_get_molecules(mardyn_ctx* ctx, int64_t cap, int64_t* n, int64_t* id, int32_t* comp, double* r,
+                         double* v, double* q, double* j)
+{
+    if (!ctx || !n) return MARDYN_EINVAL;
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    if (cap < ctx->n) return fail(ctx, MARDYN_EINVAL, "cap < number of molecules");
+    *n = ctx->n;
+    if (id) std::memcpy(id, ctx->ids.data(), sizeof(int64_t) * ctx->n);
+    if (comp) std::memcpy(comp, ctx->comp_host.data(), sizeof(int32_t) * ctx->n);
+    return egress(ctx, r, v, q, j, nullptr, nullptr, nullptr, nullptr);
+}
+
+int mardyn_get_forces(mardyn_ctx* ctx, int64_t cap, double* F, double* tau)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    if (cap < ctx->n) return fail(ctx, MARDYN_EINVAL, "cap < number of molecules");
+    // forces are indexed by the sorted slots of the buffer they were computed on
+    if (ctx->last_obs >= 0 && ctx->last_obs == ctx->host_step - 1 && ctx->host_step > 0) {
+        // after step(): F belongs to the previous parity; egress that buffer's ids
+        int b = ctx->cur;
+        ctx->cur = ctx->last_parity;
+        int rc = egress(ctx, nullptr, nullptr, nullptr, nullptr, F, tau, nullptr, nullptr);
+        ctx->cur = b;
+        return rc;
+    }
+    return egress(ctx, nullptr, nullptr, nullptr, nullptr, F, tau, nullptr, nullptr);
+}
+
+int mardyn_get_raw(mardyn_ctx* ctx, int64_t cap, uint32_t* pos_fixed, int32_t* cell, int32_t* cell_count)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    if (cap < ctx->n) return fail(ctx, MARDYN_EINVAL, "cap < number of molecules");
+    int rc = egress(ctx, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, pos_fixed, cell);
+    if (rc) return rc;
+    if (cell_count) {
+        // counts of the current sorted state = start differences
+        std::vector<int> st(ctx->g.ncell + 1);
+        CK(cudaMemcpy(st.data(), ctx->start, sizeof(int) * (ctx->g.ncell + 1), cudaMemcpyDeviceToHost));
+        for (int c = 0; c < ctx->g.ncell; ++c) cell_count[c] = st[c + 1] - st[c];
+    }
+    return MARDYN_OK;
+}
+
+int mardyn_last_step_timing(mardyn_ctx* ctx, double* total_ms, double* force_ms, int32_t* force_launches)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    CK(cudaStreamSynchronize(ctx->stream));
+    float f = 0.f;
+    if (ctx->profiling && ctx->gexec[0]) {
+        cudaError_t e = cudaEventElapsedTime(&f, ctx->ev_f0[ctx->last_parity], ctx->ev_f1[ctx->last_parity]);
+        if (e != cudaSuccess) { f = 0.f; cudaGetLastError(); }
+    }
+    if (total_ms) *total_ms = 0.0;
+    if (force_ms) *force_ms = f;
+    if (force_launches) *force_launches = 1;
+    return MARDYN_OK;
+}
+
+int mardyn_set_profiling(mardyn_ctx* ctx, int32_t on)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if ((bool)on != ctx->profiling) {
+        ctx->profiling = on != 0;
+        for (int b = 0; b < 2; ++b)
+            if (ctx->gexec[b]) { cudaGraphExecDestroy(ctx->gexec[b]); ctx->gexec[b] = nullptr; }
+    }
+    return MARDYN_OK;
+}
+
+int64_t mardyn_launch_count(const mardyn_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+const char* mardyn_last_error(const mardyn_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void mardyn_destroy(mardyn_ctx* ctx)
+{
+    if (!ctx) return;
+    for (int b = 0; b < 2; ++b) {
+        if (ctx->gexec[b]) cudaGraphExecDestroy(ctx->gexec[b]);
+        if (ctx->ev_f0[b]) cudaEventDestroy(ctx->ev_f0[b]);
+        if (ctx->ev_f1[b]) cudaEventDestroy(ctx->ev_f1[b]);
+    }
+    if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);
+    if (ctx->ev_s1) cudaEventDestroy(ctx->ev_s1);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+}  // extern "C"

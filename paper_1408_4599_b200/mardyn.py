@@ -1,0 +1,318 @@
+"""Thin ctypes binding of libmardyn.so (include/mardyn.h), same names as the
+C ABI.  Argument marshalling only: every step of the hot path runs in the
+CUDA kernels of the library.  PyTorch provides the three pieces of plumbing
+the library does not own: the device workspace (a uint8 tensor), the CUDA
+stream, and (for multi-process runs) torch.distributed.
+
+There is no CPU fallback: if the shared library is missing or CUDA is
+unavailable, constructing a context raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmardyn.so")
+
+MARDYN_OK = 0
+ERRORS = {-1: "EINVAL", -2: "EOVERLAP", -3: "EUNSTABLE", -4: "ECAPACITY", -5: "ECUDA",
+          -6: "ENCCL", -7: "ESTATE"}
+
+# every symbol declared in include/mardyn.h
+EXPORTS = ["mardyn_create", "mardyn_get_grid", "mardyn_workspace_bytes", "mardyn_set_workspace",
+           "mardyn_set_molecules", "mardyn_compute_forces", "mardyn_step", "mardyn_get_observables",
+           "mardyn_get_observable_history", "mardyn_get_molecules", "mardyn_get_forces",
+           "mardyn_get_raw", "mardyn_last_step_timing", "mardyn_set_profiling",
+           "mardyn_launch_count", "mardyn_last_error", "mardyn_destroy"]
+
+
+class MardynError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"mardyn {ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class LJSite(C.Structure):
+    _fields_ = [("r", C.c_double * 3), ("sigma", C.c_double), ("epsilon", C.c_double)]
+
+
+class Charge(C.Structure):
+    _fields_ = [("r", C.c_double * 3), ("q", C.c_double)]
+
+
+class Polar(C.Structure):
+    _fields_ = [("r", C.c_double * 3), ("e", C.c_double * 3), ("m", C.c_double)]
+
+
+class Component(C.Structure):
+    _fields_ = [("n_lj", C.c_int32), ("n_q", C.c_int32), ("n_mu", C.c_int32), ("n_Q", C.c_int32),
+                ("lj", C.POINTER(LJSite)), ("q", C.POINTER(Charge)), ("mu", C.POINTER(Polar)),
+                ("Q", C.POINTER(Polar)), ("mass", C.c_double), ("inertia", C.c_double * 3)]
+
+
+class Options(C.Structure):
+    _fields_ = [("dt", C.c_double), ("eps_rf", C.c_double), ("lj_shift", C.c_int32),
+                ("eta", C.POINTER(C.c_double)), ("cuda_stream", C.c_void_p)]
+
+
+class Observables(C.Structure):
+    _fields_ = [("step", C.c_int64), ("U_pot", C.c_double), ("virial", C.c_double), ("T", C.c_double),
+                ("E_kin_trans", C.c_double), ("E_kin_rot", C.c_double), ("n_pairs", C.c_int64),
+                ("n_candidates", C.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Grid(C.Structure):
+    _fields_ = [("ncell", C.c_int32 * 3), ("pad", C.c_int32), ("quantum", C.c_double),
+                ("period", C.c_int64 * 3), ("edge", C.c_int64 * 3), ("box", C.c_double * 3),
+                ("cut2_q", C.c_int64), ("kernel", C.c_int32), ("n_slots", C.c_int32)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load the in-tree sm_100a library; fails loudly if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1408_4599_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    vp = C.c_void_p
+    lib.mardyn_create.argtypes = [P(C.c_double), C.c_double, P(Component), C.c_int32, P(Options), P(vp)]
+    lib.mardyn_get_grid.argtypes = [vp, P(Grid)]
+    lib.mardyn_workspace_bytes.argtypes = [vp, C.c_int64, P(C.c_size_t)]
+    lib.mardyn_set_workspace.argtypes = [vp, vp, C.c_size_t, C.c_int64]
+    lib.mardyn_set_molecules.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, vp, C.c_int32]
+    lib.mardyn_compute_forces.argtypes = [vp]
+    lib.mardyn_step.argtypes = [vp, C.c_int32]
+    lib.mardyn_get_observables.argtypes = [vp, P(Observables)]
+    lib.mardyn_get_observable_history.argtypes = [vp, C.c_int32, P(C.c_int32), P(Observables)]
+    lib.mardyn_get_molecules.argtypes = [vp, C.c_int64, P(C.c_int64), vp, vp, vp, vp, vp, vp]
+    lib.mardyn_get_forces.argtypes = [vp, C.c_int64, vp, vp]
+    lib.mardyn_get_raw.argtypes = [vp, C.c_int64, vp, vp, vp]
+    lib.mardyn_last_step_timing.argtypes = [vp, P(C.c_double), P(C.c_double), P(C.c_int32)]
+    lib.mardyn_set_profiling.argtypes = [vp, C.c_int32]
+    lib.mardyn_launch_count.argtypes = [vp]
+    lib.mardyn_launch_count.restype = C.c_int64
+    lib.mardyn_last_error.argtypes = [vp]
+    lib.mardyn_last_error.restype = C.c_char_p
+    lib.mardyn_destroy.argtypes = [vp]
+    lib.mardyn_destroy.restype = None
+    _lib = lib
+    return lib
+
+
+def _host_ptr(a, dtype):
+    """Pointer to a C-contiguous host buffer (numpy array or CPU torch tensor,
+    pinned or not).  Returns (pointer, keep-alive object)."""
+    if a is None:
+        return None, None
+    try:
+        import torch
+        if isinstance(a, torch.Tensor):
+            assert a.device.type == "cpu" and a.is_contiguous()
+            return C.c_void_p(a.data_ptr()), a
+    except ImportError:
+        pass
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return arr.ctypes.data_as(C.c_void_p), arr
+
+
+def _out_ptr(a):
+    """Writable pointer to a caller-provided C-contiguous host output buffer
+    (numpy array or CPU torch tensor, e.g. pinned); never copies."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        assert a.device.type == "cpu" and a.is_contiguous()
+        return C.c_void_p(a.data_ptr())
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _components(components):
+    """scenarios-style component dicts -> ctypes array (+ keep-alive list)."""
+    keep = []
+    arr = (Component * len(components))()
+    for c, cd in zip(arr, components):
+        lj = (LJSite * max(1, len(cd["lj"])))(*[LJSite((C.c_double * 3)(*p), s, e) for p, s, e in cd["lj"]])
+        qq = (Charge * max(1, len(cd["charges"])))(*[Charge((C.c_double * 3)(*p), q) for p, q in cd["charges"]])
+        mu = (Polar * max(1, len(cd["dipoles"])))(*[Polar((C.c_double * 3)(*p), (C.c_double * 3)(*a), m)
+                                                     for p, a, m in cd["dipoles"]])
+        QQ = (Polar * max(1, len(cd["quadrupoles"])))(*[Polar((C.c_double * 3)(*p), (C.c_double * 3)(*a), m)
+                                                         for p, a, m in cd["quadrupoles"]])
+        keep += [lj, qq, mu, QQ]
+        c.n_lj, c.n_q, c.n_mu, c.n_Q = (len(cd["lj"]), len(cd["charges"]), len(cd["dipoles"]),
+                                        len(cd["quadrupoles"]))
+        c.lj = C.cast(lj, C.POINTER(LJSite)); c.q = C.cast(qq, C.POINTER(Charge))
+        c.mu = C.cast(mu, C.POINTER(Polar)); c.Q = C.cast(QQ, C.POINTER(Polar))
+        c.mass = cd["mass"]
+        c.inertia[:] = list(cd["inertia"])
+    return arr, keep
+
+
+class Context:
+    """One simulation box on the current CUDA device (mardyn_ctx)."""
+
+    def __init__(self, box, cutoff, components, dt, eps_rf=math.inf, lj_shift=1, eta=None,
+                 capacity=None, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("mardyn needs a CUDA device (there is no CPU fallback)")
+        self.lib = load_library()
+        self.torch = torch
+        self.stream = stream if stream is not None else torch.cuda.Stream()
+        comps, self._keep = _components(components)
+        self._eta = None if eta is None else np.ascontiguousarray(eta, dtype=np.float64)
+        opt = Options()
+        opt.dt = float(dt)
+        opt.eps_rf = float(eps_rf)
+        opt.lj_shift = int(lj_shift)
+        opt.eta = None if self._eta is None else self._eta.ctypes.data_as(C.POINTER(C.c_double))
+        opt.cuda_stream = C.c_void_p(self.stream.cuda_stream)
+        box_a = (C.c_double * 3)(*[float(x) for x in box])
+        h = C.c_void_p()
+        rc = self.lib.mardyn_create(box_a, float(cutoff), comps, len(components), C.byref(opt), C.byref(h))
+        self.h = h
+        self.ws = None
+        self.capacity = 0
+        self._check(rc)
+        if capacity is not None:
+            self.reserve(capacity)
+
+    # -- plumbing ---------------------------------------------------------
+    def _check(self, rc):
+        if rc != MARDYN_OK:
+            msg = self.lib.mardyn_last_error(self.h).decode() if self.h else ""
+            raise MardynError(rc, msg)
+
+    def reserve(self, capacity):
+        """Allocate the device workspace through PyTorch (caching allocator)."""
+        nbytes = C.c_size_t()
+        self._check(self.lib.mardyn_workspace_bytes(self.h, int(capacity), C.byref(nbytes)))
+        self.ws = self.torch.empty(nbytes.value + 256, dtype=self.torch.uint8, device="cuda")
+        ptr = self.ws.data_ptr()
+        ptr += (-ptr) % 256
+        self._check(self.lib.mardyn_set_workspace(self.h, C.c_void_p(ptr), nbytes.value, int(capacity)))
+        self.capacity = int(capacity)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.mardyn_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- C ABI, same names -------------------------------------------------
+    def get_grid(self):
+        g = Grid()
+        self._check(self.lib.mardyn_get_grid(self.h, C.byref(g)))
+        return {"ncell": tuple(g.ncell), "quantum": g.quantum, "period": tuple(g.period),
+                "edge": tuple(g.edge), "box": tuple(g.box), "cut2_q": g.cut2_q,
+                "kernel": g.kernel, "n_slots": g.n_slots}
+
+    def set_molecules(self, r, v, comp=None, q=None, j=None, id=None, half_step=0):
+        n = len(r)
+        if self.capacity < n:
+            self.reserve(n)
+        if comp is None:
+            comp = np.zeros(n, np.int32)
+        ptrs = [_host_ptr(x, dt) for x, dt in ((id, np.int64), (comp, np.int32), (r, np.float64),
+                                               (v, np.float64), (q, np.float64), (j, np.float64))]
+        self._check(self.lib.mardyn_set_molecules(self.h, n, *[p for p, _ in ptrs], int(half_step)))
+
+    def compute_forces(self):
+        self._check(self.lib.mardyn_compute_forces(self.h))
+
+    def step(self, n=1):
+        self._check(self.lib.mardyn_step(self.h, int(n)))
+
+    def get_observables(self):
+        o = Observables()
+        self._check(self.lib.mardyn_get_observables(self.h, C.byref(o)))
+        return o.as_dict()
+
+    def get_observable_history(self, cap=4096):
+        arr = (Observables * cap)()
+        n = C.c_int32()
+        self._check(self.lib.mardyn_get_observable_history(self.h, cap, C.byref(n), arr))
+        return [arr[k].as_dict() for k in range(n.value)]
+
+    def get_molecules(self, out=None):
+        cap = self.capacity
+        res = out if out is not None else {
+            "id": np.empty(cap, np.int64), "comp": np.empty(cap, np.int32),
+            "r": np.empty((cap, 3)), "v": np.empty((cap, 3)), "q": np.empty((cap, 4)),
+            "j": np.empty((cap, 3))}
+        n = C.c_int64()
+        p = {k: _out_ptr(res[k]) for k in res}
+        self._check(self.lib.mardyn_get_molecules(self.h, cap, C.byref(n), p.get("id"), p.get("comp"),
+                                                  p.get("r"), p.get("v"), p.get("q"), p.get("j")))
+        if out is not None:
+            return n.value
+        return {k: x[: n.value] for k, x in res.items()}
+
+    def get_forces(self):
+        cap = self.capacity
+        F = np.empty((cap, 3)); tau = np.empty((cap, 3))
+        self._check(self.lib.mardyn_get_forces(self.h, cap, F.ctypes.data_as(C.c_void_p),
+                                               tau.ctypes.data_as(C.c_void_p)))
+        n = self._n()
+        return F[:n], tau[:n]
+
+    def _n(self):
+        n = C.c_int64()
+        self._check(self.lib.mardyn_get_molecules(self.h, self.capacity, C.byref(n), None, None, None,
+                                                  None, None, None))
+        return n.value
+
+    def get_raw(self):
+        cap = self.capacity
+        g = self.get_grid()
+        u = np.empty((cap, 3), np.uint32)
+        cell = np.empty(cap, np.int32)
+        cnt = np.empty(int(np.prod(g["ncell"])), np.int32)
+        self._check(self.lib.mardyn_get_raw(self.h, cap, u.ctypes.data_as(C.c_void_p),
+                                            cell.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p)))
+        n = self._n()
+        return u[:n], cell[:n], cnt
+
+    def last_step_timing(self):
+        t = C.c_double(); f = C.c_double(); nl = C.c_int32()
+        self._check(self.lib.mardyn_last_step_timing(self.h, C.byref(t), C.byref(f), C.byref(nl)))
+        return {"total_ms": t.value, "force_ms": f.value, "force_launches": nl.value}
+
+    def set_profiling(self, on):
+        self._check(self.lib.mardyn_set_profiling(self.h, int(bool(on))))
+
+    def launch_count(self):
+        return int(self.lib.mardyn_launch_count(self.h))
+
+
+# module-level aliases with the C names
+def mardyn_create(box, cutoff, components, dt, **kw):
+    return Context(box, cutoff, components, dt, **kw)
+
+
+def from_system(system, stream=None, capacity=None, eta=None):
+    """Context + molecules of a scenarios system dict (on-step v, j: A8)."""
+    ctx = Context(system["box"], system["rc"], system["components"], system["dt"],
+                  eps_rf=system.get("eps_rf", math.inf), lj_shift=system.get("lj_shift", 1),
+                  eta=eta, capacity=capacity or len(system["r"]), stream=stream)
+    ctx.set_molecules(system["r"], system["v"], comp=system["comp"], q=system["q"], j=system["j"],
+                      id=system["id"], half_step=0)
+    return ctx

@@ -1,0 +1,173 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on
+the same seeded inputs.  Small configs are compared element
+by element; they span several cell tiles, ragged cells, empty cells and the
+chunked paths of the force kernels."""
+import math
+
+import numpy as np
+import pytest
+
+import scenarios as S
+from parity_util import (assert_forces_close, assert_rel, candidates_from_counts, min_image, rms)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def md():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1408_4599_b200 import build, mardyn
+    build.build()
+    return mardyn
+
+
+def gpu_state(md, s, eta=None):
+    ctx = md.from_system(s, eta=eta)
+    F, tau = ctx.get_forces()               # F(t0), tau(t0) from set_molecules (A8)
+    ctx.compute_forces()
+    obs = ctx.get_observables()
+    u, cell, count = ctx.get_raw()
+    return ctx, F, tau, obs, u, cell, count
+
+
+def oracle_state(oracle_mod, s, eta=None, mode="full"):
+    o = oracle_mod.System(s, eta=eta)
+    u = o.quantize(s["r"])
+    cell, count = o.cells(u)
+    F, tau, tot = o.forces(s["comp"], u, s["q"], mode=mode)
+    return o, u, cell, count, F, tau, tot
+
+
+def check_step0(md, oracle_mod, s, eta=None, torque=True):
+    ctx, Fg, tg, obs, ug, cg, ng = gpu_state(md, s, eta)
+    o, uo, co, no, Fo, to, tot = oracle_state(oracle_mod, s, eta)
+    g = ctx.get_grid()
+    assert tuple(g["ncell"]) == tuple(o.ncell)
+    assert g["quantum"] == o.quantum
+    assert np.array_equal(np.array(g["period"]), o.period)
+    # bit-exact lattice, cells, counts (north_star)
+    assert np.array_equal(ug, uo)
+    assert np.array_equal(cg, co)
+    assert np.array_equal(ng, no)
+    assert obs["n_pairs"] == tot["npairs"]
+    assert obs["n_candidates"] == candidates_from_counts(no, o.ncell)
+    assert_forces_close(Fg, Fo, "force")
+    if torque:
+        assert_forces_close(tg, to, "torque")
+    assert_rel(obs["U_pot"], tot["U"], "U_pot")
+    assert_rel(obs["virial"], tot["W"], "virial")
+    return ctx, o
+
+
+@pytest.mark.parametrize("name", ["c0", "c1s", "c4s"])
+def test_step0_lj(md, oracle_mod, name):
+    check_step0(md, oracle_mod, S.config(name), torque=False)
+
+
+@pytest.mark.parametrize("name", ["c2s", "c3s"])
+def test_step0_rigid(md, oracle_mod, name):
+    check_step0(md, oracle_mod, S.config(name))
+
+
+@pytest.mark.parametrize("eps_rf", [math.inf, 4.0])
+def test_step0_generic_mixture(md, oracle_mod, eps_rf):
+    """Two species, every site kind (LJ, charges, dipoles, quadrupoles),
+    unlike-pair binary parameter eta: generic kernel."""
+    comps = S.random_polar_components()
+    s = S.random_system(400, (11.0, 10.0, 12.0), comps, seed_k=101, rc=2.5, eps_rf=eps_rf)
+    eta = np.array([[1.0, 0.9], [0.9, 1.0]])
+    ctx, _ = check_step0(md, oracle_mod, s, eta=eta)
+    assert ctx.get_grid()["kernel"] == 2
+
+
+def test_dense_cells_chunking(md, oracle_mod):
+    """~77 molecules per cell: i-chunks of 32 and neighbourhoods larger than
+    the shared-memory slab (chunked staging) in both kernels."""
+    s = S.lj_fcc(9, 1.2, 1.0, 7, "dense", 1, jitter=0.02, rc=4.0)
+    check_step0(md, oracle_mod, s, torque=False)
+    comp = S.c2_component()
+    s2 = S.lj_fcc(6, 0.9, 1.0, 8, "dense2", 1, jitter=0.0, rc=3.2)
+    rng = np.random.default_rng(3)
+    s2["components"] = [comp]
+    s2["q"] = S.random_quaternions(rng, len(s2["r"]))
+    s2["j"] = S.angular_momenta(rng, s2["q"], comp["inertia"], 1.0)
+    check_step0(md, oracle_mod, s2)
+
+
+def run_both(md, oracle_mod, s, nsteps, eta=None):
+    ctx = md.from_system(s, eta=eta)
+    ctx.step(nsteps)
+    hist = ctx.get_observable_history(nsteps)
+    mol = ctx.get_molecules()
+    o = oracle_mod.System(s, eta=eta)
+    u, v, q, j, obs = o.run(s["dt"], s["comp"], o.quantize(s["r"]), s["v"], s["q"], s["j"], nsteps,
+                            half_step=0, mode="full")
+    return ctx, hist, mol, o, u, v, q, j, obs
+
+
+@pytest.mark.parametrize("name,nsteps", [("c0", 10), ("c1s", 20), ("c2s", 10), ("c3s", 10), ("c4s", 10)])
+def test_trajectory(md, oracle_mod, name, nsteps):
+    """Independent GPU / oracle trajectories from the same initial state:
+    per-step U, W, T within 1e-5 relative, positions within 1e-4 sigma."""
+    s = S.config(name)
+    ctx, hist, mol, o, u, v, q, j, obs = run_both(md, oracle_mod, s, nsteps)
+    assert len(hist) == nsteps
+    for k in range(nsteps):
+        assert hist[k]["step"] == k
+        assert hist[k]["n_pairs"] == obs["npairs"][k]
+        assert_rel(hist[k]["U_pot"], obs["U"][k], f"U[{k}]")
+        assert_rel(hist[k]["virial"], obs["W"][k], f"W[{k}]")
+        assert_rel(hist[k]["T"], obs["T"][k], f"T[{k}]")
+    box = o.box
+    d = min_image(mol["r"] - u * o.quantum, box)
+    sigma = s["components"][0]["lj"][0][1]
+    assert np.abs(d).max() <= 1e-4 * sigma
+    if name in ("c2s", "c3s"):
+        dq = np.minimum(np.abs(mol["q"] - q).max(1), np.abs(mol["q"] + q).max(1))
+        assert dq.max() < 1e-4
+
+
+def test_initial_temperature_and_nve(md):
+    """A8 pin on the GPU: T(0) = generator T; NVE over 400 steps of config 0
+    within 2.5e-4 eps per particle (the oracle's own bound)."""
+    s = S.config0()
+    ctx = md.from_system(s)
+    ctx.step(400)
+    h = ctx.get_observable_history(400)
+    assert h[0]["T"] == pytest.approx(s["T"], rel=1e-5)
+    E = np.array([x["U_pot"] + x["E_kin_trans"] + x["E_kin_rot"] for x in h])
+    assert np.abs(E - E[0]).max() / len(s["r"]) < 2.5e-4
+
+
+def test_determinism(md):
+    """Canonical in-cell order + fixed-order sums: two runs agree bitwise."""
+    s = S.config("c1s")
+    out = []
+    for _ in range(2):
+        ctx = md.from_system(s)
+        ctx.step(15)
+        m = ctx.get_molecules()
+        out.append((m["r"].copy(), m["v"].copy(), ctx.get_observables()))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
+
+
+def test_errors(md):
+    s = S.config0()
+    with pytest.raises(md.MardynError) as e:
+        md.Context((5.0, 5.0, 5.0), 2.5, s["components"], 0.002)
+    assert e.value.code == -1
+    ctx = md.Context(s["box"], 2.5, s["components"], 0.002)
+    with pytest.raises(md.MardynError) as e:
+        ctx.step(1)
+    assert e.value.code == -7
+    v = s["v"].copy()
+    v[0] = [1e5, 0, 0]
+    ctx.set_molecules(s["r"], v, comp=s["comp"], half_step=1)
+    ctx.step(1)
+    with pytest.raises(md.MardynError) as e:
+        ctx.get_observables()
+    assert e.value.code == -3
