@@ -170,13 +170,14 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_lj1(ForceArgs a)
             compute(m);
             __syncwarp();
             // combine the phases of each molecule (fixed order)
+            float sx = fx, sy = fy, sz = fz;
             for (int p = 1; p < P; ++p) {
                 const int srcl = (lane + p * ni) & 31;
-                fx += __shfl_sync(0xffffffffu, fx, srcl);
-                fy += __shfl_sync(0xffffffffu, fy, srcl);
-                fz += __shfl_sync(0xffffffffu, fz, srcl);
+                sx += __shfl_sync(0xffffffffu, fx, srcl);
+                sy += __shfl_sync(0xffffffffu, fy, srcl);
+                sz += __shfl_sync(0xffffffffu, fz, srcl);
             }
-            if (phase == 0) a.force[my] = make_float4(fx, fy, fz, 0.f);
+            if (phase == 0) a.force[my] = make_float4(sx, sy, sz, 0.f);
             Uw += (double)(a.eps4 * uacc) - (double)a.shift * hits;
             Ww += (double)wacc;
             npw += hits;
@@ -412,18 +413,19 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_rigid(ForceArgs a)
 #pragma unroll
                 for (int k = 0; k < NPOL; ++k) { T.x += ts[k].x; T.y += ts[k].y; T.z += ts[k].z; }
             }
+            float3 SF = F, ST = T;
             for (int p = 1; p < P; ++p) {
                 const int srcl = (lane + p * ni) & 31;
-                F.x += __shfl_sync(0xffffffffu, F.x, srcl);
-                F.y += __shfl_sync(0xffffffffu, F.y, srcl);
-                F.z += __shfl_sync(0xffffffffu, F.z, srcl);
-                T.x += __shfl_sync(0xffffffffu, T.x, srcl);
-                T.y += __shfl_sync(0xffffffffu, T.y, srcl);
-                T.z += __shfl_sync(0xffffffffu, T.z, srcl);
+                SF.x += __shfl_sync(0xffffffffu, F.x, srcl);
+                SF.y += __shfl_sync(0xffffffffu, F.y, srcl);
+                SF.z += __shfl_sync(0xffffffffu, F.z, srcl);
+                ST.x += __shfl_sync(0xffffffffu, T.x, srcl);
+                ST.y += __shfl_sync(0xffffffffu, T.y, srcl);
+                ST.z += __shfl_sync(0xffffffffu, T.z, srcl);
             }
             if (phase == 0) {
-                a.force[my] = make_float4(F.x, F.y, F.z, 0.f);
-                a.torque[my] = make_float4(T.x, T.y, T.z, 0.f);
+                a.force[my] = make_float4(SF.x, SF.y, SF.z, 0.f);
+                a.torque[my] = make_float4(ST.x, ST.y, ST.z, 0.f);
             }
             Uw += (double)uacc;
             Ww += (double)wacc;

@@ -10,6 +10,26 @@
 #include "common.cuh"
 
 __device__ __forceinline__ float3 f3(float4 v) { return make_float3(v.x, v.y, v.z); }
+
+// 1/x and 1/sqrt(x): MUFU approximation + one Newton step written on the
+// small residual e (y + y e / 2), which keeps e at full relative precision:
+// nearly correctly rounded and unbiased, cheaper than the IEEE sequences.
+// The raw MUFU values (and the y (1.5 - x y^2 / 2) form, whose correction is
+// quantised to ulp(1)) bias the water virial by 2-5e-5, because the site
+// terms of neutral molecules cancel.
+__device__ __forceinline__ float rcp_nr(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return fmaf(r, fmaf(-x, r, 1.f), r);
+}
+__device__ __forceinline__ float rsqrt_nr(float x)
+{
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    const float e = fmaf(-x * y, y, 1.f);
+    return fmaf(0.5f * y, e, y);
+}
 __device__ __forceinline__ float dot3(float3 a, float3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 
 // LJ 12-6 (Eq. 1), energy shifted by `shift` (LJTS, A2); force unshifted.
@@ -17,7 +37,7 @@ __device__ __forceinline__ void pair_lj(float3 r, float sig2, float eps24, float
                                         float& u, float3& fa, float3& fhit)
 {
     float r2 = r.x * r.x + r.y * r.y + r.z * r.z;
-    float ir2 = __frcp_rn(r2);
+    float ir2 = rcp_nr(r2);
     float s2 = sig2 * ir2;
     float s6 = s2 * s2 * s2;
     float fr = eps24 * ir2 * s6 * (2.f * s6 - 1.f);          // f_b = fr r
@@ -31,7 +51,7 @@ __device__ __forceinline__ void pair_qq(float3 r, float qq, float krf, float crf
                                         float3& fhit)
 {
     float r2 = r.x * r.x + r.y * r.y + r.z * r.z;
-    float ir = rsqrtf(r2);
+    float ir = rsqrt_nr(r2);
     float ir2 = ir * ir;
     u += qq * (ir + krf * r2 - crf);
     float fr = qq * (ir * ir2 - 2.f * krf);
@@ -48,7 +68,7 @@ __device__ __forceinline__ void pair_polar(float3 r, float ma, float3 ea, float 
                                            float& u, float3& fa, float3& ta, float3& fhit)
 {
     float r2 = r.x * r.x + r.y * r.y + r.z * r.z;
-    float ir = rsqrtf(r2);
+    float ir = rsqrt_nr(r2);
     float ir2 = ir * ir, ir3 = ir2 * ir;
     float3 rh = make_float3(r.x * ir, r.y * ir, r.z * ir);
     float ca = (KA == MD_CHARGE) ? 0.f : dot3(ea, rh);
