@@ -123,24 +123,30 @@ __global__ void k_scan_add(int ncell, int n, int* __restrict__ start, const int*
 }
 
 // ------------------------------------------------------------------------
-// scatter: key = (iid << 32 | unsorted index) at start[cell] + arrival rank
+// scatter: canonical key (u_x << 32 | iid) and the unsorted index at
+// start[cell] + arrival rank
 __global__ void k_scatter(int n, const uint4* __restrict__ pos, const int* __restrict__ cell_of,
                           const int* __restrict__ rank, const int* __restrict__ start,
-                          unsigned long long* __restrict__ keys)
+                          unsigned long long* __restrict__ keys, int* __restrict__ oldidx)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int slot = start[cell_of[i]] + rank[i];
-    keys[slot] = ((unsigned long long)pos[i].w << 32) | (unsigned)i;
+    const uint4 p = pos[i];
+    keys[slot] = ((unsigned long long)p.x << 32) | p.w;
+    oldidx[slot] = i;
 }
 
-// canonical gather: each sorted slot finds its rank by id inside its cell
-// (reading A13), then gathers the molecule's state from the unsorted arrays
+// canonical gather: each sorted slot finds its rank inside its cell in the
+// canonical order (x, then id; reading A13 -- deterministic, and rows of
+// three x-adjacent cells come out sorted by x, which the force kernels use
+// to prune candidates), then gathers the molecule's state from the unsorted arrays
 // and writes the staging copy (cell-relative coordinates, exact) and, for
 // rigid models, the world-frame site offsets s = R(q) d.
 template <bool RIGID>
 __global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __restrict__ keys,
-                        const int* __restrict__ cell_of, const int* __restrict__ start,
+                        const int* __restrict__ oldidx, const int* __restrict__ cell_of,
+                        const int* __restrict__ start,
                         const uint4* __restrict__ pos_s, const float4* __restrict__ vel_s,
                         const float4* __restrict__ quat_s, const float4* __restrict__ angm_s,
                         uint4* __restrict__ pos_d, float4* __restrict__ vel_d,
@@ -150,13 +156,12 @@ __global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __res
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
-    unsigned long long key = keys[t];
-    unsigned old = (unsigned)(key & 0xffffffffu);
-    unsigned id = (unsigned)(key >> 32);
+    const unsigned long long key = keys[t];
+    const int old = oldidx[t];
     int c = cell_of[old];
     int s0 = start[c], s1 = start[c + 1];
     int r = 0;
-    for (int m = s0; m < s1; ++m) r += (unsigned)(keys[m] >> 32) < id;
+    for (int m = s0; m < s1; ++m) r += keys[m] < key;
     int dst = s0 + r;
     uint4 p = pos_s[old];
     float4 v = vel_s[old];

@@ -27,7 +27,16 @@ struct HostComp {
 enum KernelKind { KER_LJ1 = 0, KER_RIGID = 1, KER_GENERIC = 2 };
 enum RigidShape { SHAPE_NONE, SHAPE_2CLJQ, SHAPE_TIP4P, SHAPE_GEN };
 
-constexpr int LJ1_WARPS = 4;
+#ifndef MD_LJ1_WARPS
+#define MD_LJ1_WARPS 4
+#endif
+#ifndef MD_LJ1_CAP
+#define MD_LJ1_CAP 512
+#endif
+constexpr int LJ1_WARPS = MD_LJ1_WARPS;
+constexpr int LJ1_CAP = MD_LJ1_CAP;
+using LJ1 = LJ1Cfg<LJ1_WARPS, LJ1_CAP>;
+#define K_LJ1 k_force_lj1<LJ1_WARPS, LJ1_CAP>
 constexpr int RIG_WARPS = 4;
 constexpr int GEN_WARPS = 1;
 
@@ -74,6 +83,7 @@ struct mardyn_ctx {
     int* start = nullptr;
     int* tsum = nullptr;
     unsigned long long* keys = nullptr;
+    int* oldidx = nullptr;
     ForcePartial* fpart = nullptr;
     double* kpart = nullptr;
     ObsRec* hist = nullptr;
@@ -262,10 +272,10 @@ static int build_model(mardyn_ctx* ctx)
 }
 
 template <typename K>
-static int occupancy_grid(mardyn_ctx* ctx, K kernel, int threads)
+static int occupancy_grid(mardyn_ctx* ctx, K kernel, int threads, size_t smem = 0)
 {
     int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
     return per_sm * ctx->num_sms;
 }
@@ -283,6 +293,7 @@ static int launch_force(mardyn_ctx* ctx, int buf)
     a.force = ctx->force;
     a.torque = ctx->torque;
     a.part = ctx->fpart;
+    a.flag = ctx->flag;
     a.model = ctx->dmodel;
     const DevComp& C0 = ctx->model.comp[0];
     (void)C0;
@@ -302,7 +313,7 @@ static int launch_force(mardyn_ctx* ctx, int buf)
         k_force_rigid<4, 4, 2, 2, true, GEN_WARPS><<<ctx->force_blocks, threads, 0, ctx->stream>>>(a);
         break;
     default:
-        k_force_lj1<LJ1_WARPS><<<ctx->force_blocks, threads, 0, ctx->stream>>>(a);
+        K_LJ1<<<ctx->force_blocks, threads, LJ1::SMEM, ctx->stream>>>(a);
     }
     ctx->launches += 1;
     return MARDYN_OK;
@@ -319,14 +330,15 @@ static int enqueue_sort(mardyn_ctx* ctx, int src, int dst)
     k_scan_tiles<<<ctx->ntiles, 1024, 0, s>>>(ncell, ctx->count, ctx->start, ctx->tsum);
     k_scan_sums<<<1, 1024, 0, s>>>(ctx->ntiles, ctx->tsum);
     k_scan_add<<<nblk(ncell, 256), 256, 0, s>>>(ncell, n, ctx->start, ctx->tsum);
-    k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->pos[src], ctx->cell_of, ctx->rank, ctx->start, ctx->keys);
+    k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->pos[src], ctx->cell_of, ctx->rank, ctx->start, ctx->keys,
+                                            ctx->oldidx);
     if (ctx->rigid)
-        k_canon<true><<<nblk(n, 256), 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->cell_of, ctx->start,
+        k_canon<true><<<nblk(n, 256), 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->oldidx, ctx->cell_of, ctx->start,
                                                    ctx->pos[src], ctx->vel[src], ctx->quat[src], ctx->angm[src],
                                                    ctx->pos[dst], ctx->vel[dst], ctx->quat[dst], ctx->angm[dst],
                                                    ctx->xs, ctx->site, ctx->dmodel);
     else
-        k_canon<false><<<nblk(n, 256), 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->cell_of, ctx->start,
+        k_canon<false><<<nblk(n, 256), 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->oldidx, ctx->cell_of, ctx->start,
                                                     ctx->pos[src], ctx->vel[src], nullptr, nullptr,
                                                     ctx->pos[dst], ctx->vel[dst], nullptr, nullptr, ctx->xs,
                                                     nullptr, ctx->dmodel);
@@ -454,7 +466,9 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
     case SHAPE_2CLJQ: ctx->force_blocks = occupancy_grid(ctx, k_force_rigid<2, 0, 0, 1, false, RIG_WARPS>, threads); break;
     case SHAPE_TIP4P: ctx->force_blocks = occupancy_grid(ctx, k_force_rigid<1, 3, 0, 0, false, RIG_WARPS>, threads); break;
     case SHAPE_GEN: ctx->force_blocks = occupancy_grid(ctx, k_force_rigid<4, 4, 2, 2, true, GEN_WARPS>, threads); break;
-    default: ctx->force_blocks = occupancy_grid(ctx, k_force_lj1<LJ1_WARPS>, threads);
+    default:
+        CK(cudaFuncSetAttribute(K_LJ1, cudaFuncAttributeMaxDynamicSharedMemorySize, LJ1::SMEM));
+        ctx->force_blocks = occupancy_grid(ctx, K_LJ1, threads, LJ1::SMEM);
     }
     for (int b = 0; b < 2; ++b) {
         CK(cudaEventCreate(&ctx->ev_f0[b]));
@@ -514,6 +528,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     int* cell_of = (int*)take(4 * cap);
     int* rank = (int*)take(4 * cap);
     unsigned long long* keys = (unsigned long long*)take(8 * cap);
+    int* oldidx = (int*)take(4 * cap);
     int* count = (int*)take(4 * (size_t)ncell_pad);
     int* start = (int*)take(4 * ((size_t)ncell + 1));
     int* tsum = (int*)take(4 * (size_t)std::max(ntiles, 1));
@@ -529,7 +544,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         ctx->pos[0] = pos0; ctx->pos[1] = pos1; ctx->vel[0] = vel0; ctx->vel[1] = vel1;
         ctx->quat[0] = q0; ctx->quat[1] = q1; ctx->angm[0] = j0; ctx->angm[1] = j1;
         ctx->site = site; ctx->torque = tq; ctx->xs = xs; ctx->force = force;
-        ctx->cell_of = cell_of; ctx->rank = rank; ctx->keys = keys; ctx->count = count;
+        ctx->cell_of = cell_of; ctx->rank = rank; ctx->keys = keys; ctx->oldidx = oldidx; ctx->count = count;
         ctx->start = start; ctx->tsum = tsum; ctx->fpart = fpart; ctx->kpart = kpart;
         ctx->hist = hist; ctx->step_ctr = step_ctr; ctx->flag = flag; ctx->dmodel = dmodel;
         ctx->stage = stage; ctx->stage_bytes = stage_bytes;
@@ -689,6 +704,8 @@ static int sync_check(mardyn_ctx* ctx)
     CK(cudaStreamSynchronize(ctx->stream));
     int flag = 0;
     CK(cudaMemcpy(&flag, ctx->flag, 4, cudaMemcpyDeviceToHost));
+    if (flag & 4) return fail(ctx, MARDYN_ECAPACITY, "a row of three cells exceeds the force kernel's shared-memory slab");
+    if (flag & 2) return fail(ctx, MARDYN_EOVERLAP, "two molecule centres coincide");
     if (flag) return fail(ctx, MARDYN_EUNSTABLE, "non-finite force/torque or a molecule moved more than one cell edge in a step");
     return MARDYN_OK;
 }

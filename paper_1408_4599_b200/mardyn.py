@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmardyn.so")
+LIB_PATH = os.environ.get("MARDYN_LIB") or os.path.join(_HERE, "libmardyn.so")
 
 MARDYN_OK = 0
 ERRORS = {-1: "EINVAL", -2: "EOVERLAP", -3: "EUNSTABLE", -4: "ECAPACITY", -5: "ECUDA",
