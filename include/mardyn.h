@@ -185,6 +185,26 @@ int mardyn_set_profiling(struct mardyn_ctx* ctx, int32_t on);
 /* Number of device kernel launches enqueued so far by this context.        */
 int64_t mardyn_launch_count(const struct mardyn_ctx* ctx);
 
+/*
+ * Host-side load model and spatial decomposition (no device work; usable
+ * without a GPU).  PAPER.md §4: per-cell cost Eq. 6
+ *     n_d(i) = N_i / 2 (N_i + sum_{j in the 26 neighbours} N_j)
+ * and the k-d tree: recursive bisection with planes
+ * perpendicular to alternating axes (x, y, z by depth; the next axis if the
+ * depth's axis cannot be cut), each plane minimising
+ * |load_left / p_left - load_right / p_right| over all admissible planes
+ * (ties: the more central plane), >= 2 cells per subvolume per axis,
+ * child process counts ceil(p/2), floor(p/2).
+ * Arrays are x-fastest over (nx, ny, nz) cells, periodic.
+ */
+int mardyn_cell_cost(const int32_t* counts, int32_t nx, int32_t ny, int32_t nz, double* cost);
+
+/* boxes: p * 6 int32 (lo_x, lo_y, lo_z, hi_x, hi_y, hi_z; half-open) in rank
+ * order; loads: p doubles (sum of cost per box) or NULL.  Returns
+ * MARDYN_EINVAL if the 2-cell constraint cannot be met.                    */
+int mardyn_kd_decompose(const double* cost, int32_t nx, int32_t ny, int32_t nz, int32_t p,
+                        int32_t* boxes, double* loads);
+
 const char* mardyn_last_error(const struct mardyn_ctx* ctx);
 void mardyn_destroy(struct mardyn_ctx* ctx);
 

@@ -11,6 +11,7 @@
 
 #include "../../include/mardyn.h"
 #include "common.cuh"
+#include "decomp.hpp"
 #include "kernels_force.cuh"
 #include "kernels_state.cuh"
 
@@ -864,6 +865,34 @@ int mardyn_set_profiling(mardyn_ctx* ctx, int32_t on)
 }
 
 int64_t mardyn_launch_count(const mardyn_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int mardyn_cell_cost(const int32_t* counts, int32_t nx, int32_t ny, int32_t nz, double* cost)
+{
+    if (!counts || !cost || nx < 1 || ny < 1 || nz < 1) return MARDYN_EINVAL;
+    mdd::cell_cost(counts, nx, ny, nz, cost);
+    return MARDYN_OK;
+}
+
+int mardyn_kd_decompose(const double* cost, int32_t nx, int32_t ny, int32_t nz, int32_t p, int32_t* boxes,
+                        double* loads)
+{
+    if (!cost || !boxes || p < 1 || nx < 1 || ny < 1 || nz < 1) return MARDYN_EINVAL;
+    std::vector<mdd::Box> leaves;
+    mdd::Box all;
+    all.lo[0] = all.lo[1] = all.lo[2] = 0;
+    all.hi[0] = nx; all.hi[1] = ny; all.hi[2] = nz;
+    if (!mdd::kd_split(cost, nx, ny, all, p, 0, leaves) || (int)leaves.size() != p) return MARDYN_EINVAL;
+    for (int r = 0; r < p; ++r) {
+        const mdd::Box& b = leaves[r];
+        double l = 0.0;
+        for (int z = b.lo[2]; z < b.hi[2]; ++z)
+            for (int y = b.lo[1]; y < b.hi[1]; ++y)
+                for (int x = b.lo[0]; x < b.hi[0]; ++x) l += cost[x + nx * (y + ny * z)];
+        for (int k = 0; k < 3; ++k) { boxes[6 * r + k] = b.lo[k]; boxes[6 * r + 3 + k] = b.hi[k]; }
+        if (loads) loads[r] = l;
+    }
+    return MARDYN_OK;
+}
 
 const char* mardyn_last_error(const mardyn_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 

@@ -27,7 +27,8 @@ EXPORTS = ["mardyn_create", "mardyn_get_grid", "mardyn_workspace_bytes", "mardyn
            "mardyn_set_molecules", "mardyn_compute_forces", "mardyn_step", "mardyn_get_observables",
            "mardyn_get_observable_history", "mardyn_get_molecules", "mardyn_get_forces",
            "mardyn_get_raw", "mardyn_last_step_timing", "mardyn_set_profiling",
-           "mardyn_launch_count", "mardyn_last_error", "mardyn_destroy"]
+           "mardyn_launch_count", "mardyn_cell_cost", "mardyn_kd_decompose", "mardyn_last_error",
+           "mardyn_destroy"]
 
 
 class MardynError(RuntimeError):
@@ -104,6 +105,8 @@ def load_library():
     lib.mardyn_set_profiling.argtypes = [vp, C.c_int32]
     lib.mardyn_launch_count.argtypes = [vp]
     lib.mardyn_launch_count.restype = C.c_int64
+    lib.mardyn_cell_cost.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, vp]
+    lib.mardyn_kd_decompose.argtypes = [vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp, vp]
     lib.mardyn_last_error.argtypes = [vp]
     lib.mardyn_last_error.restype = C.c_char_p
     lib.mardyn_destroy.argtypes = [vp]
@@ -301,6 +304,34 @@ class Context:
 
     def launch_count(self):
         return int(self.lib.mardyn_launch_count(self.h))
+
+
+# host-side decomposition (no GPU needed)
+def cell_cost(counts):
+    """Eq. 6 per cell; counts is an (nz, ny, nx) int array (x fastest)."""
+    lib = load_library()
+    c = np.ascontiguousarray(counts, dtype=np.int32)
+    nz, ny, nx = c.shape
+    out = np.empty(c.shape, dtype=np.float64)
+    rc = lib.mardyn_cell_cost(c.ctypes.data_as(C.c_void_p), nx, ny, nz, out.ctypes.data_as(C.c_void_p))
+    if rc:
+        raise MardynError(rc, "cell_cost")
+    return out
+
+
+def kd_decompose(cost, p):
+    """k-d tree decomposition of an (nz, ny, nx) cost array into p boxes:
+    returns (boxes (p, 2, 3) [lo, hi] in (x, y, z), loads (p,))."""
+    lib = load_library()
+    c = np.ascontiguousarray(cost, dtype=np.float64)
+    nz, ny, nx = c.shape
+    boxes = np.empty((p, 6), dtype=np.int32)
+    loads = np.empty(p, dtype=np.float64)
+    rc = lib.mardyn_kd_decompose(c.ctypes.data_as(C.c_void_p), nx, ny, nz, int(p),
+                                 boxes.ctypes.data_as(C.c_void_p), loads.ctypes.data_as(C.c_void_p))
+    if rc:
+        raise MardynError(rc, "kd_decompose: 2-cell constraint cannot be met")
+    return boxes.reshape(p, 2, 3), loads
 
 
 # module-level aliases with the C names
