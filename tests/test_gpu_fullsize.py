@@ -1,0 +1,76 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration
+bench.py times (same library, same kernels, same grid sizing).
+
+Cells and per-cell counts are compared bit-exactly for every molecule;
+forces and torques on a fixed random sample of molecules the oracle computes
+one by one (full 27-cell shell, fp64); U_pot, virial and the pair count
+against the oracle's totals over all molecules (OpenMP).  Config 1 is also
+stepped: per-step U, W, T and final positions against an independent oracle
+trajectory."""
+import numpy as np
+import pytest
+
+import scenarios as S
+from parity_util import assert_rel, min_image
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+SAMPLE = 3000
+
+
+@pytest.fixture(scope="module")
+def md():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1408_4599_b200 import build, mardyn
+    build.build()
+    return mardyn
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4"])
+def test_fullsize_step0(md, oracle_mod, name):
+    s = S.config(name)
+    N = len(s["r"])
+    ctx = md.from_system(s)
+    F, tau = ctx.get_forces()
+    ctx.compute_forces()
+    obs = ctx.get_observables()
+    u, cell, count = ctx.get_raw()
+    o = oracle_mod.System(s)
+    uo = o.quantize(s["r"])
+    co, no = o.cells(uo)
+    assert np.array_equal(u, uo)
+    assert np.array_equal(cell, co)
+    assert np.array_equal(count, no)
+    rng = np.random.default_rng(123)
+    idx = np.sort(rng.choice(N, size=SAMPLE, replace=False))
+    Fo, to, _ = o.forces(s["comp"], uo, s["q"], mode="full", idx=idx)
+    _, _, tot = o.forces(s["comp"], uo, s["q"], mode="full")
+    rms = np.sqrt(np.mean(np.sum(Fo * Fo, axis=1)))
+    assert np.abs(F[idx] - Fo).max() <= 1e-4 * rms
+    if name in ("c2", "c3"):
+        trms = np.sqrt(np.mean(np.sum(to * to, axis=1)))
+        assert np.abs(tau[idx] - to).max() <= 1e-4 * trms
+    assert obs["n_pairs"] == tot["npairs"]
+    assert_rel(obs["U_pot"], tot["U"], "U_pot")
+    assert_rel(obs["virial"], tot["W"], "virial")
+
+
+def test_fullsize_c1_trajectory(md, oracle_mod):
+    s = S.config("c1")
+    n = 3
+    ctx = md.from_system(s)
+    ctx.step(n)
+    hist = ctx.get_observable_history(n)
+    mol = ctx.get_molecules()
+    o = oracle_mod.System(s)
+    u, v, q, j, obs = o.run(s["dt"], s["comp"], o.quantize(s["r"]), s["v"], s["q"], s["j"], n,
+                            half_step=0, mode="full")
+    for k in range(n):
+        assert hist[k]["n_pairs"] == obs["npairs"][k]
+        assert_rel(hist[k]["U_pot"], obs["U"][k], f"U[{k}]")
+        assert_rel(hist[k]["virial"], obs["W"][k], f"W[{k}]")
+        assert_rel(hist[k]["T"], obs["T"][k], f"T[{k}]")
+    d = min_image(mol["r"] - u * o.quantum, o.box)
+    assert np.abs(d).max() <= 1e-4
