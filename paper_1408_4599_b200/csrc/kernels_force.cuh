@@ -112,7 +112,7 @@ __device__ __forceinline__ int row_src(const Row& r, int kk, float edge, float& 
 // =========================================================================
 template <int WARPS, int CAP>
 struct LJ1Cfg {
-    static constexpr int SMEM_PER_WARP = CAP * 16 + 16 * 4;
+    static constexpr int SMEM_PER_WARP = CAP * 16 + 32 * 4;      // slab + piece offsets/rows
     static constexpr int SMEM = WARPS * SMEM_PER_WARP;
 };
 
@@ -162,23 +162,25 @@ __device__ __forceinline__ void lj1_row(const float4* __restrict__ buf, const in
     }
 }
 
-// all staged rows [r0, r1) for this lane's molecule
+// all staged pieces (x-sorted row segments) for this lane's molecule:
+// piece k = buf[poff[k], poff[k+1]) of row prow[k]
 template <bool EXACT>
-__device__ __forceinline__ void lj1_rows(const float4* __restrict__ buf, const int* __restrict__ roff,
-                                         const int r0, const int r1, const float4 xi, const int phase,
-                                         const int P, const GridP& g, const float sig2, const float eps24,
-                                         const float hi, const float lo, float& fx, float& fy, float& fz,
-                                         float& uacc, float& wacc, int& hits, int& band)
+__device__ __forceinline__ void lj1_rows(const float4* __restrict__ buf, const int* __restrict__ poff,
+                                         const int* __restrict__ prow, const int np, const float4 xi,
+                                         const int phase, const int P, const GridP& g, const float sig2,
+                                         const float eps24, const float hi, const float lo, float& fx, float& fy,
+                                         float& fz, float& uacc, float& wacc, int& hits, int& band)
 {
     const float rc2w = hi * (1.f + 1.f / 4096.f);           // generous window (necessary condition only)
-    for (int r = r0; r < r1; ++r) {
+    for (int k = 0; k < np; ++k) {
+        const int r = prow[k];
         const int dy = r % 3 - 1, dz = r / 3 - 1;
         const float Dy = dy == 0 ? 0.f : (dy > 0 ? g.edge[1] - xi.y : xi.y);
         const float Dz = dz == 0 ? 0.f : (dz > 0 ? g.edge[2] - xi.z : xi.z);
         const float w2 = rc2w - Dy * Dy - Dz * Dz;
         if (w2 <= 0.f) continue;
-        lj1_row<EXACT>(buf, roff[r - r0], roff[r - r0 + 1], xi, sqrtf(w2), phase, P, g, sig2, eps24, hi, lo,
-                       fx, fy, fz, uacc, wacc, hits, band);
+        lj1_row<EXACT>(buf, poff[k], poff[k + 1], xi, sqrtf(w2), phase, P, g, sig2, eps24, hi, lo, fx, fy, fz,
+                       uacc, wacc, hits, band);
     }
 }
 
@@ -190,7 +192,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_lj1(ForceArgs a)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     char* wbase = reinterpret_cast<char*>(smem_lj1) + wib * CFG::SMEM_PER_WARP;
     float4* buf = reinterpret_cast<float4*>(wbase);
-    int* roff = reinterpret_cast<int*>(wbase + CAP * 16);
+    int* poff = reinterpret_cast<int*>(wbase + CAP * 16);       // <= 16 pieces per slab
+    int* prow = poff + 16;
     const GridP& g = a.g;
     const int gw = blockIdx.x * WARPS + wib, nw = gridDim.x * WARPS;
     double Uw = 0.0, Ww = 0.0;
@@ -214,42 +217,40 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_lj1(ForceArgs a)
             if (!active) xi.x = 1e30f;                  // idle lanes: empty windows
             float fx = 0.f, fy = 0.f, fz = 0.f, uacc = 0.f, wacc = 0.f;
             int hits = 0, band = 0, mtot = 0;
-            // stage rows in groups that fit the slab; process each group
-            int row = 0;
+            // stage the 9 rows into the slab as pieces (a row that does not fit
+            // is split: its pieces stay x-sorted); process each full slab
+            int row = 0, k0 = 0;
             while (row < 9) {
-                const int r0 = row;
-                int m = 0;
-                if (lane == 0) roff[0] = 0;
-                while (row < 9) {
+                int m = 0, np = 0;
+                __syncwarp();
+                while (row < 9 && m < CAP) {
                     const int dy = row % 3 - 1, dz = row / 3 - 1;
                     const Row r = load_row(a.start, g, cx, cy, cz, dy, dz);
                     const int tot = r.n0 + r.n1 + r.n2;
-                    if (m + tot > CAP) {
-                        if (m == 0) { if (lane == 0) atomicOr(a.flag, 4); row = 9; }   // row larger than the slab
-                        break;
-                    }
+                    const int take = min(tot - k0, CAP - m);
                     const float offy = dy * g.edge[1], offz = dz * g.edge[2];
-                    for (int k = lane; k < tot; k += 32) {
+                    for (int k = lane; k < take; k += 32) {
                         float offx;
-                        const int src = row_src(r, k, g.edge[0], offx);
+                        const int src = row_src(r, k0 + k, g.edge[0], offx);
                         const float4 x = __ldg(a.xs + src);
                         buf[m + k] = make_float4(x.x + offx, x.y + offy, x.z + offz, 0.f);
                     }
-                    m += tot;
-                    mtot += tot;
-                    ++row;
-                    if (lane == 0) roff[row - r0] = m;
+                    if (lane == 0) { prow[np] = row; poff[np] = m; }
+                    m += take;
+                    ++np;
+                    if (k0 + take == tot) { mtot += tot; ++row; k0 = 0; }
+                    else k0 += take;
                 }
+                if (lane == 0) poff[np] = m;
                 __syncwarp();
                 band = 0;
-                lj1_rows<false>(buf, roff, r0, row, xi, phase, P, g, sig2, eps24, hi, lo, fx, fy, fz, uacc, wacc,
+                lj1_rows<false>(buf, poff, prow, np, xi, phase, P, g, sig2, eps24, hi, lo, fx, fy, fz, uacc, wacc,
                                 hits, band);
                 if (band) {   // rare: add the guard-band pairs the exact test keeps
                     int dummy = 0;
-                    lj1_rows<true>(buf, roff, r0, row, xi, phase, P, g, sig2, eps24, hi, lo, fx, fy, fz, uacc,
+                    lj1_rows<true>(buf, poff, prow, np, xi, phase, P, g, sig2, eps24, hi, lo, fx, fy, fz, uacc,
                                    wacc, hits, dummy);
                 }
-                __syncwarp();
             }
             float sx = fx, sy = fy, sz = fz;
             for (int p = 1; p < P; ++p) {
@@ -305,8 +306,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_rigid(ForceArgs a)
     constexpr int NPOL = (NMU + NQQ) > 0 ? (NMU + NQQ) : 1;
     __shared__ float4 scom[WARPS][RIG_CAP];
     __shared__ float4 ssite[WARPS][NSLOT][RIG_CAP];
+    __shared__ uint8_t squeue[WARPS][RIG_CAP * 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     float4* com = scom[wib];
+    uint8_t* qcol = squeue[wib] + lane;              // this lane's queue column
     const GridP& g = a.g;
     const DevModel* __restrict__ M = a.model;
     const int gw = blockIdx.x * WARPS + wib, nw = gridDim.x * WARPS;
@@ -344,15 +347,30 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_rigid(ForceArgs a)
             int hits = 0, mtot = 0, m = 0;
 
             auto compute = [&](int mm) {
-                if (!active) return;
-                for (int j = phase; j < mm; j += P) {
+                // distance phase: COM test (A1) for this lane's candidates,
+                // hits appended to the lane's queue column (slab indices)
+                int cnt = 0;
+                if (active) {
+                    for (int j = phase; j < mm; j += P) {
+                        const float4 X = com[j];
+                        const float dx = X.x - xi.x, dy = X.y - xi.y, dz = X.z - xi.z;
+                        const float r2 = dx * dx + dy * dy + dz * dz;
+                        bool hit = (r2 < g.cut2_hi) && ((__float_as_int(X.w) >> 3) != my);
+                        if (hit && r2 >= g.cut2_lo) hit = exact_in_range(dx, dy, dz, g);   // guard band (rare)
+                        qcol[cnt * 32] = (uint8_t)j;         // unconditional; the slot is reused on a miss
+                        cnt += hit ? 1 : 0;
+                    }
+                }
+                hits += cnt;
+                __syncwarp();
+                // force phase: all site pairs of the queued molecule pairs
+                const int cmax = __reduce_max_sync(0xffffffffu, cnt);
+                for (int k = 0; k < cmax; ++k) {
+                    if (k >= cnt) continue;
+                    const int j = qcol[k * 32];
                     const float4 X = com[j];
                     const float dx = X.x - xi.x, dy = X.y - xi.y, dz = X.z - xi.z;
-                    const float r2 = dx * dx + dy * dy + dz * dz;
                     const int wj = __float_as_int(X.w);
-                    if (!(r2 < g.cut2_hi) || (wj >> 3) == my) continue;
-                    if (r2 >= g.cut2_lo && !exact_in_range(dx, dy, dz, g)) continue;
-                    ++hits;
                     const int cj = wj & 7;
                     const DevComp& Cj = M->comp[cj];
                     const float3 d = make_float3(dx, dy, dz);

@@ -32,7 +32,7 @@ enum RigidShape { SHAPE_NONE, SHAPE_2CLJQ, SHAPE_TIP4P, SHAPE_GEN };
 #define MD_LJ1_WARPS 4
 #endif
 #ifndef MD_LJ1_CAP
-#define MD_LJ1_CAP 512
+#define MD_LJ1_CAP 256
 #endif
 constexpr int LJ1_WARPS = MD_LJ1_WARPS;
 constexpr int LJ1_CAP = MD_LJ1_CAP;
