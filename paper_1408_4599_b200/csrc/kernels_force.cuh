@@ -289,7 +289,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_lj1(ForceArgs a)
 // Slot layout per molecule: [LJ pos][charge pos, w = q][dipole pos, axis]
 // [quadrupole pos, axis], world frame relative to the COM.
 // =========================================================================
-#define RIG_CAP 96
+#ifndef RIG_CAP
+#define RIG_CAP 128
+#endif
+
+template <int NLJ, int NQ, int NMU, int NQQ, int WARPS>
+constexpr int rigid_smem() { return WARPS * ((1 + NLJ + NQ + 2 * NMU + 2 * NQQ) * RIG_CAP + RIG_CAP * 2) * 16; }
 
 template <int NLJ, int NQ, int NMU, int NQQ>
 struct Shape {
@@ -304,16 +309,26 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_rigid(ForceArgs a)
     using SH = Shape<NLJ, NQ, NMU, NQQ>;
     constexpr int NSLOT = SH::NSLOT;
     constexpr int NPOL = (NMU + NQQ) > 0 ? (NMU + NQQ) : 1;
-    __shared__ float4 scom[WARPS][RIG_CAP];
-    __shared__ float4 ssite[WARPS][NSLOT][RIG_CAP];
-    __shared__ uint8_t squeue[WARPS][RIG_CAP * 32];
+    extern __shared__ float4 smem_rig[];
+    constexpr int PER_WARP = (1 + NSLOT) * RIG_CAP + RIG_CAP * 2;     // float4 units (queue: RIG_CAP*32 B)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    float4* com = scom[wib];
-    uint8_t* qcol = squeue[wib] + lane;              // this lane's queue column
+    float4* com = smem_rig + wib * PER_WARP;
+    float4* ssw = com + RIG_CAP;                     // ssw[slot * RIG_CAP + j]
+    uint8_t* qcol = reinterpret_cast<uint8_t*>(ssw + NSLOT * RIG_CAP) + lane;   // this lane's queue column
     const GridP& g = a.g;
     const DevModel* __restrict__ M = a.model;
     const int gw = blockIdx.x * WARPS + wib, nw = gridDim.x * WARPS;
     const float krf = M->krf, crf = M->crf, kmm = M->krf_mumu;
+    // single-component shapes: LJ pair parameters in registers (no per-pair loads)
+    float4 ljp[NLJ > 0 ? NLJ * NLJ : 1];
+#pragma unroll
+    for (int ia = 0; ia < NLJ; ++ia)
+#pragma unroll
+        for (int ib = 0; ib < NLJ; ++ib) {
+            const int t = ia * MD_MAX_LJ_TOTAL + ib;
+            ljp[ia * NLJ + ib] = GEN ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                     : make_float4(M->sig2[t], M->eps24[t], M->eps4[t], M->shift[t]);
+        }
     double Uw = 0.0, Ww = 0.0;
     long long npw = 0, ncw = 0;
 
@@ -382,11 +397,16 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_rigid(ForceArgs a)
 #pragma unroll
                         for (int ib = 0; ib < NLJ; ++ib) {
                             if (GEN && ib >= Cj.n_lj) break;
-                            const float4 sb = ssite[wib][ib][j];
+                            const float4 sb = ssw[(ib) * RIG_CAP + (j)];
                             const float3 rv = make_float3(d.x + sb.x - si[ia].x, d.y + sb.y - si[ia].y,
                                                           d.z + sb.z - si[ia].z);
-                            const int t = (Ci.lj0 + ia) * MD_MAX_LJ_TOTAL + Cj.lj0 + ib;
-                            pair_lj(rv, M->sig2[t], M->eps24[t], M->eps4[t], M->shift[t], uacc, fs[ia], fh);
+                            if (GEN) {
+                                const int t = (Ci.lj0 + ia) * MD_MAX_LJ_TOTAL + Cj.lj0 + ib;
+                                pair_lj(rv, M->sig2[t], M->eps24[t], M->eps4[t], M->shift[t], uacc, fs[ia], fh);
+                            } else {
+                                const float4 pp = ljp[ia * NLJ + ib];
+                                pair_lj(rv, pp.x, pp.y, pp.z, pp.w, uacc, fs[ia], fh);
+                            }
                         }
                     }
                     // ---- charge x charge
@@ -397,7 +417,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_rigid(ForceArgs a)
 #pragma unroll
                         for (int ib = 0; ib < NQ; ++ib) {
                             if (GEN && ib >= Cj.n_q) break;
-                            const float4 sb = ssite[wib][GEN ? Cj.n_lj + ib : SH::SQ + ib][j];
+                            const float4 sb = ssw[(GEN ? Cj.n_lj + ib : SH::SQ + ib) * RIG_CAP + (j)];
                             const float3 rv = make_float3(d.x + sb.x - sa.x, d.y + sb.y - sa.y, d.z + sb.z - sa.z);
                             pair_qq(rv, sa.w * sb.w, krf, crf, uacc, fs[NLJ + ia], fh);
                         }
@@ -418,8 +438,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_rigid(ForceArgs a)
         {                                                                                              \
             if (GEN && ib >= (CNTB)) break;                                                            \
             const int slb = (SLB) + ib * STB;                                                          \
-            const float4 pb = ssite[wib][slb][j];                                                      \
-            const float4 eb4 = (STB == 2) ? ssite[wib][(slb + 1) % NSLOT][j] : make_float4(0.f, 0.f, 0.f, 0.f); \
+            const float4 pb = ssw[(slb) * RIG_CAP + (j)];                                                      \
+            const float4 eb4 = (STB == 2) ? ssw[((slb + 1) % NSLOT) * RIG_CAP + (j)] : make_float4(0.f, 0.f, 0.f, 0.f); \
             const float3 rv = make_float3(d.x + pb.x - pa.x, d.y + pb.y - pa.y, d.z + pb.z - pa.z);  \
             float3 tdummy = make_float3(0.f, 0.f, 0.f);                                                \
             pair_polar<KA, KB>(rv, pa.w, f3(ea4), pb.w, f3(eb4), kmm, uacc, fs[FIDX + ia],            \
@@ -475,7 +495,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_rigid(ForceArgs a)
                         const int nsl = GEN ? M->comp[cj].n_slots : NSLOT;
 #pragma unroll
                         for (int s = 0; s < NSLOT; ++s)
-                            if (s < nsl) ssite[wib][s][m + k] = a.site[(size_t)s * a.cap + src];
+                            if (s < nsl) ssw[(s) * RIG_CAP + (m + k)] = a.site[(size_t)s * a.cap + src];
                     }
                     m += take;
                     k0 += take;

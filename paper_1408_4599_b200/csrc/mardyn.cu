@@ -305,13 +305,16 @@ static int launch_force(mardyn_ctx* ctx, int buf)
     const int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ:
-        k_force_rigid<2, 0, 0, 1, false, RIG_WARPS><<<ctx->force_blocks, threads, 0, ctx->stream>>>(a);
+        k_force_rigid<2, 0, 0, 1, false, RIG_WARPS>
+            <<<ctx->force_blocks, threads, rigid_smem<2, 0, 0, 1, RIG_WARPS>(), ctx->stream>>>(a);
         break;
     case SHAPE_TIP4P:
-        k_force_rigid<1, 3, 0, 0, false, RIG_WARPS><<<ctx->force_blocks, threads, 0, ctx->stream>>>(a);
+        k_force_rigid<1, 3, 0, 0, false, RIG_WARPS>
+            <<<ctx->force_blocks, threads, rigid_smem<1, 3, 0, 0, RIG_WARPS>(), ctx->stream>>>(a);
         break;
     case SHAPE_GEN:
-        k_force_rigid<4, 4, 2, 2, true, GEN_WARPS><<<ctx->force_blocks, threads, 0, ctx->stream>>>(a);
+        k_force_rigid<4, 4, 2, 2, true, GEN_WARPS>
+            <<<ctx->force_blocks, threads, rigid_smem<4, 4, 2, 2, GEN_WARPS>(), ctx->stream>>>(a);
         break;
     default:
         K_LJ1<<<ctx->force_blocks, threads, LJ1::SMEM, ctx->stream>>>(a);
@@ -464,9 +467,27 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
     }
     int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
-    case SHAPE_2CLJQ: ctx->force_blocks = occupancy_grid(ctx, k_force_rigid<2, 0, 0, 1, false, RIG_WARPS>, threads); break;
-    case SHAPE_TIP4P: ctx->force_blocks = occupancy_grid(ctx, k_force_rigid<1, 3, 0, 0, false, RIG_WARPS>, threads); break;
-    case SHAPE_GEN: ctx->force_blocks = occupancy_grid(ctx, k_force_rigid<4, 4, 2, 2, true, GEN_WARPS>, threads); break;
+    case SHAPE_2CLJQ: {
+        auto k = k_force_rigid<2, 0, 0, 1, false, RIG_WARPS>;
+        const int sm = rigid_smem<2, 0, 0, 1, RIG_WARPS>();
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        ctx->force_blocks = occupancy_grid(ctx, k, threads, sm);
+        break;
+    }
+    case SHAPE_TIP4P: {
+        auto k = k_force_rigid<1, 3, 0, 0, false, RIG_WARPS>;
+        const int sm = rigid_smem<1, 3, 0, 0, RIG_WARPS>();
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        ctx->force_blocks = occupancy_grid(ctx, k, threads, sm);
+        break;
+    }
+    case SHAPE_GEN: {
+        auto k = k_force_rigid<4, 4, 2, 2, true, GEN_WARPS>;
+        const int sm = rigid_smem<4, 4, 2, 2, GEN_WARPS>();
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        ctx->force_blocks = occupancy_grid(ctx, k, threads, sm);
+        break;
+    }
     default:
         CK(cudaFuncSetAttribute(K_LJ1, cudaFuncAttributeMaxDynamicSharedMemorySize, LJ1::SMEM));
         ctx->force_blocks = occupancy_grid(ctx, K_LJ1, threads, LJ1::SMEM);
