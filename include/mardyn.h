@@ -160,13 +160,16 @@ int mardyn_get_observable_history(struct mardyn_ctx* ctx, int32_t cap, int32_t* 
 
 /* Molecule state in the caller's original order (index of set_molecules):
  * r (n*3), v (n*3, at t - dt/2), q (n*4), j (n*3, at t - dt/2); any output
- * pointer may be NULL.  cap must be >= n.                                  */
+ * pointer may be NULL.  cap must be >= n.  For a decomposed context: the
+ * molecules this rank owns, compacted in index order, with their ids.     */
 int mardyn_get_molecules(struct mardyn_ctx* ctx, int64_t cap, int64_t* n, int64_t* id,
                          int32_t* comp, double* r, double* v, double* q, double* j);
 
 /* Forces F (n*3) and torques tau (n*3) of the last force evaluation, in the
- * caller's original order.                                                  */
-int mardyn_get_forces(struct mardyn_ctx* ctx, int64_t cap, double* F, double* tau);
+ * caller's original order; *n_out (may be NULL) = molecules written.  For a
+ * decomposed context: the rank's owned molecules, compacted, ids in ids.    */
+int mardyn_get_forces(struct mardyn_ctx* ctx, int64_t cap, double* F, double* tau, int64_t* n_out,
+                      int64_t* ids);
 
 /* Raw parity hook: fixed-point positions u (n*3, original order), cell of
  * each molecule (n) and count per cell (n_cells), as used by the last force
@@ -204,6 +207,31 @@ int mardyn_cell_cost(const int32_t* counts, int32_t nx, int32_t ny, int32_t nz, 
  * MARDYN_EINVAL if the 2-cell constraint cannot be met.                    */
 int mardyn_kd_decompose(const double* cost, int32_t nx, int32_t ny, int32_t nz, int32_t p,
                         int32_t* boxes, double* loads);
+
+/*
+ * Spatial decomposition across GPUs (§4; one context per
+ * rank, same box/cutoff/components on every rank).  boxes = nranks * 6 cell
+ * ranges (from mardyn_kd_decompose, tiling the grid); this rank owns the
+ * molecules in boxes[rank] and holds halo copies of the molecules in the
+ * cells within one cell (>= rc) of its box.  ndof_global: the
+ * degrees of freedom of the whole system (T of the rank-local observables
+ * then sums to the global T).  Must precede mardyn_workspace_bytes.
+ * set_molecules then takes the GLOBAL arrays on every rank and keeps owned
+ * and halo molecules.  A time step is
+ *     mardyn_dd_begin_step -> transport -> mardyn_dd_end_step
+ * where the transport delivers, for every pair of ranks (src, dst), the
+ * send_counts[dst] records of src's send segment dst into dst's receive
+ * buffer (contiguous, any order: the cell rebuild sorts canonically).
+ * Observables and get_* report rank-local values (owned molecules); there
+ * n_pairs counts ordered pairs (i owned by the rank), so the global unique
+ * pair count is the sum over ranks divided by 2.
+ */
+int mardyn_set_decomposition(struct mardyn_ctx* ctx, int32_t rank, int32_t nranks, const int32_t* boxes,
+                             double ndof_global);
+int mardyn_dd_begin_step(struct mardyn_ctx* ctx, int64_t* send_counts);
+int mardyn_dd_buffers(struct mardyn_ctx* ctx, void** send, int64_t* seg_cap, void** recv, int64_t* recv_cap,
+                      int32_t* record_bytes);
+int mardyn_dd_end_step(struct mardyn_ctx* ctx, int64_t n_recv);
 
 const char* mardyn_last_error(const struct mardyn_ctx* ctx);
 void mardyn_destroy(struct mardyn_ctx* ctx);

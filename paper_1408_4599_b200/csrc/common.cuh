@@ -62,6 +62,39 @@ struct GridP {
     float cut2_lo, cut2_hi;      // guard band around rc^2 for the exact test
     long long cut2_q;            // exact threshold in quanta^2: in range iff r2q < cut2_q
     float dt;
+    int hlo[3], hdim[3];         // home cells of this rank: box [hlo, hlo + hdim) (whole grid if 1 rank)
+    int nhome;
+};
+
+// home cell t (0 <= t < nhome) of the rank's box, x fastest
+__device__ __forceinline__ int home_cell(const GridP& g, int t, int& cx, int& cy, int& cz)
+{
+    cx = g.hlo[0] + t % g.hdim[0];
+    cy = g.hlo[1] + (t / g.hdim[0]) % g.hdim[1];
+    cz = g.hlo[2] + t / (g.hdim[0] * g.hdim[1]);
+    return cx + g.nc[0] * (cy + g.nc[1] * cz);
+}
+
+// vel.w carries the component id (bits 0-7) and the ghost flag (bit 8) of
+// a molecule held only as a halo copy on this rank (spatial decomposition)
+__device__ __forceinline__ int md_comp(float w) { return __float_as_int(w) & 0xff; }
+__device__ __forceinline__ bool md_ghost(float w) { return (__float_as_int(w) >> 8) & 1; }
+
+// spatial decomposition: exchange record of one molecule
+struct DDRec {
+    uint4 pos;                   // global fixed-point position + id
+    float4 vel;                  // v(t - dt/2), comp | ghost << 8
+    float4 quat, angm;
+};
+
+struct DDArgs {
+    int rank, nranks;
+    const uint8_t* owner;        // owning rank of every global cell
+    const uint32_t* gmask;       // bit r: cell is in rank r's halo (and not owned by r)
+    DDRec* send;                 // nranks segments of seg_cap records
+    int seg_cap;
+    int* send_cnt;               // nranks counters
+    int* flag;                   // bit 8: send segment overflow
 };
 
 struct ObsRec {                  // one history entry (matches mardyn_observables order)

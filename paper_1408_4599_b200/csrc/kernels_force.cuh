@@ -201,11 +201,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_lj1(ForceArgs a)
     const float sig2 = a.sig2, eps24 = a.eps24;
     const float lo = g.cut2_lo, hi = g.cut2_hi;
 
-    for (int c = gw; c < g.ncell; c += nw) {
+    for (int t = gw; t < g.nhome; t += nw) {
+        int cx, cy, cz;
+        const int c = home_cell(g, t, cx, cy, cz);
         const int s_i = __ldg(a.start + c);
         const int n_all = __ldg(a.start + c + 1) - s_i;
         if (n_all == 0) continue;
-        const int cx = c % g.nc[0], cy = (c / g.nc[0]) % g.nc[1], cz = c / (g.nc[0] * g.nc[1]);
         for (int i0 = 0; i0 < n_all; i0 += 32) {
             const int ni = min(32, n_all - i0);
             const int P = 32 / ni;
@@ -332,11 +333,12 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_rigid(ForceArgs a)
     double Uw = 0.0, Ww = 0.0;
     long long npw = 0, ncw = 0;
 
-    for (int c = gw; c < g.ncell; c += nw) {
+    for (int t = gw; t < g.nhome; t += nw) {
+        int cx, cy, cz;
+        const int c = home_cell(g, t, cx, cy, cz);
         const int s_i = __ldg(a.start + c);
         const int n_all = __ldg(a.start + c + 1) - s_i;
         if (n_all == 0) continue;
-        const int cx = c % g.nc[0], cy = (c / g.nc[0]) % g.nc[1], cz = c / (g.nc[0] * g.nc[1]);
         for (int i0 = 0; i0 < n_all; i0 += 32) {
             const int ni = min(32, n_all - i0);
             const int P = 32 / ni;

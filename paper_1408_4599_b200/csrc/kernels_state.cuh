@@ -15,7 +15,9 @@ __global__ void k_ingest(int n, const double* __restrict__ r, const double* __re
                          const int* __restrict__ comp, GridP g, uint4* __restrict__ pos,
                          float4* __restrict__ vel, float4* __restrict__ quat,
                          float4* __restrict__ angm, int* __restrict__ cell_of,
-                         int* __restrict__ rank, int* __restrict__ count)
+                         int* __restrict__ rank, int* __restrict__ count,
+                         const uint8_t* __restrict__ owner = nullptr,
+                         const uint32_t* __restrict__ gmask = nullptr, int me = 0)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -30,9 +32,16 @@ __global__ void k_ingest(int n, const double* __restrict__ r, const double* __re
         u[k] = (uint32_t)x;
         c[k] = (int)(u[k] / g.E[k]);
     }
+    const int cl0 = c[0] + g.nc[0] * (c[1] + g.nc[1] * c[2]);
+    int gflag = 0;
+    if (owner) {                            // spatial decomposition: keep owned + halo molecules
+        const bool ghost = (gmask[cl0] >> me) & 1u;
+        if (owner[cl0] != me && !ghost) { cell_of[i] = -1; return; }
+        gflag = ghost ? 256 : 0;
+    }
     pos[i] = make_uint4(u[0], u[1], u[2], (uint32_t)i);
     vel[i] = make_float4((float)v[3 * i], (float)v[3 * i + 1], (float)v[3 * i + 2],
-                         __int_as_float(comp[i]));
+                         __int_as_float(comp[i] | gflag));
     if (quat) {
         quat[i] = q ? make_float4((float)q[4 * i], (float)q[4 * i + 1], (float)q[4 * i + 2], (float)q[4 * i + 3])
                     : make_float4(1.f, 0.f, 0.f, 0.f);
@@ -115,11 +124,14 @@ __global__ void __launch_bounds__(1024) k_scan_sums(int ntiles, int* __restrict_
     }
 }
 
-__global__ void k_scan_add(int ncell, int n, int* __restrict__ start, const int* __restrict__ tsum)
+__global__ void k_scan_add(int ncell, const int* __restrict__ count, int* __restrict__ start,
+                           const int* __restrict__ tsum)
 {
     int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c < ncell) start[c] += tsum[c / SCAN_TILE];
-    if (c == 0) start[ncell] = n;
+    if (c < ncell) {
+        start[c] += tsum[c / SCAN_TILE];
+        if (c == ncell - 1) start[ncell] = start[c] + count[c];
+    }
 }
 
 // ------------------------------------------------------------------------
@@ -131,7 +143,9 @@ __global__ void k_scatter(int n, const uint4* __restrict__ pos, const int* __res
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    int slot = start[cell_of[i]] + rank[i];
+    const int cl = cell_of[i];
+    if (cl < 0) return;                     // dropped ghost or migrant (spatial decomposition)
+    int slot = start[cl] + rank[i];
     const uint4 p = pos[i];
     keys[slot] = ((unsigned long long)p.x << 32) | p.w;
     oldidx[slot] = i;
@@ -155,7 +169,7 @@ __global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __res
                         const DevModel* __restrict__ model)
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
+    if (t >= n || t >= start[g.ncell]) return;
     const unsigned long long key = keys[t];
     const int old = oldidx[t];
     int c = cell_of[old];
@@ -174,13 +188,13 @@ __global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __res
     x.x = (float)(int)(p.x - (uint32_t)cx * g.E[0]) * g.s;    // exact (A12)
     x.y = (float)(int)(p.y - (uint32_t)cy * g.E[1]) * g.s;
     x.z = (float)(int)(p.z - (uint32_t)cz * g.E[2]) * g.s;
-    x.w = v.w;                                                  // comp bits
+    x.w = __int_as_float(md_comp(v.w));                         // comp bits
     xs[dst] = x;
     if (RIGID) {
         float4 q = quat_s[old];
         quat_d[dst] = q;
         angm_d[dst] = angm_s[old];
-        const DevComp& C = model->comp[__float_as_int(v.w)];
+        const DevComp& C = model->comp[md_comp(v.w)];
         int ns = C.n_lj + C.n_q;
         for (int k = 0; k < ns; ++k) {
             float3 w = qrot(q, C.bpos[k][0], C.bpos[k][1], C.bpos[k][2]);
@@ -230,7 +244,21 @@ __device__ __forceinline__ void block_sum2_d(double a, double b, double* out_a, 
     }
 }
 
-template <bool RIGID>
+// append one exchange record to destination `dst`'s send segment
+__device__ __forceinline__ void dd_push(const DDArgs& d, int dst, uint4 p, float4 v, float4 q, float4 j)
+{
+    const int k = atomicAdd(&d.send_cnt[dst], 1);
+    if (k >= d.seg_cap) { atomicOr(d.flag, 256); return; }
+    DDRec r;
+    r.pos = p; r.vel = v; r.quat = q; r.angm = j;
+    d.send[(size_t)dst * d.seg_cap + k] = r;
+}
+
+// DD = spatial decomposition: ghosts are skipped and
+// dropped; an owned molecule whose new cell belongs to another rank is
+// packed as a migrant for it (and dropped here); an owned molecule whose new
+// cell lies in other ranks' halos is also packed as a ghost for each of them.
+template <bool RIGID, bool DD = false>
 __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevModel* __restrict__ model,
                                                    uint4* __restrict__ pos, float4* __restrict__ vel,
                                                    float4* __restrict__ quat, float4* __restrict__ angm,
@@ -238,15 +266,20 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
                                                    const float4* __restrict__ torque,
                                                    int* __restrict__ cell_of, int* __restrict__ rank,
                                                    int* __restrict__ count, double* __restrict__ ke_part,
-                                                   int* __restrict__ flag)
+                                                   int* __restrict__ flag, DDArgs dd = DDArgs())
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     double ket = 0.0, ker = 0.0;
-    if (t < n) {
+    bool ghost = false;
+    if (DD && t < n) {
+        ghost = md_ghost(vel[t].w);
+        if (ghost) cell_of[t] = -1;
+    }
+    if (t < n && !ghost) {
         uint4 p = pos[t];
         float4 v = vel[t];
         float4 F = force[t];
-        const DevComp& C = model->comp[__float_as_int(v.w)];
+        const DevComp& C = model->comp[md_comp(v.w)];
         const float dt = g.dt, im = C.inv_mass;
         // A9: KE_t(t) from v(t) = v(t - dt/2) + dt/2 F/m
         float vx = v.x + 0.5f * dt * F.x * im, vy = v.y + 0.5f * dt * F.y * im,
@@ -296,10 +329,52 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
             if (!(isfinite(jn.x) && isfinite(jn.y) && isfinite(jn.z))) atomicOr(flag, 1);
         }
         int cl = c[0] + g.nc[0] * (c[1] + g.nc[1] * c[2]);
-        cell_of[t] = cl;
-        rank[t] = atomicAdd(&count[cl], 1);
+        if (DD) {
+            const uint4 pn = pos[t];
+            const float4 vn = vel[t];
+            const float4 qn = RIGID ? quat[t] : make_float4(1.f, 0.f, 0.f, 0.f);
+            const float4 jn = RIGID ? angm[t] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const int own = dd.owner[cl];
+            unsigned gm = dd.gmask[cl] & ~(1u << dd.rank);
+            while (gm) {                                   // halo copies for the other ranks
+                const int r = __ffs(gm) - 1;
+                gm &= gm - 1u;
+                dd_push(dd, r, pn, make_float4(vn.x, vn.y, vn.z, __int_as_float(md_comp(vn.w) | 256)), qn, jn);
+            }
+            if (own != dd.rank) {                          // migrant
+                dd_push(dd, own, pn, vn, qn, jn);
+                if ((dd.gmask[cl] >> dd.rank) & 1u) {      // its new cell is in my halo: keep a copy
+                    vel[t] = make_float4(vn.x, vn.y, vn.z, __int_as_float(md_comp(vn.w) | 256));
+                } else {
+                    cell_of[t] = -1;
+                    cl = -1;
+                }
+            }
+        }
+        if (cl >= 0) {
+            cell_of[t] = cl;
+            rank[t] = atomicAdd(&count[cl], 1);
+        }
     }
     block_sum2_d<256>(ket, ker, &ke_part[2 * blockIdx.x], &ke_part[2 * blockIdx.x + 1]);
+}
+
+// import n exchange records (migrants and ghosts) at unsorted slots
+// base .. base + n - 1 and bin them
+__global__ void k_import(int n, int base, GridP g, const DDRec* __restrict__ recv, uint4* __restrict__ pos,
+                         float4* __restrict__ vel, float4* __restrict__ quat, float4* __restrict__ angm,
+                         int* __restrict__ cell_of, int* __restrict__ rank, int* __restrict__ count)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const DDRec r = recv[k];
+    const int t = base + k;
+    pos[t] = r.pos;
+    vel[t] = r.vel;
+    if (quat) { quat[t] = r.quat; angm[t] = r.angm; }
+    const int cl = (int)(r.pos.x / g.E[0]) + g.nc[0] * ((int)(r.pos.y / g.E[1]) + g.nc[1] * (int)(r.pos.z / g.E[2]));
+    cell_of[t] = cl;
+    rank[t] = atomicAdd(&count[cl], 1);
 }
 
 // kinetic energy at t without integrating (compute_forces, A9)
@@ -314,10 +389,10 @@ __global__ void __launch_bounds__(256) k_kinetic(int n, GridP g, const DevModel*
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     double ket = 0.0, ker = 0.0;
-    if (t < n) {
+    if (t < n && !md_ghost(vel[t].w)) {
         float4 v = vel[t];
         float4 F = force[t];
-        const DevComp& C = model->comp[__float_as_int(v.w)];
+        const DevComp& C = model->comp[md_comp(v.w)];
         const float dt = g.dt, im = C.inv_mass;
         float vx = v.x + 0.5f * dt * F.x * im, vy = v.y + 0.5f * dt * F.y * im,
               vz = v.z + 0.5f * dt * F.z * im;
@@ -343,7 +418,7 @@ __global__ void k_half_kick(int n, GridP g, const DevModel* __restrict__ model, 
     if (t >= n) return;
     float4 v = vel[t];
     float4 F = force[t];
-    const DevComp& C = model->comp[__float_as_int(v.w)];
+    const DevComp& C = model->comp[md_comp(v.w)];
     const float h = 0.5f * g.dt;
     v.x -= h * F.x * C.inv_mass; v.y -= h * F.y * C.inv_mass; v.z -= h * F.z * C.inv_mass;
     vel[t] = v;
@@ -358,7 +433,7 @@ __global__ void k_half_kick(int n, GridP g, const DevModel* __restrict__ model, 
 __global__ void __launch_bounds__(1024) k_finalize(int nfp, const ForcePartial* __restrict__ fp,
                                                    int nkp, const double* __restrict__ kp,
                                                    double ndof, long long* __restrict__ step_ctr,
-                                                   int advance, ObsRec* __restrict__ hist)
+                                                   int advance, ObsRec* __restrict__ hist, int halve = 1)
 {
     double U = 0, W = 0, Kt = 0, Kr = 0;
     long long np = 0, nc = 0;
@@ -381,7 +456,8 @@ __global__ void __launch_bounds__(1024) k_finalize(int nfp, const ForcePartial* 
             o.U += sU[k]; o.W += sW[k]; o.KEt += sKt[k]; o.KEr += sKr[k];
             o.npairs += snp[k]; o.ncand += snc[k];
         }
-        o.npairs /= 2;                       // full shell sees every pair twice
+        if (halve) o.npairs /= 2;            // full shell sees every pair twice (a decomposed
+                                             // rank reports ordered pairs of its owned molecules)
         o.T = 2.0 * (o.KEt + o.KEr) / ndof;
         long long s = *step_ctr;
         o.step = s;
@@ -398,12 +474,14 @@ __global__ void k_egress(int n, GridP g, const uint4* __restrict__ pos, const fl
                          const float4* __restrict__ force, const float4* __restrict__ torque,
                          double* __restrict__ r, double* __restrict__ v, double* __restrict__ q,
                          double* __restrict__ j, double* __restrict__ F, double* __restrict__ tau,
-                         uint32_t* __restrict__ ufix, int* __restrict__ cell)
+                         uint32_t* __restrict__ ufix, int* __restrict__ cell, int8_t* __restrict__ owned = nullptr)
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
+    if (md_ghost(vel[t].w)) return;          // halo copies are reported by their owner
     uint4 p = pos[t];
     int i = (int)p.w;
+    if (owned) owned[i] = 1;
     if (r) { r[3 * i] = (double)p.x * g.s; r[3 * i + 1] = (double)p.y * g.s; r[3 * i + 2] = (double)p.z * g.s; }
     if (ufix) { ufix[3 * i] = p.x; ufix[3 * i + 1] = p.y; ufix[3 * i + 2] = p.z; }
     if (cell) {

@@ -112,6 +112,22 @@ struct mardyn_ctx {
     long long launches = 0;
     double last_total_ms = 0, last_force_ms = 0;
     int last_force_launches = 0;
+    // spatial decomposition (§4): this rank's box, cell owners, halos
+    int dd_rank = 0, nranks = 1;
+    std::vector<int32_t> boxes;
+    std::vector<uint8_t> h_owner;
+    std::vector<uint32_t> h_gmask;
+    double ndof_global = -1.0;
+    uint8_t* owner = nullptr;
+    uint32_t* gmask = nullptr;
+    int8_t* owned = nullptr;
+    DDRec* sendbuf = nullptr;
+    DDRec* recvbuf = nullptr;
+    int* send_cnt = nullptr;
+    int64_t seg_cap = 0, recv_cap = 0;
+    int64_t n_input = 0;
+    int64_t n_force = 0;       // molecules (sorted slots) of the buffer the last forces belong to
+    int rank_id() const { return dd_rank; }
 };
 
 // ------------------------------------------------------------------------
@@ -178,6 +194,8 @@ static int setup_grid(mardyn_ctx* ctx)
     g.cut2_hi = std::nextafterf((float)(rc2 * (1.0 + std::ldexp(1.0, -20))), INFINITY);
     g.cut2_q = (long long)std::ceil(rc2 / (s * s));
     g.dt = (float)ctx->dt;
+    for (int k = 0; k < 3; ++k) { g.hlo[k] = 0; g.hdim[k] = g.nc[k]; }
+    g.nhome = g.ncell;
     return MARDYN_OK;
 }
 
@@ -284,6 +302,7 @@ static int occupancy_grid(mardyn_ctx* ctx, K kernel, int threads, size_t smem = 
 static int launch_force(mardyn_ctx* ctx, int buf)
 {
     (void)buf;
+    ctx->n_force = ctx->n;
     ForceArgs a;
     a.g = ctx->g;
     a.n = (int)ctx->n;
@@ -327,13 +346,13 @@ static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 // counting sort of the unsorted buffer `src` (cell_of / rank / count
 // filled) into buffer `dst`, canonical in-cell order (A13)
-static int enqueue_sort(mardyn_ctx* ctx, int src, int dst)
+static int enqueue_sort(mardyn_ctx* ctx, int src, int dst, int64_t n_unsorted = -1)
 {
-    const int n = (int)ctx->n, ncell = ctx->g.ncell;
+    const int n = (int)(n_unsorted < 0 ? ctx->n : n_unsorted), ncell = ctx->g.ncell;
     cudaStream_t s = ctx->stream;
     k_scan_tiles<<<ctx->ntiles, 1024, 0, s>>>(ncell, ctx->count, ctx->start, ctx->tsum);
     k_scan_sums<<<1, 1024, 0, s>>>(ctx->ntiles, ctx->tsum);
-    k_scan_add<<<nblk(ncell, 256), 256, 0, s>>>(ncell, n, ctx->start, ctx->tsum);
+    k_scan_add<<<nblk(ncell, 256), 256, 0, s>>>(ncell, ctx->count, ctx->start, ctx->tsum);
     k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->pos[src], ctx->cell_of, ctx->rank, ctx->start, ctx->keys,
                                             ctx->oldidx);
     if (ctx->rigid)
@@ -562,6 +581,21 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     DevModel* dmodel = (DevModel*)take(sizeof(DevModel));
     const size_t stage_bytes = (size_t)cap * (19 * 8 + 3 * 4 + 4 + 4);
     char* stage = take(stage_bytes);
+    uint8_t* owner = nullptr;
+    uint32_t* gmask = nullptr;
+    int8_t* owned = nullptr;
+    DDRec *sendbuf = nullptr, *recvbuf = nullptr;
+    int* send_cnt = nullptr;
+    const int64_t seg_cap = ctx->nranks > 1 ? cap / ctx->nranks + 4096 : 0;
+    const int64_t recv_cap = ctx->nranks > 1 ? cap : 0;
+    if (ctx->nranks > 1) {
+        owner = (uint8_t*)take((size_t)ncell);
+        gmask = (uint32_t*)take(4 * (size_t)ncell);
+        owned = (int8_t*)take((size_t)cap);
+        sendbuf = (DDRec*)take(sizeof(DDRec) * (size_t)seg_cap * ctx->nranks);
+        recvbuf = (DDRec*)take(sizeof(DDRec) * (size_t)recv_cap);
+        send_cnt = (int*)take(4 * (size_t)ctx->nranks);
+    }
     if (assign) {
         ctx->pos[0] = pos0; ctx->pos[1] = pos1; ctx->vel[0] = vel0; ctx->vel[1] = vel1;
         ctx->quat[0] = q0; ctx->quat[1] = q1; ctx->angm[0] = j0; ctx->angm[1] = j1;
@@ -570,6 +604,8 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         ctx->start = start; ctx->tsum = tsum; ctx->fpart = fpart; ctx->kpart = kpart;
         ctx->hist = hist; ctx->step_ctr = step_ctr; ctx->flag = flag; ctx->dmodel = dmodel;
         ctx->stage = stage; ctx->stage_bytes = stage_bytes;
+        ctx->owner = owner; ctx->gmask = gmask; ctx->owned = owned; ctx->sendbuf = sendbuf;
+        ctx->recvbuf = recvbuf; ctx->send_cnt = send_cnt; ctx->seg_cap = seg_cap; ctx->recv_cap = recv_cap;
         ctx->ncell_pad = ncell_pad; ctx->ntiles = ntiles; ctx->nkblocks = nk;
     }
     return off;
@@ -598,6 +634,12 @@ int mardyn_set_workspace(mardyn_ctx* ctx, void* device_ptr, size_t bytes, int64_
     CK(cudaMemsetAsync(ctx->step_ctr, 0, 8, ctx->stream));
     CK(cudaMemsetAsync(ctx->flag, 0, 4, ctx->stream));
     CK(cudaMemsetAsync(ctx->hist, 0, sizeof(ObsRec) * MD_HISTORY, ctx->stream));
+    if (ctx->nranks > 1) {
+        CK(cudaMemcpyAsync(ctx->owner, ctx->h_owner.data(), ctx->g.ncell, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->gmask, ctx->h_gmask.data(), 4 * (size_t)ctx->g.ncell, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
     for (int b = 0; b < 2; ++b)
         if (ctx->gexec[b]) { cudaGraphExecDestroy(ctx->gexec[b]); ctx->gexec[b] = nullptr; }
     return MARDYN_OK;
@@ -630,7 +672,8 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
     for (int64_t i = 0; i < n; ++i) ctx->ids[i] = id ? id[i] : i;
     double ndof = 3.0 * n;
     for (int64_t i = 0; i < n; ++i) ndof += ctx->model.comp[comp[i]].rot * (ctx->rigid ? 1 : 0);
-    ctx->ndof = ndof;
+    ctx->ndof = ctx->ndof_global > 0 ? ctx->ndof_global : ndof;
+    ctx->n_input = n;
     cudaStream_t s = ctx->stream;
     // host -> device (the caller's buffers; pinned ones are DMA'd directly)
     double* dr = (double*)ctx->stage;
@@ -650,12 +693,20 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
     const int src = 1, dst = 0;
     k_ingest<<<nblk(n, 256), 256, 0, s>>>((int)n, dr, dv, ctx->rigid ? dq : nullptr, ctx->rigid ? dj : nullptr, dc,
                                            ctx->g, ctx->pos[src], ctx->vel[src], ctx->rigid ? ctx->quat[src] : nullptr,
-                                           ctx->rigid ? ctx->angm[src] : nullptr, ctx->cell_of, ctx->rank, ctx->count);
+                                           ctx->rigid ? ctx->angm[src] : nullptr, ctx->cell_of, ctx->rank, ctx->count,
+                                           ctx->nranks > 1 ? ctx->owner : nullptr,
+                                           ctx->nranks > 1 ? ctx->gmask : nullptr, ctx->rank_id());
     ctx->launches += 1;
-    int rc = enqueue_sort(ctx, src, dst);
+    int rc = enqueue_sort(ctx, src, dst, n);
     if (rc) return rc;
     CK(cudaGetLastError());
     ctx->cur = dst;
+    if (ctx->nranks > 1) {        // owned + halo molecules kept by this rank
+        int kept = 0;
+        CK(cudaMemcpyAsync(&kept, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        ctx->n = kept;
+    }
     long long step = ctx->host_step;
     CK(cudaMemcpyAsync(ctx->step_ctr, &step, 8, cudaMemcpyHostToDevice, s));
     if (!half_step) {   // A8: backward half kick with F(t0), tau(t0)
@@ -704,6 +755,7 @@ int mardyn_step(mardyn_ctx* ctx, int32_t nsteps)
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
     if (nsteps < 0) return fail(ctx, MARDYN_EINVAL, "n must be >= 0");
+    if (ctx->nranks > 1) return fail(ctx, MARDYN_ESTATE, "decomposed context: use mardyn_dd_begin_step / dd_end_step");
     if (nsteps == 0) return MARDYN_OK;
     if (!ctx->gexec[0]) {
         int rc = build_graphs(ctx);
@@ -773,42 +825,78 @@ int mardyn_get_observable_history(mardyn_ctx* ctx, int32_t cap, int32_t* n, mard
     return MARDYN_OK;
 }
 
+// Copy molecule data (caller's original order = set_molecules index) to
+// host arrays.  Single rank: all n molecules.  Decomposed: the molecules this
+// rank owns, compacted in index order; their ids go to ids_out.
 static int egress(mardyn_ctx* ctx, double* r, double* v, double* q, double* j, double* F, double* tau,
-                  uint32_t* ufix, int32_t* cell)
+                  uint32_t* ufix, int32_t* cell, int64_t n_slots = -1, int64_t* n_out = nullptr,
+                  int64_t* ids_out = nullptr, int32_t* comp_out = nullptr)
 {
-    const int64_t n = ctx->n;
+    const bool dd = ctx->nranks > 1;
+    const int64_t n = n_slots < 0 ? ctx->n : n_slots;          // sorted slots to read
+    const int64_t N = dd ? ctx->n_input : ctx->n;               // index space of the output
     cudaStream_t s = ctx->stream;
     double* d_r = (double*)ctx->stage;
-    double* d_v = d_r + 3 * n;
-    double* d_q = d_v + 3 * n;
-    double* d_j = d_q + 4 * n;
-    double* d_F = d_j + 3 * n;
-    double* d_t = d_F + 3 * n;
-    uint32_t* d_u = (uint32_t*)(d_t + 3 * n);
-    int* d_c = (int*)(d_u + 3 * n);
+    double* d_v = d_r + 3 * N;
+    double* d_q = d_v + 3 * N;
+    double* d_j = d_q + 4 * N;
+    double* d_F = d_j + 3 * N;
+    double* d_t = d_F + 3 * N;
+    uint32_t* d_u = (uint32_t*)(d_t + 3 * N);
+    int* d_c = (int*)(d_u + 3 * N);
     const int b = ctx->cur;
+    if (dd) CK(cudaMemsetAsync(ctx->owned, 0, (size_t)N, s));
     if (ctx->rigid)
         k_egress<true><<<nblk(n, 256), 256, 0, s>>>((int)n, ctx->g, ctx->pos[b], ctx->vel[b], ctx->quat[b],
                                                     ctx->angm[b], ctx->force, ctx->torque, r ? d_r : nullptr,
                                                     v ? d_v : nullptr, q ? d_q : nullptr, j ? d_j : nullptr,
                                                     F ? d_F : nullptr, tau ? d_t : nullptr, ufix ? d_u : nullptr,
-                                                    cell ? d_c : nullptr);
+                                                    cell ? d_c : nullptr, dd ? ctx->owned : nullptr);
     else
         k_egress<false><<<nblk(n, 256), 256, 0, s>>>((int)n, ctx->g, ctx->pos[b], ctx->vel[b], nullptr, nullptr,
                                                      ctx->force, nullptr, r ? d_r : nullptr, v ? d_v : nullptr,
                                                      q ? d_q : nullptr, j ? d_j : nullptr, F ? d_F : nullptr,
-                                                     tau ? d_t : nullptr, ufix ? d_u : nullptr, cell ? d_c : nullptr);
+                                                     tau ? d_t : nullptr, ufix ? d_u : nullptr, cell ? d_c : nullptr,
+                                                     dd ? ctx->owned : nullptr);
     ctx->launches += 1;
     CK(cudaGetLastError());
-    if (r) CK(cudaMemcpyAsync(r, d_r, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
-    if (v) CK(cudaMemcpyAsync(v, d_v, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
-    if (q) CK(cudaMemcpyAsync(q, d_q, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, s));
-    if (j) CK(cudaMemcpyAsync(j, d_j, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
-    if (F) CK(cudaMemcpyAsync(F, d_F, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
-    if (tau) CK(cudaMemcpyAsync(tau, d_t, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
-    if (ufix) CK(cudaMemcpyAsync(ufix, d_u, sizeof(uint32_t) * 3 * n, cudaMemcpyDeviceToHost, s));
-    if (cell) CK(cudaMemcpyAsync(cell, d_c, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
-    return sync_check(ctx);
+    if (!dd) {
+        if (r) CK(cudaMemcpyAsync(r, d_r, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+        if (v) CK(cudaMemcpyAsync(v, d_v, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+        if (q) CK(cudaMemcpyAsync(q, d_q, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, s));
+        if (j) CK(cudaMemcpyAsync(j, d_j, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+        if (F) CK(cudaMemcpyAsync(F, d_F, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+        if (tau) CK(cudaMemcpyAsync(tau, d_t, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+        if (ufix) CK(cudaMemcpyAsync(ufix, d_u, sizeof(uint32_t) * 3 * n, cudaMemcpyDeviceToHost, s));
+        if (cell) CK(cudaMemcpyAsync(cell, d_c, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+        if (n_out) *n_out = n;
+        return sync_check(ctx);
+    }
+    std::vector<int8_t> mask((size_t)N);
+    CK(cudaMemcpyAsync(mask.data(), ctx->owned, (size_t)N, cudaMemcpyDeviceToHost, s));
+    struct Out { void* host; void* dev; size_t width; };
+    const Out outs[] = {{r, d_r, 24}, {v, d_v, 24}, {q, d_q, 32}, {j, d_j, 24}, {F, d_F, 24}, {tau, d_t, 24},
+                        {ufix, d_u, 12}, {cell, d_c, 4}};
+    std::vector<std::vector<char>> tmp(8);
+    for (int k = 0; k < 8; ++k)
+        if (outs[k].host) {
+            tmp[k].resize(outs[k].width * (size_t)N);
+            CK(cudaMemcpyAsync(tmp[k].data(), outs[k].dev, outs[k].width * (size_t)N, cudaMemcpyDeviceToHost, s));
+        }
+    int rc = sync_check(ctx);
+    if (rc) return rc;
+    int64_t m = 0;
+    for (int64_t i = 0; i < N; ++i) {
+        if (!mask[i]) continue;
+        for (int k = 0; k < 8; ++k)
+            if (outs[k].host)
+                std::memcpy((char*)outs[k].host + outs[k].width * m, tmp[k].data() + outs[k].width * i, outs[k].width);
+        if (ids_out) ids_out[m] = ctx->ids[i];
+        if (comp_out) comp_out[m] = ctx->comp_host[i];
+        ++m;
+    }
+    if (n_out) *n_out = m;
+    return MARDYN_OK;
 }
 
 int mardyn_get_molecules(mardyn_ctx* ctx, int64_t cap, int64_t* n, int64_t* id, int32_t* comp, double* r,
@@ -818,28 +906,36 @@ int mardyn_get_molecules(mardyn_ctx* ctx, int64_t cap, int64_t* n, int64_t* id, 
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
     if (cap < ctx->n) return fail(ctx, MARDYN_EINVAL, "cap < number of molecules");
+    if (ctx->nranks > 1)      // the rank's owned molecules, with their ids
+        return egress(ctx, r, v, q, j, nullptr, nullptr, nullptr, nullptr, -1, n, id, comp);
     *n = ctx->n;
     if (id) std::memcpy(id, ctx->ids.data(), sizeof(int64_t) * ctx->n);
     if (comp) std::memcpy(comp, ctx->comp_host.data(), sizeof(int32_t) * ctx->n);
     return egress(ctx, r, v, q, j, nullptr, nullptr, nullptr, nullptr);
 }
 
-int mardyn_get_forces(mardyn_ctx* ctx, int64_t cap, double* F, double* tau)
+int mardyn_get_forces(mardyn_ctx* ctx, int64_t cap, double* F, double* tau, int64_t* n_out, int64_t* ids)
 {
     if (!ctx) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
     if (cap < ctx->n) return fail(ctx, MARDYN_EINVAL, "cap < number of molecules");
     // forces are indexed by the sorted slots of the buffer they were computed on
+    int64_t* idp = nullptr;
+    int64_t nn = 0;
+    if (ctx->nranks > 1) idp = ids;
     if (ctx->last_obs >= 0 && ctx->last_obs == ctx->host_step - 1 && ctx->host_step > 0) {
-        // after step(): F belongs to the previous parity; egress that buffer's ids
+        // after a step: F belongs to the previous parity; egress that buffer's ids
         int b = ctx->cur;
         ctx->cur = ctx->last_parity;
-        int rc = egress(ctx, nullptr, nullptr, nullptr, nullptr, F, tau, nullptr, nullptr);
+        int rc = egress(ctx, nullptr, nullptr, nullptr, nullptr, F, tau, nullptr, nullptr, ctx->n_force, &nn, idp);
         ctx->cur = b;
+        if (n_out) *n_out = nn;
         return rc;
     }
-    return egress(ctx, nullptr, nullptr, nullptr, nullptr, F, tau, nullptr, nullptr);
+    int rc = egress(ctx, nullptr, nullptr, nullptr, nullptr, F, tau, nullptr, nullptr, ctx->n_force, &nn, idp);
+    if (n_out) *n_out = nn;
+    return rc;
 }
 
 int mardyn_get_raw(mardyn_ctx* ctx, int64_t cap, uint32_t* pos_fixed, int32_t* cell, int32_t* cell_count)
@@ -864,7 +960,7 @@ int mardyn_last_step_timing(mardyn_ctx* ctx, double* total_ms, double* force_ms,
     if (!ctx) return MARDYN_EINVAL;
     CK(cudaStreamSynchronize(ctx->stream));
     float f = 0.f;
-    if (ctx->profiling && ctx->gexec[0]) {
+    if (ctx->profiling && (ctx->gexec[0] || ctx->nranks > 1)) {
         cudaError_t e = cudaEventElapsedTime(&f, ctx->ev_f0[ctx->last_parity], ctx->ev_f1[ctx->last_parity]);
         if (e != cudaSuccess) { f = 0.f; cudaGetLastError(); }
     }
@@ -886,6 +982,151 @@ int mardyn_set_profiling(mardyn_ctx* ctx, int32_t on)
 }
 
 int64_t mardyn_launch_count(const mardyn_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---------------------------------------------------------------------------
+// spatial decomposition (§4)
+
+int mardyn_set_decomposition(mardyn_ctx* ctx, int32_t rank, int32_t nranks, const int32_t* boxes,
+                             double ndof_global)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (ctx->ws) return fail(ctx, MARDYN_ESTATE, "set_decomposition must precede workspace_bytes/set_workspace");
+    if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks || !boxes)
+        return fail(ctx, MARDYN_EINVAL, "bad rank / nranks (1..32) / boxes");
+    const GridP& g0 = ctx->g;
+    const int nx = g0.nc[0], ny = g0.nc[1], nz = g0.nc[2];
+    std::vector<uint8_t> owner((size_t)g0.ncell, 255);
+    for (int r = 0; r < nranks; ++r) {
+        const int32_t* b = boxes + 6 * r;
+        for (int k = 0; k < 3; ++k)
+            if (b[k] < 0 || b[3 + k] > g0.nc[k] || b[3 + k] - b[k] < 2)
+                return fail(ctx, MARDYN_EINVAL, "every box needs >= 2 cells per axis inside the grid (P:213)");
+        for (int z = b[2]; z < b[5]; ++z)
+            for (int y = b[1]; y < b[4]; ++y)
+                for (int x = b[0]; x < b[3]; ++x) {
+                    uint8_t& o = owner[x + (size_t)nx * (y + (size_t)ny * z)];
+                    if (o != 255) return fail(ctx, MARDYN_EINVAL, "boxes overlap");
+                    o = (uint8_t)r;
+                }
+    }
+    for (uint8_t o : owner)
+        if (o == 255) return fail(ctx, MARDYN_EINVAL, "boxes do not tile the grid");
+    // halo of rank r: cells within one cell (periodic) of its box, owned by another rank
+    std::vector<uint32_t> gmask((size_t)g0.ncell, 0u);
+    for (int r = 0; r < nranks; ++r) {
+        const int32_t* b = boxes + 6 * r;
+        for (int z = b[2] - 1; z <= b[5]; ++z)
+            for (int y = b[1] - 1; y <= b[4]; ++y)
+                for (int x = b[0] - 1; x <= b[3]; ++x) {
+                    const size_t c = (size_t)((x + nx) % nx) + (size_t)nx * (((y + ny) % ny) + (size_t)ny * ((z + nz) % nz));
+                    if (owner[c] != r) gmask[c] |= 1u << r;
+                }
+    }
+    ctx->dd_rank = rank;
+    ctx->nranks = nranks;
+    ctx->boxes.assign(boxes, boxes + 6 * nranks);
+    ctx->h_owner.swap(owner);
+    ctx->h_gmask.swap(gmask);
+    ctx->ndof_global = ndof_global;
+    const int32_t* b = boxes + 6 * rank;
+    GridP& g = ctx->g;
+    for (int k = 0; k < 3; ++k) { g.hlo[k] = b[k]; g.hdim[k] = b[3 + k] - b[k]; }
+    g.nhome = g.hdim[0] * g.hdim[1] * g.hdim[2];
+    return MARDYN_OK;
+}
+
+// forces at t_k on the home box, observables (rank-local partials), kick /
+// drift / rotation of the owned molecules, binning, and packing of the
+// exchange records: migrants for their new owners, halo copies for the
+// ranks whose halo holds the molecule's new cell.  Returns the records per
+// destination rank.
+int mardyn_dd_begin_step(mardyn_ctx* ctx, int64_t* send_counts)
+{
+    if (!ctx || !send_counts) return MARDYN_EINVAL;
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "no decomposition: use mardyn_step");
+    cudaStream_t s = ctx->stream;
+    const int b = ctx->cur, n = (int)ctx->n;
+    long long step = ctx->host_step;
+    CK(cudaMemcpyAsync(ctx->step_ctr, &step, 8, cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(ctx->ev_f0[b], s));
+    launch_force(ctx, b);
+    CK(cudaEventRecord(ctx->ev_f1[b], s));
+    CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
+    CK(cudaMemsetAsync(ctx->send_cnt, 0, sizeof(int) * ctx->nranks, s));
+    DDArgs dd;
+    dd.rank = ctx->dd_rank; dd.nranks = ctx->nranks; dd.owner = ctx->owner; dd.gmask = ctx->gmask;
+    dd.send = ctx->sendbuf; dd.seg_cap = (int)ctx->seg_cap; dd.send_cnt = ctx->send_cnt; dd.flag = ctx->flag;
+    const int nkb = nblk(n, 256);
+    if (ctx->rigid)
+        k_integrate<true, true><<<nkb, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b], ctx->quat[b],
+                                                    ctx->angm[b], ctx->force, ctx->torque, ctx->cell_of, ctx->rank,
+                                                    ctx->count, ctx->kpart, ctx->flag, dd);
+    else
+        k_integrate<false, true><<<nkb, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b], nullptr,
+                                                     nullptr, ctx->force, ctx->torque, ctx->cell_of, ctx->rank,
+                                                     ctx->count, ctx->kpart, ctx->flag, dd);
+    k_finalize<<<1, 1024, 0, s>>>(ctx->force_blocks * ctx->force_warps_per_block, ctx->fpart, nkb, ctx->kpart,
+                                  ctx->ndof, ctx->step_ctr, 1, ctx->hist, 0);
+    ctx->launches += 3;
+    CK(cudaGetLastError());
+    std::vector<int> cnt(ctx->nranks);
+    CK(cudaMemcpyAsync(cnt.data(), ctx->send_cnt, 4 * ctx->nranks, cudaMemcpyDeviceToHost, s));
+    int flag = 0;
+    CK(cudaMemcpyAsync(&flag, ctx->flag, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (flag & 256) return fail(ctx, MARDYN_ECAPACITY, "exchange segment overflow");
+    for (int r = 0; r < ctx->nranks; ++r) send_counts[r] = cnt[r];
+    ctx->last_parity = b;
+    return MARDYN_OK;
+}
+
+// device addresses of the exchange buffers: send segment r at
+// send + r * seg_cap records; the receive buffer holds records contiguously
+int mardyn_dd_buffers(mardyn_ctx* ctx, void** send, int64_t* seg_cap, void** recv, int64_t* recv_cap,
+                      int32_t* record_bytes)
+{
+    if (!ctx || !send || !seg_cap || !recv || !recv_cap || !record_bytes) return MARDYN_EINVAL;
+    if (ctx->nranks < 2 || !ctx->ws) return fail(ctx, MARDYN_ESTATE, "no decomposition workspace");
+    *send = ctx->sendbuf;
+    *seg_cap = ctx->seg_cap;
+    *recv = ctx->recvbuf;
+    *recv_cap = ctx->recv_cap;
+    *record_bytes = (int32_t)sizeof(DDRec);
+    return MARDYN_OK;
+}
+
+// import the n_recv records placed in the receive buffer, then rebuild the
+// cells (counting sort of owned + halo molecules) for the next step
+int mardyn_dd_end_step(mardyn_ctx* ctx, int64_t n_recv)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "no decomposition");
+    if (n_recv < 0 || n_recv > ctx->recv_cap || ctx->n + n_recv > ctx->cap)
+        return fail(ctx, MARDYN_ECAPACITY, "received records exceed the capacity");
+    cudaStream_t s = ctx->stream;
+    const int b = ctx->cur;
+    if (n_recv > 0) {
+        k_import<<<nblk(n_recv, 256), 256, 0, s>>>((int)n_recv, (int)ctx->n, ctx->g, ctx->recvbuf, ctx->pos[b],
+                                                   ctx->vel[b], ctx->rigid ? ctx->quat[b] : nullptr,
+                                                   ctx->rigid ? ctx->angm[b] : nullptr, ctx->cell_of, ctx->rank,
+                                                   ctx->count);
+        ctx->launches += 1;
+    }
+    int rc = enqueue_sort(ctx, b, 1 - b, ctx->n + n_recv);
+    if (rc) return rc;
+    CK(cudaGetLastError());
+    int kept = 0;
+    CK(cudaMemcpyAsync(&kept, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ctx->n = kept;
+    ctx->cur = 1 - b;
+    ctx->host_step += 1;
+    ctx->last_obs = ctx->host_step - 1;
+    return MARDYN_OK;
+}
 
 int mardyn_cell_cost(const int32_t* counts, int32_t nx, int32_t ny, int32_t nz, double* cost)
 {

@@ -27,8 +27,9 @@ EXPORTS = ["mardyn_create", "mardyn_get_grid", "mardyn_workspace_bytes", "mardyn
            "mardyn_set_molecules", "mardyn_compute_forces", "mardyn_step", "mardyn_get_observables",
            "mardyn_get_observable_history", "mardyn_get_molecules", "mardyn_get_forces",
            "mardyn_get_raw", "mardyn_last_step_timing", "mardyn_set_profiling",
-           "mardyn_launch_count", "mardyn_cell_cost", "mardyn_kd_decompose", "mardyn_last_error",
-           "mardyn_destroy"]
+           "mardyn_launch_count", "mardyn_cell_cost", "mardyn_kd_decompose",
+           "mardyn_set_decomposition", "mardyn_dd_begin_step", "mardyn_dd_buffers", "mardyn_dd_end_step",
+           "mardyn_last_error", "mardyn_destroy"]
 
 
 class MardynError(RuntimeError):
@@ -99,7 +100,11 @@ def load_library():
     lib.mardyn_get_observables.argtypes = [vp, P(Observables)]
     lib.mardyn_get_observable_history.argtypes = [vp, C.c_int32, P(C.c_int32), P(Observables)]
     lib.mardyn_get_molecules.argtypes = [vp, C.c_int64, P(C.c_int64), vp, vp, vp, vp, vp, vp]
-    lib.mardyn_get_forces.argtypes = [vp, C.c_int64, vp, vp]
+    lib.mardyn_get_forces.argtypes = [vp, C.c_int64, vp, vp, P(C.c_int64), vp]
+    lib.mardyn_set_decomposition.argtypes = [vp, C.c_int32, C.c_int32, vp, C.c_double]
+    lib.mardyn_dd_begin_step.argtypes = [vp, vp]
+    lib.mardyn_dd_buffers.argtypes = [vp, P(vp), P(C.c_int64), P(vp), P(C.c_int64), P(C.c_int32)]
+    lib.mardyn_dd_end_step.argtypes = [vp, C.c_int64]
     lib.mardyn_get_raw.argtypes = [vp, C.c_int64, vp, vp, vp]
     lib.mardyn_last_step_timing.argtypes = [vp, P(C.c_double), P(C.c_double), P(C.c_int32)]
     lib.mardyn_set_profiling.argtypes = [vp, C.c_int32]
@@ -269,13 +274,45 @@ class Context:
             return n.value
         return {k: x[: n.value] for k, x in res.items()}
 
-    def get_forces(self):
+    def get_forces(self, with_ids=False):
         cap = self.capacity
-        F = np.empty((cap, 3)); tau = np.empty((cap, 3))
+        F = np.empty((cap, 3)); tau = np.empty((cap, 3)); ids = np.empty(cap, np.int64)
+        n = C.c_int64()
         self._check(self.lib.mardyn_get_forces(self.h, cap, F.ctypes.data_as(C.c_void_p),
-                                               tau.ctypes.data_as(C.c_void_p)))
-        n = self._n()
-        return F[:n], tau[:n]
+                                               tau.ctypes.data_as(C.c_void_p), C.byref(n),
+                                               ids.ctypes.data_as(C.c_void_p)))
+        m = n.value
+        if with_ids:
+            return F[:m], tau[:m], ids[:m]
+        return F[:m], tau[:m]
+
+    # -- spatial decomposition (one context per rank) ----------------------
+    def set_decomposition(self, rank, nranks, boxes, ndof_global):
+        b = np.ascontiguousarray(np.asarray(boxes, dtype=np.int32).reshape(nranks, 6))
+        self._dd_boxes = b
+        self._check(self.lib.mardyn_set_decomposition(self.h, int(rank), int(nranks),
+                                                      b.ctypes.data_as(C.c_void_p), float(ndof_global)))
+        self.rank, self.nranks = int(rank), int(nranks)
+
+    def dd_begin_step(self):
+        cnt = np.zeros(self.nranks, np.int64)
+        self._check(self.lib.mardyn_dd_begin_step(self.h, cnt.ctypes.data_as(C.c_void_p)))
+        return cnt
+
+    def dd_buffers(self):
+        """(send tensor view [nranks, seg_cap, rec], recv tensor view [recv_cap, rec])
+        as uint8 slices of the workspace tensor (zero copy)."""
+        send = C.c_void_p(); seg = C.c_int64(); recv = C.c_void_p(); rcap = C.c_int64(); rb = C.c_int32()
+        self._check(self.lib.mardyn_dd_buffers(self.h, C.byref(send), C.byref(seg), C.byref(recv),
+                                               C.byref(rcap), C.byref(rb)))
+        base = self.ws.data_ptr()
+        so, ro = send.value - base, recv.value - base
+        sb = self.ws[so: so + self.nranks * seg.value * rb.value].view(self.nranks, seg.value, rb.value)
+        rv = self.ws[ro: ro + rcap.value * rb.value].view(rcap.value, rb.value)
+        return sb, rv
+
+    def dd_end_step(self, n_recv):
+        self._check(self.lib.mardyn_dd_end_step(self.h, int(n_recv)))
 
     def _n(self):
         n = C.c_int64()
@@ -332,6 +369,141 @@ def kd_decompose(cost, p):
     if rc:
         raise MardynError(rc, "kd_decompose: 2-cell constraint cannot be met")
     return boxes.reshape(p, 2, 3), loads
+
+
+def system_ndof(system):
+    """3 N + rotational degrees of freedom (nonzero principal moments), A9."""
+    rot = np.array([sum(1 for x in c["inertia"] if x > 0) for c in system["components"]])
+    return float(3 * len(system["r"]) + rot[np.asarray(system["comp"])].sum())
+
+
+def global_costs(system):
+    """Eq. 6 per cell of the global grid (x fastest) for the k-d tree, from
+    the molecule counts per cell of edge >= rc (every rank computes the same)."""
+    box = np.asarray(system["box"], float)
+    n = np.floor(box / system["rc"]).astype(int)
+    c = np.minimum((np.asarray(system["r"]) % box / box * n).astype(int), n - 1)
+    counts = np.zeros((n[2], n[1], n[0]), np.int32)
+    np.add.at(counts, (c[:, 2], c[:, 1], c[:, 0]), 1)
+    return cell_cost(counts)
+
+
+def exchange_records(send, cnt, recv, nranks, dist):
+    """Halo/migration transport between ranks:
+    send[d, :cnt[d]] goes to rank d; records from all ranks land contiguously
+    in recv in source-rank order.  Counts travel first (all_to_all_single),
+    then the records as grouped point-to-point send/recv (NCCL over NVLink on
+    GPUs, gloo on CPU).  Returns the number of records received."""
+    import torch
+    dev = send.device
+    sc = torch.tensor([int(x) for x in cnt], dtype=torch.int64, device=dev)
+    rc = torch.empty_like(sc)
+    dist.all_to_all_single(rc, sc)
+    rcounts = rc.cpu().tolist()
+    outs, off = [], 0
+    for k in rcounts:
+        outs.append(recv[off: off + k])
+        off += k
+    me = dist.get_rank()
+    ops = []
+    for d in range(nranks):
+        if d == me:
+            if int(cnt[d]):
+                outs[d].copy_(send[d, : int(cnt[d])])
+            continue
+        if int(cnt[d]):
+            ops.append(dist.P2POp(dist.isend, send[d, : int(cnt[d])].contiguous(), d))
+        if rcounts[d]:
+            ops.append(dist.P2POp(dist.irecv, outs[d], d))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    return off
+
+
+class DecomposedRun:
+    """p spatial subdomains (k-d tree, §4) stepping together.
+
+    transport = "loopback": all ranks' contexts live in this process on one
+    device and records move by device copies (correctness path, 1 GPU).
+    transport = "nccl": one rank per process/GPU, records move with
+    torch.distributed all_to_all over NCCL (NVLink)."""
+
+    def __init__(self, system, nranks, transport="loopback", rank=None, eta=None, boxes=None, stream=None):
+        import torch
+        self.torch = torch
+        self.system = system
+        self.nranks = nranks
+        self.transport = transport
+        cost = global_costs(system)
+        if boxes is None:
+            boxes, loads = kd_decompose(cost, nranks)
+        self.boxes = np.asarray(boxes).reshape(nranks, 2, 3)
+        flat = np.concatenate([self.boxes[:, 0, :], self.boxes[:, 1, :]], axis=1)
+        ndof = system_ndof(system)
+        ranks = range(nranks) if transport == "loopback" else [rank]
+        self.ctxs = []
+        for r in ranks:
+            ctx = Context(system["box"], system["rc"], system["components"], system["dt"],
+                          eps_rf=system.get("eps_rf", math.inf), lj_shift=system.get("lj_shift", 1), eta=eta,
+                          stream=stream)
+            ctx.set_decomposition(r, nranks, flat, ndof)
+            ctx.reserve(2 * len(system["r"]))        # owned + halo + received records
+            ctx.set_molecules(system["r"], system["v"], comp=system["comp"], q=system["q"], j=system["j"],
+                              id=system["id"], half_step=0)
+            self.ctxs.append(ctx)
+        self.bufs = [c.dd_buffers() for c in self.ctxs]
+
+    def step(self, n=1):
+        for _ in range(n):
+            counts = [c.dd_begin_step() for c in self.ctxs]
+            if self.transport == "loopback":
+                for dst, cd in enumerate(self.ctxs):
+                    recv = self.bufs[dst][1]
+                    off = 0
+                    for src in range(self.nranks):
+                        k = int(counts[src][dst])
+                        if k:
+                            recv[off: off + k].copy_(self.bufs[src][0][dst, :k])
+                            off += k
+                    cd.dd_end_step(off)
+            else:
+                self._nccl_exchange(counts[0])
+
+    def _nccl_exchange(self, cnt):
+        import torch.distributed as dist
+        ctx = self.ctxs[0]
+        send, recv = self.bufs[0]
+        n = exchange_records(send, cnt, recv, self.nranks, dist)
+        ctx.dd_end_step(n)
+
+    def observables(self):
+        keys = ("U_pot", "virial", "T", "E_kin_trans", "E_kin_rot", "n_pairs", "n_candidates")
+        if self.transport == "loopback":
+            parts = [c.get_observables() for c in self.ctxs]
+        else:
+            import torch.distributed as dist
+            parts = [None] * self.nranks
+            dist.all_gather_object(parts, self.ctxs[0].get_observables())
+        out = dict(parts[0])
+        for k in keys:
+            out[k] = sum(p[k] for p in parts)        # rank order: deterministic
+        out["n_pairs"] //= 2                         # ranks report ordered pairs of owned molecules
+        return out
+
+    def molecules(self):
+        """Owned molecules of the local ranks, merged and ordered by id."""
+        parts = [c.get_molecules() for c in self.ctxs]
+        ids = np.concatenate([p["id"] for p in parts])
+        order = np.argsort(ids)
+        return {k: np.concatenate([p[k] for p in parts])[order] for k in parts[0]}
+
+    def forces(self):
+        parts = [c.get_forces(with_ids=True) for c in self.ctxs]
+        ids = np.concatenate([p[2] for p in parts])
+        order = np.argsort(ids)
+        return (np.concatenate([p[0] for p in parts])[order], np.concatenate([p[1] for p in parts])[order],
+                ids[order])
 
 
 # module-level aliases with the C names

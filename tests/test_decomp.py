@@ -158,3 +158,41 @@ def test_gloo_two_ranks_agree():
     assert g0[0] == g0[1] == g1[0] == g1[1]          # every rank builds the same tree
     assert n0 == n1 == len(S.config("c4s")["r"])
     assert imb0 == imb1 and imb0 < 1.2
+
+
+def _xchg_main(rank, world, port, result):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rec = 64
+    seg = 8
+    send = torch.zeros((world, seg, rec), dtype=torch.uint8)
+    cnt = [(rank + d) % 3 + 1 for d in range(world)]          # records for rank d
+    for d in range(world):
+        for k in range(cnt[d]):
+            send[d, k, 0] = rank
+            send[d, k, 1] = d
+            send[d, k, 2] = k
+    recv = torch.zeros((world * seg, rec), dtype=torch.uint8)
+    n = M.exchange_records(send, cnt, recv, world, dist)
+    result[rank] = (n, recv[:n, :3].tolist())
+    dist.destroy_process_group()
+
+
+def test_gloo_exchange_records():
+    """The multi-rank record transport (counts, then records in source-rank
+    order) on world_size 2 with gloo."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_xchg_main, args=(2, port, result), nprocs=2, join=True)
+    for dst in range(2):
+        n, rows = result[dst]
+        expect = [[src, dst, k] for src in range(2) for k in range((src + dst) % 3 + 1)]
+        assert n == len(expect) and rows == expect
