@@ -27,7 +27,7 @@
  *  - One context per host thread; calls are not reentrant.
  *
  * Positions (reading A12).  Positions are stored as unsigned fixed point
- * u_k in [0, P_k) with one quantum s = 2^(ceil(log2(max cell edge)) - 23)
+ * u_k in [0, P_k) with one quantum s = 2^(ceil(log2(max cell edge)) - 22)
  * common to all axes; each cell edge is E_k quanta, P_k = n_k E_k, and the
  * box is snapped to P_k s (a relative change below 1e-6; mardyn_get_grid
  * returns it).  Cell assignment cell_k = floor(u_k / E_k) is exact integer

@@ -76,12 +76,12 @@ int or_setup(or_sys* S)
         S->nc[k] = (int32_t)floor(S->L[k] / S->rc);   /* edge = L/n >= rc */
         if (S->nc[k] < 2) return -1;
     }
-    /* quantum s = 2^(ceil(log2(max edge)) - 23): a cell edge is <= 2^23 quanta */
+    /* quantum s = 2^(ceil(log2(max edge)) - 22): a cell edge is <= 2^22 quanta   */
     for (int it = 0; it < 4; ++it) {
         double emax = 0;
         for (int k = 0; k < 3; ++k) emax = fmax(emax, S->L[k] / S->nc[k]);
         int ex = (int)ceil(log2(emax));
-        S->s = ldexp(1.0, ex - 23);
+        S->s = ldexp(1.0, ex - 22);
         int again = 0;
         for (int k = 0; k < 3; ++k) {
             S->E[k] = llround(S->L[k] / (S->nc[k] * S->s));

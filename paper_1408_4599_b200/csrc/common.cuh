@@ -8,8 +8,8 @@
 //   vel   float4 (v_x, v_y, v_z, comp bits)  v(t - dt/2)
 //   quat  float4 (w, x, y, z)                rigid only
 //   angm  float4 (j_x, j_y, j_z, 0)          world frame, j(t - dt/2), rigid
-//   xs    float4 (x, y, z cell-relative, comp bits)  staging copy read by the
-//                force kernels; exact multiples of s below 2^23 s
+//   xs    float4 (x, y, z cell-relative, comp bits | cell x index)  staging copy read by the
+//                force kernels; exact multiples of s below 2^24 s
 //   site  float4 [n_slots][cap]              world-frame site offsets / axes
 //   force float4 (F, 0), torque float4 (tau, 0)
 #pragma once
@@ -53,7 +53,7 @@ struct DevModel {
 struct GridP {
     int nc[3];
     int ncell;
-    uint32_t E[3];               // cell edge in quanta (<= 2^23)
+    uint32_t E[3];               // cell edge in quanta (<= 2^22)
     uint32_t P[3];               // period in quanta (P may be 2^32 - wrap with 64-bit)
     uint64_t P64[3];
     float s, inv_s;              // quantum, 1/s (powers of two)
@@ -149,3 +149,22 @@ __device__ __forceinline__ float3 qrotT(float4 q, float3 v)
     r.z = 2.f * (x * z + w * y) * v.x + 2.f * (y * z - w * x) * v.y + (1.f - 2.f * (x * x + y * y)) * v.z;
     return r;
 }
+
+// ---- helpers shared by the force kernels
+__device__ __forceinline__ float rcp_approx(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// exact cutoff decision in quanta for separations in the guard band
+__device__ __forceinline__ bool exact_in_range(float dx, float dy, float dz, const GridP& g)
+{
+    long long kx = __float2int_rn(dx * g.inv_s);
+    long long ky = __float2int_rn(dy * g.inv_s);
+    long long kz = __float2int_rn(dz * g.inv_s);
+    return kx * kx + ky * ky + kz * kz < g.cut2_q;
+}
+
+__device__ __forceinline__ int wrapi(int c, int n) { return c < 0 ? c + n : (c >= n ? c - n : c); }

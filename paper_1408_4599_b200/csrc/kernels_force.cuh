@@ -37,24 +37,6 @@ struct ForceArgs {
     float sig2, eps24, eps4, shift;   // single-site LJ fast path
 };
 
-__device__ __forceinline__ float rcp_approx(float x)
-{
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-// exact cutoff decision in quanta for separations in the guard band
-__device__ __forceinline__ bool exact_in_range(float dx, float dy, float dz, const GridP& g)
-{
-    long long kx = __float2int_rn(dx * g.inv_s);
-    long long ky = __float2int_rn(dy * g.inv_s);
-    long long kz = __float2int_rn(dz * g.inv_s);
-    return kx * kx + ky * ky + kz * kz < g.cut2_q;
-}
-
-__device__ __forceinline__ int wrapi(int c, int n) { return c < 0 ? c + n : (c >= n ? c - n : c); }
-
 // Row descriptor of the 27-cell neighbourhood: the 3 cells (dx = -1, 0, 1)
 // of row (dy, dz).  Lanes 0..2 fetch start/count, broadcast by shuffles.
 struct Row {
@@ -91,194 +73,7 @@ __device__ __forceinline__ int row_src(const Row& r, int kk, float edge, float& 
     return r.st2 + kk - r.n0 - r.n1;
 }
 
-// =========================================================================
-// Single LJ site at the COM (configs 0, 1, 4): one thread per site.
-//
-// Candidate pruning by x-windows.  Cells are sorted
-// canonically by (x, id) (k_canon), so each of the 9 neighbour rows -- three
-// x-adjacent cells -- staged with its cell offsets is a list sorted by x.
-// For home molecule i and row (dy, dz) only candidates with
-// |X - x_i| < w = sqrt(rc^2 - Dy^2 - Dz^2) can be within rc, Dy, Dz being
-// the distances from y_i, z_i to the row's slab; that window is found by a
-// binary search and scanned until X passes x_i + w.  This keeps ~42 % of the
-// 27-cell candidates (c1) and the results unchanged: every pair inside rc is
-// still visited.  Inside the window the LJ force is evaluated branch-free
-// (masked by the exact cutoff test), because ~37 % of the window candidates
-// hit and a divergent branch would cost as much.
-// Lanes are (i-slot, phase) pairs; phase p scans window elements p, p+P, ...
-// Separations are exact fp32 multiples of s (A12); hits whose r^2 falls in
-// the +-2^-20 band around rc^2 are re-decided exactly in integer quanta by a
-// rare slow pass.
-// =========================================================================
-template <int WARPS, int CAP>
-struct LJ1Cfg {
-    static constexpr int SMEM_PER_WARP = CAP * 16 + 32 * 4;      // slab + piece offsets/rows
-    static constexpr int SMEM = WARPS * SMEM_PER_WARP;
-};
-
-// lower bound of v in buf[lo, hi) by x
-__device__ __forceinline__ int lj1_lower(const float4* __restrict__ buf, int lo, int hi, const float v)
-{
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (buf[mid].x < v) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
-// one row window.  Fast pass (EXACT = false): pairs with 0 < r^2 < lo are
-// hits, pairs in the guard band lo <= r^2 < hi are only counted.  Slow pass
-// (EXACT = true, rare): only band pairs, decided in integer quanta (A12).
-template <bool EXACT>
-__device__ __forceinline__ void lj1_row(const float4* __restrict__ buf, const int rs, const int re,
-                                        const float4 xi, const float w, const int phase, const int P,
-                                        const GridP& g, const float sig2, const float eps24, const float hi,
-                                        const float lo, float& fx, float& fy, float& fz, float& uacc,
-                                        float& wacc, int& hits, int& band)
-{
-    const float xhi = xi.x + w;
-    const unsigned lob = __float_as_uint(lo) - 1u;
-    for (int j = lj1_lower(buf, rs, re, xi.x - w) + phase; j < re; j += P) {
-        const float4 X = buf[j];
-        if (!(X.x < xhi)) break;
-        const float dx = X.x - xi.x, dy = X.y - xi.y, dz = X.z - xi.z;
-        const float r2 = dx * dx + dy * dy + dz * dz;
-        bool hit;
-        if (EXACT) {
-            hit = (r2 >= lo) && (r2 < hi) && exact_in_range(dx, dy, dz, g);
-        } else {
-            hit = (__float_as_uint(r2) - 1u) < lob;          // 0 < r2 < lo (excludes the self pair)
-            band += ((r2 >= lo) & (r2 < hi)) ? 1 : 0;
-        }
-        const float ir2 = hit ? rcp_approx(r2) : 0.f;
-        const float s2 = sig2 * ir2;
-        const float s6 = s2 * s2 * s2;
-        const float fr = eps24 * ir2 * s6 * (2.f * s6 - 1.f);
-        fx -= fr * dx; fy -= fr * dy; fz -= fr * dz;
-        uacc += s6 * (s6 - 1.f);
-        wacc += fr * r2;
-        hits += hit ? 1 : 0;
-    }
-}
-
-// all staged pieces (x-sorted row segments) for this lane's molecule:
-// piece k = buf[poff[k], poff[k+1]) of row prow[k]
-template <bool EXACT>
-__device__ __forceinline__ void lj1_rows(const float4* __restrict__ buf, const int* __restrict__ poff,
-                                         const int* __restrict__ prow, const int np, const float4 xi,
-                                         const int phase, const int P, const GridP& g, const float sig2,
-                                         const float eps24, const float hi, const float lo, float& fx, float& fy,
-                                         float& fz, float& uacc, float& wacc, int& hits, int& band)
-{
-    const float rc2w = hi * (1.f + 1.f / 4096.f);           // generous window (necessary condition only)
-    for (int k = 0; k < np; ++k) {
-        const int r = prow[k];
-        const int dy = r % 3 - 1, dz = r / 3 - 1;
-        const float Dy = dy == 0 ? 0.f : (dy > 0 ? g.edge[1] - xi.y : xi.y);
-        const float Dz = dz == 0 ? 0.f : (dz > 0 ? g.edge[2] - xi.z : xi.z);
-        const float w2 = rc2w - Dy * Dy - Dz * Dz;
-        if (w2 <= 0.f) continue;
-        lj1_row<EXACT>(buf, poff[k], poff[k + 1], xi, sqrtf(w2), phase, P, g, sig2, eps24, hi, lo, fx, fy, fz,
-                       uacc, wacc, hits, band);
-    }
-}
-
-template <int WARPS, int CAP>
-__global__ void __launch_bounds__(WARPS * 32) k_force_lj1(ForceArgs a)
-{
-    using CFG = LJ1Cfg<WARPS, CAP>;
-    extern __shared__ float4 smem_lj1[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    char* wbase = reinterpret_cast<char*>(smem_lj1) + wib * CFG::SMEM_PER_WARP;
-    float4* buf = reinterpret_cast<float4*>(wbase);
-    int* poff = reinterpret_cast<int*>(wbase + CAP * 16);       // <= 16 pieces per slab
-    int* prow = poff + 16;
-    const GridP& g = a.g;
-    const int gw = blockIdx.x * WARPS + wib, nw = gridDim.x * WARPS;
-    double Uw = 0.0, Ww = 0.0;
-    long long npw = 0, ncw = 0;
-    const float sig2 = a.sig2, eps24 = a.eps24;
-    const float lo = g.cut2_lo, hi = g.cut2_hi;
-
-    for (int t = gw; t < g.nhome; t += nw) {
-        int cx, cy, cz;
-        const int c = home_cell(g, t, cx, cy, cz);
-        const int s_i = __ldg(a.start + c);
-        const int n_all = __ldg(a.start + c + 1) - s_i;
-        if (n_all == 0) continue;
-        for (int i0 = 0; i0 < n_all; i0 += 32) {
-            const int ni = min(32, n_all - i0);
-            const int P = 32 / ni;
-            const int islot = lane % ni;
-            const bool active = lane / ni < P;
-            const int phase = active ? lane / ni : 0;
-            const int my = s_i + i0 + islot;
-            float4 xi = a.xs[my];
-            if (!active) xi.x = 1e30f;                  // idle lanes: empty windows
-            float fx = 0.f, fy = 0.f, fz = 0.f, uacc = 0.f, wacc = 0.f;
-            int hits = 0, band = 0, mtot = 0;
-            // stage the 9 rows into the slab as pieces (a row that does not fit
-            // is split: its pieces stay x-sorted); process each full slab
-            int row = 0, k0 = 0;
-            while (row < 9) {
-                int m = 0, np = 0;
-                __syncwarp();
-                while (row < 9 && m < CAP) {
-                    const int dy = row % 3 - 1, dz = row / 3 - 1;
-                    const Row r = load_row(a.start, g, cx, cy, cz, dy, dz);
-                    const int tot = r.n0 + r.n1 + r.n2;
-                    const int take = min(tot - k0, CAP - m);
-                    const float offy = dy * g.edge[1], offz = dz * g.edge[2];
-                    for (int k = lane; k < take; k += 32) {
-                        float offx;
-                        const int src = row_src(r, k0 + k, g.edge[0], offx);
-                        const float4 x = __ldg(a.xs + src);
-                        buf[m + k] = make_float4(x.x + offx, x.y + offy, x.z + offz, 0.f);
-                    }
-                    if (lane == 0) { prow[np] = row; poff[np] = m; }
-                    m += take;
-                    ++np;
-                    if (k0 + take == tot) { mtot += tot; ++row; k0 = 0; }
-                    else k0 += take;
-                }
-                if (lane == 0) poff[np] = m;
-                __syncwarp();
-                band = 0;
-                lj1_rows<false>(buf, poff, prow, np, xi, phase, P, g, sig2, eps24, hi, lo, fx, fy, fz, uacc, wacc,
-                                hits, band);
-                if (band) {   // rare: add the guard-band pairs the exact test keeps
-                    int dummy = 0;
-                    lj1_rows<true>(buf, poff, prow, np, xi, phase, P, g, sig2, eps24, hi, lo, fx, fy, fz, uacc,
-                                   wacc, hits, dummy);
-                }
-            }
-            float sx = fx, sy = fy, sz = fz;
-            for (int p = 1; p < P; ++p) {
-                const int srcl = (lane + p * ni) & 31;
-                sx += __shfl_sync(0xffffffffu, fx, srcl);
-                sy += __shfl_sync(0xffffffffu, fy, srcl);
-                sz += __shfl_sync(0xffffffffu, fz, srcl);
-            }
-            if (active && phase == 0) a.force[my] = make_float4(sx, sy, sz, 0.f);
-            Uw += (double)(a.eps4 * uacc) - (double)a.shift * hits;
-            Ww += (double)wacc;
-            npw += hits;
-            if (lane == 0) ncw += (long long)ni * (mtot - 1);
-        }
-    }
-    Uw = warp_sum_d(Uw);
-    Ww = warp_sum_d(Ww);
-    npw = warp_sum_ll(npw);
-    if (lane == 0) {
-        ForcePartial p;
-        p.U = 0.5 * Uw;
-        p.W = 0.5 * Ww;
-        p.npairs = npw;
-        p.ncand = ncw;
-        a.part[gw] = p;
-    }
-}
+// The single-site LJ kernel (configs 0, 1, 4) is in kernels_lj1.cuh.
 
 // =========================================================================
 // Rigid multi-centre molecules (configs 2, 3; mixtures and dipoles through

@@ -1,0 +1,514 @@
+// kernels_lj1.cuh -- single-site Lennard-Jones force kernel (configs 0, 1, 4):
+// the hot loop of the method ("the largest part of the computational cost is
+// caused by the force and distance calculations"; linked
+// cells of edge >= rc; LJTS P:76).
+//
+// Work decomposition.  The sorted state is cut into blocks of
+// 32 consecutive molecules; a warp takes a block, one lane per home molecule
+// (the north_star's thread per site), and splits it into "sub-chunks": runs
+// of lanes in one x-row of cells spanning at most KMAX cells.  For a
+// sub-chunk the warp stages the 9 neighbour rows (cells cA-1 .. cB+1 of the
+// rows dy, dz in {-1, 0, 1}) into shared memory, relative to a common origin
+// at the sub-chunk's middle cell.  With the quantum of reading A12 every
+// staged coordinate is an exact fp32 multiple of s (|x| < 4 cell edges), so
+// every separation is exact.  Rows are sorted by x (canonical in-cell order
+// (x, id), A13, and cells in x order), so for row (dy, dz) a molecule only
+// needs the x-window |X - x_i| < sqrt(rc^2 - Dy^2 - Dz^2); the window is found
+// by binary search and all windows of a lane are concatenated into one
+// segment list, so that each lane iterates over exactly its own candidates
+// and the warp does not diverge on window lengths.  Candidates are processed
+// two at a time with the packed fp32x2 instructions of sm_100 (FADD2 /
+// FMUL2 / FFMA2), which halves the issue slots of the arithmetic; the LJ
+// force is evaluated branch-free (masked by the cutoff test).
+//
+// Cutoff (readings A1, A12): strict r < rc on the COM separation; fp32 r^2
+// outside the +-2^-20 relative band around rc^2 decides; a pair in the band is
+// re-decided exactly in integer quanta by a rare second pass.
+// Blocks that would need more than two sub-chunks (sparse gas) take a
+// per-lane path that walks the molecule's own 27 cells.
+#pragma once
+#include "common.cuh"
+
+namespace lj1 {
+
+constexpr int KMAX = 6;          // home cells per sub-chunk: staged |x| < 4 E (A12 quantum)
+constexpr int NSEG = 11;         // per-lane segments: 9 rows + self split + sentinel
+constexpr float FAR = 1.0e18f;   // padding coordinate (r^2 ~ 1e36, finite, never a hit)
+
+struct Args {
+    GridP g;
+    const int* start;            // ncell + 1
+    const uint4* pos;            // sorted fixed-point positions
+    const float4* xs;            // cell-relative staging copy, w = cell x index (k_canon<false>)
+    float4* force;
+    ForcePartial* part;          // one per warp of the grid (n_candidates)
+    ForcePartial* bpart;         // one per block of 32 sorted molecules (U, W, n_pairs), nbcap entries
+    int nbcap;
+    int* ctr;                    // block counter (zeroed before the launch): dynamic block scheduling
+    float sig2, eps24, eps4, shift;
+};
+
+// origin (in quanta, mod 2^32) to subtract from the stored u of a molecule
+// in the cell at unwrapped index cu (0 <= cu + 1, cu - 1 < n) so that the
+// result is its coordinate relative to `base` in the image next to base
+__device__ __forceinline__ uint32_t img_origin(uint32_t base, int cu, int n, uint32_t P)
+{
+    return base + (cu < 0 ? P : 0u) - (cu >= n ? P : 0u);
+}
+
+// fixed-point difference (u - o) mod 2^32 as an exact float multiple of s
+__device__ __forceinline__ float qdiff(uint32_t u, uint32_t o, float s)
+{
+    return __int2float_rn((int)(u - o)) * s;
+}
+
+template <int WARPS, int CAPP>
+struct Cfg {
+    // per warp: pair arrays xy[CAPP] (x0, x1, y0, y1), z[CAPP] (z0, z1),
+    // segments seg[NSEG][32] (pair begin, pair end), row table
+    static constexpr int BYTES_PER_WARP = CAPP * 24 + NSEG * 32 * 8 + 64 * 4;
+    static constexpr int SMEM = WARPS * BYTES_PER_WARP;
+};
+
+struct Acc {
+    float2 gx, gy, gz;           // sum ir2 s6 (s6 - 1/2) d   (force = -48 eps g)
+    float2 a, b, h;              // sum s6^2, sum s6, sum ir2 r2 (= hit count)
+    int hits_exact;              // hits found by the exact band pass / scalar paths
+    int band;                    // a pair fell into the guard band
+};
+
+__device__ __forceinline__ void acc_zero(Acc& A)
+{
+    A.gx = A.gy = A.gz = A.a = A.b = A.h = make_float2(0.f, 0.f);
+    A.hits_exact = 0;
+    A.band = 0;
+}
+
+// one candidate pair (j, j+1) against molecule (xi, yi, zi), fast pass
+__device__ __forceinline__ void pair2(const float4 xy, const float2 z, const float2 nxi, const float2 nyi,
+                                      const float2 nzi, const float2 sig2, const float lo, const float hi,
+                                      Acc& A)
+{
+    const float2 dx = __fadd2_rn(make_float2(xy.x, xy.y), nxi);
+    const float2 dy = __fadd2_rn(make_float2(xy.z, xy.w), nyi);
+    const float2 dz = __fadd2_rn(z, nzi);
+    float2 r2 = __fmul2_rn(dx, dx);
+    r2 = __ffma2_rn(dy, dy, r2);
+    r2 = __ffma2_rn(dz, dz, r2);
+    const bool h0 = r2.x < lo, h1 = r2.y < lo;
+    A.band |= (int)(((r2.x < hi) & !h0) | ((r2.y < hi) & !h1));
+    float2 ir2;
+    ir2.x = h0 ? rcp_approx(r2.x) : 0.f;
+    ir2.y = h1 ? rcp_approx(r2.y) : 0.f;
+    const float2 s2 = __fmul2_rn(ir2, sig2);
+    const float2 s4 = __fmul2_rn(s2, s2);
+    const float2 s6 = __fmul2_rn(s4, s2);
+    const float2 t = __fadd2_rn(s6, make_float2(-0.5f, -0.5f));
+    const float2 fr = __fmul2_rn(__fmul2_rn(s6, ir2), t);
+    A.gx = __ffma2_rn(fr, dx, A.gx);
+    A.gy = __ffma2_rn(fr, dy, A.gy);
+    A.gz = __ffma2_rn(fr, dz, A.gz);
+    A.a = __ffma2_rn(s6, s6, A.a);
+    A.b = __fadd2_rn(s6, A.b);
+    A.h = __ffma2_rn(ir2, r2, A.h);
+}
+
+// one element in the exact (guard-band) pass or the scalar paths: the same
+// fp32 r^2 as the fast pass; BAND_ONLY: only band pairs, decided exactly
+template <bool BAND_ONLY>
+__device__ __forceinline__ void elem1(float X, float Y, float Z, float xi, float yi, float zi, float sig2,
+                                      float lo, float hi, const GridP& g, Acc& A)
+{
+    const float dx = __fadd_rn(X, -xi), dy = __fadd_rn(Y, -yi), dz = __fadd_rn(Z, -zi);
+    const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));   // = the packed path's r^2
+    bool hit;
+    if (BAND_ONLY) {
+        hit = (r2 >= lo) && (r2 < hi) && exact_in_range(dx, dy, dz, g);
+    } else {
+        const bool inband = (r2 >= lo) && (r2 < hi);
+        hit = (r2 < lo) || (inband && exact_in_range(dx, dy, dz, g));
+    }
+    if (!hit) return;
+    const float ir2 = rcp_approx(r2);
+    const float s2 = ir2 * sig2;
+    const float s6 = s2 * s2 * s2;
+    const float fr = s6 * ir2 * (s6 - 0.5f);
+    A.gx.x += fr * dx;
+    A.gy.x += fr * dy;
+    A.gz.x += fr * dz;
+    A.a.x += s6 * s6;
+    A.b.x += s6;
+    A.hits_exact += 1;
+}
+
+// lower bound: first pair p in [rb, re) with X[2p + ODD] (>= if !STRICT, > if
+// STRICT) v, starting from the guess g (rows are x-sorted; the guess from the
+// row's mean pitch is within a pair or two in a liquid)
+template <int ODD, bool STRICT>
+__device__ __forceinline__ int find_from(const float* __restrict__ sxf, int rb, int re, int g, float v)
+{
+    auto below = [&](int p) { const float x = sxf[4 * p + ODD]; return STRICT ? (x <= v) : (x < v); };
+    if (g < re && below(g)) {
+        do { ++g; } while (g < re && below(g));
+    } else {
+        while (g > rb && !below(g - 1)) --g;
+    }
+    return g;
+}
+
+template <int WARPS, int CAPP, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
+{
+    using C = Cfg<WARPS, CAPP>;
+    extern __shared__ float4 smem_lj1[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    char* wbase = reinterpret_cast<char*>(smem_lj1) + wib * C::BYTES_PER_WARP;
+    float4* sxy = reinterpret_cast<float4*>(wbase);
+    float2* sz = reinterpret_cast<float2*>(wbase + CAPP * 16);
+    int2* sseg = reinterpret_cast<int2*>(wbase + CAPP * 24);
+    int* srow = reinterpret_cast<int*>(wbase + CAPP * 24 + NSEG * 32 * 8);   // [0..9] row pair bases
+    uint16_t* scb = reinterpret_cast<uint16_t*>(srow + 12);                  // [9][10] staged-cell element offsets
+    float* sxf = reinterpret_cast<float*>(sxy);
+    float* szf = reinterpret_cast<float*>(sz);
+
+    const GridP& g = a.g;
+    const int gw = blockIdx.x * WARPS + wib, nw = gridDim.x * WARPS;
+    const int nx = g.nc[0], ny = g.nc[1], nz = g.nc[2];
+    const int kmax = min(KMAX, nx - 2);
+    const float lo = g.cut2_lo, hi = g.cut2_hi;
+    const float2 sig2 = make_float2(a.sig2, a.sig2);
+    const float rc2w = hi * (1.f + 1.f / 4096.f);       // generous window (necessary condition only)
+    const float ex = g.edge[0], inv_ex = 1.f / g.edge[0];
+    long long ncw = 0;
+
+    // ---- n_candidates (27-cell full-shell count, reported observable):
+    //      sum over home cells of N_c (sum_27 N_c' - 1), lane-parallel over cells
+    for (int t = gw * 32 + lane; t < g.nhome; t += nw * 32) {
+        int cx, cy, cz;
+        const int c = home_cell(g, t, cx, cy, cz);
+        const int nc = __ldg(a.start + c + 1) - __ldg(a.start + c);
+        if (nc == 0) continue;
+        int tot = 0;
+        for (int dz = -1; dz <= 1; ++dz)
+            for (int dy = -1; dy <= 1; ++dy) {
+                const int rowc = nx * (wrapi(cy + dy, ny) + ny * wrapi(cz + dz, nz));
+                if (cx >= 1 && cx + 1 < nx) {
+                    tot += __ldg(a.start + rowc + cx + 2) - __ldg(a.start + rowc + cx - 1);
+                } else {
+                    for (int dx = -1; dx <= 1; ++dx) {
+                        const int c2 = rowc + wrapi(cx + dx, nx);
+                        tot += __ldg(a.start + c2 + 1) - __ldg(a.start + c2);
+                    }
+                }
+            }
+        ncw += (long long)nc * (tot - 1);
+    }
+
+    const int nsorted = __ldg(a.start + g.ncell);
+    const int nblocks = (nsorted + 31) >> 5;
+    for (int b = nblocks + gw * 32 + lane; b < a.nbcap; b += nw * 32)     // unused block partials
+        a.bpart[b] = ForcePartial{0.0, 0.0, 0, 0};
+    // blocks are handed out in sorted order by an atomic counter (load balance);
+    // each block's sums go to its own slot, so totals do not depend on the schedule
+    for (;;) {
+        int blk = 0;
+        if (lane == 0) blk = atomicAdd(a.ctr, 1);
+        blk = __shfl_sync(0xffffffffu, blk, 0);
+        if (blk >= nblocks) break;
+        double Uw = 0.0, Ww = 0.0;
+        long long npw = 0;
+        const int mi = blk * 32 + lane;
+        bool valid = mi < nsorted;
+        uint4 pi = valid ? a.pos[mi] : make_uint4(0, 0, 0, 0);
+        const int cx = (int)(pi.x / g.E[0]), cy = (int)(pi.y / g.E[1]), cz = (int)(pi.z / g.E[2]);
+        const bool home = valid && cx >= g.hlo[0] && cx < g.hlo[0] + g.hdim[0] && cy >= g.hlo[1] &&
+                          cy < g.hlo[1] + g.hdim[1] && cz >= g.hlo[2] && cz < g.hlo[2] + g.hdim[2];
+        const int row = cy + ny * cz;
+        unsigned todo = __ballot_sync(0xffffffffu, home);
+        int passes = 0, klim = kmax;
+        while (todo) {
+            const int leader = __ffs(todo) - 1;
+            const int R = __shfl_sync(0xffffffffu, row, leader);
+            const int cA = __shfl_sync(0xffffffffu, cx, leader);
+            const bool mine = ((todo >> lane) & 1u) && row == R && cx < cA + klim;
+            const unsigned members = __ballot_sync(0xffffffffu, mine);
+            const int cB = __shfl_sync(0xffffffffu, cx, 31 - __clz(members));
+            const int hy = __shfl_sync(0xffffffffu, cy, leader), hz = __shfl_sync(0xffffffffu, cz, leader);
+            // ---------------- staging plan: lanes 0..8 own one neighbour row each
+            int p_a0 = 0, p_n1 = 0, p_b0 = 0, p_n2 = 0, p_c0 = 0, p_n3 = 0, plen = 0;
+            const int cm = (cA + cB + 1) >> 1;           // origin cell (x); y, z: the home row's corner
+            if (lane < 9) {
+                const int dy = lane % 3 - 1, dz = lane / 3 - 1;
+                const int rowc = nx * (wrapi(hy + dy, ny) + ny * wrapi(hz + dz, nz));
+                const int mlo = max(cA - 1, 0), mhi = min(cB + 1, nx - 1);
+                p_b0 = __ldg(a.start + rowc + mlo);
+                p_n2 = __ldg(a.start + rowc + mhi + 1) - p_b0;
+                if (cA == 0) { p_a0 = __ldg(a.start + rowc + nx - 1); p_n1 = __ldg(a.start + rowc + nx) - p_a0; }
+                if (cB == nx - 1) { p_c0 = __ldg(a.start + rowc); p_n3 = __ldg(a.start + rowc + 1) - p_c0; }
+                plen = (p_n1 + p_n2 + p_n3 + 1) >> 1;        // real pairs; the row adds a far pad pair at each end
+                // element offset of staged cell k (x-index cA - 1 + k) in the row: the window search
+                // only looks inside the cell that holds the bound
+#pragma unroll
+                for (int k = 0; k <= KMAX + 2; ++k) {
+                    const int cu = cA - 1 + k;
+                    if (k <= cB - cA + 3) {
+                        int off;
+                        if (cu < 0) off = 0;
+                        else if (cu >= nx) off = p_n1 + p_n2;
+                        else if (cu > mhi) off = p_n1 + p_n2;
+                        else off = p_n1 + __ldg(a.start + rowc + cu) - p_b0;
+                        if (k == cB - cA + 3) off = p_n1 + p_n2 + p_n3;
+                        scb[10 * lane + k] = (uint16_t)off;
+                    }
+                }
+            }
+            // scan of the row strides (plen + 2) over lanes 0..8 -> row pair bases
+            int incl = lane < 9 ? plen + 2 : 0;
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const int total = __shfl_sync(0xffffffffu, incl, 8);
+            if (total + 2 > CAPP && cB > cA) {         // over capacity: fewer home cells
+                klim = (cB - cA + 1) >> 1;
+                continue;
+            }
+            if (total + 2 > CAPP || passes >= 2) {
+                // sparse or over-full: per-lane path for the remaining lanes
+                Acc A;
+                acc_zero(A);
+                if ((todo >> lane) & 1u) {
+                    const float xi = qdiff(pi.x, (uint32_t)cx * g.E[0], g.s);
+                    const float yi = qdiff(pi.y, (uint32_t)cy * g.E[1], g.s);
+                    const float zi = qdiff(pi.z, (uint32_t)cz * g.E[2], g.s);
+                    for (int dz = -1; dz <= 1; ++dz)
+                        for (int dy = -1; dy <= 1; ++dy) {
+                            const int ryu = cy + dy, rzu = cz + dz;
+                            const int rowc = nx * (wrapi(ryu, ny) + ny * wrapi(rzu, nz));
+                            const uint32_t oyy = img_origin((uint32_t)cy * g.E[1], ryu, ny, g.P[1]);
+                            const uint32_t ozz = img_origin((uint32_t)cz * g.E[2], rzu, nz, g.P[2]);
+                            for (int dx = -1; dx <= 1; ++dx) {
+                                const int cxu = cx + dx;
+                                const uint32_t oxx = img_origin((uint32_t)cx * g.E[0], cxu, nx, g.P[0]);
+                                const int c2 = rowc + wrapi(cxu, nx);
+                                const int j0 = __ldg(a.start + c2), j1 = __ldg(a.start + c2 + 1);
+                                for (int j = j0; j < j1; ++j) {
+                                    if (j == mi) continue;
+                                    const uint4 pj = a.pos[j];
+                                    elem1<false>(qdiff(pj.x, oxx, g.s), qdiff(pj.y, oyy, g.s), qdiff(pj.z, ozz, g.s),
+                                                 xi, yi, zi, a.sig2, lo, hi, g, A);
+                                }
+                            }
+                        }
+                    const float f = -2.f * a.eps24;
+                    a.force[mi] = make_float4(f * A.gx.x, f * A.gy.x, f * A.gz.x, 0.f);
+                    const double Ad = A.a.x, Bd = A.b.x;
+                    Uw += (double)a.eps4 * (Ad - Bd) - (double)a.shift * A.hits_exact;
+                    Ww += (double)a.eps24 * (2.0 * Ad - Bd);
+                    npw += A.hits_exact;
+                }
+                break;
+            }
+            const int rbase = incl - plen - 1;         // first real pair of the row (lanes 0..8)
+            const float xlo = (float)(cA - 1 - cm) * ex;          // staged x range [xlo, xlo + (cB-cA+3) ex)
+            if (lane < 10) srow[lane] = (lane < 9) ? rbase : total + 1;    // real end of row r = srow[r + 1] - 2
+            if (lane < 9) {
+                sxy[rbase - 1] = make_float4(FAR, FAR, FAR, FAR);
+                sz[rbase - 1] = make_float2(FAR, FAR);
+                sxy[rbase + plen] = make_float4(FAR, FAR, FAR, FAR);
+                sz[rbase + plen] = make_float2(FAR, FAR);
+            }
+            // ---------------- staging copy: 3 lanes per row (lanes 0..26), 4 loads in flight per lane;
+            //                  x = xs.x + (cx - cm') edge exactly (A12), y, z + the row's offsets
+            __syncwarp();
+            {
+                const int r3 = min(lane / 3, 8);
+                const int a0 = __shfl_sync(0xffffffffu, p_a0, r3), n1 = __shfl_sync(0xffffffffu, p_n1, r3);
+                const int b0 = __shfl_sync(0xffffffffu, p_b0, r3), n2 = __shfl_sync(0xffffffffu, p_n2, r3);
+                const int c0 = __shfl_sync(0xffffffffu, p_c0, r3), n3 = __shfl_sync(0xffffffffu, p_n3, r3);
+                const int base = __shfl_sync(0xffffffffu, rbase, r3), np = __shfl_sync(0xffffffffu, plen, r3);
+                if (lane < 27) {
+                    const float offy = (float)(r3 % 3 - 1) * g.edge[1], offz = (float)(r3 / 3 - 1) * g.edge[2];
+                    const int len = n1 + n2 + n3;
+                    // element e of the row -> xs index e + d(e), origin cell cm'(e) (branch-free)
+                    const int d1 = a0, d2 = b0 - n1, d3 = c0 - n1 - n2, n12 = n1 + n2;
+                    const float cm1 = (float)(cm + nx), cm2 = (float)cm, cm3 = (float)(cm - nx);
+                    auto fetch = [&](int e, float4& v, float& c) {
+                        const int ee = min(e, len - 1);          // len >= 1 whenever the row has a pair
+                        const int gi = ee + (ee < n1 ? d1 : (ee < n12 ? d2 : d3));
+                        c = ee < n1 ? cm1 : (ee < n12 ? cm2 : cm3);
+                        v = __ldg(a.xs + gi);
+                    };
+                    for (int q0 = lane - 3 * r3; q0 < np; q0 += 6) {   // pairs q0, q0 + 3 (4 loads in flight)
+                        float4 v[4];
+                        float c[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) fetch(2 * (q0 + 3 * (u >> 1)) + (u & 1), v[u], c[u]);
+#pragma unroll
+                        for (int k = 0; k < 2; ++k) {
+                            const int q = q0 + 3 * k;
+                            if (q < np) {
+                                float X[2], Y[2], Z[2];
+#pragma unroll
+                                for (int h = 0; h < 2; ++h) {
+                                    const bool real = 2 * q + h < len;
+                                    const float4 w = v[2 * k + h];
+                                    X[h] = real ? __fmaf_rn(w.w - c[2 * k + h], ex, w.x) : FAR;
+                                    Y[h] = real ? w.y + offy : FAR;
+                                    Z[h] = real ? w.z + offz : FAR;
+                                }
+                                sxy[base + q] = make_float4(X[0], X[1], Y[0], Y[1]);
+                                sz[base + q] = make_float2(Z[0], Z[1]);
+                            }
+                        }
+                    }
+                }
+            }
+            if (lane < 2) {                             // dummy pairs for exhausted lanes
+                sxy[total + lane] = make_float4(FAR, FAR, FAR, FAR);
+                sz[total + lane] = make_float2(FAR, FAR);
+            }
+            __syncwarp();
+            // ---------------- windows -> segment list
+            const int hb0 = __shfl_sync(0xffffffffu, p_b0, 4), hn1 = __shfl_sync(0xffffffffu, p_n1, 4);
+            const int hbase = __shfl_sync(0xffffffffu, rbase, 4);
+            const int eself = hn1 + (mi - hb0);          // own element in the staged home row
+            const int pself = hbase + (eself >> 1);
+            const bool act = (members >> lane) & 1u;
+            float xi = 0.f, yi = 0.f, zi = 0.f;
+            if (act) {
+                xi = sxf[4 * pself + (eself & 1)];
+                yi = sxf[4 * pself + 2 + (eself & 1)];
+                zi = szf[2 * pself + (eself & 1)];
+            }
+            int nseg = 0, ttot = 0;
+            if (act) {
+                const float Dyl = yi, Dyh = g.edge[1] - yi, Dzl = zi, Dzh = g.edge[2] - zi;
+#pragma unroll
+                for (int r = 0; r < 9; ++r) {
+                    const int dy = r % 3 - 1, dz = r / 3 - 1;
+                    const float Dy = dy == 0 ? 0.f : (dy > 0 ? Dyh : Dyl);
+                    const float Dz = dz == 0 ? 0.f : (dz > 0 ? Dzh : Dzl);
+                    const float w2 = rc2w - Dy * Dy - Dz * Dz;
+                    if (w2 > 0.f) {
+                        const float w = sqrtf(w2);
+                        const int rb = srow[r], re = srow[r + 1] - 2;
+                        // first pair whose odd element reaches xi - w; first pair whose even element passes xi + w
+                        const float xl = xi - w, xh = xi + w;
+                        // cells holding the bounds (x of staged cell k: [xlo + k ex, xlo + (k+1) ex), exact)
+                        const int nsc = cB - cA + 3;
+                        int kl = min(max((int)floorf((xl - xlo) * inv_ex), 0), nsc - 1);
+                        if (kl > 0 && xl < xlo + (float)kl * ex) --kl;
+                        if (kl < nsc - 1 && xl >= xlo + (float)(kl + 1) * ex) ++kl;
+                        int kh = min(max((int)floorf((xh - xlo) * inv_ex), 0), nsc - 1);
+                        if (kh > 0 && xh < xlo + (float)kh * ex) --kh;
+                        if (kh < nsc - 1 && xh >= xlo + (float)(kh + 1) * ex) ++kh;
+                        // lower: first pair whose odd element is >= xl, in [floor(off_kl/2), floor(off_kl+1/2)]
+                        int pa = rb + (scb[10 * r + kl] >> 1), n = rb + (scb[10 * r + kl + 1] >> 1) - pa;
+                        while (n > 0) {
+                            const int h = n >> 1;
+                            const bool lt = sxf[4 * (pa + h) + 1] < xl;
+                            pa = lt ? pa + h + 1 : pa;
+                            n = lt ? n - h - 1 : h;
+                        }
+                        // upper: first pair whose even element is > xh, in [ceil(off_kh/2), ceil(off_kh+1/2)]
+                        int pb = rb + ((scb[10 * r + kh] + 1) >> 1);
+                        n = rb + ((scb[10 * r + kh + 1] + 1) >> 1) - pb;
+                        while (n > 0) {
+                            const int h = n >> 1;
+                            const bool le = sxf[4 * (pb + h)] <= xh;
+                            pb = le ? pb + h + 1 : pb;
+                            n = le ? n - h - 1 : h;
+                        }
+                        (void)re;
+                        // segments of even length, so that the main loop takes two pairs per
+                        // step from one segment: an odd one grows by a pair inside its row
+                        // (the far pads at both row ends keep it there)
+                        if (r == 4) {                    // exclude the pair holding the self element
+                            if (pself > pa) {
+                                const int qa = pa - ((pself - pa) & 1);
+                                sseg[32 * nseg + lane] = make_int2(qa, pself); ++nseg; ttot += pself - qa;
+                            }
+                            pa = pself + 1;
+                        }
+                        if (pb > pa) {
+                            const int qb = pb + ((pb - pa) & 1);
+                            sseg[32 * nseg + lane] = make_int2(pa, qb); ++nseg; ttot += qb - pa;
+                        }
+                    }
+                }
+            }
+            sseg[32 * nseg + lane] = make_int2(total, total + 2);    // sentinel
+            const int tmax = __reduce_max_sync(0xffffffffu, ttot);
+            __syncwarp();
+            // ---------------- main loop: each lane walks its own segments, two candidates per pair;
+            //                  the next segment is kept in registers so that the pair index never
+            //                  waits on a shared-memory load
+            Acc A;
+            acc_zero(A);
+            const float2 nxi = make_float2(-xi, -xi), nyi = make_float2(-yi, -yi), nzi = make_float2(-zi, -zi);
+            {
+                int si = lane;
+                const int siend = 32 * nseg + lane;
+                int2 sg = sseg[si];
+                int p = sg.x, e = sg.y;
+                for (int it = 0; it < tmax; it += 2) {
+                    const float4 xy0 = sxy[p], xy1 = sxy[p + 1];
+                    const float2 z0 = sz[p], z1 = sz[p + 1];
+                    p += 2;
+                    if (p == e) {                            // next segment (used by the next step)
+                        si = min(si + 32, siend);
+                        sg = sseg[si];
+                        p = sg.x;
+                        e = sg.y;
+                    }
+                    pair2(xy0, z0, nxi, nyi, nzi, sig2, lo, hi, A);
+                    pair2(xy1, z1, nxi, nyi, nzi, sig2, lo, hi, A);
+                }
+            }
+            // the other element of the self pair
+            if (act) {
+                const int eo = eself ^ 1;
+                elem1<false>(sxf[4 * pself + (eo & 1)], sxf[4 * pself + 2 + (eo & 1)], szf[2 * pself + (eo & 1)],
+                             xi, yi, zi, a.sig2, lo, hi, g, A);
+            }
+            // guard band (rare): exact re-decision of the band pairs of the lanes that saw one
+            if (__any_sync(0xffffffffu, A.band)) {
+                if (A.band) {
+                    for (int k = 0; k < nseg; ++k) {
+                        const int2 sg = sseg[32 * k + lane];
+                        for (int p = sg.x; p < sg.y; ++p) {
+                            const float4 xy = sxy[p];
+                            const float2 zz = sz[p];
+                            elem1<true>(xy.x, xy.z, zz.x, xi, yi, zi, a.sig2, lo, hi, g, A);
+                            elem1<true>(xy.y, xy.w, zz.y, xi, yi, zi, a.sig2, lo, hi, g, A);
+                        }
+                    }
+                }
+            }
+            if (act) {
+                const float f = -2.f * a.eps24;
+                const float gx = A.gx.x + A.gx.y, gy = A.gy.x + A.gy.y, gz = A.gz.x + A.gz.y;
+                a.force[mi] = make_float4(f * gx, f * gy, f * gz, 0.f);
+                const int hits = __float2int_rn(A.h.x + A.h.y) + A.hits_exact;
+                const double Ad = (double)A.a.x + (double)A.a.y, Bd = (double)A.b.x + (double)A.b.y;
+                Uw += (double)a.eps4 * (Ad - Bd) - (double)a.shift * hits;
+                Ww += (double)a.eps24 * (2.0 * Ad - Bd);
+                npw += hits;
+            }
+            __syncwarp();
+            todo &= ~members;
+            ++passes;
+            klim = kmax;
+        }
+        Uw = warp_sum_d(Uw);
+        Ww = warp_sum_d(Ww);
+        npw = warp_sum_ll(npw);
+        if (lane == 0) a.bpart[blk] = ForcePartial{0.5 * Uw, 0.5 * Ww, npw, 0};
+    }
+    ncw = warp_sum_ll(ncw);
+    if (lane == 0) a.part[gw] = ForcePartial{0.0, 0.0, 0, ncw};
+}
+
+}  // namespace lj1

@@ -188,7 +188,9 @@ __global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __res
     x.x = (float)(int)(p.x - (uint32_t)cx * g.E[0]) * g.s;    // exact (A12)
     x.y = (float)(int)(p.y - (uint32_t)cy * g.E[1]) * g.s;
     x.z = (float)(int)(p.z - (uint32_t)cz * g.E[2]) * g.s;
-    x.w = __int_as_float(md_comp(v.w));                         // comp bits
+    // rigid kernels: component bits; single-site kernel: the cell's x index
+    // (it rebuilds sub-chunk-relative x = xs.x + (cx - c_origin) * edge exactly)
+    x.w = RIGID ? __int_as_float(md_comp(v.w)) : (float)cx;
     xs[dst] = x;
     if (RIGID) {
         float4 q = quat_s[old];

@@ -13,6 +13,7 @@
 #include "common.cuh"
 #include "decomp.hpp"
 #include "kernels_force.cuh"
+#include "kernels_lj1.cuh"
 #include "kernels_state.cuh"
 
 namespace {
@@ -31,13 +32,16 @@ enum RigidShape { SHAPE_NONE, SHAPE_2CLJQ, SHAPE_TIP4P, SHAPE_GEN };
 #ifndef MD_LJ1_WARPS
 #define MD_LJ1_WARPS 4
 #endif
-#ifndef MD_LJ1_CAP
-#define MD_LJ1_CAP 256
+#ifndef MD_LJ1_CAPP
+#define MD_LJ1_CAPP 448
+#endif
+#ifndef MD_LJ1_MINB
+#define MD_LJ1_MINB 4
 #endif
 constexpr int LJ1_WARPS = MD_LJ1_WARPS;
-constexpr int LJ1_CAP = MD_LJ1_CAP;
-using LJ1 = LJ1Cfg<LJ1_WARPS, LJ1_CAP>;
-#define K_LJ1 k_force_lj1<LJ1_WARPS, LJ1_CAP>
+constexpr int LJ1_CAPP = MD_LJ1_CAPP;
+using LJ1 = lj1::Cfg<LJ1_WARPS, LJ1_CAPP>;
+#define K_LJ1 lj1::k_force_lj1<LJ1_WARPS, LJ1_CAPP, MD_LJ1_MINB>
 constexpr int RIG_WARPS = 4;
 constexpr int GEN_WARPS = 1;
 
@@ -85,7 +89,10 @@ struct mardyn_ctx {
     int* tsum = nullptr;
     unsigned long long* keys = nullptr;
     int* oldidx = nullptr;
-    ForcePartial* fpart = nullptr;
+    ForcePartial* fpart = nullptr;     // per-warp partials, then (single-site kernel) per-block partials
+    int nfpart = 0;                    // entries k_finalize sums
+    int nfw = 0;                       // per-warp entries
+    int* blk_ctr = nullptr;
     double* kpart = nullptr;
     ObsRec* hist = nullptr;
     long long* step_ctr = nullptr;
@@ -162,7 +169,7 @@ static int setup_grid(mardyn_ctx* ctx)
         double emax = 0;
         for (int k = 0; k < 3; ++k) emax = std::fmax(emax, ctx->L[k] / nc[k]);
         int ex = (int)std::ceil(std::log2(emax));
-        s = std::ldexp(1.0, ex - 23);
+        s = std::ldexp(1.0, ex - 22);
         bool again = false;
         for (int k = 0; k < 3; ++k) {
             E[k] = std::llround(ctx->L[k] / (nc[k] * s));
@@ -301,7 +308,6 @@ static int occupancy_grid(mardyn_ctx* ctx, K kernel, int threads, size_t smem = 
 
 static int launch_force(mardyn_ctx* ctx, int buf)
 {
-    (void)buf;
     ctx->n_force = ctx->n;
     ForceArgs a;
     a.g = ctx->g;
@@ -335,8 +341,21 @@ static int launch_force(mardyn_ctx* ctx, int buf)
         k_force_rigid<4, 4, 2, 2, true, GEN_WARPS>
             <<<ctx->force_blocks, threads, rigid_smem<4, 4, 2, 2, GEN_WARPS>(), ctx->stream>>>(a);
         break;
-    default:
-        K_LJ1<<<ctx->force_blocks, threads, LJ1::SMEM, ctx->stream>>>(a);
+    default: {
+        lj1::Args b;
+        b.g = ctx->g;
+        b.start = ctx->start;
+        b.pos = ctx->pos[buf];
+        b.xs = ctx->xs;
+        b.force = ctx->force;
+        b.part = ctx->fpart;
+        b.bpart = ctx->fpart + ctx->nfw;
+        b.nbcap = ctx->nfpart - ctx->nfw;
+        b.ctr = ctx->blk_ctr;
+        CK(cudaMemsetAsync(ctx->blk_ctr, 0, sizeof(int), ctx->stream));
+        b.sig2 = a.sig2; b.eps24 = a.eps24; b.eps4 = a.eps4; b.shift = a.shift;
+        K_LJ1<<<ctx->force_blocks, threads, LJ1::SMEM, ctx->stream>>>(b);
+    }
     }
     ctx->launches += 1;
     return MARDYN_OK;
@@ -387,7 +406,7 @@ static int enqueue_step(mardyn_ctx* ctx, int b, bool timing_events)
         k_integrate<false><<<ctx->nkblocks, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
                                                          nullptr, nullptr, ctx->force, ctx->torque, ctx->cell_of,
                                                          ctx->rank, ctx->count, ctx->kpart, ctx->flag);
-    k_finalize<<<1, 1024, 0, s>>>(ctx->force_blocks * ctx->force_warps_per_block, ctx->fpart, ctx->nkblocks,
+    k_finalize<<<1, 1024, 0, s>>>(ctx->nfpart, ctx->fpart, ctx->nkblocks,
                                   ctx->kpart, ctx->ndof, ctx->step_ctr, 1, ctx->hist);
     ctx->launches += 2;
     return enqueue_sort(ctx, b, 1 - b);
@@ -553,6 +572,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     const int ntiles = ncell_pad / SCAN_TILE;
     const int nk = std::max(1, nblk(cap, 256));
     const int nfw = std::max(1, ctx->force_blocks * ctx->force_warps_per_block);
+    const int nbc = ctx->kernel == KER_LJ1 ? nblk(cap, 32) + 1 : 0;
     uint4* pos0 = (uint4*)take(16 * cap);
     uint4* pos1 = (uint4*)take(16 * cap);
     float4* vel0 = (float4*)take(16 * cap);
@@ -573,7 +593,8 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     int* count = (int*)take(4 * (size_t)ncell_pad);
     int* start = (int*)take(4 * ((size_t)ncell + 1));
     int* tsum = (int*)take(4 * (size_t)std::max(ntiles, 1));
-    ForcePartial* fpart = (ForcePartial*)take(sizeof(ForcePartial) * nfw);
+    ForcePartial* fpart = (ForcePartial*)take(sizeof(ForcePartial) * (nfw + nbc));
+    int* blk_ctr = (int*)take(sizeof(int));
     double* kpart = (double*)take(16 * (size_t)nk);
     ObsRec* hist = (ObsRec*)take(sizeof(ObsRec) * MD_HISTORY);
     long long* step_ctr = (long long*)take(8);
@@ -602,6 +623,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         ctx->site = site; ctx->torque = tq; ctx->xs = xs; ctx->force = force;
         ctx->cell_of = cell_of; ctx->rank = rank; ctx->keys = keys; ctx->oldidx = oldidx; ctx->count = count;
         ctx->start = start; ctx->tsum = tsum; ctx->fpart = fpart; ctx->kpart = kpart;
+        ctx->nfw = nfw; ctx->nfpart = nfw + nbc; ctx->blk_ctr = blk_ctr;
         ctx->hist = hist; ctx->step_ctr = step_ctr; ctx->flag = flag; ctx->dmodel = dmodel;
         ctx->stage = stage; ctx->stage_bytes = stage_bytes;
         ctx->owner = owner; ctx->gmask = gmask; ctx->owned = owned; ctx->sendbuf = sendbuf;
@@ -741,7 +763,7 @@ int mardyn_compute_forces(mardyn_ctx* ctx)
         k_kinetic<false><<<ctx->nkblocks, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->vel[b], nullptr, nullptr,
                                                        ctx->force, nullptr, ctx->kpart);
     // kpart beyond the used blocks stays from earlier steps: same block count
-    k_finalize<<<1, 1024, 0, s>>>(ctx->force_blocks * ctx->force_warps_per_block, ctx->fpart, ctx->nkblocks,
+    k_finalize<<<1, 1024, 0, s>>>(ctx->nfpart, ctx->fpart, ctx->nkblocks,
                                   ctx->kpart, ctx->ndof, ctx->step_ctr, 0, ctx->hist);
     ctx->launches += 3;
     CK(cudaGetLastError());
@@ -1067,7 +1089,7 @@ int mardyn_dd_begin_step(mardyn_ctx* ctx, int64_t* send_counts)
         k_integrate<false, true><<<nkb, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b], nullptr,
                                                      nullptr, ctx->force, ctx->torque, ctx->cell_of, ctx->rank,
                                                      ctx->count, ctx->kpart, ctx->flag, dd);
-    k_finalize<<<1, 1024, 0, s>>>(ctx->force_blocks * ctx->force_warps_per_block, ctx->fpart, nkb, ctx->kpart,
+    k_finalize<<<1, 1024, 0, s>>>(ctx->nfpart, ctx->fpart, nkb, ctx->kpart,
                                   ctx->ndof, ctx->step_ctr, 1, ctx->hist, 0);
     ctx->launches += 3;
     CK(cudaGetLastError());

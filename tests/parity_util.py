@@ -21,7 +21,7 @@ def assert_forces_close(Fg, Fo, what="force", tol=F_TOL):
     scale = rms(Fo)
     err = float(np.abs(Fg - Fo).max())
     assert err <= tol * scale, f"{what}: max |d| = {err:.3e} > {tol} * RMS {scale:.3e}"
-    return err / scale
+    return err / scale if scale > 0 else 0.0
 
 
 def assert_rel(a, b, what, tol=E_TOL):

@@ -96,6 +96,22 @@ def test_dense_cells_chunking(md, oracle_mod):
     check_step0(md, oracle_mod, s2)
 
 
+@pytest.mark.parametrize("n_cells,rho,rc", [(5, 0.75, 2.5), (6, 0.75, 2.5), (7, 0.8, 2.5), (6, 0.9, 1.6)])
+def test_step0_lj_boxes(md, oracle_mod, n_cells, rho, rc):
+    """Single-site kernel on small boxes (3-6 cells per axis: sub-chunks
+    limited to nx - 2 cells, periodic wrap pieces in every staged row)."""
+    s = S.lj_fcc(n_cells, rho, 1.0, 40 + n_cells, f"box{n_cells}", 1, jitter=0.05, rc=rc)
+    check_step0(md, oracle_mod, s, torque=False)
+
+
+@pytest.mark.parametrize("n,box", [(700, (30.0, 30.0, 30.0)), (1500, (60.0, 25.0, 20.0))])
+def test_step0_lj_gas(md, oracle_mod, n, box):
+    """Gases (0.2-0.5 molecules per cell): blocks of 32 molecules spanning
+    many cells and rows take the per-lane path."""
+    s = S.random_system(n, box, [S.lj1_component()], seed_k=120 + n, rc=2.5, dmin=1.0)
+    check_step0(md, oracle_mod, s, torque=False)
+
+
 def run_both(md, oracle_mod, s, nsteps, eta=None):
     ctx = md.from_system(s, eta=eta)
     ctx.step(nsteps)

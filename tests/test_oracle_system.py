@@ -177,7 +177,7 @@ def test_cells_definition(oracle_mod):
 
 def test_grid_geometry(oracle_mod):
     """n_k = floor(L_k / rc) cells of edge >= rc, quantum a power of
-    two with edge <= 2^23 quanta, snapped box within 1e-6 relative."""
+    two with edge <= 2^22 quanta, snapped box within 1e-6 relative."""
     for name in ("c0", "c1s", "c2s", "c3s", "c4s"):
         s = S.config(name)
         o = oracle_mod.System(s)
@@ -185,7 +185,7 @@ def test_grid_geometry(oracle_mod):
         assert tuple(o.ncell) == tuple(np.floor(L / s["rc"]).astype(int))
         assert np.all(o.box / np.array(o.ncell) >= s["rc"])
         assert math.log2(o.quantum) == int(math.log2(o.quantum))
-        assert np.all(o.edge_q <= 2 ** 23)
+        assert np.all(o.edge_q <= 2 ** 22)
         assert np.abs(o.box / L - 1).max() < 1e-6
 
 
