@@ -54,6 +54,7 @@ struct GridP {
     int nc[3];
     int ncell;
     uint32_t E[3];               // cell edge in quanta (<= 2^22)
+    uint64_t Einv[3];            // ceil(2^64 / E): u / E == __umul64hi(u, Einv) for every u < 2^32
     uint32_t P[3];               // period in quanta (P may be 2^32 - wrap with 64-bit)
     uint64_t P64[3];
     float s, inv_s;              // quantum, 1/s (powers of two)
@@ -65,6 +66,14 @@ struct GridP {
     int hlo[3], hdim[3];         // home cells of this rank: box [hlo, hlo + hdim) (whole grid if 1 rank)
     int nhome;
 };
+
+// cell index along axis k of a fixed-point coordinate: floor(u / E_k) by a
+// multiply-high (exact for u < 2^32, E_k <= 2^23: the rounding excess of
+// ceil(2^64 / E) is below 2^-9 / E, smaller than the gap 1 / E to the next integer)
+__device__ __forceinline__ int cell_of_u(const GridP& g, int k, uint32_t u)
+{
+    return (int)__umul64hi((unsigned long long)u, g.Einv[k]);
+}
 
 // home cell t (0 <= t < nhome) of the rank's box, x fastest
 __device__ __forceinline__ int home_cell(const GridP& g, int t, int& cx, int& cy, int& cz)

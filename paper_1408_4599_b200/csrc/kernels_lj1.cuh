@@ -32,6 +32,7 @@
 namespace lj1 {
 
 constexpr int KMAX = 6;          // home cells per sub-chunk: staged |x| < 4 E (A12 quantum)
+constexpr int BLOCKS_PER_FETCH = 2;
 constexpr int NSEG = 11;         // per-lane segments: 9 rows + self split + sentinel
 constexpr float FAR = 1.0e18f;   // padding coordinate (r^2 ~ 1e36, finite, never a hit)
 
@@ -210,17 +211,21 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
         a.bpart[b] = ForcePartial{0.0, 0.0, 0, 0};
     // blocks are handed out in sorted order by an atomic counter (load balance);
     // each block's sums go to its own slot, so totals do not depend on the schedule
+    // (two consecutive blocks per fetch: they share most staged cells, which then hit in L1)
+    int nextb = 0;
+    if (lane == 0) nextb = atomicAdd(a.ctr, BLOCKS_PER_FETCH);
     for (;;) {
-        int blk = 0;
-        if (lane == 0) blk = atomicAdd(a.ctr, 1);
-        blk = __shfl_sync(0xffffffffu, blk, 0);
-        if (blk >= nblocks) break;
+        const int blk0 = __shfl_sync(0xffffffffu, nextb, 0);
+        if (blk0 >= nblocks) break;
+        if (lane == 0) nextb = atomicAdd(a.ctr, BLOCKS_PER_FETCH);     // in flight during this fetch's work
+        const int blk1 = min(blk0 + BLOCKS_PER_FETCH, nblocks);
+    for (int blk = blk0; blk < blk1; ++blk) {
         double Uw = 0.0, Ww = 0.0;
         long long npw = 0;
         const int mi = blk * 32 + lane;
         bool valid = mi < nsorted;
         uint4 pi = valid ? a.pos[mi] : make_uint4(0, 0, 0, 0);
-        const int cx = (int)(pi.x / g.E[0]), cy = (int)(pi.y / g.E[1]), cz = (int)(pi.z / g.E[2]);
+        const int cx = cell_of_u(g, 0, pi.x), cy = cell_of_u(g, 1, pi.y), cz = cell_of_u(g, 2, pi.z);
         const bool home = valid && cx >= g.hlo[0] && cx < g.hlo[0] + g.hdim[0] && cy >= g.hlo[1] &&
                           cy < g.hlo[1] + g.hdim[1] && cz >= g.hlo[2] && cz < g.hlo[2] + g.hdim[2];
         const int row = cy + ny * cz;
@@ -340,13 +345,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                         c = ee < n1 ? cm1 : (ee < n12 ? cm2 : cm3);
                         v = __ldg(a.xs + gi);
                     };
-                    for (int q0 = lane - 3 * r3; q0 < np; q0 += 6) {   // pairs q0, q0 + 3 (4 loads in flight)
-                        float4 v[4];
-                        float c[4];
+                    constexpr int UP = 4;                         // pairs per lane per round: 8 loads in flight
+                    for (int q0 = lane - 3 * r3; q0 < np; q0 += 3 * UP) {
+                        float4 v[2 * UP];
+                        float c[2 * UP];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) fetch(2 * (q0 + 3 * (u >> 1)) + (u & 1), v[u], c[u]);
+                        for (int u = 0; u < 2 * UP; ++u) fetch(2 * (q0 + 3 * (u >> 1)) + (u & 1), v[u], c[u]);
 #pragma unroll
-                        for (int k = 0; k < 2; ++k) {
+                        for (int k = 0; k < UP; ++k) {
                             const int q = q0 + 3 * k;
                             if (q < np) {
                                 float X[2], Y[2], Z[2];
@@ -383,59 +389,78 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                 zi = szf[2 * pself + (eself & 1)];
             }
             int nseg = 0, ttot = 0;
-            if (act) {
+            {
+                // pass 1 (branch-free, all rows): window half-width, cells holding the bounds
+                // (x of staged cell k: [xlo + k ex, xlo + (k+1) ex), exact), initial search ranges
                 const float Dyl = yi, Dyh = g.edge[1] - yi, Dzl = zi, Dzh = g.edge[2] - zi;
+                const int nsc = cB - cA + 3;
+                float wl[9], wh[9];
+                int la[9], lb[9], ua[9], ub[9];
 #pragma unroll
                 for (int r = 0; r < 9; ++r) {
                     const int dy = r % 3 - 1, dz = r / 3 - 1;
                     const float Dy = dy == 0 ? 0.f : (dy > 0 ? Dyh : Dyl);
                     const float Dz = dz == 0 ? 0.f : (dz > 0 ? Dzh : Dzl);
                     const float w2 = rc2w - Dy * Dy - Dz * Dz;
-                    if (w2 > 0.f) {
-                        const float w = sqrtf(w2);
-                        const int rb = srow[r], re = srow[r + 1] - 2;
-                        // first pair whose odd element reaches xi - w; first pair whose even element passes xi + w
-                        const float xl = xi - w, xh = xi + w;
-                        // cells holding the bounds (x of staged cell k: [xlo + k ex, xlo + (k+1) ex), exact)
-                        const int nsc = cB - cA + 3;
-                        int kl = min(max((int)floorf((xl - xlo) * inv_ex), 0), nsc - 1);
-                        if (kl > 0 && xl < xlo + (float)kl * ex) --kl;
-                        if (kl < nsc - 1 && xl >= xlo + (float)(kl + 1) * ex) ++kl;
-                        int kh = min(max((int)floorf((xh - xlo) * inv_ex), 0), nsc - 1);
-                        if (kh > 0 && xh < xlo + (float)kh * ex) --kh;
-                        if (kh < nsc - 1 && xh >= xlo + (float)(kh + 1) * ex) ++kh;
-                        // lower: first pair whose odd element is >= xl, in [floor(off_kl/2), floor(off_kl+1/2)]
-                        int pa = rb + (scb[10 * r + kl] >> 1), n = rb + (scb[10 * r + kl + 1] >> 1) - pa;
-                        while (n > 0) {
-                            const int h = n >> 1;
-                            const bool lt = sxf[4 * (pa + h) + 1] < xl;
-                            pa = lt ? pa + h + 1 : pa;
-                            n = lt ? n - h - 1 : h;
+                    float w;                                     // approximate: rc2w is generous by 2^-12
+                    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(fmaxf(w2, 0.f)));
+                    const bool on = act && w2 > 0.f;
+                    const float xl = on ? xi - w : FAR, xh = on ? xi + w : -FAR;   // off: empty window
+                    int kl = min(max((int)floorf((xl - xlo) * inv_ex), 0), nsc - 1);
+                    kl -= (kl > 0 && xl < xlo + (float)kl * ex) ? 1 : 0;
+                    kl += (kl < nsc - 1 && xl >= xlo + (float)(kl + 1) * ex) ? 1 : 0;
+                    int kh = min(max((int)floorf((xh - xlo) * inv_ex), 0), nsc - 1);
+                    kh -= (kh > 0 && xh < xlo + (float)kh * ex) ? 1 : 0;
+                    kh += (kh < nsc - 1 && xh >= xlo + (float)(kh + 1) * ex) ? 1 : 0;
+                    const int rb = srow[r];
+                    // lower: first pair whose odd element is >= xl, in [floor(off_kl/2), floor(off_kl+1/2)]
+                    la[r] = rb + (scb[10 * r + kl] >> 1);
+                    lb[r] = rb + (scb[10 * r + kl + 1] >> 1) - la[r];
+                    // upper: first pair whose even element is > xh, in [ceil(off_kh/2), ceil(off_kh+1/2)]
+                    ua[r] = rb + ((scb[10 * r + kh] + 1) >> 1);
+                    ub[r] = rb + ((scb[10 * r + kh + 1] + 1) >> 1) - ua[r];
+                    wl[r] = xl;
+                    wh[r] = xh;
+                }
+                // pass 2: the 18 binary searches step by step, interleaved (independent chains)
+                int nmax = 0;
+#pragma unroll
+                for (int r = 0; r < 9; ++r) nmax = max(nmax, max(lb[r], ub[r]));
+                nmax = __reduce_max_sync(0xffffffffu, nmax);
+                for (int n = nmax; n > 0; n >>= 1) {
+#pragma unroll
+                    for (int r = 0; r < 9; ++r) {
+                        {
+                            const int h = lb[r] >> 1;
+                            const bool lt = lb[r] > 0 && sxf[4 * (la[r] + h) + 1] < wl[r];
+                            la[r] = lt ? la[r] + h + 1 : la[r];
+                            lb[r] = lt ? lb[r] - h - 1 : h;
                         }
-                        // upper: first pair whose even element is > xh, in [ceil(off_kh/2), ceil(off_kh+1/2)]
-                        int pb = rb + ((scb[10 * r + kh] + 1) >> 1);
-                        n = rb + ((scb[10 * r + kh + 1] + 1) >> 1) - pb;
-                        while (n > 0) {
-                            const int h = n >> 1;
-                            const bool le = sxf[4 * (pb + h)] <= xh;
-                            pb = le ? pb + h + 1 : pb;
-                            n = le ? n - h - 1 : h;
+                        {
+                            const int h = ub[r] >> 1;
+                            const bool le = ub[r] > 0 && sxf[4 * (ua[r] + h)] <= wh[r];
+                            ua[r] = le ? ua[r] + h + 1 : ua[r];
+                            ub[r] = le ? ub[r] - h - 1 : h;
                         }
-                        (void)re;
-                        // segments of even length, so that the main loop takes two pairs per
-                        // step from one segment: an odd one grows by a pair inside its row
-                        // (the far pads at both row ends keep it there)
-                        if (r == 4) {                    // exclude the pair holding the self element
-                            if (pself > pa) {
-                                const int qa = pa - ((pself - pa) & 1);
-                                sseg[32 * nseg + lane] = make_int2(qa, pself); ++nseg; ttot += pself - qa;
-                            }
-                            pa = pself + 1;
+                    }
+                }
+                // pass 3: segments of even length, so that the main loop takes two pairs per step
+                // from one segment: an odd one grows by a pair inside its row (the far pads at
+                // both row ends keep it there); the pair holding the self element is excluded
+#pragma unroll
+                for (int r = 0; r < 9; ++r) {
+                    int pa = la[r];
+                    const int pb = ua[r];
+                    if (r == 4 && act) {
+                        if (pself > pa) {
+                            const int qa = pa - ((pself - pa) & 1);
+                            sseg[32 * nseg + lane] = make_int2(qa, pself); ++nseg; ttot += pself - qa;
                         }
-                        if (pb > pa) {
-                            const int qb = pb + ((pb - pa) & 1);
-                            sseg[32 * nseg + lane] = make_int2(pa, qb); ++nseg; ttot += qb - pa;
-                        }
+                        pa = pself + 1;
+                    }
+                    if (pb > pa) {
+                        const int qb = pb + ((pb - pa) & 1);
+                        sseg[32 * nseg + lane] = make_int2(pa, qb); ++nseg; ttot += qb - pa;
                     }
                 }
             }
@@ -506,6 +531,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
         Ww = warp_sum_d(Ww);
         npw = warp_sum_ll(npw);
         if (lane == 0) a.bpart[blk] = ForcePartial{0.5 * Uw, 0.5 * Ww, npw, 0};
+    }
     }
     ncw = warp_sum_ll(ncw);
     if (lane == 0) a.part[gw] = ForcePartial{0.0, 0.0, 0, ncw};

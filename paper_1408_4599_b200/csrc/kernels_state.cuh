@@ -30,7 +30,7 @@ __global__ void k_ingest(int n, const double* __restrict__ r, const double* __re
         x %= P;
         if (x < 0) x += P;
         u[k] = (uint32_t)x;
-        c[k] = (int)(u[k] / g.E[k]);
+        c[k] = cell_of_u(g, k, u[k]);
     }
     const int cl0 = c[0] + g.nc[0] * (c[1] + g.nc[1] * c[2]);
     int gflag = 0;
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
             if (x < 0) x += P;
             else if (x >= P) x -= P;
             uu[k] = (uint32_t)x;
-            c[k] = (int)(uu[k] / g.E[k]);
+            c[k] = cell_of_u(g, k, uu[k]);
         }
         if (bad) atomicOr(flag, 1);
         pos[t] = make_uint4(uu[0], uu[1], uu[2], p.w);
@@ -374,7 +374,7 @@ __global__ void k_import(int n, int base, GridP g, const DDRec* __restrict__ rec
     pos[t] = r.pos;
     vel[t] = r.vel;
     if (quat) { quat[t] = r.quat; angm[t] = r.angm; }
-    const int cl = (int)(r.pos.x / g.E[0]) + g.nc[0] * ((int)(r.pos.y / g.E[1]) + g.nc[1] * (int)(r.pos.z / g.E[2]));
+    const int cl = cell_of_u(g, 0, r.pos.x) + g.nc[0] * (cell_of_u(g, 1, r.pos.y) + g.nc[1] * cell_of_u(g, 2, r.pos.z));
     cell_of[t] = cl;
     rank[t] = atomicAdd(&count[cl], 1);
 }
@@ -487,7 +487,7 @@ __global__ void k_egress(int n, GridP g, const uint4* __restrict__ pos, const fl
     if (r) { r[3 * i] = (double)p.x * g.s; r[3 * i + 1] = (double)p.y * g.s; r[3 * i + 2] = (double)p.z * g.s; }
     if (ufix) { ufix[3 * i] = p.x; ufix[3 * i + 1] = p.y; ufix[3 * i + 2] = p.z; }
     if (cell) {
-        int cx = p.x / g.E[0], cy = p.y / g.E[1], cz = p.z / g.E[2];
+        int cx = cell_of_u(g, 0, p.x), cy = cell_of_u(g, 1, p.y), cz = cell_of_u(g, 2, p.z);
         cell[i] = cx + g.nc[0] * (cy + g.nc[1] * cz);
     }
     if (v) { float4 x = vel[t]; v[3 * i] = x.x; v[3 * i + 1] = x.y; v[3 * i + 2] = x.z; }

@@ -184,6 +184,8 @@ static int setup_grid(mardyn_ctx* ctx)
     for (int k = 0; k < 3; ++k) {
         g.nc[k] = nc[k];
         g.E[k] = (uint32_t)E[k];
+        // ceil(2^64 / E) for the multiply-high division (E >= 2, so no overflow)
+        g.Einv[k] = (uint64_t)(~0ull / (uint64_t)E[k]) + 1ull;
         uint64_t P = (uint64_t)E[k] * (uint64_t)nc[k];
         if (P > (1ull << 32)) return fail(ctx, MARDYN_EINVAL, "box too large for 32-bit fixed point");
         g.P64[k] = P;
