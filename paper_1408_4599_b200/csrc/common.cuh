@@ -112,10 +112,50 @@ struct ObsRec {                  // one history entry (matches mardyn_observable
     long long npairs, ncand;
 };
 
-struct ForcePartial {            // per warp of a force kernel
+struct ForcePartial {            // per warp / block of a force kernel
     double U, W;
     long long npairs, ncand;
+    double K;                    // translational kinetic energy (force kernels that fuse the step)
 };
+
+// translational leapfrog of one molecule (Eqs. 2-3 with readings A9, A12):
+// KE_t(t) from v(t) = v(t - dt/2) + dt/2 F/m, kick, fixed-point drift with
+// periodic wrap, next cell.  Shared by k_integrate and the fused LJ1 step.
+struct LeapOut {
+    uint4 p;
+    float4 v;
+    int c[3];
+    bool bad;
+    double ket;
+};
+__device__ __forceinline__ LeapOut md_leapfrog(const GridP& g, uint4 p, float4 v, float Fx, float Fy, float Fz,
+                                               float mass, float im)
+{
+    LeapOut o;
+    const float dt = g.dt;
+    const float vx = v.x + 0.5f * dt * Fx * im, vy = v.y + 0.5f * dt * Fy * im, vz = v.z + 0.5f * dt * Fz * im;
+    o.ket = 0.5 * (double)mass * ((double)vx * vx + (double)vy * vy + (double)vz * vz);
+    v.x += dt * Fx * im; v.y += dt * Fy * im; v.z += dt * Fz * im;
+    const float vv[3] = {v.x, v.y, v.z};
+    uint32_t uu[3] = {p.x, p.y, p.z};
+    bool bad = !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float d = (dt * vv[k]) * g.inv_s;
+        bad |= !(fabsf(d) < (float)g.E[k]);
+        const long long du = bad ? 0 : __float2ll_rn(d);
+        long long x = (long long)uu[k] + du;
+        const long long P = (long long)g.P64[k];
+        if (x < 0) x += P;
+        else if (x >= P) x -= P;
+        uu[k] = (uint32_t)x;
+        o.c[k] = (int)__umul64hi((unsigned long long)uu[k], g.Einv[k]);
+    }
+    o.p = make_uint4(uu[0], uu[1], uu[2], p.w);
+    o.v = v;
+    o.bad = bad;
+    return o;
+}
 
 __device__ __forceinline__ int warp_lane() { return threadIdx.x & 31; }
 

@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_force_rigid(ForceArgs a)
         p.W = 0.5 * Ww;
         p.npairs = npw;
         p.ncand = ncw;
+        p.K = 0.0;
         a.part[gw] = p;
     }
 }

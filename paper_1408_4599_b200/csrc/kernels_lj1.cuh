@@ -39,7 +39,7 @@ constexpr float FAR = 1.0e18f;   // padding coordinate (r^2 ~ 1e36, finite, neve
 struct Args {
     GridP g;
     const int* start;            // ncell + 1
-    const uint4* pos;            // sorted fixed-point positions
+    uint4* pos;                  // sorted fixed-point positions (advanced in place by the fused step)
     const float4* xs;            // cell-relative staging copy, w = cell x index (k_canon<false>)
     float4* force;
     ForcePartial* part;          // one per warp of the grid (n_candidates)
@@ -47,6 +47,13 @@ struct Args {
     int nbcap;
     int* ctr;                    // block counter (zeroed before the launch): dynamic block scheduling
     float sig2, eps24, eps4, shift;
+    // fused leapfrog step (STEP): v(t - dt/2) in / v(t + dt/2) out, next-step binning
+    float4* vel;
+    int* cell_of;
+    int* rank;
+    int* count;
+    int* flag;
+    float mass, inv_mass;
 };
 
 // origin (in quanta, mod 2^32) to subtract from the stored u of a molecule
@@ -157,7 +164,7 @@ __device__ __forceinline__ int find_from(const float* __restrict__ sxf, int rb, 
     return g;
 }
 
-template <int WARPS, int CAPP, int MINB>
+template <int WARPS, int CAPP, int MINB, bool STEP>
 __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
 {
     using C = Cfg<WARPS, CAPP>;
@@ -208,12 +215,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
     const int nsorted = __ldg(a.start + g.ncell);
     const int nblocks = (nsorted + 31) >> 5;
     for (int b = nblocks + gw * 32 + lane; b < a.nbcap; b += nw * 32)     // unused block partials
-        a.bpart[b] = ForcePartial{0.0, 0.0, 0, 0};
+        a.bpart[b] = ForcePartial{0.0, 0.0, 0, 0, 0.0};
     // blocks are handed out in sorted order by an atomic counter (load balance);
     // each block's sums go to its own slot, so totals do not depend on the schedule
     // (two consecutive blocks per fetch: they share most staged cells, which then hit in L1)
     int nextb = 0;
     if (lane == 0) nextb = atomicAdd(a.ctr, BLOCKS_PER_FETCH);
+    int pend_mi = -1, pend_b = 0, pend_r = 0;          // deferred arrival rank (STEP)
+    unsigned pend_m = 0;
     for (;;) {
         const int blk0 = __shfl_sync(0xffffffffu, nextb, 0);
         if (blk0 >= nblocks) break;
@@ -222,9 +231,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
     for (int blk = blk0; blk < blk1; ++blk) {
         double Uw = 0.0, Ww = 0.0;
         long long npw = 0;
+        float3 Fown = make_float3(0.f, 0.f, 0.f);  // this lane's molecule (STEP)
         const int mi = blk * 32 + lane;
         bool valid = mi < nsorted;
         uint4 pi = valid ? a.pos[mi] : make_uint4(0, 0, 0, 0);
+        const float4 vi = (STEP && valid) ? a.vel[mi] : make_float4(0.f, 0.f, 0.f, 0.f);   // in flight during the forces
         const int cx = cell_of_u(g, 0, pi.x), cy = cell_of_u(g, 1, pi.y), cz = cell_of_u(g, 2, pi.z);
         const bool home = valid && cx >= g.hlo[0] && cx < g.hlo[0] + g.hdim[0] && cy >= g.hlo[1] &&
                           cy < g.hlo[1] + g.hdim[1] && cz >= g.hlo[2] && cz < g.hlo[2] + g.hdim[2];
@@ -284,30 +295,28 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                 Acc A;
                 acc_zero(A);
                 if ((todo >> lane) & 1u) {
-                    const float xi = qdiff(pi.x, (uint32_t)cx * g.E[0], g.s);
-                    const float yi = qdiff(pi.y, (uint32_t)cy * g.E[1], g.s);
-                    const float zi = qdiff(pi.z, (uint32_t)cz * g.E[2], g.s);
+                    // cell-relative coordinates of the staging copy (read-only while the fused
+                    // step advances pos in place): neighbour cell (dx, dy, dz) adds its offset, exact
+                    const float4 xsi = __ldg(a.xs + mi);
                     for (int dz = -1; dz <= 1; ++dz)
                         for (int dy = -1; dy <= 1; ++dy) {
-                            const int ryu = cy + dy, rzu = cz + dz;
-                            const int rowc = nx * (wrapi(ryu, ny) + ny * wrapi(rzu, nz));
-                            const uint32_t oyy = img_origin((uint32_t)cy * g.E[1], ryu, ny, g.P[1]);
-                            const uint32_t ozz = img_origin((uint32_t)cz * g.E[2], rzu, nz, g.P[2]);
+                            const int rowc = nx * (wrapi(cy + dy, ny) + ny * wrapi(cz + dz, nz));
+                            const float oy = (float)dy * g.edge[1], oz = (float)dz * g.edge[2];
                             for (int dx = -1; dx <= 1; ++dx) {
-                                const int cxu = cx + dx;
-                                const uint32_t oxx = img_origin((uint32_t)cx * g.E[0], cxu, nx, g.P[0]);
-                                const int c2 = rowc + wrapi(cxu, nx);
+                                const float ox = (float)dx * ex;
+                                const int c2 = rowc + wrapi(cx + dx, nx);
                                 const int j0 = __ldg(a.start + c2), j1 = __ldg(a.start + c2 + 1);
                                 for (int j = j0; j < j1; ++j) {
                                     if (j == mi) continue;
-                                    const uint4 pj = a.pos[j];
-                                    elem1<false>(qdiff(pj.x, oxx, g.s), qdiff(pj.y, oyy, g.s), qdiff(pj.z, ozz, g.s),
-                                                 xi, yi, zi, a.sig2, lo, hi, g, A);
+                                    const float4 xj = __ldg(a.xs + j);
+                                    elem1<false>(xj.x + ox, xj.y + oy, xj.z + oz, xsi.x, xsi.y, xsi.z, a.sig2, lo,
+                                                 hi, g, A);
                                 }
                             }
                         }
                     const float f = -2.f * a.eps24;
-                    a.force[mi] = make_float4(f * A.gx.x, f * A.gy.x, f * A.gz.x, 0.f);
+                    Fown = make_float3(f * A.gx.x, f * A.gy.x, f * A.gz.x);
+                    a.force[mi] = make_float4(Fown.x, Fown.y, Fown.z, 0.f);
                     const double Ad = A.a.x, Bd = A.b.x;
                     Uw += (double)a.eps4 * (Ad - Bd) - (double)a.shift * A.hits_exact;
                     Ww += (double)a.eps24 * (2.0 * Ad - Bd);
@@ -515,7 +524,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
             if (act) {
                 const float f = -2.f * a.eps24;
                 const float gx = A.gx.x + A.gx.y, gy = A.gy.x + A.gy.y, gz = A.gz.x + A.gz.y;
-                a.force[mi] = make_float4(f * gx, f * gy, f * gz, 0.f);
+                Fown = make_float3(f * gx, f * gy, f * gz);
+                a.force[mi] = make_float4(Fown.x, Fown.y, Fown.z, 0.f);
                 const int hits = __float2int_rn(A.h.x + A.h.y) + A.hits_exact;
                 const double Ad = (double)A.a.x + (double)A.a.y, Bd = (double)A.b.x + (double)A.b.y;
                 Uw += (double)a.eps4 * (Ad - Bd) - (double)a.shift * hits;
@@ -527,14 +537,44 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
             ++passes;
             klim = kmax;
         }
+        double Kw = 0.0;
+        if (STEP) {
+            // fused leapfrog (Eqs. 2-3): this block's molecules are only read by this warp
+            // (neighbours are staged from xs), so they are advanced in place
+            int clb = -1;
+            if (home) {
+                const LeapOut o = md_leapfrog(g, pi, vi, Fown.x, Fown.y, Fown.z, a.mass, a.inv_mass);
+                if (o.bad) atomicOr(a.flag, 1);
+                a.pos[mi] = o.p;
+                a.vel[mi] = o.v;
+                clb = o.c[0] + nx * (o.c[1] + ny * o.c[2]);
+                a.cell_of[mi] = clb;
+                Kw = o.ket;
+            }
+            // arrival ranks: one atomic per distinct cell; the rank store waits for the
+            // atomic's reply, so it is deferred to after the next block's forces
+            if (pend_mi >= 0) a.rank[pend_mi] = __shfl_sync(pend_m, pend_b, __ffs(pend_m) - 1) + pend_r;
+            const unsigned m = __match_any_sync(0xffffffffu, clb);
+            pend_mi = -1;
+            if (clb >= 0) {
+                const int leader = __ffs(m) - 1;
+                pend_b = 0;
+                if (lane == leader) pend_b = atomicAdd(a.count + clb, __popc(m));
+                pend_m = m;
+                pend_r = __popc(m & ((1u << lane) - 1u));
+                pend_mi = mi;
+            }
+            Kw = warp_sum_d(Kw);
+        }
         Uw = warp_sum_d(Uw);
         Ww = warp_sum_d(Ww);
         npw = warp_sum_ll(npw);
-        if (lane == 0) a.bpart[blk] = ForcePartial{0.5 * Uw, 0.5 * Ww, npw, 0};
+        if (lane == 0) a.bpart[blk] = ForcePartial{0.5 * Uw, 0.5 * Ww, npw, 0, Kw};
     }
     }
+    if (STEP && pend_mi >= 0) a.rank[pend_mi] = __shfl_sync(pend_m, pend_b, __ffs(pend_m) - 1) + pend_r;
     ncw = warp_sum_ll(ncw);
-    if (lane == 0) a.part[gw] = ForcePartial{0.0, 0.0, 0, ncw};
+    if (lane == 0) a.part[gw] = ForcePartial{0.0, 0.0, 0, ncw, 0.0};
 }
 
 }  // namespace lj1

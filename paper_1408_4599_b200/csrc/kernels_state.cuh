@@ -89,48 +89,72 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total)
     return res;
 }
 
-__global__ void __launch_bounds__(1024) k_scan_tiles(int ncell, const int* __restrict__ count,
-                                                     int* __restrict__ start, int* __restrict__ tsum)
+// Single-pass exclusive scan with decoupled look-back: tiles are claimed in
+// order through a counter; each tile publishes its aggregate, then walks
+// back over its predecessors' published values (an inclusive prefix ends
+// the walk) and publishes its own inclusive prefix.  flags[] and the tile
+// counter are zeroed before every launch.  start[ncell] = total.
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p)
 {
-    __shared__ int tot;
-    int base = blockIdx.x * SCAN_TILE + threadIdx.x * 4;
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+#define SCAN_AGG (1ull << 32)
+#define SCAN_INC (2ull << 32)
+
+__global__ void __launch_bounds__(1024) k_scan(int ncell, const int* __restrict__ count, int* __restrict__ start,
+                                               unsigned long long* __restrict__ flags, int* __restrict__ tile_ctr)
+{
+    __shared__ int tot, tile_s, excl_s;
+    if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1);
+    __syncthreads();
+    const int tile = tile_s;
+    const int base = tile * SCAN_TILE + threadIdx.x * 4;
     int a[4];
+    const int4 c4 = (base + 3 < ncell) ? *reinterpret_cast<const int4*>(count + base) : make_int4(0, 0, 0, 0);
+    if (base + 3 < ncell) { a[0] = c4.x; a[1] = c4.y; a[2] = c4.z; a[3] = c4.w; }
+    else {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) a[k] = (base + k < ncell) ? count[base + k] : 0;
-    int s = a[0] + a[1] + a[2] + a[3];
-    int ex = block_excl_scan(s, &tot);
+        for (int k = 0; k < 4; ++k) a[k] = (base + k < ncell) ? count[base + k] : 0;
+    }
+    int ex = block_excl_scan(a[0] + a[1] + a[2] + a[3], &tot);
+    if (threadIdx.x < 32) {                  // warp 0: publish, then look back 32 tiles at a time
+        const int lane = threadIdx.x;
+        const int agg = tot;
+        if (lane == 0) st_release_u64(flags + tile, (tile == 0 ? SCAN_INC : SCAN_AGG) | (unsigned)agg);
+        int prefix = 0;
+        for (int j = tile - 1; j >= 0; j -= 32) {
+            const int jj = j - lane;                          // lane 0 nearest
+            unsigned long long f = SCAN_INC;                  // beyond tile 0: an empty inclusive prefix
+            if (jj >= 0) {
+                do { f = ld_acquire_u64(flags + jj); } while ((f >> 32) == 0);
+            }
+            const unsigned inc = __ballot_sync(0xffffffffu, (f >> 32) == 2);
+            const int stop = inc ? __ffs(inc) - 1 : 31;       // nearest inclusive prefix ends the walk
+            int v = lane <= stop ? (int)(unsigned)(f & 0xffffffffu) : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            prefix += v;
+            if (inc) break;
+        }
+        if (lane == 0) {
+            if (tile > 0) st_release_u64(flags + tile, SCAN_INC | (unsigned)(prefix + agg));
+            excl_s = prefix;
+            if (tile == (ncell - 1) / SCAN_TILE) start[ncell] = prefix + agg;
+        }
+    }
+    __syncthreads();
+    ex += excl_s;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if (base + k < ncell) start[base + k] = ex;
         ex += a[k];
-    }
-    if (threadIdx.x == 0) tsum[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(1024) k_scan_sums(int ntiles, int* __restrict__ tsum)
-{
-    __shared__ int tot;
-    // ntiles <= 4096: 4 per thread
-    int base = threadIdx.x * 4;
-    int a[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) a[k] = (base + k < ntiles) ? tsum[base + k] : 0;
-    int s = a[0] + a[1] + a[2] + a[3];
-    int ex = block_excl_scan(s, &tot);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        if (base + k < ntiles) tsum[base + k] = ex;
-        ex += a[k];
-    }
-}
-
-__global__ void k_scan_add(int ncell, const int* __restrict__ count, int* __restrict__ start,
-                           const int* __restrict__ tsum)
-{
-    int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c < ncell) {
-        start[c] += tsum[c / SCAN_TILE];
-        if (c == ncell - 1) start[ncell] = start[c] + count[c];
     }
 }
 
@@ -272,6 +296,7 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     double ket = 0.0, ker = 0.0;
+    int cl_bin = -1;
     bool ghost = false;
     if (DD && t < n) {
         ghost = md_ghost(vel[t].w);
@@ -282,32 +307,13 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
         float4 v = vel[t];
         float4 F = force[t];
         const DevComp& C = model->comp[md_comp(v.w)];
-        const float dt = g.dt, im = C.inv_mass;
-        // A9: KE_t(t) from v(t) = v(t - dt/2) + dt/2 F/m
-        float vx = v.x + 0.5f * dt * F.x * im, vy = v.y + 0.5f * dt * F.y * im,
-              vz = v.z + 0.5f * dt * F.z * im;
-        ket = 0.5 * (double)C.mass * ((double)vx * vx + (double)vy * vy + (double)vz * vz);
-        // Eq. 2 kick, Eq. 3 drift on the fixed-point lattice (A12)
-        v.x += dt * F.x * im; v.y += dt * F.y * im; v.z += dt * F.z * im;
-        float vv[3] = {v.x, v.y, v.z};
-        uint32_t uu[3] = {p.x, p.y, p.z};
-        int c[3];
-        bool bad = !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z));
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            float d = (dt * vv[k]) * g.inv_s;
-            bad |= !(fabsf(d) < (float)g.E[k]);
-            long long du = bad ? 0 : __float2ll_rn(d);
-            long long x = (long long)uu[k] + du;
-            long long P = (long long)g.P64[k];
-            if (x < 0) x += P;
-            else if (x >= P) x -= P;
-            uu[k] = (uint32_t)x;
-            c[k] = cell_of_u(g, k, uu[k]);
-        }
-        if (bad) atomicOr(flag, 1);
-        pos[t] = make_uint4(uu[0], uu[1], uu[2], p.w);
-        vel[t] = v;
+        const float dt = g.dt;
+        const LeapOut lo = md_leapfrog(g, p, v, F.x, F.y, F.z, C.mass, C.inv_mass);
+        ket = lo.ket;
+        int c[3] = {lo.c[0], lo.c[1], lo.c[2]};
+        if (lo.bad) atomicOr(flag, 1);
+        pos[t] = lo.p;
+        vel[t] = lo.v;
         if (RIGID && C.rot) {
             // Fincham rotational leapfrog (reading A7 of Eqs. 4-5)
             float4 q = quat[t];
@@ -353,10 +359,19 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
                 }
             }
         }
-        if (cl >= 0) {
-            cell_of[t] = cl;
-            rank[t] = atomicAdd(&count[cl], 1);
-        }
+        if (cl >= 0) cell_of[t] = cl;
+        cl_bin = cl;
+    }
+    // next step's cell histogram + arrival rank: molecules are in cell order, so
+    // the lanes of a warp share few cells; one atomic per distinct cell (the arrival
+    // order only places molecules before the canonical in-cell ordering)
+    const unsigned m = __match_any_sync(0xffffffffu, cl_bin);
+    if (cl_bin >= 0) {
+        const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+        int b = 0;
+        if (lane == leader) b = atomicAdd(&count[cl_bin], __popc(m));
+        b = __shfl_sync(m, b, leader);
+        rank[t] = b + __popc(m & ((1u << lane) - 1u));
     }
     block_sum2_d<256>(ket, ker, &ke_part[2 * blockIdx.x], &ke_part[2 * blockIdx.x + 1]);
 }
@@ -430,41 +445,80 @@ __global__ void k_half_kick(int n, GridP g, const DevModel* __restrict__ model, 
     }
 }
 
-// observables of one time t_k: fixed-order sums of the per-warp force
-// partials and the per-block kinetic partials, written to the ring buffer.
-__global__ void __launch_bounds__(1024) k_finalize(int nfp, const ForcePartial* __restrict__ fp,
-                                                   int nkp, const double* __restrict__ kp,
-                                                   double ndof, long long* __restrict__ step_ctr,
-                                                   int advance, ObsRec* __restrict__ hist, int halve = 1)
+// observables of one time t_k: fixed-order sums of the per-warp / per-block
+// force partials and the per-block kinetic partials, written to the ring
+// buffer.  FIN_BLOCKS blocks each sum a fixed contiguous range (fixed
+// thread order, fixed tree); the last block to finish (ticket) adds the
+// block results in block order -- the result does not depend on timing.
+#define FIN_BLOCKS 48
+#define FIN_THREADS 256
+struct FinPart {
+    double U, W, Kt, Kr;
+    long long np, nc;
+};
+
+__device__ __forceinline__ void block_sum_fin(FinPart& v)
 {
-    double U = 0, W = 0, Kt = 0, Kr = 0;
-    long long np = 0, nc = 0;
-    for (int k = threadIdx.x; k < nfp; k += 1024) {
-        ForcePartial f = fp[k];
-        U += f.U; W += f.W; np += f.npairs; nc += f.ncand;
-    }
-    for (int k = threadIdx.x; k < nkp; k += 1024) { Kt += kp[2 * k]; Kr += kp[2 * k + 1]; }
-    __shared__ double sU[32], sW[32], sKt[32], sKr[32];
-    __shared__ long long snp[32], snc[32];
-    U = warp_sum_d(U); W = warp_sum_d(W); Kt = warp_sum_d(Kt); Kr = warp_sum_d(Kr);
-    np = warp_sum_ll(np); nc = warp_sum_ll(nc);
+    __shared__ FinPart sp[FIN_THREADS / 32];
+    v.U = warp_sum_d(v.U); v.W = warp_sum_d(v.W); v.Kt = warp_sum_d(v.Kt); v.Kr = warp_sum_d(v.Kr);
+    v.np = warp_sum_ll(v.np); v.nc = warp_sum_ll(v.nc);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (lane == 0) { sU[w] = U; sW[w] = W; sKt[w] = Kt; sKr[w] = Kr; snp[w] = np; snc[w] = nc; }
+    if (lane == 0) sp[w] = v;
     __syncthreads();
     if (threadIdx.x == 0) {
-        ObsRec o;
-        o.U = 0; o.W = 0; o.KEt = 0; o.KEr = 0; o.npairs = 0; o.ncand = 0;
-        for (int k = 0; k < 32; ++k) {
-            o.U += sU[k]; o.W += sW[k]; o.KEt += sKt[k]; o.KEr += sKr[k];
-            o.npairs += snp[k]; o.ncand += snc[k];
+        FinPart o = sp[0];
+        for (int k = 1; k < FIN_THREADS / 32; ++k) {
+            o.U += sp[k].U; o.W += sp[k].W; o.Kt += sp[k].Kt; o.Kr += sp[k].Kr; o.np += sp[k].np; o.nc += sp[k].nc;
         }
+        v = o;
+    }
+}
+
+__global__ void __launch_bounds__(FIN_THREADS) k_finalize(int nfp, const ForcePartial* __restrict__ fp,
+                                                          int nkp, const double* __restrict__ kp,
+                                                          double ndof, long long* __restrict__ step_ctr,
+                                                          int advance, ObsRec* __restrict__ hist,
+                                                          FinPart* __restrict__ scratch, int* __restrict__ ticket,
+                                                          int halve = 1)
+{
+    FinPart v{0, 0, 0, 0, 0, 0};
+    const int cf = (nfp + FIN_BLOCKS - 1) / FIN_BLOCKS, ck = (nkp + FIN_BLOCKS - 1) / FIN_BLOCKS;
+    const int f0 = blockIdx.x * cf, f1 = min(f0 + cf, nfp), k0 = blockIdx.x * ck, k1 = min(k0 + ck, nkp);
+    for (int k = f0 + threadIdx.x; k < f1; k += FIN_THREADS) {
+        const ForcePartial f = fp[k];
+        v.U += f.U; v.W += f.W; v.np += f.npairs; v.nc += f.ncand; v.Kt += f.K;
+    }
+    for (int k = k0 + threadIdx.x; k < k1; k += FIN_THREADS) {
+        const double2 q = reinterpret_cast<const double2*>(kp)[k];
+        v.Kt += q.x; v.Kr += q.y;
+    }
+    block_sum_fin(v);
+    __shared__ int last;
+    if (threadIdx.x == 0) {
+        scratch[blockIdx.x] = v;
+        __threadfence();
+        last = atomicAdd(ticket, 1) == FIN_BLOCKS - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    FinPart w{0, 0, 0, 0, 0, 0};
+    if (threadIdx.x < FIN_BLOCKS) {
+        const volatile FinPart* sv = scratch + threadIdx.x;
+        w.U = sv->U; w.W = sv->W; w.Kt = sv->Kt; w.Kr = sv->Kr; w.np = sv->np; w.nc = sv->nc;
+    }
+    block_sum_fin(w);
+    if (threadIdx.x == 0) {
+        ObsRec o;
+        o.U = w.U; o.W = w.W; o.KEt = w.Kt; o.KEr = w.Kr; o.npairs = w.np; o.ncand = w.nc;
         if (halve) o.npairs /= 2;            // full shell sees every pair twice (a decomposed
                                              // rank reports ordered pairs of its owned molecules)
         o.T = 2.0 * (o.KEt + o.KEr) / ndof;
-        long long s = *step_ctr;
-        o.step = s;
-        hist[s % MD_HISTORY] = o;
-        if (advance) *step_ctr = s + 1;
+        const long long st = *step_ctr;
+        o.step = st;
+        hist[st % MD_HISTORY] = o;
+        if (advance) *step_ctr = st + 1;
+        *ticket = 0;
     }
 }
 

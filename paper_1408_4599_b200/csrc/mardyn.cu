@@ -41,7 +41,8 @@ enum RigidShape { SHAPE_NONE, SHAPE_2CLJQ, SHAPE_TIP4P, SHAPE_GEN };
 constexpr int LJ1_WARPS = MD_LJ1_WARPS;
 constexpr int LJ1_CAPP = MD_LJ1_CAPP;
 using LJ1 = lj1::Cfg<LJ1_WARPS, LJ1_CAPP>;
-#define K_LJ1 lj1::k_force_lj1<LJ1_WARPS, LJ1_CAPP, MD_LJ1_MINB>
+#define K_LJ1 lj1::k_force_lj1<LJ1_WARPS, LJ1_CAPP, MD_LJ1_MINB, false>
+#define K_LJ1_STEP lj1::k_force_lj1<LJ1_WARPS, LJ1_CAPP, MD_LJ1_MINB, true>
 constexpr int RIG_WARPS = 4;
 constexpr int GEN_WARPS = 1;
 
@@ -86,7 +87,9 @@ struct mardyn_ctx {
     int* rank = nullptr;
     int* count = nullptr;
     int* start = nullptr;
-    int* tsum = nullptr;
+    unsigned long long* scan_flags = nullptr;   // ntiles look-back flags + tile counter
+    FinPart* fin_scratch = nullptr;
+    int* fin_ticket = nullptr;
     unsigned long long* keys = nullptr;
     int* oldidx = nullptr;
     ForcePartial* fpart = nullptr;     // per-warp partials, then (single-site kernel) per-block partials
@@ -308,7 +311,10 @@ static int occupancy_grid(mardyn_ctx* ctx, K kernel, int threads, size_t smem = 
     return per_sm * ctx->num_sms;
 }
 
-static int launch_force(mardyn_ctx* ctx, int buf)
+// forces at the current state of buffer `buf`; step = true (single-site
+// kernel, one domain) also advances the molecules by one leapfrog step and
+// bins them for the next cell rebuild (count must be zeroed before)
+static int launch_force(mardyn_ctx* ctx, int buf, bool step = false)
 {
     ctx->n_force = ctx->n;
     ForceArgs a;
@@ -356,7 +362,15 @@ static int launch_force(mardyn_ctx* ctx, int buf)
         b.ctr = ctx->blk_ctr;
         CK(cudaMemsetAsync(ctx->blk_ctr, 0, sizeof(int), ctx->stream));
         b.sig2 = a.sig2; b.eps24 = a.eps24; b.eps4 = a.eps4; b.shift = a.shift;
-        K_LJ1<<<ctx->force_blocks, threads, LJ1::SMEM, ctx->stream>>>(b);
+        b.vel = ctx->vel[buf];
+        b.cell_of = ctx->cell_of;
+        b.rank = ctx->rank;
+        b.count = ctx->count;
+        b.flag = ctx->flag;
+        b.mass = ctx->model.comp[0].mass;
+        b.inv_mass = ctx->model.comp[0].inv_mass;
+        if (step) K_LJ1_STEP<<<ctx->force_blocks, threads, LJ1::SMEM, ctx->stream>>>(b);
+        else K_LJ1<<<ctx->force_blocks, threads, LJ1::SMEM, ctx->stream>>>(b);
     }
     }
     ctx->launches += 1;
@@ -371,9 +385,9 @@ static int enqueue_sort(mardyn_ctx* ctx, int src, int dst, int64_t n_unsorted = 
 {
     const int n = (int)(n_unsorted < 0 ? ctx->n : n_unsorted), ncell = ctx->g.ncell;
     cudaStream_t s = ctx->stream;
-    k_scan_tiles<<<ctx->ntiles, 1024, 0, s>>>(ncell, ctx->count, ctx->start, ctx->tsum);
-    k_scan_sums<<<1, 1024, 0, s>>>(ctx->ntiles, ctx->tsum);
-    k_scan_add<<<nblk(ncell, 256), 256, 0, s>>>(ncell, ctx->count, ctx->start, ctx->tsum);
+    CK(cudaMemsetAsync(ctx->scan_flags, 0, sizeof(unsigned long long) * (ctx->ntiles + 1), s));
+    k_scan<<<ctx->ntiles, 1024, 0, s>>>(ncell, ctx->count, ctx->start, ctx->scan_flags,
+                                        reinterpret_cast<int*>(ctx->scan_flags + ctx->ntiles));
     k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->pos[src], ctx->cell_of, ctx->rank, ctx->start, ctx->keys,
                                             ctx->oldidx);
     if (ctx->rigid)
@@ -386,7 +400,7 @@ static int enqueue_sort(mardyn_ctx* ctx, int src, int dst, int64_t n_unsorted = 
                                                     ctx->pos[src], ctx->vel[src], nullptr, nullptr,
                                                     ctx->pos[dst], ctx->vel[dst], nullptr, nullptr, ctx->xs,
                                                     nullptr, ctx->dmodel);
-    ctx->launches += 5;
+    ctx->launches += 3;      // scan, scatter, canon
     return MARDYN_OK;
 }
 
@@ -396,9 +410,18 @@ static int enqueue_step(mardyn_ctx* ctx, int b, bool timing_events)
 {
     cudaStream_t s = ctx->stream;
     const int n = (int)ctx->n;
+    const bool fused = ctx->kernel == KER_LJ1 && ctx->nranks == 1;
+    if (fused) CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
     if (timing_events) CK(cudaEventRecordWithFlags(ctx->ev_f0[b], s, cudaEventRecordExternal));
-    launch_force(ctx, b);
+    launch_force(ctx, b, fused);
     if (timing_events) CK(cudaEventRecordWithFlags(ctx->ev_f1[b], s, cudaEventRecordExternal));
+    if (fused) {
+        // the single-site kernel has advanced and binned the molecules (kinetic energy in its partials)
+        k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, 0, ctx->kpart, ctx->ndof,
+                                                      ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket);
+        ctx->launches += 1;
+        return enqueue_sort(ctx, b, 1 - b);
+    }
     CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
     if (ctx->rigid)
         k_integrate<true><<<ctx->nkblocks, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
@@ -408,8 +431,8 @@ static int enqueue_step(mardyn_ctx* ctx, int b, bool timing_events)
         k_integrate<false><<<ctx->nkblocks, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
                                                          nullptr, nullptr, ctx->force, ctx->torque, ctx->cell_of,
                                                          ctx->rank, ctx->count, ctx->kpart, ctx->flag);
-    k_finalize<<<1, 1024, 0, s>>>(ctx->nfpart, ctx->fpart, ctx->nkblocks,
-                                  ctx->kpart, ctx->ndof, ctx->step_ctr, 1, ctx->hist);
+    k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, ctx->nkblocks, ctx->kpart, ctx->ndof,
+                                                  ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket);
     ctx->launches += 2;
     return enqueue_sort(ctx, b, 1 - b);
 }
@@ -432,7 +455,10 @@ static int build_graphs(mardyn_ctx* ctx)
     return MARDYN_OK;
 }
 
-static int launches_per_step(const mardyn_ctx*) { return 8; }
+static int launches_per_step(const mardyn_ctx* ctx)
+{   // force (+ integrate unless fused), finalize, scan, scatter, canon
+    return (ctx->kernel == KER_LJ1 && ctx->nranks == 1) ? 5 : 6;
+}
 
 // ------------------------------------------------------------------------
 // C ABI
@@ -530,6 +556,7 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
     }
     default:
         CK(cudaFuncSetAttribute(K_LJ1, cudaFuncAttributeMaxDynamicSharedMemorySize, LJ1::SMEM));
+        CK(cudaFuncSetAttribute(K_LJ1_STEP, cudaFuncAttributeMaxDynamicSharedMemorySize, LJ1::SMEM));
         ctx->force_blocks = occupancy_grid(ctx, K_LJ1, threads, LJ1::SMEM);
     }
     for (int b = 0; b < 2; ++b) {
@@ -594,7 +621,9 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     int* oldidx = (int*)take(4 * cap);
     int* count = (int*)take(4 * (size_t)ncell_pad);
     int* start = (int*)take(4 * ((size_t)ncell + 1));
-    int* tsum = (int*)take(4 * (size_t)std::max(ntiles, 1));
+    unsigned long long* scan_flags = (unsigned long long*)take(8 * (size_t)(std::max(ntiles, 1) + 1));
+    FinPart* fin_scratch = (FinPart*)take(sizeof(FinPart) * FIN_BLOCKS);
+    int* fin_ticket = (int*)take(sizeof(int));
     ForcePartial* fpart = (ForcePartial*)take(sizeof(ForcePartial) * (nfw + nbc));
     int* blk_ctr = (int*)take(sizeof(int));
     double* kpart = (double*)take(16 * (size_t)nk);
@@ -624,7 +653,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         ctx->quat[0] = q0; ctx->quat[1] = q1; ctx->angm[0] = j0; ctx->angm[1] = j1;
         ctx->site = site; ctx->torque = tq; ctx->xs = xs; ctx->force = force;
         ctx->cell_of = cell_of; ctx->rank = rank; ctx->keys = keys; ctx->oldidx = oldidx; ctx->count = count;
-        ctx->start = start; ctx->tsum = tsum; ctx->fpart = fpart; ctx->kpart = kpart;
+        ctx->start = start; ctx->scan_flags = scan_flags; ctx->fin_scratch = fin_scratch; ctx->fin_ticket = fin_ticket; ctx->fpart = fpart; ctx->kpart = kpart;
         ctx->nfw = nfw; ctx->nfpart = nfw + nbc; ctx->blk_ctr = blk_ctr;
         ctx->hist = hist; ctx->step_ctr = step_ctr; ctx->flag = flag; ctx->dmodel = dmodel;
         ctx->stage = stage; ctx->stage_bytes = stage_bytes;
@@ -657,6 +686,7 @@ int mardyn_set_workspace(mardyn_ctx* ctx, void* device_ptr, size_t bytes, int64_
     CK(cudaMemcpyAsync(ctx->dmodel, &ctx->model, sizeof(DevModel), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemsetAsync(ctx->step_ctr, 0, 8, ctx->stream));
     CK(cudaMemsetAsync(ctx->flag, 0, 4, ctx->stream));
+    CK(cudaMemsetAsync(ctx->fin_ticket, 0, 4, ctx->stream));
     CK(cudaMemsetAsync(ctx->hist, 0, sizeof(ObsRec) * MD_HISTORY, ctx->stream));
     if (ctx->nranks > 1) {
         CK(cudaMemcpyAsync(ctx->owner, ctx->h_owner.data(), ctx->g.ncell, cudaMemcpyHostToDevice, ctx->stream));
@@ -765,8 +795,8 @@ int mardyn_compute_forces(mardyn_ctx* ctx)
         k_kinetic<false><<<ctx->nkblocks, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->vel[b], nullptr, nullptr,
                                                        ctx->force, nullptr, ctx->kpart);
     // kpart beyond the used blocks stays from earlier steps: same block count
-    k_finalize<<<1, 1024, 0, s>>>(ctx->nfpart, ctx->fpart, ctx->nkblocks,
-                                  ctx->kpart, ctx->ndof, ctx->step_ctr, 0, ctx->hist);
+    k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, ctx->nkblocks, ctx->kpart, ctx->ndof,
+                                                  ctx->step_ctr, 0, ctx->hist, ctx->fin_scratch, ctx->fin_ticket);
     ctx->launches += 3;
     CK(cudaGetLastError());
     ctx->last_obs = ctx->host_step;
@@ -1091,8 +1121,8 @@ int mardyn_dd_begin_step(mardyn_ctx* ctx, int64_t* send_counts)
         k_integrate<false, true><<<nkb, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b], nullptr,
                                                      nullptr, ctx->force, ctx->torque, ctx->cell_of, ctx->rank,
                                                      ctx->count, ctx->kpart, ctx->flag, dd);
-    k_finalize<<<1, 1024, 0, s>>>(ctx->nfpart, ctx->fpart, nkb, ctx->kpart,
-                                  ctx->ndof, ctx->step_ctr, 1, ctx->hist, 0);
+    k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, nkb, ctx->kpart, ctx->ndof,
+                                                  ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket, 0);
     ctx->launches += 3;
     CK(cudaGetLastError());
     std::vector<int> cnt(ctx->nranks);
