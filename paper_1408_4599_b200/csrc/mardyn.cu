@@ -14,6 +14,7 @@
 #include "decomp.hpp"
 #include "kernels_force.cuh"
 #include "kernels_lj1.cuh"
+#include "kernels_rigid.cuh"
 #include "kernels_state.cuh"
 
 namespace {
@@ -338,12 +339,12 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false)
     const int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ:
-        k_force_rigid<2, 0, 0, 1, false, RIG_WARPS>
-            <<<ctx->force_blocks, threads, rigid_smem<2, 0, 0, 1, RIG_WARPS>(), ctx->stream>>>(a);
+        rig2::k_force_rigid2<2, 0, 0, 1, RIG_WARPS>
+            <<<ctx->force_blocks, threads, rig2::smem_bytes<2, 0, 0, 1, RIG_WARPS>(), ctx->stream>>>(a);
         break;
     case SHAPE_TIP4P:
-        k_force_rigid<1, 3, 0, 0, false, RIG_WARPS>
-            <<<ctx->force_blocks, threads, rigid_smem<1, 3, 0, 0, RIG_WARPS>(), ctx->stream>>>(a);
+        rig2::k_force_rigid2<1, 3, 0, 0, RIG_WARPS>
+            <<<ctx->force_blocks, threads, rig2::smem_bytes<1, 3, 0, 0, RIG_WARPS>(), ctx->stream>>>(a);
         break;
     case SHAPE_GEN:
         k_force_rigid<4, 4, 2, 2, true, GEN_WARPS>
@@ -534,15 +535,15 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
     int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ: {
-        auto k = k_force_rigid<2, 0, 0, 1, false, RIG_WARPS>;
-        const int sm = rigid_smem<2, 0, 0, 1, RIG_WARPS>();
+        auto k = rig2::k_force_rigid2<2, 0, 0, 1, RIG_WARPS>;
+        const int sm = rig2::smem_bytes<2, 0, 0, 1, RIG_WARPS>();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         ctx->force_blocks = occupancy_grid(ctx, k, threads, sm);
         break;
     }
     case SHAPE_TIP4P: {
-        auto k = k_force_rigid<1, 3, 0, 0, false, RIG_WARPS>;
-        const int sm = rigid_smem<1, 3, 0, 0, RIG_WARPS>();
+        auto k = rig2::k_force_rigid2<1, 3, 0, 0, RIG_WARPS>;
+        const int sm = rig2::smem_bytes<1, 3, 0, 0, RIG_WARPS>();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         ctx->force_blocks = occupancy_grid(ctx, k, threads, sm);
         break;
