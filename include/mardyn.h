@@ -137,7 +137,11 @@ int mardyn_set_workspace(struct mardyn_ctx* ctx, void* device_ptr, size_t bytes,
  * t0 and the library applies the backward half kick v -= dt/2 F/m,
  * j -= dt/2 tau with F(t0), tau(t0) (A8); 1: v, j are already
  * v(t0 - dt/2), j(t0 - dt/2), as returned by mardyn_get_molecules.
- * The arrays are copied to the device and converted there.
+ * The arrays are copied to the device and converted and validated there
+ * (pinned host buffers are DMA'd directly).  Errors: MARDYN_EINVAL for n
+ * outside [1, capacity], missing arrays, or any molecule with a non-finite
+ * r or v, a component id outside [0, n_comps) or |q|^2 off 1 by 1e-5 (the
+ * context then holds no molecules); MARDYN_ESTATE before set_workspace.
  */
 int mardyn_set_molecules(struct mardyn_ctx* ctx, int64_t n, const int64_t* id,
                          const int32_t* comp, const double* r, const double* v,

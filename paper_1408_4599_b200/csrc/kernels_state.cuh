@@ -15,12 +15,27 @@ __global__ void k_ingest(int n, const double* __restrict__ r, const double* __re
                          const int* __restrict__ comp, GridP g, uint4* __restrict__ pos,
                          float4* __restrict__ vel, float4* __restrict__ quat,
                          float4* __restrict__ angm, int* __restrict__ cell_of,
-                         int* __restrict__ rank, int* __restrict__ count,
+                         int* __restrict__ rank, int* __restrict__ count, int ncomp, int* __restrict__ flag,
                          const uint8_t* __restrict__ owner = nullptr,
                          const uint32_t* __restrict__ gmask = nullptr, int me = 0)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
+    // input validation (mardyn.h: finite r, v; component in range; unit quaternions):
+    // an invalid molecule is dropped and flags the call (MARDYN_EINVAL)
+    bool ok = comp[i] >= 0 && comp[i] < ncomp;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ok = ok && isfinite(r[3 * i + k]) && isfinite(v[3 * i + k]);
+    if (q) {
+        const double qn = q[4 * i] * q[4 * i] + q[4 * i + 1] * q[4 * i + 1] + q[4 * i + 2] * q[4 * i + 2] +
+                          q[4 * i + 3] * q[4 * i + 3];
+        ok = ok && fabs(qn - 1.0) < 1e-5;
+    }
+    if (!ok) {
+        atomicOr(flag, 512);
+        cell_of[i] = -1;
+        return;
+    }
     uint32_t u[3];
     int c[3];
 #pragma unroll
@@ -51,6 +66,12 @@ __global__ void k_ingest(int n, const double* __restrict__ r, const double* __re
     int cl = c[0] + g.nc[0] * (c[1] + g.nc[1] * c[2]);
     cell_of[i] = cl;
     rank[i] = atomicAdd(&count[cl], 1);
+}
+
+__global__ void k_iota64(int n, int64_t* __restrict__ a)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = i;
 }
 
 // ------------------------------------------------------------------------

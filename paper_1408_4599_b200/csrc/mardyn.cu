@@ -113,7 +113,9 @@ struct mardyn_ctx {
     long long host_step = 0;       // number of completed steps
     long long last_obs = -1;       // history index of the last evaluated time
     std::vector<int64_t> ids;
-    std::vector<int32_t> comp_host;
+    std::vector<int32_t> comp_host;    // decomposed runs only (host-side egress merge)
+    int64_t* ids_dev = nullptr;        // caller ids, input order
+    int32_t* comp_dev = nullptr;       // components, input order
     // graphs: one time step starting from buffer parity 0 / 1
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     cudaEvent_t ev_f0[2] = {nullptr, nullptr}, ev_f1[2] = {nullptr, nullptr};
@@ -634,6 +636,8 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     DevModel* dmodel = (DevModel*)take(sizeof(DevModel));
     const size_t stage_bytes = (size_t)cap * (19 * 8 + 3 * 4 + 4 + 4);
     char* stage = take(stage_bytes);
+    int64_t* ids_dev = (int64_t*)take(8 * (size_t)cap);
+    int32_t* comp_dev = (int32_t*)take(4 * (size_t)cap);
     uint8_t* owner = nullptr;
     uint32_t* gmask = nullptr;
     int8_t* owned = nullptr;
@@ -658,6 +662,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         ctx->nfw = nfw; ctx->nfpart = nfw + nbc; ctx->blk_ctr = blk_ctr;
         ctx->hist = hist; ctx->step_ctr = step_ctr; ctx->flag = flag; ctx->dmodel = dmodel;
         ctx->stage = stage; ctx->stage_bytes = stage_bytes;
+        ctx->ids_dev = ids_dev; ctx->comp_dev = comp_dev;
         ctx->owner = owner; ctx->gmask = gmask; ctx->owned = owned; ctx->sendbuf = sendbuf;
         ctx->recvbuf = recvbuf; ctx->send_cnt = send_cnt; ctx->seg_cap = seg_cap; ctx->recv_cap = recv_cap;
         ctx->ncell_pad = ncell_pad; ctx->ntiles = ntiles; ctx->nkblocks = nk;
@@ -710,23 +715,21 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
     if (!comp || !r || !v) return fail(ctx, MARDYN_EINVAL, "comp, r, v are required");
     if (ctx->rigid && (!q || !j)) return fail(ctx, MARDYN_EINVAL, "q and j are required for rigid molecules");
     const int ncomp = (int)ctx->comps.size();
-    for (int64_t i = 0; i < n; ++i) {
-        if (comp[i] < 0 || comp[i] >= ncomp) return fail(ctx, MARDYN_EINVAL, "component id out of range");
-        for (int k = 0; k < 3; ++k)
-            if (!std::isfinite(r[3 * i + k]) || !std::isfinite(v[3 * i + k]))
-                return fail(ctx, MARDYN_EINVAL, "non-finite position or velocity");
-        if (ctx->rigid) {
-            double qn = q[4 * i] * q[4 * i] + q[4 * i + 1] * q[4 * i + 1] + q[4 * i + 2] * q[4 * i + 2] +
-                        q[4 * i + 3] * q[4 * i + 3];
-            if (!(std::fabs(qn - 1.0) < 1e-5)) return fail(ctx, MARDYN_EINVAL, "quaternions must be unit");
-        }
-    }
+    // per-molecule validation runs on the device (k_ingest); the host keeps copies of
+    // ids and components only for the decomposed egress
     ctx->n = n;
-    ctx->ids.resize(n);
-    ctx->comp_host.assign(comp, comp + n);
-    for (int64_t i = 0; i < n; ++i) ctx->ids[i] = id ? id[i] : i;
+    if (ctx->nranks > 1) {
+        ctx->ids.resize(n);
+        ctx->comp_host.assign(comp, comp + n);
+        for (int64_t i = 0; i < n; ++i) ctx->ids[i] = id ? id[i] : i;
+    }
     double ndof = 3.0 * n;
-    for (int64_t i = 0; i < n; ++i) ndof += ctx->model.comp[comp[i]].rot * (ctx->rigid ? 1 : 0);
+    if (ctx->rigid) {
+        if (ncomp == 1) ndof += (double)ctx->model.comp[0].rot * n;
+        else
+            for (int64_t i = 0; i < n; ++i)
+                if (comp[i] >= 0 && comp[i] < ncomp) ndof += ctx->model.comp[comp[i]].rot;
+    }
     ctx->ndof = ctx->ndof_global > 0 ? ctx->ndof_global : ndof;
     ctx->n_input = n;
     cudaStream_t s = ctx->stream;
@@ -742,13 +745,18 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
         CK(cudaMemcpyAsync(dq, q, sizeof(double) * 4 * n, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(dj, j, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
     }
-    CK(cudaMemcpyAsync(dc, comp, sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->comp_dev, comp, sizeof(int) * n, cudaMemcpyHostToDevice, s));
+    if (id) CK(cudaMemcpyAsync(ctx->ids_dev, id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
+    else k_iota64<<<nblk(n, 256), 256, 0, s>>>((int)n, ctx->ids_dev);
+    (void)dc;
     CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
     CK(cudaMemsetAsync(ctx->flag, 0, 4, s));
     const int src = 1, dst = 0;
-    k_ingest<<<nblk(n, 256), 256, 0, s>>>((int)n, dr, dv, ctx->rigid ? dq : nullptr, ctx->rigid ? dj : nullptr, dc,
-                                           ctx->g, ctx->pos[src], ctx->vel[src], ctx->rigid ? ctx->quat[src] : nullptr,
+    k_ingest<<<nblk(n, 256), 256, 0, s>>>((int)n, dr, dv, ctx->rigid ? dq : nullptr, ctx->rigid ? dj : nullptr,
+                                           ctx->comp_dev, ctx->g, ctx->pos[src], ctx->vel[src],
+                                           ctx->rigid ? ctx->quat[src] : nullptr,
                                            ctx->rigid ? ctx->angm[src] : nullptr, ctx->cell_of, ctx->rank, ctx->count,
+                                           ncomp, ctx->flag,
                                            ctx->nranks > 1 ? ctx->owner : nullptr,
                                            ctx->nranks > 1 ? ctx->gmask : nullptr, ctx->rank_id());
     ctx->launches += 1;
@@ -775,7 +783,15 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
         ctx->launches += 1;
     }
     CK(cudaGetLastError());
+    int hflag = 0;
+    CK(cudaMemcpyAsync(&hflag, ctx->flag, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (hflag & 512) {
+        ctx->loaded = false;
+        CK(cudaMemsetAsync(ctx->flag, 0, 4, s));
+        return fail(ctx, MARDYN_EINVAL, "invalid input: non-finite position or velocity, component id out of "
+                                        "range, or non-unit quaternion");
+    }
     ctx->loaded = true;
     ctx->last_obs = -1;
     return MARDYN_OK;
@@ -964,8 +980,8 @@ int mardyn_get_molecules(mardyn_ctx* ctx, int64_t cap, int64_t* n, int64_t* id, 
     if (ctx->nranks > 1)      // the rank's owned molecules, with their ids
         return egress(ctx, r, v, q, j, nullptr, nullptr, nullptr, nullptr, -1, n, id, comp);
     *n = ctx->n;
-    if (id) std::memcpy(id, ctx->ids.data(), sizeof(int64_t) * ctx->n);
-    if (comp) std::memcpy(comp, ctx->comp_host.data(), sizeof(int32_t) * ctx->n);
+    if (id) CK(cudaMemcpyAsync(id, ctx->ids_dev, sizeof(int64_t) * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
+    if (comp) CK(cudaMemcpyAsync(comp, ctx->comp_dev, sizeof(int32_t) * ctx->n, cudaMemcpyDeviceToHost, ctx->stream));
     return egress(ctx, r, v, q, j, nullptr, nullptr, nullptr, nullptr);
 }
 

@@ -180,6 +180,16 @@ def test_errors(md):
     with pytest.raises(md.MardynError) as e:
         ctx.step(1)
     assert e.value.code == -7
+    r = s["r"].copy()
+    r[17, 1] = np.nan                             # invalid input: validated on the device
+    with pytest.raises(md.MardynError) as e:
+        ctx.set_molecules(r, s["v"], comp=s["comp"], half_step=1)
+    assert e.value.code == -1
+    comp = s["comp"].copy()
+    comp[5] = 3
+    with pytest.raises(md.MardynError) as e:
+        ctx.set_molecules(s["r"], s["v"], comp=comp, half_step=1)
+    assert e.value.code == -1
     v = s["v"].copy()
     v[0] = [1e5, 0, 0]
     ctx.set_molecules(s["r"], v, comp=s["comp"], half_step=1)
