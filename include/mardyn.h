@@ -219,7 +219,10 @@ int mardyn_kd_decompose(const double* cost, int32_t nx, int32_t ny, int32_t nz, 
  * molecules in boxes[rank] and holds halo copies of the molecules in the
  * cells within one cell (>= rc) of its box.  ndof_global: the
  * degrees of freedom of the whole system (T of the rank-local observables
- * then sums to the global T).  Must precede mardyn_workspace_bytes.
+ * then sums to the global T).  The first call must precede
+ * mardyn_workspace_bytes; a later call with the same nranks re-partitions
+ * (rebalancing): the context then holds no molecules until
+ * the next set_molecules (half_step = 1 resumes exactly).
  * set_molecules then takes the GLOBAL arrays on every rank and keeps owned
  * and halo molecules.  A time step is
  *     mardyn_dd_begin_step -> transport -> mardyn_dd_end_step

@@ -1061,7 +1061,10 @@ int mardyn_set_decomposition(mardyn_ctx* ctx, int32_t rank, int32_t nranks, cons
                              double ndof_global)
 {
     if (!ctx) return MARDYN_EINVAL;
-    if (ctx->ws) return fail(ctx, MARDYN_ESTATE, "set_decomposition must precede workspace_bytes/set_workspace");
+    // first call before the workspace (its layout depends on nranks); later calls
+    // (rebalancing) keep nranks and re-upload the cell maps
+    if (ctx->ws && nranks != ctx->nranks)
+        return fail(ctx, MARDYN_ESTATE, "set_decomposition after set_workspace must keep nranks");
     if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks || !boxes)
         return fail(ctx, MARDYN_EINVAL, "bad rank / nranks (1..32) / boxes");
     const GridP& g0 = ctx->g;
@@ -1103,6 +1106,13 @@ int mardyn_set_decomposition(mardyn_ctx* ctx, int32_t rank, int32_t nranks, cons
     GridP& g = ctx->g;
     for (int k = 0; k < 3; ++k) { g.hlo[k] = b[k]; g.hdim[k] = b[3 + k] - b[k]; }
     g.nhome = g.hdim[0] * g.hdim[1] * g.hdim[2];
+    if (ctx->ws) {          // rebalance: new maps; the caller reloads the molecules (set_molecules)
+        CK(cudaMemcpyAsync(ctx->owner, ctx->h_owner.data(), ctx->g.ncell, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->gmask, ctx->h_gmask.data(), 4 * (size_t)ctx->g.ncell, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->loaded = false;
+    }
     return MARDYN_OK;
 }
 

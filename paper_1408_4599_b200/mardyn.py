@@ -429,18 +429,23 @@ class DecomposedRun:
     transport = "nccl": one rank per process/GPU, records move with
     torch.distributed all_to_all over NCCL (NVLink)."""
 
-    def __init__(self, system, nranks, transport="loopback", rank=None, eta=None, boxes=None, stream=None):
+    def __init__(self, system, nranks, transport="loopback", rank=None, eta=None, boxes=None, stream=None,
+                 rebalance_interval=0):
         import torch
         self.torch = torch
         self.system = system
         self.nranks = nranks
         self.transport = transport
+        self.rank = rank
+        self.rebalance_interval = int(rebalance_interval)   # steps between re-partitions (0: static)
+        self.nsteps = 0
         cost = global_costs(system)
         if boxes is None:
             boxes, loads = kd_decompose(cost, nranks)
         self.boxes = np.asarray(boxes).reshape(nranks, 2, 3)
         flat = np.concatenate([self.boxes[:, 0, :], self.boxes[:, 1, :]], axis=1)
         ndof = system_ndof(system)
+        self.ndof = ndof
         ranks = range(nranks) if transport == "loopback" else [rank]
         self.ctxs = []
         for r in ranks:
@@ -454,8 +459,50 @@ class DecomposedRun:
             self.ctxs.append(ctx)
         self.bufs = [c.dd_buffers() for c in self.ctxs]
 
+    def gather_molecules(self):
+        """All owned molecules of all ranks (v, j at t - dt/2), ordered by id."""
+        if self.transport == "loopback":
+            return self.molecules()
+        import torch.distributed as dist
+        parts = [None] * self.nranks
+        dist.all_gather_object(parts, self.ctxs[0].get_molecules())
+        ids = np.concatenate([p["id"] for p in parts])
+        order = np.argsort(ids)
+        return {k: np.concatenate([p[k] for p in parts])[order] for k in parts[0]}
+
+    def rebalance(self, boxes=None):
+        """Re-partition from the current cell counts (Eq. 6 cost of reading A19,
+        k-d tree with alternating axes and minimum-imbalance planes)
+        and reload every rank's owned + halo molecules (exact resume).  Returns
+        the new boxes."""
+        m = self.gather_molecules()
+        now = dict(self.system)
+        now["r"], now["comp"] = m["r"], m["comp"]
+        if boxes is None:
+            boxes, _ = kd_decompose(global_costs(now), self.nranks)
+        self.boxes = np.asarray(boxes).reshape(self.nranks, 2, 3)
+        flat = np.concatenate([self.boxes[:, 0, :], self.boxes[:, 1, :]], axis=1)
+        ranks = range(self.nranks) if self.transport == "loopback" else [self.rank]
+        for r, ctx in zip(ranks, self.ctxs):
+            ctx.set_decomposition(r, self.nranks, flat, self.ndof)
+            ctx.set_molecules(m["r"], m["v"], comp=m["comp"], q=m["q"], j=m["j"], id=m["id"], half_step=1)
+        self.bufs = [c.dd_buffers() for c in self.ctxs]
+        return self.boxes
+
+    def owned_counts(self):
+        """Owned molecules per rank (load balance check)."""
+        if self.transport == "loopback":
+            return [len(c.get_molecules()["id"]) for c in self.ctxs]
+        import torch.distributed as dist
+        parts = [None] * self.nranks
+        dist.all_gather_object(parts, len(self.ctxs[0].get_molecules()["id"]))
+        return parts
+
     def step(self, n=1):
         for _ in range(n):
+            if self.rebalance_interval and self.nsteps and self.nsteps % self.rebalance_interval == 0:
+                self.rebalance()
+            self.nsteps += 1
             counts = [c.dd_begin_step() for c in self.ctxs]
             if self.transport == "loopback":
                 for dst, cd in enumerate(self.ctxs):

@@ -365,15 +365,53 @@ def _pairs_within(P, L, dmin):
     return out
 
 
+def droplet(L=30.0, R=8.0, centre=(0.3, 0.55, 0.5), rho_l=0.73, rho_v=0.02, T=0.8, steps=100, seed_k=5):
+    """Off-centre LJTS droplet in its vapour (the paper's
+    heterogeneous droplet workload): liquid FCC points of
+    density rho_l inside a sphere of radius R at centre * L, vapour at rho_v
+    outside it (uniform candidates, 1 sigma sequential rejection against
+    accepted vapour and 1 sigma clear of the sphere), cubic periodic box."""
+    rng = np.random.default_rng(SEED + seed_k)
+    box = np.array([L, L, L])
+    a = (4.0 / rho_l) ** (1.0 / 3.0)
+    n = int(np.ceil(L / a))
+    X = fcc(n, a)
+    c = np.asarray(centre) * L
+    d = X - c
+    d -= box * np.round(d / box)
+    liq = X[np.einsum("ij,ij->i", d, d) < R * R]
+    vol_v = L ** 3 - 4.0 / 3.0 * np.pi * (R + 1.0) ** 3
+    N_v = int(round(rho_v * vol_v))
+    acc = np.zeros((0, 3))
+    while len(acc) < N_v:
+        cand = rng.uniform(size=(4096, 3)) * box
+        dc = cand - c
+        dc -= box * np.round(dc / box)
+        cand = cand[np.einsum("ij,ij->i", dc, dc) > (R + 1.0) ** 2]
+        for p in cand:
+            if len(acc) >= N_v:
+                break
+            if len(acc):
+                dd = acc - p
+                dd -= box * np.round(dd / box)
+                if np.min(np.einsum("ij,ij->i", dd, dd)) < 1.0:
+                    continue
+            acc = np.vstack([acc, p])
+    X = np.concatenate([liq, acc]) % box
+    V = maxwell_boltzmann(rng, len(X), 1.0, T)
+    return _system("droplet", box, 2.5, 0.002, steps, T, [lj1_component()], X, V)
+
+
 def config(name):
     """Config by name: 'c0'..'c4' at full size, or scaled parity variants
-    'c1s', 'c2s', 'c3s', 'c4s'."""
+    'c1s', 'c2s', 'c3s', 'c4s'; 'droplet' (heterogeneous, off-centre)."""
     table = {
         "c0": config0,
         "c1": config1, "c1s": lambda: config1(10),
         "c2": config2, "c2s": lambda: config2(16),
         "c3": config3, "c3s": lambda: config3(7),
         "c4": config4, "c4s": lambda: config4(16),
+        "droplet": droplet,
     }
     return table[name]()
 

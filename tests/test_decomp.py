@@ -196,3 +196,23 @@ def test_gloo_exchange_records():
         n, rows = result[dst]
         expect = [[src, dst, k] for src in range(2) for k in range((src + dst) % 3 + 1)]
         assert n == len(expect) and rows == expect
+
+
+def test_droplet_kd_beats_static_split():
+    """Heterogeneous workload (off-centre droplet; the
+    direction of Fig. 7): the cost-weighted k-d tree balances the
+    Eq. 6 load far better than equal-volume boxes."""
+    s = S.droplet(L=50.0, R=13.0)                # 20 cells per axis
+    cost = M.global_costs(s)
+    nz, ny, nx = cost.shape
+    for p in (2, 4, 8):
+        boxes, loads = M.kd_decompose(cost, p)
+        assert loads.sum() == pytest.approx(cost.sum())
+        kd = loads.max() / loads.mean()
+        # static: equal slabs along x (p = 2), then also y (4), then z (8)
+        cuts = [[0, nx // 2, nx], [0, ny // 2, ny] if p >= 4 else [0, ny], [0, nz // 2, nz] if p >= 8 else [0, nz]]
+        st = [cost[z0:z1, y0:y1, x0:x1].sum()
+              for x0, x1 in zip(cuts[0], cuts[0][1:]) for y0, y1 in zip(cuts[1], cuts[1][1:])
+              for z0, z1 in zip(cuts[2], cuts[2][1:])]
+        static = max(st) / np.mean(st)
+        assert kd < 1.25 and static > 1.5 * kd, (p, kd, static)
