@@ -91,6 +91,10 @@ def lib():
         _lib.or_run.argtypes = [P(Sys), C.c_double, C.c_int64, C.c_void_p, C.c_void_p,
                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                 C.c_int, C.c_int, P(Obs)]
+        _lib.or_run_nvt.argtypes = [P(Sys), C.c_double, C.c_int64, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
+                                    C.c_int, C.c_int, C.c_double, C.c_int, P(Obs)]
+        _lib.or_lj_tail.argtypes = [P(Sys), C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
     return _lib
 
 
@@ -210,9 +214,19 @@ class System:
             raise RuntimeError(f"oracle forces failed ({rc})")
         return F, tau, {"U": tot.U, "W": tot.W, "npairs": tot.npairs}
 
-    def run(self, dt, comp, u, v, q, j, nsteps, half_step=0, mode="full", nthreads=0):
+    def lj_tail(self, counts, volume):
+        """Isotropic LJ tail corrections (U_lrc, W_lrc) for molecule counts per
+        component in the given volume (reading A3)."""
+        c = np.ascontiguousarray(counts, np.int64)
+        U = np.zeros(1); W = np.zeros(1)
+        lib().or_lj_tail(C.byref(self.s), _ptr(c), float(volume), _ptr(U), _ptr(W))
+        return float(U[0]), float(W[0])
+
+    def run(self, dt, comp, u, v, q, j, nsteps, half_step=0, mode="full", nthreads=0, T_target=0.0,
+            thermostat_interval=0):
         """Leapfrog + Fincham for nsteps; returns (u, v, q, j, obs) with obs a
-        structured array of per-step (U, W, KEt, KEr, T, npairs) at t_k."""
+        structured array of per-step (U, W, KEt, KEr, T, npairs) at t_k.
+        T_target > 0: NVT velocity rescaling every thermostat_interval steps (A24)."""
         comp = np.ascontiguousarray(comp, np.int32)
         u = np.array(u, dtype=np.uint32, order="C")
         v = np.array(v, dtype=np.float64, order="C")
@@ -220,8 +234,9 @@ class System:
         j = np.array(j, dtype=np.float64, order="C")
         obs = (Obs * max(nsteps, 1))()
         m = {"brute": 0, "cells": 1, "full": 2}[mode]
-        rc = lib().or_run(C.byref(self.s), float(dt), len(u), _ptr(comp), _ptr(u), _ptr(v),
-                          _ptr(q), _ptr(j), int(nsteps), int(half_step), m, int(nthreads), obs)
+        rc = lib().or_run_nvt(C.byref(self.s), float(dt), len(u), _ptr(comp), _ptr(u), _ptr(v),
+                              _ptr(q), _ptr(j), int(nsteps), int(half_step), m, int(nthreads),
+                              float(T_target), int(thermostat_interval), obs)
         if rc:
             raise RuntimeError(f"or_run failed ({rc})")
         out = np.array([(o.U, o.W, o.KEt, o.KEr, o.T, o.npairs) for o in obs[:nsteps]],

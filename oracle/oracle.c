@@ -21,7 +21,10 @@
  *             (the plain definition), the linked-cell Newton-3 half shell
  *             (Fig. 1) and a full 27-cell shell per molecule.
  *   integrate leapfrog Eqs. 2-3 and the Fincham quaternion
- *             leapfrog reading of Eqs. 4-5 (A7), A8 start, A9 T.
+ *             leapfrog reading of Eqs. 4-5 (A7), A8 start, A9 T;
+ *             NVT by velocity rescaling (reading A24).
+ *   tail      isotropic mean-field LJ corrections of U and W beyond rc
+ *             (reading A3: reported separately, not part of U_pot).
  */
 #include <math.h>
 #include <stdint.h>
@@ -597,9 +600,9 @@ typedef struct {
  * On return u, v, q, j hold r(t_n), v(t_n - dt/2), q(t_n), j(t_n - dt/2).
  * mode 0 = brute force, 1 = linked cells (half shell), 2 = full shell/OpenMP.
  */
-int or_run(const or_sys* S, double dt, int64_t n, const int32_t* comp, uint32_t* u,
-           double* v, double* q, double* j, int nsteps, int half_step, int mode,
-           int nthreads, or_obs* obs)
+int or_run_nvt(const or_sys* S, double dt, int64_t n, const int32_t* comp, uint32_t* u,
+               double* v, double* q, double* j, int nsteps, int half_step, int mode,
+               int nthreads, double T_target, int interval, or_obs* obs)
 {
     double* F = (double*)malloc(sizeof(double) * 3 * (n ? n : 1));
     double* tau = (double*)malloc(sizeof(double) * 3 * (n ? n : 1));
@@ -677,7 +680,59 @@ int or_run(const or_sys* S, double dt, int64_t n, const int32_t* comp, uint32_t*
         obs[step].KEr = KEr;
         obs[step].T = 2.0 * (KEt + KEr) / (double)ndof;
         obs[step].npairs = tot.npairs;
+        /* NVT ("kept constant by velocity rescaling"; reading A24): after every
+         * interval-th step the half-step velocities and angular momenta are scaled by
+         * lambda = sqrt(T_target / T(t_k)) */
+        if (T_target > 0 && interval > 0 && (step + 1) % interval == 0) {
+            if (!(obs[step].T > 0)) { rc = -3; break; }
+            const double lambda = sqrt(T_target / obs[step].T);
+            for (int64_t i = 0; i < 3 * n; ++i) { v[i] *= lambda; j[i] *= lambda; }
+        }
     }
     free(F); free(tau); free(ui); free(wi); free(npi);
     return rc;
+}
+
+int or_run(const or_sys* S, double dt, int64_t n, const int32_t* comp, uint32_t* u,
+           double* v, double* q, double* j, int nsteps, int half_step, int mode,
+           int nthreads, or_obs* obs)
+{
+    return or_run_nvt(S, dt, n, comp, u, v, q, j, nsteps, half_step, mode, nthreads, 0.0, 0, obs);
+}
+
+/* ------------------------------------------------------------------------ */
+/* isotropic LJ tail corrections ("isotropic cut-off corrections ... a  */
+/* mean-field integral for the dispersive interaction"; reading A3): with     */
+/* g(r) = 1 beyond rc, for every ordered pair of components and every LJ     */
+/* site pair (a, b) with sigma, eps mixed as in the forces:           */
+/*   U_lrc = (1/2) sum N_ci N_cj / V  int_rc^inf u_ab(r) 4 pi r^2 dr          */
+/*   W_lrc = -(1/2) sum N_ci N_cj / V int_rc^inf r u_ab'(r) 4 pi r^2 dr        */
+/* with u_ab the plain 12-6 potential (the shift of LJTS does not act beyond  */
+/* rc).  The integrals in closed form:                                        */
+/*   int_rc^inf u 4 pi r^2 dr    = 16 pi eps sig^3 [ (sig/rc)^9 / 9 - (sig/rc)^3 / 3 ] */
+/*   int_rc^inf r u' 4 pi r^2 dr = 16 pi eps sig^3 [ -4/3 (sig/rc)^9 + 2 (sig/rc)^3 ] */
+void or_lj_tail(const or_sys* S, const int64_t* counts, double volume, double* U, double* W)
+{
+    double u = 0.0, w = 0.0;
+    for (int ci = 0; ci < S->n_comp; ++ci)
+        for (int cj = 0; cj < S->n_comp; ++cj) {
+            const double eta = S->eta ? S->eta[ci * S->n_comp + cj] : 1.0;
+            const double nn = (double)counts[ci] * (double)counts[cj] / volume;
+            const or_comp* A = &S->comp[ci];
+            const or_comp* B = &S->comp[cj];
+            for (int a = 0; a < A->nsites; ++a)
+                for (int b = 0; b < B->nsites; ++b) {
+                    const or_site* sa = &S->sites[A->site0 + a];
+                    const or_site* sb = &S->sites[B->site0 + b];
+                    if (sa->type != OR_LJ || sb->type != OR_LJ) continue;
+                    const double sig = 0.5 * (sa->sigma + sb->sigma);
+                    const double eps = eta * sqrt(sa->eps * sb->eps);
+                    const double x3 = pow(sig / S->rc, 3.0), x9 = x3 * x3 * x3;
+                    const double pre = 16.0 * 3.14159265358979323846 * eps * sig * sig * sig;
+                    u += 0.5 * nn * pre * (x9 / 9.0 - x3 / 3.0);
+                    w -= 0.5 * nn * pre * (-4.0 / 3.0 * x9 + 2.0 * x3);
+                }
+        }
+    *U = u;
+    *W = w;
 }

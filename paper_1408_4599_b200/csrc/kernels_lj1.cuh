@@ -189,29 +189,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
     const float ex = g.edge[0], inv_ex = 1.f / g.edge[0];
     long long ncw = 0;
 
-    // ---- n_candidates (27-cell full-shell count, reported observable):
-    //      sum over home cells of N_c (sum_27 N_c' - 1), lane-parallel over cells
-    for (int t = gw * 32 + lane; t < g.nhome; t += nw * 32) {
-        int cx, cy, cz;
-        const int c = home_cell(g, t, cx, cy, cz);
-        const int nc = __ldg(a.start + c + 1) - __ldg(a.start + c);
-        if (nc == 0) continue;
-        int tot = 0;
-        for (int dz = -1; dz <= 1; ++dz)
-            for (int dy = -1; dy <= 1; ++dy) {
-                const int rowc = nx * (wrapi(cy + dy, ny) + ny * wrapi(cz + dz, nz));
-                if (cx >= 1 && cx + 1 < nx) {
-                    tot += __ldg(a.start + rowc + cx + 2) - __ldg(a.start + rowc + cx - 1);
-                } else {
-                    for (int dx = -1; dx <= 1; ++dx) {
-                        const int c2 = rowc + wrapi(cx + dx, nx);
-                        tot += __ldg(a.start + c2 + 1) - __ldg(a.start + c2);
-                    }
-                }
-            }
-        ncw += (long long)nc * (tot - 1);
-    }
-
+    // n_candidates (27-cell full-shell count, reported observable): each home lane
+    // adds sum_27 N_c' - 1 for its molecule (from the staged cell table or start[])
     const int nsorted = __ldg(a.start + g.ncell);
     const int nblocks = (nsorted + 31) >> 5;
     for (int b = nblocks + gw * 32 + lane; b < a.nbcap; b += nw * 32)     // unused block partials
@@ -219,14 +198,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
     // blocks are handed out in sorted order by an atomic counter (load balance);
     // each block's sums go to its own slot, so totals do not depend on the schedule
     // (two consecutive blocks per fetch: they share most staged cells, which then hit in L1)
-    int nextb = 0;
-    if (lane == 0) nextb = atomicAdd(a.ctr, BLOCKS_PER_FETCH);
+    // first fetch static (no start-up contention on the counter), then dynamic
+    int nextb = BLOCKS_PER_FETCH * gw;
     int pend_mi = -1, pend_b = 0, pend_r = 0;          // deferred arrival rank (STEP)
     unsigned pend_m = 0;
     for (;;) {
         const int blk0 = __shfl_sync(0xffffffffu, nextb, 0);
         if (blk0 >= nblocks) break;
-        if (lane == 0) nextb = atomicAdd(a.ctr, BLOCKS_PER_FETCH);     // in flight during this fetch's work
+        if (lane == 0) nextb = BLOCKS_PER_FETCH * nw + atomicAdd(a.ctr, BLOCKS_PER_FETCH);   // in flight meanwhile
         const int blk1 = min(blk0 + BLOCKS_PER_FETCH, nblocks);
     for (int blk = blk0; blk < blk1; ++blk) {
         double Uw = 0.0, Ww = 0.0;
@@ -295,6 +274,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                 Acc A;
                 acc_zero(A);
                 if ((todo >> lane) & 1u) {
+                    int ncand_l = -1;                      // the molecule itself is no candidate
                     // cell-relative coordinates of the staging copy (read-only while the fused
                     // step advances pos in place): neighbour cell (dx, dy, dz) adds its offset, exact
                     const float4 xsi = __ldg(a.xs + mi);
@@ -306,6 +286,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                                 const float ox = (float)dx * ex;
                                 const int c2 = rowc + wrapi(cx + dx, nx);
                                 const int j0 = __ldg(a.start + c2), j1 = __ldg(a.start + c2 + 1);
+                                ncand_l += j1 - j0;
                                 for (int j = j0; j < j1; ++j) {
                                     if (j == mi) continue;
                                     const float4 xj = __ldg(a.xs + j);
@@ -318,6 +299,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                     Fown = make_float3(f * A.gx.x, f * A.gy.x, f * A.gz.x);
                     a.force[mi] = make_float4(Fown.x, Fown.y, Fown.z, 0.f);
                     const double Ad = A.a.x, Bd = A.b.x;
+                    ncw += ncand_l;
                     Uw += (double)a.eps4 * (Ad - Bd) - (double)a.shift * A.hits_exact;
                     Ww += (double)a.eps24 * (2.0 * Ad - Bd);
                     npw += A.hits_exact;
@@ -522,6 +504,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                 }
             }
             if (act) {
+                int nc27 = -1;                             // the molecule itself is no candidate
+                const int kk = cx - cA;                    // staged cells kk, kk+1, kk+2 hold its 27-cell rows
+#pragma unroll
+                for (int r = 0; r < 9; ++r) nc27 += scb[10 * r + kk + 3] - scb[10 * r + kk];
+                ncw += nc27;
                 const float f = -2.f * a.eps24;
                 const float gx = A.gx.x + A.gx.y, gy = A.gy.x + A.gy.y, gz = A.gz.x + A.gz.y;
                 Fown = make_float3(f * gx, f * gy, f * gz);
