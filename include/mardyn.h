@@ -151,8 +151,37 @@ int mardyn_set_molecules(struct mardyn_ctx* ctx, int64_t n, const int64_t* id,
 int mardyn_compute_forces(struct mardyn_ctx* ctx);
 
 /* n leapfrog steps (asynchronous; per step: forces at t_k, observables of
- * t_k, kick + drift + rotation, cell rebuild by counting sort).            */
+ * t_k, kick + drift + rotation, (NVT rescaling,) cell rebuild by counting
+ * sort).                                                                    */
 int mardyn_step(struct mardyn_ctx* ctx, int32_t n);
+
+/*
+ * NVT by velocity rescaling ("kept constant by velocity rescaling";
+ * reading A24 of DESIGN.md): after every interval-th step k the half-step
+ * velocities and angular momenta are scaled by sqrt(T_target / T(t_k)).
+ * T_target = 0 or interval = 0: NVE (default).  Errors: MARDYN_EINVAL for a
+ * negative or non-finite T_target or a negative interval; MARDYN_ESTATE on a
+ * decomposed context; a step with T(t_k) = 0 reports MARDYN_EUNSTABLE.
+ */
+int mardyn_set_thermostat(struct mardyn_ctx* ctx, double T_target, int32_t interval);
+
+/*
+ * Isotropic LJ tail corrections beyond the cutoff ("isotropic cut-off
+ * corrections", a mean-field integral with g(r) = 1; reading A3: reported
+ * beside U_pot and the virial, never added to them):
+ *   U = sum_{a,b} N_a N_b / (2V) sum_{LJ sites i of a, k of b} 16 pi eps sig^3 [(sig/rc)^9/9 - (sig/rc)^3/3]
+ *   W = sum_{a,b} N_a N_b / (2V) sum_{i,k} 16 pi eps sig^3 [4/3 (sig/rc)^9 - 2 (sig/rc)^3]
+ * with sig, eps mixed as in the forces (Lorentz-Berthelot * eta) and
+ * W in the convention of the reported virial (pressure correction W/(3V)).
+ * mardyn_lj_tail needs no context or GPU: comps as for mardyn_create, eta
+ * n_comps^2 or NULL, counts[a] molecules of component a in volume.
+ * mardyn_get_tail_corrections evaluates it for a loaded context (global
+ * counts, snapped box).  Errors: MARDYN_EINVAL (null pointers, volume or
+ * cutoff <= 0), MARDYN_ESTATE (no molecules).
+ */
+int mardyn_lj_tail(const mardyn_component* comps, int32_t n_comps, const double* eta, const int64_t* counts,
+                   double volume, double cutoff, double* U, double* W);
+int mardyn_get_tail_corrections(struct mardyn_ctx* ctx, double* U, double* W);
 
 /* Observables of the last evaluated time (A23): after step(n) from t0 this
  * is t_{n-1}; after compute_forces it is the current t.                     */

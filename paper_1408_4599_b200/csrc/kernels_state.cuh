@@ -543,6 +543,34 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finalize(int nfp, const ForcePa
     }
 }
 
+// NVT velocity rescaling ("kept constant by velocity rescaling";
+// reading A24): after the finalize of step k (step_ctr = k + 1), if
+// (k + 1) % interval == 0 the half-step velocities and angular momenta are
+// scaled by lambda = sqrt(T_target / T(t_k)).
+__global__ void k_rescale(int n, float4* __restrict__ vel, float4* __restrict__ angm,
+                          const ObsRec* __restrict__ hist, const long long* __restrict__ step_ctr,
+                          double T_target, int interval, int* __restrict__ flag)
+{
+    const long long k = *step_ctr - 1;
+    if (k < 0 || (k + 1) % interval != 0) return;
+    const double T = hist[k % MD_HISTORY].T;
+    if (!(T > 0.0)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flag, 1);
+        return;
+    }
+    const float lam = (float)sqrt(T_target / T);
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    float4 v = vel[t];
+    v.x *= lam; v.y *= lam; v.z *= lam;
+    vel[t] = v;
+    if (angm) {
+        float4 j = angm[t];
+        j.x *= lam; j.y *= lam; j.z *= lam;
+        angm[t] = j;
+    }
+}
+
 // ------------------------------------------------------------------------
 // egress: sorted state -> caller order (index = iid), doubles
 template <bool RIGID>

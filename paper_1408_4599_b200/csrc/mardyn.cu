@@ -115,6 +115,9 @@ struct mardyn_ctx {
     std::vector<int64_t> ids;
     std::vector<int32_t> comp_host;    // decomposed runs only (host-side egress merge)
     int64_t* ids_dev = nullptr;        // caller ids, input order
+    double T_target = 0.0;             // NVT (A24): 0 = NVE
+    int thermo_interval = 0;
+    std::vector<int64_t> comp_counts;  // molecules per component (tail corrections)
     int32_t* comp_dev = nullptr;       // components, input order
     // graphs: one time step starting from buffer parity 0 / 1
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
@@ -409,6 +412,17 @@ static int enqueue_sort(mardyn_ctx* ctx, int src, int dst, int64_t n_unsorted = 
 
 // one time step from buffer parity b (A23): forces at t_k, observables of
 // t_k, leapfrog + rotation, cell rebuild into parity 1-b
+// NVT (reading A24): rescale the half-step velocities of buffer b after the
+// finalize of the step (the kernel checks the cadence on the device)
+static void enqueue_thermostat(mardyn_ctx* ctx, int b)
+{
+    if (!(ctx->T_target > 0) || ctx->thermo_interval < 1) return;
+    const int n = (int)ctx->n;
+    k_rescale<<<nblk(n, 256), 256, 0, ctx->stream>>>(n, ctx->vel[b], ctx->rigid ? ctx->angm[b] : nullptr, ctx->hist,
+                                                     ctx->step_ctr, ctx->T_target, ctx->thermo_interval, ctx->flag);
+    ctx->launches += 1;
+}
+
 static int enqueue_step(mardyn_ctx* ctx, int b, bool timing_events)
 {
     cudaStream_t s = ctx->stream;
@@ -423,6 +437,7 @@ static int enqueue_step(mardyn_ctx* ctx, int b, bool timing_events)
         k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, 0, ctx->kpart, ctx->ndof,
                                                       ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket);
         ctx->launches += 1;
+        enqueue_thermostat(ctx, b);
         return enqueue_sort(ctx, b, 1 - b);
     }
     CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
@@ -437,6 +452,7 @@ static int enqueue_step(mardyn_ctx* ctx, int b, bool timing_events)
     k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, ctx->nkblocks, ctx->kpart, ctx->ndof,
                                                   ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket);
     ctx->launches += 2;
+    enqueue_thermostat(ctx, b);
     return enqueue_sort(ctx, b, 1 - b);
 }
 
@@ -459,8 +475,9 @@ static int build_graphs(mardyn_ctx* ctx)
 }
 
 static int launches_per_step(const mardyn_ctx* ctx)
-{   // force (+ integrate unless fused), finalize, scan, scatter, canon
-    return (ctx->kernel == KER_LJ1 && ctx->nranks == 1) ? 5 : 6;
+{   // force (+ integrate unless fused), finalize, (rescale,) scan, scatter, canon
+    return ((ctx->kernel == KER_LJ1 && ctx->nranks == 1) ? 5 : 6) +
+           ((ctx->T_target > 0 && ctx->thermo_interval > 0) ? 1 : 0);
 }
 
 // ------------------------------------------------------------------------
@@ -723,6 +740,11 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
         ctx->comp_host.assign(comp, comp + n);
         for (int64_t i = 0; i < n; ++i) ctx->ids[i] = id ? id[i] : i;
     }
+    ctx->comp_counts.assign(ncomp, 0);
+    if (ncomp == 1) ctx->comp_counts[0] = n;
+    else
+        for (int64_t i = 0; i < n; ++i)
+            if (comp[i] >= 0 && comp[i] < ncomp) ctx->comp_counts[comp[i]] += 1;
     double ndof = 3.0 * n;
     if (ctx->rigid) {
         if (ncomp == 1) ndof += (double)ctx->model.comp[0].rot * n;
@@ -818,6 +840,65 @@ int mardyn_compute_forces(mardyn_ctx* ctx)
     CK(cudaGetLastError());
     ctx->last_obs = ctx->host_step;
     return MARDYN_OK;
+}
+
+int mardyn_set_thermostat(mardyn_ctx* ctx, double T_target, int32_t interval)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (!(T_target >= 0) || !std::isfinite(T_target) || interval < 0)
+        return fail(ctx, MARDYN_EINVAL, "T_target must be finite and >= 0, interval >= 0");
+    if (ctx->nranks > 1 && T_target > 0)
+        return fail(ctx, MARDYN_ESTATE, "NVT rescaling is not available on decomposed contexts");
+    ctx->T_target = T_target;
+    ctx->thermo_interval = interval;
+    for (int b = 0; b < 2; ++b)                       // the step graphs change
+        if (ctx->gexec[b]) { cudaGraphExecDestroy(ctx->gexec[b]); ctx->gexec[b] = nullptr; }
+    return MARDYN_OK;
+}
+
+// isotropic LJ tail corrections (reading A3): with g(r) = 1 beyond rc,
+//   U = sum_{ci,cj} N_ci N_cj / (2V) sum_{LJ sites a,b} int_rc^inf u_ab 4 pi r^2 dr,
+//   W = -sum_{ci,cj} N_ci N_cj / (2V) sum_{a,b} int_rc^inf r u_ab' 4 pi r^2 dr,
+// u_ab the plain 12-6 potential with Lorentz-Berthelot * eta parameters
+int mardyn_lj_tail(const mardyn_component* comps, int32_t n_comps, const double* eta, const int64_t* counts,
+                   double volume, double cutoff, double* U, double* W)
+{
+    if (!comps || n_comps < 1 || !counts || !U || !W || !(volume > 0) || !(cutoff > 0)) return MARDYN_EINVAL;
+    const double pi = 3.14159265358979323846;
+    double u = 0.0, w = 0.0;
+    for (int a = 0; a < n_comps; ++a)
+        for (int b = 0; b < n_comps; ++b) {
+            const double e_ab = eta ? eta[a * n_comps + b] : 1.0;
+            const double dens = (double)counts[a] * (double)counts[b] / (2.0 * volume);
+            for (int i = 0; i < comps[a].n_lj; ++i)
+                for (int k = 0; k < comps[b].n_lj; ++k) {
+                    const mardyn_lj_site& p = comps[a].lj[i];
+                    const mardyn_lj_site& q = comps[b].lj[k];
+                    const double sig = 0.5 * (p.sigma + q.sigma), eps = e_ab * std::sqrt(p.epsilon * q.epsilon);
+                    const double s3 = (sig / cutoff) * (sig / cutoff) * (sig / cutoff), s9 = s3 * s3 * s3;
+                    const double c = 16.0 * pi * eps * sig * sig * sig * dens;
+                    u += c * (s9 / 9.0 - s3 / 3.0);
+                    w += c * (4.0 / 3.0 * s9 - 2.0 * s3);
+                }
+        }
+    *U = u;
+    *W = w;
+    return MARDYN_OK;
+}
+
+int mardyn_get_tail_corrections(mardyn_ctx* ctx, double* U, double* W)
+{
+    if (!ctx || !U || !W) return MARDYN_EINVAL;
+    if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    std::vector<mardyn_component> cs(ctx->comps.size());
+    for (size_t c = 0; c < cs.size(); ++c) {
+        std::memset(&cs[c], 0, sizeof(mardyn_component));
+        cs[c].n_lj = (int32_t)ctx->comps[c].lj.size();
+        cs[c].lj = ctx->comps[c].lj.data();
+    }
+    const double V = (double)ctx->g.P64[0] * ctx->g.P64[1] * ctx->g.P64[2] * (double)ctx->g.s * ctx->g.s * ctx->g.s;
+    return mardyn_lj_tail(cs.data(), (int32_t)cs.size(), ctx->eta.empty() ? nullptr : ctx->eta.data(),
+                          ctx->comp_counts.data(), V, ctx->rc, U, W);
 }
 
 int mardyn_step(mardyn_ctx* ctx, int32_t nsteps)

@@ -29,6 +29,7 @@ EXPORTS = ["mardyn_create", "mardyn_get_grid", "mardyn_workspace_bytes", "mardyn
            "mardyn_get_raw", "mardyn_last_step_timing", "mardyn_set_profiling",
            "mardyn_launch_count", "mardyn_cell_cost", "mardyn_kd_decompose",
            "mardyn_set_decomposition", "mardyn_dd_begin_step", "mardyn_dd_buffers", "mardyn_dd_end_step",
+           "mardyn_set_thermostat", "mardyn_lj_tail", "mardyn_get_tail_corrections",
            "mardyn_last_error", "mardyn_destroy"]
 
 
@@ -102,6 +103,10 @@ def load_library():
     lib.mardyn_get_molecules.argtypes = [vp, C.c_int64, P(C.c_int64), vp, vp, vp, vp, vp, vp]
     lib.mardyn_get_forces.argtypes = [vp, C.c_int64, vp, vp, P(C.c_int64), vp]
     lib.mardyn_set_decomposition.argtypes = [vp, C.c_int32, C.c_int32, vp, C.c_double]
+    lib.mardyn_set_thermostat.argtypes = [vp, C.c_double, C.c_int32]
+    lib.mardyn_lj_tail.argtypes = [P(Component), C.c_int32, vp, vp, C.c_double, C.c_double, P(C.c_double),
+                                   P(C.c_double)]
+    lib.mardyn_get_tail_corrections.argtypes = [vp, P(C.c_double), P(C.c_double)]
     lib.mardyn_dd_begin_step.argtypes = [vp, vp]
     lib.mardyn_dd_buffers.argtypes = [vp, P(vp), P(C.c_int64), P(vp), P(C.c_int64), P(C.c_int32)]
     lib.mardyn_dd_end_step.argtypes = [vp, C.c_int64]
@@ -287,6 +292,16 @@ class Context:
         return F[:m], tau[:m]
 
     # -- spatial decomposition (one context per rank) ----------------------
+    def set_thermostat(self, T_target, interval=1):
+        """NVT velocity rescaling every `interval` steps (reading A24); T_target = 0: NVE."""
+        self._check(self.lib.mardyn_set_thermostat(self.h, float(T_target), int(interval)))
+
+    def get_tail_corrections(self):
+        """Isotropic LJ tail corrections (U_lrc, W_lrc) of the loaded system (reading A3)."""
+        U, W = C.c_double(), C.c_double()
+        self._check(self.lib.mardyn_get_tail_corrections(self.h, C.byref(U), C.byref(W)))
+        return U.value, W.value
+
     def set_decomposition(self, rank, nranks, boxes, ndof_global):
         b = np.ascontiguousarray(np.asarray(boxes, dtype=np.int32).reshape(nranks, 6))
         self._dd_boxes = b
@@ -341,6 +356,21 @@ class Context:
 
     def launch_count(self):
         return int(self.lib.mardyn_launch_count(self.h))
+
+
+def lj_tail(components, counts, volume, cutoff, eta=None):
+    """Isotropic LJ tail corrections (U_lrc, W_lrc) for molecule counts per
+    component in a volume (mardyn_lj_tail; host code, no GPU needed)."""
+    lib = load_library()
+    arr, keep = _components(components)
+    c = np.ascontiguousarray(counts, dtype=np.int64)
+    e = None if eta is None else np.ascontiguousarray(eta, dtype=np.float64)
+    U, W = C.c_double(), C.c_double()
+    rc = lib.mardyn_lj_tail(arr, len(components), None if e is None else e.ctypes.data_as(C.c_void_p),
+                            c.ctypes.data_as(C.c_void_p), float(volume), float(cutoff), C.byref(U), C.byref(W))
+    if rc:
+        raise MardynError(rc, "lj_tail")
+    return U.value, W.value
 
 
 # host-side decomposition (no GPU needed)

@@ -48,3 +48,25 @@ def test_create_fails_loudly_without_gpu():
     s = S.config0()
     with pytest.raises(RuntimeError):
         mardyn.Context(s["box"], s["rc"], s["components"], s["dt"])
+
+
+def test_lj_tail_library_equals_oracle(oracle_mod):
+    """mardyn_lj_tail (host code of the library) against the oracle's
+    independent implementation (itself pinned by quadrature in
+    test_oracle_ensembles.py): single component and a mixture with eta."""
+    import numpy as np
+    import scenarios as S
+    from paper_1408_4599_b200 import mardyn
+    s = S.config0()
+    o = oracle_mod.System(s)
+    V = float(np.prod(o.box))
+    U, W = mardyn.lj_tail(s["components"], [4000], V, s["rc"])
+    Uo, Wo = o.lj_tail([4000], V)
+    assert U == pytest.approx(Uo, rel=1e-13) and W == pytest.approx(Wo, rel=1e-13)
+    comps = [S.c2_component(), S.lj1_component(sigma=1.2, eps=0.8)]
+    eta = np.array([[1.0, 0.9], [0.9, 1.0]])
+    s["components"] = comps
+    o = oracle_mod.System(s, eta=eta)
+    U, W = mardyn.lj_tail(comps, [300, 500], 2000.0, s["rc"], eta=eta)
+    Uo, Wo = o.lj_tail([300, 500], 2000.0)
+    assert U == pytest.approx(Uo, rel=1e-13) and W == pytest.approx(Wo, rel=1e-13)

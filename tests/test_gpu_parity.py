@@ -197,3 +197,31 @@ def test_errors(md):
     with pytest.raises(md.MardynError) as e:
         ctx.get_observables()
     assert e.value.code == -3
+
+
+def test_nvt_trajectory_and_tail(md, oracle_mod):
+    """NVT velocity rescaling (reading A24) toward T = 1.2 every 5 steps:
+    per-step U, W, T and final positions match the oracle's NVT run; the
+    tail corrections of the loaded system match the oracle's."""
+    s = S.config0()
+    nsteps = 20
+    ctx = md.from_system(s)
+    ctx.set_thermostat(1.2, 5)
+    ctx.step(nsteps)
+    hist = ctx.get_observable_history(nsteps)
+    mol = ctx.get_molecules()
+    o = oracle_mod.System(s)
+    u, v, q, j, obs = o.run(s["dt"], s["comp"], o.quantize(s["r"]), s["v"], s["q"], s["j"], nsteps,
+                            half_step=0, mode="full", T_target=1.2, thermostat_interval=5)
+    for k in range(nsteps):
+        assert hist[k]["n_pairs"] == obs["npairs"][k]
+        for key, ok in (("U_pot", "U"), ("virial", "W"), ("T", "T")):
+            assert_rel(hist[k][key], obs[ok][k], f"{key}[{k}]")
+    assert abs(hist[-1]["T"] - 1.2) < 0.1
+    d = min_image(mol["r"] - u * o.quantum, o.box)
+    assert np.abs(d).max() <= 1e-4
+    U, W = ctx.get_tail_corrections()
+    Uo, Wo = o.lj_tail([len(s["r"])], float(np.prod(o.box)))
+    assert U == pytest.approx(Uo, rel=1e-12) and W == pytest.approx(Wo, rel=1e-12)
+    with pytest.raises(md.MardynError):
+        ctx.set_thermostat(-1.0, 5)
