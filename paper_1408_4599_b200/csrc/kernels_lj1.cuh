@@ -397,12 +397,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(fmaxf(w2, 0.f)));
                     const bool on = act && w2 > 0.f;
                     const float xl = on ? xi - w : FAR, xh = on ? xi + w : -FAR;   // off: empty window
-                    int kl = min(max((int)floorf((xl - xlo) * inv_ex), 0), nsc - 1);
-                    kl -= (kl > 0 && xl < xlo + (float)kl * ex) ? 1 : 0;
-                    kl += (kl < nsc - 1 && xl >= xlo + (float)(kl + 1) * ex) ? 1 : 0;
-                    int kh = min(max((int)floorf((xh - xlo) * inv_ex), 0), nsc - 1);
-                    kh -= (kh > 0 && xh < xlo + (float)kh * ex) ? 1 : 0;
-                    kh += (kh < nsc - 1 && xh >= xlo + (float)(kh + 1) * ex) ? 1 : 0;
+                    // cell of each bound, rounded outward by 1e-3 cell (>> the 1e-6 rounding of the
+                    // product): a lower cell for xl / a higher cell for xh only widens the window
+                    const int kl = min(max(__float2int_rd(fmaf(xl - xlo, inv_ex, -1e-3f)), 0), nsc - 1);
+                    const int kh = min(max(__float2int_rd(fmaf(xh - xlo, inv_ex, 1e-3f)), 0), nsc - 1);
                     const int rb = srow[r];
                     // lower: first pair whose odd element is >= xl, in [floor(off_kl/2), floor(off_kl+1/2)]
                     la[r] = rb + (scb[10 * r + kl] >> 1);
