@@ -32,7 +32,7 @@
 namespace lj1 {
 
 constexpr int KMAX = 6;          // home cells per sub-chunk: staged |x| < 4 E (A12 quantum)
-constexpr int BLOCKS_PER_FETCH = 2;
+constexpr int BLOCKS_PER_FETCH = 1;
 constexpr int NSEG = 11;         // per-lane segments: 9 rows + self split + sentinel
 constexpr float FAR = 1.0e18f;   // padding coordinate (r^2 ~ 1e36, finite, never a hit)
 
