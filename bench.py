@@ -130,7 +130,7 @@ def run_reference(args, system, rank, world):
     line = {
         "impl": "reference", "metric": "MMUPS (million molecule-updates/s)", "value": value,
         "unit": "MMUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, BASELINE configs)",
         "config": {"workload": system["name"], "n_molecules": N, "sample_per_step": len(sample)},
         "cpu_baseline": {"value": value, "unit": "MMUPS", "cores": cores, "kind": "oracle",
@@ -293,12 +293,13 @@ def main():
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
         "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32 (fixed-point u32 positions, fp64 sums)",
+        "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded generator of BASELINE configs, no checkpoints)",
         "config": {"workload": system["name"], "n_molecules": N, "steps_per_run": args.steps,
                    "parallelism": (f"k-d tree spatial decomposition over {world} GPUs, halo exchange + "
                                    "migration with NCCL send/recv every step") if world > 1 else "single GPU",
                    "l2": "flushed between timed steps (256 MB write)",
+                   "arithmetic": "fp32 forces (packed fp32x2), u32 fixed-point positions, fp64 sums",
                    "pair_interactions_per_s": obs["n_pairs"] * args.steps / (tot_ms / 1e3)},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk,

@@ -1,0 +1,97 @@
+"""Golden values (tests/golden/, each with its citation) against the oracle
+and the generators: Table 1 of the paper (with reading A16), the
+hit rates the paper prints for linked cells, and the site-pair
+examples of SPEC.md / SURVEY.md 8(c) (not GPU)."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import scenarios as S
+
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    return json.load(open(os.path.join(G, name)))
+
+
+def test_table1_printed_values():
+    """The printed Table 1 row values follow from l0 = Bohr, q0 = e, m0 = 1 kg/mol,
+    k_B = k_C = 1 with E0 = one Hartree (A16: the printed E0 4.35946e-18 J is a
+    typo, the other rows are consistent with 4.359745e-18 J); a0 and q0 exponents
+    printed as 1e-15 and 1e9 are typos for 1e16 and 1e4 (A16)."""
+    t = load("paper_table1_units.json")["printed"]
+    NA, e, D = S.AVOGADRO, 1.602176634e-19, 3.33564e-30
+    l0, E0 = S.BOHR_M, S.E0_J
+    m0 = 1.0 / NA
+    t0 = l0 * math.sqrt(m0 / E0)
+    rho0 = 1.0 / l0 ** 3 / NA / 1e3                         # mol/l
+    assert l0 == pytest.approx(t["l0_m"], rel=1e-5)
+    assert rho0 == pytest.approx(t["rho0_mol_per_l"], rel=1e-5)
+    assert E0 / 1.380649e-23 == pytest.approx(t["T0_K"], rel=1e-5)
+    assert E0 == pytest.approx(t["E0_J"], rel=1e-4)          # printed value off by 6.4e-5 (A16)
+    assert rho0 * 1e3 * NA * E0 == pytest.approx(t["p0_Pa"], rel=1e-5)
+    assert t0 == pytest.approx(t["t0_s"], rel=1e-5)
+    assert l0 / t0 == pytest.approx(t["v0_m_per_s"], rel=1e-5)
+    assert l0 / t0 ** 2 == pytest.approx(t["a0_m_per_s2"] * 1e31, rel=1e-5)   # exponent typo (A16)
+    assert e * NA == pytest.approx(t["q0_C_per_mol"] * 1e-5, rel=1e-5)       # exponent typo (A16)
+    assert l0 * e / D == pytest.approx(t["D0_debye"], rel=1e-4)
+    assert l0 * l0 * e / (D * 1e-10) == pytest.approx(t["Q0_debye_angstrom"], rel=1e-4)
+
+
+def test_paper_hit_rates(oracle_mod):
+    """the sphere of radius rc fills 4.2 of the 27 rc^3 of the
+    27-cell shell (16 % hits); cells of edge rc/2 (125 cells, 15.6 rc^3) give
+    27 %.  The ratios are checked as printed; the oracle's measured hit rate
+    on an ideal gas is in test_oracle_system.py::test_hit_rate_ideal_gas."""
+    h = load("paper_hit_rates.json")
+    assert 4 * math.pi / 3 == pytest.approx(h["cells_rc"]["sphere_volume_rc3"], abs=0.02)   # "approx 4.2"
+    assert 4 * math.pi / 3 / 27 == pytest.approx(h["cells_rc"]["hit_fraction"], abs=0.005)
+    # rc/2 cells: the candidate volume averaged over positions in the home cell is 125/8
+    assert 125 / 8 == pytest.approx(h["cells_rc_half"]["candidate_volume_rc3"], abs=0.05)
+    assert 4 * math.pi / 3 / (125 / 8) == pytest.approx(h["cells_rc_half"]["hit_fraction"], abs=0.005)
+
+
+def _sys(oracle_mod, rc=2.5, eps_rf=math.inf, lj_shift=0):
+    s = S.config0()
+    s["rc"] = rc
+    s["box"] = (max(20.0, 4 * rc),) * 3
+    s["eps_rf"] = eps_rf
+    s["lj_shift"] = lj_shift
+    return oracle_mod.System(s)
+
+
+def test_site_pair_golden(oracle_mod):
+    g = load("spec_site_values.json")
+    z = [0, 0, 1]
+    lj = oracle_mod.make_site(0, (0, 0, 0), sigma=1.0, eps=1.0)
+    o = _sys(oracle_mod, lj_shift=0)
+    for c in g["lj"]:
+        u = o.site_pair(lj, z, lj, z, [c["r"], 0, 0])[0]
+        if "tol_abs" in c:
+            assert abs(u - c["u"]) <= c["tol_abs"], c["cite"]
+        else:
+            assert u == pytest.approx(c["u"], rel=c["tol_rel"]), c["cite"]
+    o = _sys(oracle_mod, lj_shift=1)
+    c = g["ljts"][0]
+    assert o.site_pair(lj, z, lj, z, [c["r"], 0, 0])[0] == pytest.approx(c["u"], rel=c["tol_rel"]), c["cite"]
+    c = g["ljts"][1]
+    assert o.site_pair(lj, z, lj, z, [c["r"], 0, 0])[1][0] == pytest.approx(c["f_b_x"], rel=c["tol_rel"])
+    ax = {"x": [1, 0, 0], "y": [0, 1, 0]}
+    o = _sys(oracle_mod, rc=50.0, eps_rf=1.0)
+    for key, ka, kb in (("dipole_dipole", 2, 2), ("quadrupole_quadrupole", 3, 3), ("dipole_quadrupole", 2, 3)):
+        for c in g[key]:
+            ma = c.get("mu", c.get("Q")) if ka == 2 else c["Q"]
+            mb = c.get("Q", c.get("mu")) if kb == 3 else c["mu"]
+            a = oracle_mod.make_site(ka, (0, 0, 0), ax[c["axes"][0]], ma)
+            b = oracle_mod.make_site(kb, (0, 0, 0), ax[c["axes"][1]], mb)
+            u = o.site_pair(a, ax[c["axes"][0]], b, ax[c["axes"][1]], [c["r"], 0, 0])[0]
+            assert u == pytest.approx(c["u"], rel=1e-13), c["cite"]
+    c = g["reaction_field"][0]
+    d = oracle_mod.make_site(2, (0, 0, 0), z, 1.0)
+    u_inf = _sys(oracle_mod, rc=2.5, eps_rf=math.inf).site_pair(d, z, d, z, [1.0, 0, 0])[0]
+    u_one = _sys(oracle_mod, rc=2.5, eps_rf=1.0).site_pair(d, z, d, z, [1.0, 0, 0])[0]
+    assert u_inf - u_one == pytest.approx(c["delta_u"], rel=1e-13), c["cite"]
