@@ -111,10 +111,13 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total)
 }
 
 // Single-pass exclusive scan with decoupled look-back: tiles are claimed in
-// order through a counter; each tile publishes its aggregate, then walks
-// back over its predecessors' published values (an inclusive prefix ends
-// the walk) and publishes its own inclusive prefix.  flags[] and the tile
-// counter are zeroed before every launch.  start[ncell] = total.
+// order through a counter that is never reset (tile = ticket mod ntiles,
+// epoch = ticket / ntiles + 1); each tile publishes (epoch, status, value),
+// status 1 = its aggregate, 2 = its inclusive prefix, and walks back over
+// its predecessors' values of the same epoch (an inclusive prefix ends the
+// walk).  The counts are zeroed as they are read (the next step's binning
+// starts from zero) and blk_ctr (the force kernel's block counter) is reset.
+// start[ncell] = total.
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p)
 {
     unsigned long long v;
@@ -126,37 +129,49 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned l
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-#define SCAN_AGG (1ull << 32)
-#define SCAN_INC (2ull << 32)
-
-__global__ void __launch_bounds__(1024) k_scan(int ncell, const int* __restrict__ count, int* __restrict__ start,
-                                               unsigned long long* __restrict__ flags, int* __restrict__ tile_ctr)
+__device__ __forceinline__ unsigned long long scan_word(unsigned epoch, unsigned status, int value)
 {
-    __shared__ int tot, tile_s, excl_s;
-    if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1);
+    return ((unsigned long long)epoch << 34) | ((unsigned long long)status << 32) | (unsigned)value;
+}
+
+__global__ void __launch_bounds__(1024) k_scan(int ncell, int* __restrict__ count, int* __restrict__ start,
+                                               unsigned long long* __restrict__ flags,
+                                               unsigned* __restrict__ tile_ctr, int* __restrict__ blk_ctr)
+{
+    __shared__ int tot, excl_s;
+    __shared__ unsigned ticket_s;
+    const int ntiles = (ncell + SCAN_TILE - 1) / SCAN_TILE;
+    if (threadIdx.x == 0) ticket_s = atomicAdd(tile_ctr, 1u);
     __syncthreads();
-    const int tile = tile_s;
+    const int tile = (int)(ticket_s % (unsigned)ntiles);
+    const unsigned epoch = (ticket_s / (unsigned)ntiles + 1u) & 0x3fffffffu;
+    if (tile == 0 && threadIdx.x == 0 && blk_ctr) *blk_ctr = 0;
     const int base = tile * SCAN_TILE + threadIdx.x * 4;
     int a[4];
-    const int4 c4 = (base + 3 < ncell) ? *reinterpret_cast<const int4*>(count + base) : make_int4(0, 0, 0, 0);
-    if (base + 3 < ncell) { a[0] = c4.x; a[1] = c4.y; a[2] = c4.z; a[3] = c4.w; }
-    else {
+    if (base + 3 < ncell) {
+        const int4 c4 = *reinterpret_cast<const int4*>(count + base);
+        a[0] = c4.x; a[1] = c4.y; a[2] = c4.z; a[3] = c4.w;
+        *reinterpret_cast<int4*>(count + base) = make_int4(0, 0, 0, 0);
+    } else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) a[k] = (base + k < ncell) ? count[base + k] : 0;
+        for (int k = 0; k < 4; ++k) {
+            a[k] = (base + k < ncell) ? count[base + k] : 0;
+            if (base + k < ncell) count[base + k] = 0;
+        }
     }
     int ex = block_excl_scan(a[0] + a[1] + a[2] + a[3], &tot);
     if (threadIdx.x < 32) {                  // warp 0: publish, then look back 32 tiles at a time
         const int lane = threadIdx.x;
         const int agg = tot;
-        if (lane == 0) st_release_u64(flags + tile, (tile == 0 ? SCAN_INC : SCAN_AGG) | (unsigned)agg);
+        if (lane == 0) st_release_u64(flags + tile, scan_word(epoch, tile == 0 ? 2u : 1u, agg));
         int prefix = 0;
         for (int j = tile - 1; j >= 0; j -= 32) {
             const int jj = j - lane;                          // lane 0 nearest
-            unsigned long long f = SCAN_INC;                  // beyond tile 0: an empty inclusive prefix
+            unsigned long long f = scan_word(epoch, 2u, 0);   // beyond tile 0: an empty inclusive prefix
             if (jj >= 0) {
-                do { f = ld_acquire_u64(flags + jj); } while ((f >> 32) == 0);
+                do { f = ld_acquire_u64(flags + jj); } while ((unsigned)(f >> 34) != epoch || ((f >> 32) & 3u) == 0);
             }
-            const unsigned inc = __ballot_sync(0xffffffffu, (f >> 32) == 2);
+            const unsigned inc = __ballot_sync(0xffffffffu, ((f >> 32) & 3u) == 2u);
             const int stop = inc ? __ffs(inc) - 1 : 31;       // nearest inclusive prefix ends the walk
             int v = lane <= stop ? (int)(unsigned)(f & 0xffffffffu) : 0;
 #pragma unroll
@@ -165,9 +180,9 @@ __global__ void __launch_bounds__(1024) k_scan(int ncell, const int* __restrict_
             if (inc) break;
         }
         if (lane == 0) {
-            if (tile > 0) st_release_u64(flags + tile, SCAN_INC | (unsigned)(prefix + agg));
+            if (tile > 0) st_release_u64(flags + tile, scan_word(epoch, 2u, prefix + agg));
             excl_s = prefix;
-            if (tile == (ncell - 1) / SCAN_TILE) start[ncell] = prefix + agg;
+            if (tile == ntiles - 1) start[ncell] = prefix + agg;
         }
     }
     __syncthreads();

@@ -122,7 +122,8 @@ struct mardyn_ctx {
     // graphs: one time step starting from buffer parity 0 / 1
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     cudaEvent_t ev_f0[2] = {nullptr, nullptr}, ev_f1[2] = {nullptr, nullptr};
-    cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;
+    cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;      // fork / join of the graph's side branch
+    cudaStream_t side_stream = nullptr;
     int last_parity = 0;
     bool profiling = true;
     long long launches = 0;
@@ -320,7 +321,7 @@ static int occupancy_grid(mardyn_ctx* ctx, K kernel, int threads, size_t smem = 
 // forces at the current state of buffer `buf`; step = true (single-site
 // kernel, one domain) also advances the molecules by one leapfrog step and
 // bins them for the next cell rebuild (count must be zeroed before)
-static int launch_force(mardyn_ctx* ctx, int buf, bool step = false)
+static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_graph = false)
 {
     ctx->n_force = ctx->n;
     ForceArgs a;
@@ -366,7 +367,9 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false)
         b.bpart = ctx->fpart + ctx->nfw;
         b.nbcap = ctx->nfpart - ctx->nfw;
         b.ctr = ctx->blk_ctr;
-        CK(cudaMemsetAsync(ctx->blk_ctr, 0, sizeof(int), ctx->stream));
+        // the block counter is zero whenever no force kernel runs (the scan resets it after a
+        // step); calls outside the step graph restore that invariant themselves
+        if (!in_graph) CK(cudaMemsetAsync(ctx->blk_ctr, 0, sizeof(int), ctx->stream));
         b.sig2 = a.sig2; b.eps24 = a.eps24; b.eps4 = a.eps4; b.shift = a.shift;
         b.vel = ctx->vel[buf];
         b.cell_of = ctx->cell_of;
@@ -377,6 +380,7 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false)
         b.inv_mass = ctx->model.comp[0].inv_mass;
         if (step) K_LJ1_STEP<<<ctx->force_blocks, threads, LJ1::SMEM, ctx->stream>>>(b);
         else K_LJ1<<<ctx->force_blocks, threads, LJ1::SMEM, ctx->stream>>>(b);
+        if (!in_graph) CK(cudaMemsetAsync(ctx->blk_ctr, 0, sizeof(int), ctx->stream));
     }
     }
     ctx->launches += 1;
@@ -391,9 +395,9 @@ static int enqueue_sort(mardyn_ctx* ctx, int src, int dst, int64_t n_unsorted = 
 {
     const int n = (int)(n_unsorted < 0 ? ctx->n : n_unsorted), ncell = ctx->g.ncell;
     cudaStream_t s = ctx->stream;
-    CK(cudaMemsetAsync(ctx->scan_flags, 0, sizeof(unsigned long long) * (ctx->ntiles + 1), s));
+    // (look-back flags carry an epoch, counts are zeroed as read: no memsets per step)
     k_scan<<<ctx->ntiles, 1024, 0, s>>>(ncell, ctx->count, ctx->start, ctx->scan_flags,
-                                        reinterpret_cast<int*>(ctx->scan_flags + ctx->ntiles));
+                                        reinterpret_cast<unsigned*>(ctx->scan_flags + ctx->ntiles), ctx->blk_ctr);
     k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->pos[src], ctx->cell_of, ctx->rank, ctx->start, ctx->keys,
                                             ctx->oldidx);
     if (ctx->rigid)
@@ -428,19 +432,31 @@ static int enqueue_step(mardyn_ctx* ctx, int b, bool timing_events)
     cudaStream_t s = ctx->stream;
     const int n = (int)ctx->n;
     const bool fused = ctx->kernel == KER_LJ1 && ctx->nranks == 1;
-    if (fused) CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
+    // the cell counts are zero here: the previous rebuild's scan cleared them
     if (timing_events) CK(cudaEventRecordWithFlags(ctx->ev_f0[b], s, cudaEventRecordExternal));
-    launch_force(ctx, b, fused);
+    launch_force(ctx, b, fused, true);
     if (timing_events) CK(cudaEventRecordWithFlags(ctx->ev_f1[b], s, cudaEventRecordExternal));
     if (fused) {
-        // the single-site kernel has advanced and binned the molecules (kinetic energy in its partials)
-        k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, 0, ctx->kpart, ctx->ndof,
-                                                      ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket);
+        // the single-site kernel has advanced and binned the molecules (kinetic energy in its
+        // partials).  Without NVT the observables do not feed the cell rebuild: the finalize
+        // runs on a side branch of the graph, concurrently with scan / scatter / canon.
+        const bool side = !(ctx->T_target > 0 && ctx->thermo_interval > 0) && ctx->side_stream;
+        cudaStream_t fs = side ? ctx->side_stream : s;
+        if (side) {
+            CK(cudaEventRecord(ctx->ev_s0, s));
+            CK(cudaStreamWaitEvent(fs, ctx->ev_s0, 0));
+        }
+        k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, fs>>>(ctx->nfpart, ctx->fpart, 0, ctx->kpart, ctx->ndof,
+                                                       ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket);
         ctx->launches += 1;
         enqueue_thermostat(ctx, b);
-        return enqueue_sort(ctx, b, 1 - b);
+        const int rc = enqueue_sort(ctx, b, 1 - b);
+        if (side) {                          // join: the next step's force rewrites the partials
+            CK(cudaEventRecord(ctx->ev_s1, fs));
+            CK(cudaStreamWaitEvent(s, ctx->ev_s1, 0));
+        }
+        return rc;
     }
-    CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
     if (ctx->rigid)
         k_integrate<true><<<ctx->nkblocks, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
                                                         ctx->quat[b], ctx->angm[b], ctx->force, ctx->torque,
@@ -583,8 +599,9 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
         CK(cudaEventCreate(&ctx->ev_f0[b]));
         CK(cudaEventCreate(&ctx->ev_f1[b]));
     }
-    CK(cudaEventCreate(&ctx->ev_s0));
-    CK(cudaEventCreate(&ctx->ev_s1));
+    CK(cudaEventCreateWithFlags(&ctx->ev_s0, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_s1, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
     return MARDYN_OK;
 }
 
@@ -710,6 +727,9 @@ int mardyn_set_workspace(mardyn_ctx* ctx, void* device_ptr, size_t bytes, int64_
     CK(cudaMemsetAsync(ctx->step_ctr, 0, 8, ctx->stream));
     CK(cudaMemsetAsync(ctx->flag, 0, 4, ctx->stream));
     CK(cudaMemsetAsync(ctx->fin_ticket, 0, 4, ctx->stream));
+    CK(cudaMemsetAsync(ctx->scan_flags, 0, sizeof(unsigned long long) * (ctx->ntiles + 1), ctx->stream));
+    CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, ctx->stream));
+    if (ctx->blk_ctr) CK(cudaMemsetAsync(ctx->blk_ctr, 0, sizeof(int), ctx->stream));
     CK(cudaMemsetAsync(ctx->hist, 0, sizeof(ObsRec) * MD_HISTORY, ctx->stream));
     if (ctx->nranks > 1) {
         CK(cudaMemcpyAsync(ctx->owner, ctx->h_owner.data(), ctx->g.ncell, cudaMemcpyHostToDevice, ctx->stream));
@@ -1328,6 +1348,7 @@ void mardyn_destroy(mardyn_ctx* ctx)
         if (ctx->ev_f0[b]) cudaEventDestroy(ctx->ev_f0[b]);
         if (ctx->ev_f1[b]) cudaEventDestroy(ctx->ev_f1[b]);
     }
+    if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
     if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);
     if (ctx->ev_s1) cudaEventDestroy(ctx->ev_s1);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
