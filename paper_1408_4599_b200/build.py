@@ -23,7 +23,8 @@ def stale():
 
 def build(force=False, verbose=False):
     if force or stale():
-        cmd = ["nvcc"] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB, SRC]
+        extra = os.environ.get("MD_NVCC_EXTRA", "").split()      # tuning experiments, e.g. -DMD_LJ1_CAPP=384
+        cmd = ["nvcc"] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-o", LIB, SRC]
         subprocess.check_call(cmd)
     return LIB
 

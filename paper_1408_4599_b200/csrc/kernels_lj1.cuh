@@ -33,6 +33,25 @@ namespace lj1 {
 
 constexpr int KMAX = 6;          // home cells per sub-chunk: staged |x| < 4 E (A12 quantum)
 constexpr int BLOCKS_PER_FETCH = 1;
+
+// per-lane segment [begin, end) of staged pairs: packed 16-bit halves (smaller
+// shared memory per warp -> more resident warps) or two ints
+#ifndef MD_LJ1_SEG16
+#define MD_LJ1_SEG16 0
+#endif
+#if MD_LJ1_SEG16
+typedef uint32_t SegT;
+constexpr int SEGB = 4;
+__device__ __forceinline__ SegT seg_make(int b, int e) { return (uint32_t)b | ((uint32_t)e << 16); }
+__device__ __forceinline__ int seg_b(SegT s) { return (int)(s & 0xffffu); }
+__device__ __forceinline__ int seg_e(SegT s) { return (int)(s >> 16); }
+#else
+typedef int2 SegT;
+constexpr int SEGB = 8;
+__device__ __forceinline__ SegT seg_make(int b, int e) { return make_int2(b, e); }
+__device__ __forceinline__ int seg_b(SegT s) { return s.x; }
+__device__ __forceinline__ int seg_e(SegT s) { return s.y; }
+#endif
 constexpr int NSEG = 11;         // per-lane segments: 9 rows + self split + sentinel
 constexpr float FAR = 1.0e18f;   // padding coordinate (r^2 ~ 1e36, finite, never a hit)
 
@@ -74,7 +93,7 @@ template <int WARPS, int CAPP>
 struct Cfg {
     // per warp: pair arrays xy[CAPP] (x0, x1, y0, y1), z[CAPP] (z0, z1),
     // segments seg[NSEG][32] (pair begin, pair end), row table
-    static constexpr int BYTES_PER_WARP = CAPP * 24 + NSEG * 32 * 8 + 64 * 4;
+    static constexpr int BYTES_PER_WARP = CAPP * 24 + NSEG * 32 * SEGB + 64 * 4;
     static constexpr int SMEM = WARPS * BYTES_PER_WARP;
 };
 
@@ -173,8 +192,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
     char* wbase = reinterpret_cast<char*>(smem_lj1) + wib * C::BYTES_PER_WARP;
     float4* sxy = reinterpret_cast<float4*>(wbase);
     float2* sz = reinterpret_cast<float2*>(wbase + CAPP * 16);
-    int2* sseg = reinterpret_cast<int2*>(wbase + CAPP * 24);
-    int* srow = reinterpret_cast<int*>(wbase + CAPP * 24 + NSEG * 32 * 8);   // [0..9] row pair bases
+    SegT* sseg = reinterpret_cast<SegT*>(wbase + CAPP * 24);
+    int* srow = reinterpret_cast<int*>(wbase + CAPP * 24 + NSEG * 32 * SEGB);   // [0..9] row pair bases
     uint16_t* scb = reinterpret_cast<uint16_t*>(srow + 12);                  // [9][10] staged-cell element offsets
     float* sxf = reinterpret_cast<float*>(sxy);
     float* szf = reinterpret_cast<float*>(sz);
@@ -443,17 +462,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                     if (r == 4 && act) {
                         if (pself > pa) {
                             const int qa = pa - ((pself - pa) & 1);
-                            sseg[32 * nseg + lane] = make_int2(qa, pself); ++nseg; ttot += pself - qa;
+                            sseg[32 * nseg + lane] = seg_make(qa, pself); ++nseg; ttot += pself - qa;
                         }
                         pa = pself + 1;
                     }
                     if (pb > pa) {
                         const int qb = pb + ((pb - pa) & 1);
-                        sseg[32 * nseg + lane] = make_int2(pa, qb); ++nseg; ttot += qb - pa;
+                        sseg[32 * nseg + lane] = seg_make(pa, qb); ++nseg; ttot += qb - pa;
                     }
                 }
             }
-            sseg[32 * nseg + lane] = make_int2(total, total + 2);    // sentinel
+            sseg[32 * nseg + lane] = seg_make(total, total + 2);    // sentinel
             const int tmax = __reduce_max_sync(0xffffffffu, ttot);
             __syncwarp();
             // ---------------- main loop: each lane walks its own segments, two candidates per pair;
@@ -465,8 +484,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
             {
                 int si = lane;
                 const int siend = 32 * nseg + lane;
-                int2 sg = sseg[si];
-                int p = sg.x, e = sg.y;
+                SegT sg = sseg[si];
+                int p = seg_b(sg), e = seg_e(sg);
                 for (int it = 0; it < tmax; it += 2) {
                     const float4 xy0 = sxy[p], xy1 = sxy[p + 1];
                     const float2 z0 = sz[p], z1 = sz[p + 1];
@@ -474,8 +493,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                     if (p == e) {                            // next segment (used by the next step)
                         si = min(si + 32, siend);
                         sg = sseg[si];
-                        p = sg.x;
-                        e = sg.y;
+                        p = seg_b(sg);
+                        e = seg_e(sg);
                     }
                     pair2(xy0, z0, nxi, nyi, nzi, sig2, lo, hi, A);
                     pair2(xy1, z1, nxi, nyi, nzi, sig2, lo, hi, A);
@@ -491,8 +510,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
             if (__any_sync(0xffffffffu, A.band)) {
                 if (A.band) {
                     for (int k = 0; k < nseg; ++k) {
-                        const int2 sg = sseg[32 * k + lane];
-                        for (int p = sg.x; p < sg.y; ++p) {
+                        const SegT sg = sseg[32 * k + lane];
+                        for (int p = seg_b(sg); p < seg_e(sg); ++p) {
                             const float4 xy = sxy[p];
                             const float2 zz = sz[p];
                             elem1<true>(xy.x, xy.z, zz.x, xi, yi, zi, a.sig2, lo, hi, g, A);
