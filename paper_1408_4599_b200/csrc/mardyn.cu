@@ -64,7 +64,8 @@ struct mardyn_ctx {
     bool rigid = false;
     int nslots = 0;
     int force_warps_per_block = LJ1_WARPS;
-    int force_blocks = 0;
+    int force_blocks = 0;              // occupancy grid (sizes the per-warp partials)
+    int force_grid = 0;                // launched grid: the occupancy grid, or fewer CTAs for small systems
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int device = 0;
@@ -346,15 +347,15 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_gra
     switch (ctx->shape) {
     case SHAPE_2CLJQ:
         rig2::k_force_rigid2<2, 0, 0, 1, RIG_WARPS>
-            <<<ctx->force_blocks, threads, rig2::smem_bytes<2, 0, 0, 1, RIG_WARPS>(), ctx->stream>>>(a);
+            <<<ctx->force_grid, threads, rig2::smem_bytes<2, 0, 0, 1, RIG_WARPS>(), ctx->stream>>>(a);
         break;
     case SHAPE_TIP4P:
         rig2::k_force_rigid2<1, 3, 0, 0, RIG_WARPS>
-            <<<ctx->force_blocks, threads, rig2::smem_bytes<1, 3, 0, 0, RIG_WARPS>(), ctx->stream>>>(a);
+            <<<ctx->force_grid, threads, rig2::smem_bytes<1, 3, 0, 0, RIG_WARPS>(), ctx->stream>>>(a);
         break;
     case SHAPE_GEN:
         k_force_rigid<4, 4, 2, 2, true, GEN_WARPS>
-            <<<ctx->force_blocks, threads, rigid_smem<4, 4, 2, 2, GEN_WARPS>(), ctx->stream>>>(a);
+            <<<ctx->force_grid, threads, rigid_smem<4, 4, 2, 2, GEN_WARPS>(), ctx->stream>>>(a);
         break;
     default: {
         lj1::Args b;
@@ -378,8 +379,8 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_gra
         b.flag = ctx->flag;
         b.mass = ctx->model.comp[0].mass;
         b.inv_mass = ctx->model.comp[0].inv_mass;
-        if (step) K_LJ1_STEP<<<ctx->force_blocks, threads, LJ1::SMEM, ctx->stream>>>(b);
-        else K_LJ1<<<ctx->force_blocks, threads, LJ1::SMEM, ctx->stream>>>(b);
+        if (step) K_LJ1_STEP<<<ctx->force_grid, threads, LJ1::SMEM, ctx->stream>>>(b);
+        else K_LJ1<<<ctx->force_grid, threads, LJ1::SMEM, ctx->stream>>>(b);
         if (!in_graph) CK(cudaMemsetAsync(ctx->blk_ctr, 0, sizeof(int), ctx->stream));
     }
     }
@@ -775,6 +776,23 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
     ctx->ndof = ctx->ndof_global > 0 ? ctx->ndof_global : ndof;
     ctx->n_input = n;
     cudaStream_t s = ctx->stream;
+    // launched force grid: the occupancy grid, or (one domain) just enough CTAs for a
+    // small system -- 1 warp per 32-molecule block (single-site kernel) or per home cell
+    // (rigid kernels); the per-warp partials of warps not launched stay zero
+    {
+        int grid = ctx->force_blocks;
+        if (ctx->nranks == 1) {
+            const int64_t units = ctx->kernel == KER_LJ1 ? (n + 31) / 32 : (int64_t)ctx->g.nhome;
+            const int64_t need = (units + ctx->force_warps_per_block - 1) / ctx->force_warps_per_block;
+            grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, need));
+        }
+        if (grid != ctx->force_grid) {
+            ctx->force_grid = grid;
+            CK(cudaMemsetAsync(ctx->fpart, 0, sizeof(ForcePartial) * ctx->nfpart, s));
+            for (int b = 0; b < 2; ++b)                   // the step graphs hold the launch shape
+                if (ctx->gexec[b]) { cudaGraphExecDestroy(ctx->gexec[b]); ctx->gexec[b] = nullptr; }
+        }
+    }
     // host -> device (the caller's buffers; pinned ones are DMA'd directly)
     double* dr = (double*)ctx->stage;
     double* dv = dr + 3 * n;
