@@ -1,20 +1,22 @@
-// kernels_force.cuh -- the force/torque kernels (hot loop of the method:
-// "the largest part of the computational cost is caused by the force and
-// distance calculations"; linked cells P:134-155).
+// kernels_force.cuh -- the generic rigid-molecule force/torque kernel (mixtures,
+// every site kind, runtime site counts; hot loop of the method: "the largest
+// part of the computational cost is caused by the force and distance
+// calculations"; linked cells P:134-155), and the row helpers
+// it shares with the packed single-component kernel (kernels_rigid.cuh).  The
+// single-site LJ kernel is in kernels_lj1.cuh.
 //
 // Work decomposition.  Persistent grid; each warp owns a
 // home cell at a time (cells strided over warps, x fastest, so the cells in
 // flight at any moment form a few consecutive z-planes that stay in L2).  The
 // warp stages the 27-cell neighbourhood (9 rows of 3 cells) into its shared
-// memory slab with the geometric cell offset already added, so that every
+// memory in chunks with the geometric cell offset already added, so that every
 // staged coordinate is relative to the home cell's origin and every
 // separation d = X_j - x_i is an EXACT fp32 multiple of the quantum s
 // (reading A12).  Lanes are (i-slot, j-phase) pairs: n_i molecules of the
-// home cell x P = floor(32 / n_i) phases, so a 12-molecule cell keeps 24 of
-// 32 lanes busy.  Full shell (no Newton-3 scatter, no atomics): each lane
-// accumulates the force on its own molecule only; the phases of a molecule
-// are combined with warp shuffles in fixed order, energies and virials per
-// warp in fp64 in fixed order (deterministic).
+// home cell x P = floor(32 / n_i) phases.  Full shell (no Newton-3 scatter,
+// no atomics): each lane accumulates the force and torque on its own molecule
+// only; the phases of a molecule are combined with warp shuffles in fixed
+// order, energies and virials per warp in fp64 in fixed order (deterministic).
 //
 // Cutoff (reading A1, A12): COM separation, strict r < rc.  r^2 in fp32 is
 // within 3 ulp of the exact value; inside a +-2^-20 relative band around rc^2
