@@ -1,0 +1,385 @@
+// kernels_rigid3.cuh -- force/torque kernel for rigid multi-centre molecules of
+// one component (configs 2 and 3: 2CLJQ, TIP4P, linked
+// cells P:134-155; "the largest part of the computational cost is caused by
+// the force and distance calculations"), load-balanced form.
+//
+// Decomposition.  One CTA per home cell at a time (cells
+// strided over the persistent grid).  The CTA stages the whole 27-cell
+// neighbourhood once into shared memory -- COM relative to the home cell's
+// origin (exact multiples of the quantum s, reading A12) and the world-frame
+// site slots -- and its half-warps ("groups" of 16 lanes) take the home
+// molecules one at a time.  For home molecule i a group
+//   1. tests every staged molecule j against the COM cutoff (reading A1; the
+//      guard band around rc^2 is decided exactly in integer quanta), two
+//      candidates per lane per step, and appends the hits to the group's list
+//      in shared memory by ballot compaction (deterministic order);
+//   2. evaluates the site pairs of its list 32 partners per round (two per
+//      lane, packed into the fp32x2 instructions FADD2/FMUL2/FFMA2 of sm_100);
+//   3. reduces the 16 lanes' force and torque (tau = sum_a s_a x f_a + tau_a)
+//      with butterfly shuffles in fixed order.
+// Every lane of a group works on the same molecule, so the partners are spread
+// evenly over the lanes: a round is full except for the last one of a
+// molecule.  (The per-lane queues of k_force_rigid2, one home molecule per
+// lane, idle most lanes while the longest queue drains.)  Full shell: each
+// pair is evaluated from both sides, no scatter, no atomics; energies and
+// virials are summed per lane in fixed order and per warp in fp64.
+#pragma once
+#include "common.cuh"
+#include "kernels_force.cuh"
+#include "kernels_rigid.cuh"
+
+namespace rig3 {
+
+#ifndef MD_RIG3_CAP
+#define MD_RIG3_CAP 1152
+#endif
+#ifndef MD_RIG3_WARPS
+#define MD_RIG3_WARPS 8
+#endif
+constexpr int CAP = MD_RIG3_CAP;      // staged molecules per chunk of the neighbourhood
+constexpr int WARPS = MD_RIG3_WARPS;
+constexpr int HCAP = 256;             // hit-list entries per group
+constexpr int NHMAX = 64;             // home molecules per batch (force/torque accumulators)
+
+using rig2::P2;
+using rig2::V3;
+using rig2::p2;
+using rig2::v3zero;
+using rig2::bcast;
+using rig2::pack;
+using rig2::dot;
+
+template <int NLJ, int NQ, int NMU, int NQQ>
+constexpr int smem_bytes()
+{
+    // COM pairs (CAP/2 + 1 pairs x 24 B, +1: the far dummy pair), NSLOT x (CAP + 1) site float4,
+    // hit lists, accumulators, row table
+    return (CAP / 2 + 1) * 16 + ((CAP / 2 + 2) & ~1) * 8 + (NLJ + NQ + 2 * NMU + 2 * NQQ) * (CAP + 1) * 16 + WARPS * 2 * (HCAP + 2) * 2 +
+           NHMAX * 8 * 4 + 16 * 8 * 4;
+}
+
+template <int NLJ, int NQ, int NMU, int NQQ>
+__global__ void __launch_bounds__(WARPS * 32, 2) k_force_rigid3(ForceArgs a)
+{
+    using SH = Shape<NLJ, NQ, NMU, NQQ>;
+    constexpr int NSLOT = SH::NSLOT;
+    constexpr int NPOL = (NMU + NQQ) > 0 ? (NMU + NQQ) : 1;
+    constexpr int STRIDE = CAP + 1;
+    constexpr int DUMMY = CAP;                                 // far dummy element (pair CAP / 2)
+    constexpr unsigned FULL = 0xffffffffu;
+    static_assert(CAP % 2 == 0 && CAP < 32768, "CAP");
+    extern __shared__ float4 smem_rig3[];
+    // COMs as pairs: cxy[p] = (x_2p, x_2p+1, y_2p, y_2p+1), pz[p] = (z_2p, z_2p+1): two candidates
+    // are one packed operand without register moves
+    float4* cxy = smem_rig3;
+    float2* pz = reinterpret_cast<float2*>(cxy + CAP / 2 + 1);
+    float* cxf = reinterpret_cast<float*>(cxy);
+    float* czf = reinterpret_cast<float*>(pz);
+    float4* ssw = reinterpret_cast<float4*>(pz + ((CAP / 2 + 2) & ~1));   // 16-byte aligned           // ssw[slot * STRIDE + j]
+    uint16_t* hls = reinterpret_cast<uint16_t*>(ssw + NSLOT * STRIDE);     // [2 * WARPS][HCAP]
+    float* acc = reinterpret_cast<float*>(hls + 2 * WARPS * (HCAP + 2));         // [NHMAX][8]: F, tau
+    int* rinfo = reinterpret_cast<int*>(acc + NHMAX * 8);                  // [9][8] row table + [72..]: totals
+    const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+    const int half = lane >> 4, gl = lane & 15;
+    const int grp = 2 * wib + half, NG = 2 * WARPS;
+    uint16_t* hl = hls + grp * (HCAP + 2);                                 // + spare slot for misses
+    const unsigned gmask = 0xffffu << (16 * half);
+    const unsigned below = (1u << lane) - 1u;
+    const GridP& g = a.g;
+    const DevModel* __restrict__ M = a.model;
+    const float krf = M->krf, crf = M->crf, kmm = M->krf_mumu;
+    float4 ljp[NLJ > 0 ? NLJ * NLJ : 1];
+#pragma unroll
+    for (int ia = 0; ia < NLJ; ++ia)
+#pragma unroll
+        for (int ib = 0; ib < NLJ; ++ib) {
+            const int t = ia * MD_MAX_LJ_TOTAL + ib;
+            ljp[ia * NLJ + ib] = make_float4(M->sig2[t], M->eps24[t], M->eps4[t], M->shift[t]);
+        }
+    if (tid == 0) {                       // far dummy partner (padding): COM far away, sites at the COM
+        cxy[CAP / 2] = make_float4(1.0e4f, 1.0e4f, 1.0e4f, 1.0e4f);
+        pz[CAP / 2] = make_float2(1.0e4f, 1.0e4f);
+#pragma unroll
+        for (int s = 0; s < NSLOT; ++s) ssw[s * STRIDE + DUMMY] = make_float4(0.f, 0.f, 1.f, 0.f);
+    }
+    P2 uacc = p2(0.f), wacc = p2(0.f);     // per home molecule (fp32), then fp64 per lane
+    double Uw = 0.0, Ww = 0.0;
+    long long npw = 0, ncw = 0;
+    int nrej = 0;                          // flagged band entries found out of range
+
+    for (int t = blockIdx.x; t < g.nhome; t += gridDim.x) {
+        int cx, cy, cz;
+        const int c = home_cell(g, t, cx, cy, cz);
+        const int s_i = __ldg(a.start + c);
+        const int n_all = __ldg(a.start + c + 1) - s_i;
+        if (n_all == 0) continue;
+        // row table: threads 0..26 read the 27 cells' start / count
+        __syncthreads();                  // previous cell's consumers are done with smem
+        if (tid < 27) {
+            const int r = tid / 3, k = tid % 3;
+            const int dy = r % 3 - 1, dz = r / 3 - 1;
+            const int cc = wrapi(cx + k - 1, g.nc[0]) + g.nc[0] * (wrapi(cy + dy, g.nc[1]) + g.nc[1] * wrapi(cz + dz, g.nc[2]));
+            const int st = __ldg(a.start + cc);
+            rinfo[8 * r + k] = st;
+            rinfo[8 * r + 3 + k] = __ldg(a.start + cc + 1) - st;
+        }
+        __syncthreads();
+        if (tid < 32) {                   // exclusive prefix of the row lengths -> rinfo[8 r + 6]
+            const int len = lane < 9 ? rinfo[8 * lane + 3] + rinfo[8 * lane + 4] + rinfo[8 * lane + 5] : 0;
+            int incl = len;
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) {
+                const int v = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += v;
+            }
+            if (lane < 9) rinfo[8 * lane + 6] = incl - len;
+            if (lane == 8) rinfo[72] = incl;
+        }
+        __syncthreads();
+        const int mtot = rinfo[72];
+        if (tid == 0) ncw += (long long)n_all * (mtot - 1);
+        for (int ib = 0; ib < n_all; ib += NHMAX) {
+            const int nb = min(NHMAX, n_all - ib);
+            if (ib > 0) __syncthreads();          // previous batch written out
+            for (int k = tid; k < nb * 8; k += WARPS * 32) acc[k] = 0.f;
+            for (int k0 = 0; k0 < mtot; k0 += CAP) {
+                const int mm = min(CAP, mtot - k0);
+                __syncthreads();
+                // ---- stage elements k0 .. k0 + mm - 1 of the neighbourhood (rows in order)
+                for (int k = tid; k < mm; k += WARPS * 32) {
+                    const int kg = k0 + k;
+                    int r = 0;
+#pragma unroll
+                    for (int q = 1; q < 9; ++q) r += kg >= rinfo[8 * q + 6] ? 1 : 0;
+                    const int* ri = rinfo + 8 * r;
+                    int kk = kg - ri[6];
+                    int src;
+                    float offx;
+                    if (kk < ri[3]) { src = ri[0] + kk; offx = -g.edge[0]; }
+                    else if (kk < ri[3] + ri[4]) { src = ri[1] + kk - ri[3]; offx = 0.f; }
+                    else { src = ri[2] + kk - ri[3] - ri[4]; offx = g.edge[0]; }
+                    const float offy = (float)(r % 3 - 1) * g.edge[1], offz = (float)(r / 3 - 1) * g.edge[2];
+                    const float4 x = __ldg(a.xs + src);
+                    float4 sv[NSLOT];
+#pragma unroll
+                    for (int s = 0; s < NSLOT; ++s) sv[s] = __ldg(a.site + (size_t)s * a.cap + src);
+                    const int ph = k >> 1, od = k & 1;
+                    cxf[4 * ph + od] = x.x + offx;
+                    cxf[4 * ph + 2 + od] = x.y + offy;
+                    czf[2 * ph + od] = x.z + offz;
+                    if (k == mm - 1 && !od) {                   // odd chunk: far pad element
+                        cxf[4 * ph + 1] = 1.0e4f;
+                        cxf[4 * ph + 3] = 1.0e4f;
+                        czf[2 * ph + 1] = 1.0e4f;
+                    }
+#pragma unroll
+                    for (int s = 0; s < NSLOT; ++s) ssw[s * STRIDE + k] = sv[s];
+                }
+                __syncthreads();
+                // ---- home molecules of this batch, one per group (groups in lock-step per warp)
+                const int nrounds = (nb + NG - 1) / NG;
+                for (int rr = 0; rr < nrounds; ++rr) {
+                    const int il = rr * NG + grp;          // batch-local home index of this group
+                    const bool gact = il < nb;
+                    if (!__any_sync(FULL, gact)) break;
+                    const int my = s_i + ib + (gact ? il : 0);
+                    const float4 xi = __ldg(a.xs + my);
+                    float4 si[NSLOT];
+#pragma unroll
+                    for (int s = 0; s < NSLOT; ++s) si[s] = __ldg(a.site + (size_t)s * a.cap + my);
+                    V3 fs[SH::NS];
+                    V3 ts[NPOL];
+#pragma unroll
+                    for (int s = 0; s < SH::NS; ++s) fs[s] = v3zero();
+#pragma unroll
+                    for (int s = 0; s < NPOL; ++s) ts[s] = v3zero();
+
+                    // force phase over the group's list [0, cnt): entries (k + gl, k + 16 + gl) packed
+                    auto force_rounds = [&](int cnt) {
+                        const int cmax = max(__shfl_sync(FULL, cnt, 0), __shfl_sync(FULL, cnt, 16));
+                        for (int k = 0; k < cmax; k += 32) {
+                            const int e0 = k + gl, e1 = k + 16 + gl;
+                            const bool v0 = e0 < cnt, v1 = e1 < cnt;
+                            const int h0 = v0 ? hl[e0] : DUMMY, h1 = v1 ? hl[e1] : DUMMY;
+                            const int j0 = h0 & 0x7fff, j1 = h1 & 0x7fff;      // bit 15: guard band
+                            const int q0 = 4 * (j0 >> 1) + (j0 & 1), q1 = 4 * (j1 >> 1) + (j1 & 1);
+                            const V3 d = V3{p2(cxf[q0] - xi.x, cxf[q1] - xi.x),
+                                            p2(cxf[q0 + 2] - xi.y, cxf[q1 + 2] - xi.y),
+                                            p2(czf[2 * (j0 >> 1) + (j0 & 1)] - xi.z, czf[2 * (j1 >> 1) + (j1 & 1)] - xi.z)};
+                            bool ok0 = v0, ok1 = v1;
+                            if ((h0 | h1) & 0x8000) {                  // exact decision in the band (rare)
+                                if (h0 & 0x8000) ok0 = exact_in_range(d.x.v.x, d.y.v.x, d.z.v.x, g);
+                                if (h1 & 0x8000) ok1 = exact_in_range(d.x.v.y, d.y.v.y, d.z.v.y, g);
+                                nrej += (v0 && !ok0 ? 1 : 0) + (v1 && !ok1 ? 1 : 0);
+                            }
+                            const P2 msk = p2(ok0 ? 1.f : 0.f, ok1 ? 1.f : 0.f);
+                            V3 fh = v3zero();
+#pragma unroll
+                            for (int ia = 0; ia < NLJ; ++ia) {
+                                const V3 sa = bcast(si[ia]);
+#pragma unroll
+                                for (int ibb = 0; ibb < NLJ; ++ibb) {
+                                    const V3 sb = pack(ssw[ibb * STRIDE + j0], ssw[ibb * STRIDE + j1]);
+                                    const V3 rv = V3{d.x + sb.x - sa.x, d.y + sb.y - sa.y, d.z + sb.z - sa.z};
+                                    const float4 pp = ljp[ia * NLJ + ibb];
+                                    rig2::lj2(rv, pp.x, pp.y * msk, pp.z * msk, pp.w * msk, uacc, fs[ia], fh);
+                                }
+                            }
+#pragma unroll
+                            for (int ia = 0; ia < NQ; ++ia) {
+                                const float4 sa4 = si[SH::SQ + ia];
+                                const V3 sa = bcast(sa4);
+#pragma unroll
+                                for (int ibb = 0; ibb < NQ; ++ibb) {
+                                    const float4 b0 = ssw[(SH::SQ + ibb) * STRIDE + j0], b1 = ssw[(SH::SQ + ibb) * STRIDE + j1];
+                                    const V3 sb = pack(b0, b1);
+                                    const V3 rv = V3{d.x + sb.x - sa.x, d.y + sb.y - sa.y, d.z + sb.z - sa.z};
+                                    rig2::qq2(rv, sa4.w * p2(b0.w, b1.w) * msk, krf, crf, uacc, fs[NLJ + ia], fh);
+                                }
+                            }
+#define RIG3_POLAR(KA, KB, NA, NB, SLA, SLB, FIDX, TIDX, STA, STB)                                          \
+    _Pragma("unroll") for (int ia = 0; ia < NA; ++ia)                                                      \
+    {                                                                                                      \
+        const float4 pa4 = si[(SLA) + ia * STA];                                                           \
+        const V3 pa = bcast(pa4);                                                                          \
+        const V3 ea = (STA == 2) ? bcast(si[((SLA) + ia * STA + 1) % NSLOT]) : v3zero();                  \
+        _Pragma("unroll") for (int ibb = 0; ibb < NB; ++ibb)                                               \
+        {                                                                                                  \
+            const int slb = (SLB) + ibb * STB;                                                             \
+            const float4 b0 = ssw[slb * STRIDE + j0], b1 = ssw[slb * STRIDE + j1];                         \
+            const V3 pb = pack(b0, b1);                                                                    \
+            const V3 eb = (STB == 2) ? pack(ssw[((slb + 1) % NSLOT) * STRIDE + j0],                          \
+                                            ssw[((slb + 1) % NSLOT) * STRIDE + j1]) : v3zero();             \
+            const V3 rv = V3{d.x + pb.x - pa.x, d.y + pb.y - pa.y, d.z + pb.z - pa.z};                     \
+            V3 tdummy = v3zero();                                                                          \
+            rig2::polar2<KA, KB>(rv, ea, eb, pa4.w * p2(b0.w, b1.w) * msk, kmm, uacc, fs[FIDX + ia],       \
+                                 (TIDX) >= 0 ? ts[((TIDX) >= 0 ? (TIDX) : 0) + ia] : tdummy, fh);        \
+        }                                                                                                  \
+    }
+                            if (NQ > 0 && NMU > 0) {
+                                RIG3_POLAR(MD_CHARGE, MD_DIPOLE, NQ, NMU, SH::SQ, SH::SMU, NLJ, -1, 1, 2)
+                                RIG3_POLAR(MD_DIPOLE, MD_CHARGE, NMU, NQ, SH::SMU, SH::SQ, NLJ + NQ, 0, 2, 1)
+                            }
+                            if (NQ > 0 && NQQ > 0) {
+                                RIG3_POLAR(MD_CHARGE, MD_QUAD, NQ, NQQ, SH::SQ, SH::SQQ, NLJ, -1, 1, 2)
+                                RIG3_POLAR(MD_QUAD, MD_CHARGE, NQQ, NQ, SH::SQQ, SH::SQ, NLJ + NQ + NMU, NMU, 2, 1)
+                            }
+                            if (NMU > 0) {
+                                RIG3_POLAR(MD_DIPOLE, MD_DIPOLE, NMU, NMU, SH::SMU, SH::SMU, NLJ + NQ, 0, 2, 2)
+                            }
+                            if (NMU > 0 && NQQ > 0) {
+                                RIG3_POLAR(MD_DIPOLE, MD_QUAD, NMU, NQQ, SH::SMU, SH::SQQ, NLJ + NQ, 0, 2, 2)
+                                RIG3_POLAR(MD_QUAD, MD_DIPOLE, NQQ, NMU, SH::SQQ, SH::SMU, NLJ + NQ + NMU, NMU, 2, 2)
+                            }
+                            if (NQQ > 0) {
+                                RIG3_POLAR(MD_QUAD, MD_QUAD, NQQ, NQQ, SH::SQQ, SH::SQQ, NLJ + NQ + NMU, NMU, 2, 2)
+                            }
+#undef RIG3_POLAR
+                            wacc -= dot(d, fh);      // molecular virial (A6): -r_ij . F_ij
+                        }
+                    };
+
+                    // ---- distance phase: candidate pair p = base + gl (elements 2p, 2p + 1), ballot
+                    //      compaction; pairs in the guard band are flagged for the exact test
+                    int cnt = 0;
+                    const float2 nxi = make_float2(-xi.x, -xi.x), nyi = make_float2(-xi.y, -xi.y),
+                                 nzi = make_float2(-xi.z, -xi.z);
+                    // this molecule's own element in the chunk (row 4 = the home row, after cell x - 1)
+                    const int self = rinfo[8 * 4 + 6] + rinfo[8 * 4 + 3] + ib + il - k0;
+                    const int npair = (mm + 1) >> 1;
+                    const float lo = g.cut2_lo, hi = gact ? g.cut2_hi : -1.f;   // idle group: no hits
+                    // two steps per iteration; the list (HCAP - 64 entries free) is checked once per iteration
+                    for (int base = 0; base < npair; base += 32) {
+#pragma unroll
+                        for (int u = 0; u < 2; ++u) {
+                            const int p = base + 16 * u + gl;
+                            const int pp = p < npair ? p : CAP / 2;
+                            const float4 xy = cxy[pp];
+                            const float2 zz = pz[pp];
+                            const float2 dx = __fadd2_rn(make_float2(xy.x, xy.y), nxi);
+                            const float2 dy = __fadd2_rn(make_float2(xy.z, xy.w), nyi);
+                            const float2 dz = __fadd2_rn(zz, nzi);
+                            float2 r2 = __fmul2_rn(dx, dx);
+                            r2 = __ffma2_rn(dy, dy, r2);
+                            r2 = __ffma2_rn(dz, dz, r2);
+                            const int j0 = 2 * pp;
+                            const bool h0 = (r2.x < hi) && (j0 != self);
+                            const bool h1 = (r2.y < hi) && (j0 + 1 != self);
+                            const unsigned b0 = __ballot_sync(FULL, h0) & gmask, b1 = __ballot_sync(FULL, h1) & gmask;
+                            const int n0 = __popc(b0);
+                            // unconditional stores (a miss writes the spare slot HCAP)
+                            hl[h0 ? cnt + __popc(b0 & below) : HCAP] = (uint16_t)(j0 | (r2.x >= lo ? 0x8000 : 0));
+                            hl[h1 ? cnt + n0 + __popc(b1 & below) : HCAP] = (uint16_t)((j0 + 1) | (r2.y >= lo ? 0x8000 : 0));
+                            cnt += n0 + __popc(b1);
+                        }
+                        if (__any_sync(FULL, cnt > HCAP - 64)) {       // list full: evaluate it now
+                            __syncwarp();
+                            force_rounds(cnt);
+                            npw += gl == 0 ? cnt : 0;
+                            cnt = 0;
+                            __syncwarp();
+                        }
+                    }
+                    __syncwarp();
+                    force_rounds(cnt);
+                    npw += gl == 0 ? cnt : 0;
+                    __syncwarp();
+                    // ---- molecule force and torque of this lane's share, group reduction
+                    float F[3] = {0.f, 0.f, 0.f}, T[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int k = 0; k < SH::NS; ++k) {
+                        int slot;
+                        if (k < NLJ) slot = k;
+                        else if (k < NLJ + NQ) slot = NLJ + (k - NLJ);
+                        else if (k < NLJ + NQ + NMU) slot = SH::SMU + 2 * (k - NLJ - NQ);
+                        else slot = SH::SQQ + 2 * (k - NLJ - NQ - NMU);
+                        const float4 sp = si[slot < NSLOT ? slot : 0];
+                        const float fx = fs[k].x.v.x + fs[k].x.v.y, fy = fs[k].y.v.x + fs[k].y.v.y,
+                                    fz = fs[k].z.v.x + fs[k].z.v.y;
+                        F[0] += fx; F[1] += fy; F[2] += fz;
+                        T[0] += sp.y * fz - sp.z * fy;
+                        T[1] += sp.z * fx - sp.x * fz;
+                        T[2] += sp.x * fy - sp.y * fx;
+                    }
+                    if (NMU + NQQ > 0) {
+#pragma unroll
+                        for (int k = 0; k < NPOL; ++k) {
+                            T[0] += ts[k].x.v.x + ts[k].x.v.y;
+                            T[1] += ts[k].y.v.x + ts[k].y.v.y;
+                            T[2] += ts[k].z.v.x + ts[k].z.v.y;
+                        }
+                    }
+#pragma unroll
+                    for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+                        for (int q = 0; q < 3; ++q) {
+                            F[q] += __shfl_xor_sync(FULL, F[q], o);
+                            T[q] += __shfl_xor_sync(FULL, T[q], o);
+                        }
+                    Uw += (double)uacc.v.x + (double)uacc.v.y;
+                    Ww += (double)wacc.v.x + (double)wacc.v.y;
+                    uacc = p2(0.f);
+                    wacc = p2(0.f);
+                    if (gact && gl == 0) {
+                        float* A = acc + 8 * il;
+                        A[0] += F[0]; A[1] += F[1]; A[2] += F[2];
+                        A[4] += T[0]; A[5] += T[1]; A[6] += T[2];
+                    }
+                }
+            }
+            __syncthreads();
+            for (int k = tid; k < nb; k += WARPS * 32) {
+                const float* A = acc + 8 * k;
+                a.force[s_i + ib + k] = make_float4(A[0], A[1], A[2], 0.f);
+                a.torque[s_i + ib + k] = make_float4(A[4], A[5], A[6], 0.f);
+            }
+        }
+    }
+    Uw = warp_sum_d(Uw);
+    Ww = warp_sum_d(Ww);
+    npw = warp_sum_ll(npw - nrej);
+    ncw = warp_sum_ll(ncw);
+    if (lane == 0) a.part[blockIdx.x * WARPS + wib] = ForcePartial{0.5 * Uw, 0.5 * Ww, npw, ncw, 0.0};
+}
+
+}  // namespace rig3

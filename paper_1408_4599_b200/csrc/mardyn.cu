@@ -15,6 +15,7 @@
 #include "kernels_force.cuh"
 #include "kernels_lj1.cuh"
 #include "kernels_rigid.cuh"
+#include "kernels_rigid3.cuh"
 #include "kernels_state.cuh"
 
 namespace {
@@ -44,7 +45,10 @@ constexpr int LJ1_CAPP = MD_LJ1_CAPP;
 using LJ1 = lj1::Cfg<LJ1_WARPS, LJ1_CAPP>;
 #define K_LJ1 lj1::k_force_lj1<LJ1_WARPS, LJ1_CAPP, MD_LJ1_MINB, false>
 #define K_LJ1_STEP lj1::k_force_lj1<LJ1_WARPS, LJ1_CAPP, MD_LJ1_MINB, true>
-constexpr int RIG_WARPS = 4;
+#ifndef MD_RIGID3
+#define MD_RIGID3 1                       // load-balanced rigid kernel (kernels_rigid3.cuh) for configs 2, 3
+#endif
+constexpr int RIG_WARPS = MD_RIGID3 ? rig3::WARPS : 4;
 constexpr int GEN_WARPS = 1;
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -346,12 +350,20 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_gra
     const int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ:
-        rig2::k_force_rigid2<2, 0, 0, 1, RIG_WARPS>
-            <<<ctx->force_grid, threads, rig2::smem_bytes<2, 0, 0, 1, RIG_WARPS>(), ctx->stream>>>(a);
+        if (MD_RIGID3)
+            rig3::k_force_rigid3<2, 0, 0, 1>
+                <<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
+        else
+            rig2::k_force_rigid2<2, 0, 0, 1, RIG_WARPS>
+                <<<ctx->force_grid, threads, rig2::smem_bytes<2, 0, 0, 1, RIG_WARPS>(), ctx->stream>>>(a);
         break;
     case SHAPE_TIP4P:
-        rig2::k_force_rigid2<1, 3, 0, 0, RIG_WARPS>
-            <<<ctx->force_grid, threads, rig2::smem_bytes<1, 3, 0, 0, RIG_WARPS>(), ctx->stream>>>(a);
+        if (MD_RIGID3)
+            rig3::k_force_rigid3<1, 3, 0, 0>
+                <<<ctx->force_grid, threads, rig3::smem_bytes<1, 3, 0, 0>(), ctx->stream>>>(a);
+        else
+            rig2::k_force_rigid2<1, 3, 0, 0, RIG_WARPS>
+                <<<ctx->force_grid, threads, rig2::smem_bytes<1, 3, 0, 0, RIG_WARPS>(), ctx->stream>>>(a);
         break;
     case SHAPE_GEN:
         k_force_rigid<4, 4, 2, 2, true, GEN_WARPS>
@@ -571,15 +583,15 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
     int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ: {
-        auto k = rig2::k_force_rigid2<2, 0, 0, 1, RIG_WARPS>;
-        const int sm = rig2::smem_bytes<2, 0, 0, 1, RIG_WARPS>();
+        auto k = MD_RIGID3 ? rig3::k_force_rigid3<2, 0, 0, 1> : rig2::k_force_rigid2<2, 0, 0, 1, RIG_WARPS>;
+        const int sm = MD_RIGID3 ? rig3::smem_bytes<2, 0, 0, 1>() : rig2::smem_bytes<2, 0, 0, 1, RIG_WARPS>();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         ctx->force_blocks = occupancy_grid(ctx, k, threads, sm);
         break;
     }
     case SHAPE_TIP4P: {
-        auto k = rig2::k_force_rigid2<1, 3, 0, 0, RIG_WARPS>;
-        const int sm = rig2::smem_bytes<1, 3, 0, 0, RIG_WARPS>();
+        auto k = MD_RIGID3 ? rig3::k_force_rigid3<1, 3, 0, 0> : rig2::k_force_rigid2<1, 3, 0, 0, RIG_WARPS>;
+        const int sm = MD_RIGID3 ? rig3::smem_bytes<1, 3, 0, 0>() : rig2::smem_bytes<1, 3, 0, 0, RIG_WARPS>();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         ctx->force_blocks = occupancy_grid(ctx, k, threads, sm);
         break;
@@ -783,7 +795,8 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
         int grid = ctx->force_blocks;
         if (ctx->nranks == 1) {
             const int64_t units = ctx->kernel == KER_LJ1 ? (n + 31) / 32 : (int64_t)ctx->g.nhome;
-            const int64_t need = (units + ctx->force_warps_per_block - 1) / ctx->force_warps_per_block;
+            const int upb = (ctx->kernel == KER_RIGID && MD_RIGID3) ? 1 : ctx->force_warps_per_block;   // rig3: CTA per cell
+            const int64_t need = (units + upb - 1) / upb;
             grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, need));
         }
         if (grid != ctx->force_grid) {
