@@ -84,28 +84,19 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_force_rigid3(ForceArgs a)
     const int grp = 2 * wib + half, NG = 2 * WARPS;
     uint16_t* hl = hls + grp * (HCAP + 2);                                 // + spare slot for misses
     const unsigned gmask = 0xffffu << (16 * half);
-    const unsigned below = (1u << lane) - 1u;
     const GridP& g = a.g;
     const DevModel* __restrict__ M = a.model;
     const float krf = M->krf, crf = M->crf, kmm = M->krf_mumu;
-    float4 ljp[NLJ > 0 ? NLJ * NLJ : 1];
-#pragma unroll
-    for (int ia = 0; ia < NLJ; ++ia)
-#pragma unroll
-        for (int ib = 0; ib < NLJ; ++ib) {
-            const int t = ia * MD_MAX_LJ_TOTAL + ib;
-            ljp[ia * NLJ + ib] = make_float4(M->sig2[t], M->eps24[t], M->eps4[t], M->shift[t]);
-        }
     if (tid == 0) {                       // far dummy partner (padding): COM far away, sites at the COM
         cxy[CAP / 2] = make_float4(1.0e4f, 1.0e4f, 1.0e4f, 1.0e4f);
         pz[CAP / 2] = make_float2(1.0e4f, 1.0e4f);
 #pragma unroll
         for (int s = 0; s < NSLOT; ++s) ssw[s * STRIDE + DUMMY] = make_float4(0.f, 0.f, 1.f, 0.f);
     }
-    P2 uacc = p2(0.f), wacc = p2(0.f);     // per home molecule (fp32), then fp64 per lane
-    double Uw = 0.0, Ww = 0.0;
+    double Uw = 0.0, Ww = 0.0;             // per lane (fp32 per home molecule, then fp64)
     long long npw = 0, ncw = 0;
-    int nrej = 0;                          // flagged band entries found out of range
+    int nrej = 0;                          // band entries found out of range
+    int nself = 0;                         // the home molecules' own list entries
 
     for (int t = blockIdx.x; t < g.nhome; t += gridDim.x) {
         int cx, cy, cz;
@@ -184,33 +175,57 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_force_rigid3(ForceArgs a)
                     if (!__any_sync(FULL, gact)) break;
                     const int my = s_i + ib + (gact ? il : 0);
                     const float4 xi = __ldg(a.xs + my);
-                    float4 si[NSLOT];
-#pragma unroll
-                    for (int s = 0; s < NSLOT; ++s) si[s] = __ldg(a.site + (size_t)s * a.cap + my);
-                    V3 fs[SH::NS];
-                    V3 ts[NPOL];
-#pragma unroll
-                    for (int s = 0; s < SH::NS; ++s) fs[s] = v3zero();
-#pragma unroll
-                    for (int s = 0; s < NPOL; ++s) ts[s] = v3zero();
+                    // this molecule's own element in the chunk (row 4 = the home row, after cell x - 1)
+                    const int self = rinfo[8 * 4 + 6] + rinfo[8 * 4 + 3] + ib + il - k0;
 
-                    // force phase over the group's list [0, cnt): entries (k + gl, k + 16 + gl) packed
-                    auto force_rounds = [&](int cnt) {
+                    // force phase over the group's list [0, cnt): entries (k + gl, k + 16 + gl) packed;
+                    // then this lane's force and torque, group reduction, accumulation into acc[il].
+                    // Self-contained (site offsets, accumulators and LJ table are loaded here), so
+                    // that none of it is live during the distance phase
+                    auto flush = [&](int cnt) {
+                        float4 si[NSLOT];
+#pragma unroll
+                        for (int s = 0; s < NSLOT; ++s) si[s] = __ldg(a.site + (size_t)s * a.cap + my);
+                        float4 ljp[NLJ > 0 ? NLJ * NLJ : 1];
+#pragma unroll
+                        for (int ia = 0; ia < NLJ; ++ia)
+#pragma unroll
+                            for (int ibb = 0; ibb < NLJ; ++ibb) {
+                                const int t = ia * MD_MAX_LJ_TOTAL + ibb;
+                                ljp[ia * NLJ + ibb] = make_float4(__ldg(M->sig2 + t), __ldg(M->eps24 + t),
+                                                                  __ldg(M->eps4 + t), __ldg(M->shift + t));
+                            }
+                        V3 fs[SH::NS];
+                        V3 ts[NPOL];
+#pragma unroll
+                        for (int s = 0; s < SH::NS; ++s) fs[s] = v3zero();
+#pragma unroll
+                        for (int s = 0; s < NPOL; ++s) ts[s] = v3zero();
+                        P2 uacc = p2(0.f), wacc = p2(0.f);
                         const int cmax = max(__shfl_sync(FULL, cnt, 0), __shfl_sync(FULL, cnt, 16));
                         for (int k = 0; k < cmax; k += 32) {
                             const int e0 = k + gl, e1 = k + 16 + gl;
                             const bool v0 = e0 < cnt, v1 = e1 < cnt;
+                            // the molecule itself is on the list (r = 0): replaced by the dummy
                             const int h0 = v0 ? hl[e0] : DUMMY, h1 = v1 ? hl[e1] : DUMMY;
-                            const int j0 = h0 & 0x7fff, j1 = h1 & 0x7fff;      // bit 15: guard band
+                            const bool s0 = v0 && h0 == self, s1 = v1 && h1 == self;
+                            const int j0 = s0 ? DUMMY : h0, j1 = s1 ? DUMMY : h1;
                             const int q0 = 4 * (j0 >> 1) + (j0 & 1), q1 = 4 * (j1 >> 1) + (j1 & 1);
                             const V3 d = V3{p2(cxf[q0] - xi.x, cxf[q1] - xi.x),
                                             p2(cxf[q0 + 2] - xi.y, cxf[q1 + 2] - xi.y),
                                             p2(czf[2 * (j0 >> 1) + (j0 & 1)] - xi.z, czf[2 * (j1 >> 1) + (j1 & 1)] - xi.z)};
-                            bool ok0 = v0, ok1 = v1;
-                            if ((h0 | h1) & 0x8000) {                  // exact decision in the band (rare)
-                                if (h0 & 0x8000) ok0 = exact_in_range(d.x.v.x, d.y.v.x, d.z.v.x, g);
-                                if (h1 & 0x8000) ok1 = exact_in_range(d.x.v.y, d.y.v.y, d.z.v.y, g);
-                                nrej += (v0 && !ok0 ? 1 : 0) + (v1 && !ok1 ? 1 : 0);
+                            bool ok0 = v0 && !s0, ok1 = v1 && !s1;
+                            nself += (s0 ? 1 : 0) + (s1 ? 1 : 0);
+                            {
+                                // guard band (reading A12): the distance phase took r^2 < hi; a pair at
+                                // or above lo is decided exactly in integer quanta (rare)
+                                const P2 r2 = dot(d, d);
+                                const bool b0 = ok0 && r2.v.x >= g.cut2_lo, b1 = ok1 && r2.v.y >= g.cut2_lo;
+                                if (b0 || b1) {
+                                    if (b0) ok0 = exact_in_range(d.x.v.x, d.y.v.x, d.z.v.x, g);
+                                    if (b1) ok1 = exact_in_range(d.x.v.y, d.y.v.y, d.z.v.y, g);
+                                    nrej += (b0 && !ok0 ? 1 : 0) + (b1 && !ok1 ? 1 : 0);
+                                }
                             }
                             const P2 msk = p2(ok0 ? 1.f : 0.f, ok1 ? 1.f : 0.f);
                             V3 fh = v3zero();
@@ -277,6 +292,46 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_force_rigid3(ForceArgs a)
 #undef RIG3_POLAR
                             wacc -= dot(d, fh);      // molecular virial (A6): -r_ij . F_ij
                         }
+                        // ---- molecule force and torque of this lane's share, group reduction
+                        float F[3] = {0.f, 0.f, 0.f}, T[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+                        for (int k = 0; k < SH::NS; ++k) {
+                            int slot;
+                            if (k < NLJ) slot = k;
+                            else if (k < NLJ + NQ) slot = NLJ + (k - NLJ);
+                            else if (k < NLJ + NQ + NMU) slot = SH::SMU + 2 * (k - NLJ - NQ);
+                            else slot = SH::SQQ + 2 * (k - NLJ - NQ - NMU);
+                            const float4 sp = si[slot < NSLOT ? slot : 0];
+                            const float fx = fs[k].x.v.x + fs[k].x.v.y, fy = fs[k].y.v.x + fs[k].y.v.y,
+                                        fz = fs[k].z.v.x + fs[k].z.v.y;
+                            F[0] += fx; F[1] += fy; F[2] += fz;
+                            T[0] += sp.y * fz - sp.z * fy;
+                            T[1] += sp.z * fx - sp.x * fz;
+                            T[2] += sp.x * fy - sp.y * fx;
+                        }
+                        if (NMU + NQQ > 0) {
+#pragma unroll
+                            for (int k = 0; k < NPOL; ++k) {
+                                T[0] += ts[k].x.v.x + ts[k].x.v.y;
+                                T[1] += ts[k].y.v.x + ts[k].y.v.y;
+                                T[2] += ts[k].z.v.x + ts[k].z.v.y;
+                            }
+                        }
+#pragma unroll
+                        for (int o = 8; o > 0; o >>= 1)
+#pragma unroll
+                            for (int q = 0; q < 3; ++q) {
+                                F[q] += __shfl_xor_sync(FULL, F[q], o);
+                                T[q] += __shfl_xor_sync(FULL, T[q], o);
+                            }
+                        Uw += (double)uacc.v.x + (double)uacc.v.y;
+                        Ww += (double)wacc.v.x + (double)wacc.v.y;
+                        npw += gl == 0 ? cnt : 0;
+                        if (gact && gl == 0) {
+                            float* A = acc + 8 * il;
+                            A[0] += F[0]; A[1] += F[1]; A[2] += F[2];
+                            A[4] += T[0]; A[5] += T[1]; A[6] += T[2];
+                        }
                     };
 
                     // ---- distance phase: candidate pair p = base + gl (elements 2p, 2p + 1), ballot
@@ -284,87 +339,44 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_force_rigid3(ForceArgs a)
                     int cnt = 0;
                     const float2 nxi = make_float2(-xi.x, -xi.x), nyi = make_float2(-xi.y, -xi.y),
                                  nzi = make_float2(-xi.z, -xi.z);
-                    // this molecule's own element in the chunk (row 4 = the home row, after cell x - 1)
-                    const int self = rinfo[8 * 4 + 6] + rinfo[8 * 4 + 3] + ib + il - k0;
                     const int npair = (mm + 1) >> 1;
-                    const float lo = g.cut2_lo, hi = gact ? g.cut2_hi : -1.f;   // idle group: no hits
-                    // two steps per iteration; the list (HCAP - 64 entries free) is checked once per iteration
-                    for (int base = 0; base < npair; base += 32) {
+                    const float hi = gact ? g.cut2_hi : -1.f;      // idle group: no hits
+                    unsigned below;
+                    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(below));
+                    // two steps per iteration; the list (HCAP - 64 entries free) is evaluated when full
+                    int base = 0;
+                    for (;;) {
+                        for (; base < npair; base += 32) {
 #pragma unroll
-                        for (int u = 0; u < 2; ++u) {
-                            const int p = base + 16 * u + gl;
-                            const int pp = p < npair ? p : CAP / 2;
-                            const float4 xy = cxy[pp];
-                            const float2 zz = pz[pp];
-                            const float2 dx = __fadd2_rn(make_float2(xy.x, xy.y), nxi);
-                            const float2 dy = __fadd2_rn(make_float2(xy.z, xy.w), nyi);
-                            const float2 dz = __fadd2_rn(zz, nzi);
-                            float2 r2 = __fmul2_rn(dx, dx);
-                            r2 = __ffma2_rn(dy, dy, r2);
-                            r2 = __ffma2_rn(dz, dz, r2);
-                            const int j0 = 2 * pp;
-                            const bool h0 = (r2.x < hi) && (j0 != self);
-                            const bool h1 = (r2.y < hi) && (j0 + 1 != self);
-                            const unsigned b0 = __ballot_sync(FULL, h0) & gmask, b1 = __ballot_sync(FULL, h1) & gmask;
-                            const int n0 = __popc(b0);
-                            // unconditional stores (a miss writes the spare slot HCAP)
-                            hl[h0 ? cnt + __popc(b0 & below) : HCAP] = (uint16_t)(j0 | (r2.x >= lo ? 0x8000 : 0));
-                            hl[h1 ? cnt + n0 + __popc(b1 & below) : HCAP] = (uint16_t)((j0 + 1) | (r2.y >= lo ? 0x8000 : 0));
-                            cnt += n0 + __popc(b1);
+                            for (int u = 0; u < 2; ++u) {
+                                const int p = base + 16 * u + gl;
+                                const int pp = p < npair ? p : CAP / 2;
+                                const float4 xy = cxy[pp];
+                                const float2 zz = pz[pp];
+                                const float2 dx = __fadd2_rn(make_float2(xy.x, xy.y), nxi);
+                                const float2 dy = __fadd2_rn(make_float2(xy.z, xy.w), nyi);
+                                const float2 dz = __fadd2_rn(zz, nzi);
+                                float2 r2 = __fmul2_rn(dx, dx);
+                                r2 = __ffma2_rn(dy, dy, r2);
+                                r2 = __ffma2_rn(dz, dz, r2);
+                                const bool h0 = r2.x < hi, h1 = r2.y < hi;
+                                const unsigned b0 = __ballot_sync(FULL, h0) & gmask, b1 = __ballot_sync(FULL, h1) & gmask;
+                                const int n0 = __popc(b0);
+                                if (h0) hl[cnt + __popc(b0 & below)] = (uint16_t)(2 * pp);
+                                if (h1) hl[cnt + n0 + __popc(b1 & below)] = (uint16_t)(2 * pp + 1);
+                                cnt += n0 + __popc(b1);
+                            }
+                            if (__any_sync(FULL, cnt > HCAP - 64)) { base += 32; break; }
                         }
-                        if (__any_sync(FULL, cnt > HCAP - 64)) {       // list full: evaluate it now
-                            __syncwarp();
-                            force_rounds(cnt);
-                            npw += gl == 0 ? cnt : 0;
-                            cnt = 0;
-                            __syncwarp();
-                        }
+                        if (base >= npair) break;
+                        __syncwarp();                               // list full: evaluate it now
+                        flush(cnt);
+                        cnt = 0;
+                        __syncwarp();
                     }
                     __syncwarp();
-                    force_rounds(cnt);
-                    npw += gl == 0 ? cnt : 0;
+                    flush(cnt);
                     __syncwarp();
-                    // ---- molecule force and torque of this lane's share, group reduction
-                    float F[3] = {0.f, 0.f, 0.f}, T[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-                    for (int k = 0; k < SH::NS; ++k) {
-                        int slot;
-                        if (k < NLJ) slot = k;
-                        else if (k < NLJ + NQ) slot = NLJ + (k - NLJ);
-                        else if (k < NLJ + NQ + NMU) slot = SH::SMU + 2 * (k - NLJ - NQ);
-                        else slot = SH::SQQ + 2 * (k - NLJ - NQ - NMU);
-                        const float4 sp = si[slot < NSLOT ? slot : 0];
-                        const float fx = fs[k].x.v.x + fs[k].x.v.y, fy = fs[k].y.v.x + fs[k].y.v.y,
-                                    fz = fs[k].z.v.x + fs[k].z.v.y;
-                        F[0] += fx; F[1] += fy; F[2] += fz;
-                        T[0] += sp.y * fz - sp.z * fy;
-                        T[1] += sp.z * fx - sp.x * fz;
-                        T[2] += sp.x * fy - sp.y * fx;
-                    }
-                    if (NMU + NQQ > 0) {
-#pragma unroll
-                        for (int k = 0; k < NPOL; ++k) {
-                            T[0] += ts[k].x.v.x + ts[k].x.v.y;
-                            T[1] += ts[k].y.v.x + ts[k].y.v.y;
-                            T[2] += ts[k].z.v.x + ts[k].z.v.y;
-                        }
-                    }
-#pragma unroll
-                    for (int o = 8; o > 0; o >>= 1)
-#pragma unroll
-                        for (int q = 0; q < 3; ++q) {
-                            F[q] += __shfl_xor_sync(FULL, F[q], o);
-                            T[q] += __shfl_xor_sync(FULL, T[q], o);
-                        }
-                    Uw += (double)uacc.v.x + (double)uacc.v.y;
-                    Ww += (double)wacc.v.x + (double)wacc.v.y;
-                    uacc = p2(0.f);
-                    wacc = p2(0.f);
-                    if (gact && gl == 0) {
-                        float* A = acc + 8 * il;
-                        A[0] += F[0]; A[1] += F[1]; A[2] += F[2];
-                        A[4] += T[0]; A[5] += T[1]; A[6] += T[2];
-                    }
                 }
             }
             __syncthreads();
@@ -377,7 +389,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_force_rigid3(ForceArgs a)
     }
     Uw = warp_sum_d(Uw);
     Ww = warp_sum_d(Ww);
-    npw = warp_sum_ll(npw - nrej);
+    npw = warp_sum_ll(npw - nrej - nself);
     ncw = warp_sum_ll(ncw);
     if (lane == 0) a.part[blockIdx.x * WARPS + wib] = ForcePartial{0.5 * Uw, 0.5 * Ww, npw, ncw, 0.0};
 }
