@@ -31,6 +31,11 @@ import numpy as np  # noqa: E402
 
 FLOP_COM_TEST = 8      # per half-shell candidate (SURVEY §8(d) flop model)
 FLOP_LJ_PAIR = 20      # per in-range unique pair (incl. U, W)
+FLOP_SITE_DIST = 8     # site-site separation of a rigid pair's site pair
+# site-pair kernels (incl. U, W; FMA = 2): LJ 20, q-q RF 23, Q-Q ~110;
+# the other polar kinds by the same closed-form count (model values)
+FLOP_SITE = {("lj", "lj"): 20, ("q", "q"): 23, ("Q", "Q"): 110, ("q", "mu"): 40, ("q", "Q"): 50,
+             ("mu", "mu"): 60, ("mu", "Q"): 90}
 REF_SAMPLE = 32768     # molecules per --impl reference step
 
 
@@ -44,6 +49,20 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
     return p.parse_args()
+
+
+def pair_flops(system):
+    """Algorithmic flops per in-range unique molecule pair (single component):
+    every site pair of the pair (reading A1) = site separation + site kernel."""
+    c = system["components"][0]
+    n = {"lj": len(c["lj"]), "q": len(c["charges"]), "mu": len(c["dipoles"]), "Q": len(c["quadrupoles"])}
+    if n["lj"] == 1 and n["q"] + n["mu"] + n["Q"] == 0 and len(system["components"]) == 1:
+        return FLOP_LJ_PAIR                      # single-site LJ: the COM separation is the site one
+    tot = 0
+    for (ka, kb), f in FLOP_SITE.items():
+        m = n[ka] * n[kb] * (1 if ka == kb else 2)
+        tot += m * (FLOP_SITE_DIST + f)
+    return tot
 
 
 def peaks():
@@ -236,7 +255,7 @@ def main():
     value = world * N * args.steps / (tot_ms / 1e3) / 1e6
     # ---- roofline of the dominant kernel (force): algorithmic flops
     ncand_half = obs["n_candidates"] / 2.0
-    flops = FLOP_COM_TEST * ncand_half + FLOP_LJ_PAIR * obs["n_pairs"]
+    flops = FLOP_COM_TEST * ncand_half + pair_flops(system) * obs["n_pairs"]
     f_ms = float(np.mean(force_ms)) if force_ms and min(force_ms) > 0 else None
     pk = peaks()
     props = torch.cuda.get_device_properties(local)
@@ -250,9 +269,11 @@ def main():
         pass
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "kernel": "k_force_lj1" if ctx.get_grid()["kernel"] == 0 else "k_force_rigid",
+                "kernel": {0: "k_force_lj1", 1: "k_force_rigid3"}.get(ctx.get_grid()["kernel"], "k_force_rigid"),
                 "force_ms": f_ms, "force_share": (f_ms * args.steps / tot_ms) if f_ms else None,
                 "algorithmic_gflop_per_launch": flops / 1e9,
+                "flop_model": "8 x half-shell COM candidates + per unique in-range pair: sum over site pairs of "
+                              "(8 separation + kernel: LJ 20, q-q RF 23, Q-Q 110) (SURVEY 8(d)); single-site LJ: 20",
                 "peak_note": "FP32 CUDA cores: SMs x 128 x 2 x sm_max_mhz (MEASURED_PEAKS.json), derived"}
     # ---- end to end through the C ABI with pinned host buffers
     e2e = None
