@@ -96,6 +96,33 @@ def test_dense_cells_chunking(md, oracle_mod):
     check_step0(md, oracle_mod, s2)
 
 
+@pytest.mark.parametrize("comp_name", ["c2", "c3"])
+def test_dense_rigid_batches_and_chunks(md, oracle_mod, comp_name):
+    """k_force_rigid3 beyond its common case: ~76 molecules per cell (home
+    molecules in batches of 64) and 27-cell neighbourhoods of 2048 molecules
+    (staged in chunks of 1152), 2CLJQ and TIP4P shapes."""
+    s = S.lj_fcc(8, 0.9, 1.0, 9, "dense3", 1, jitter=0.01, rc=4.3)
+    rng = np.random.default_rng(4)
+    if comp_name == "c2":
+        comp = S.c2_component()
+    else:
+        # TIP4P-like shape in reduced units: the config-3 site geometry scaled to ~0.3 sigma,
+        # charges +0.3, +0.3, -0.6 on H, H, M, one LJ site (sigma = eps = 1)
+        tip = S.config("c3s")["components"][0]
+        k = 0.3 / 1.43
+        comp = dict(tip)
+        comp["lj"] = [(tuple(k * x for x in p_), 1.0, 1.0) for p_, _, _ in tip["lj"]]
+        comp["charges"] = [(tuple(k * x for x in p_), 0.3 if q > 0 else -0.6) for p_, q in tip["charges"]]
+        comp["mass"] = 1.0
+        comp["inertia"] = (0.02, 0.05, 0.03)
+        s["eps_rf"] = math.inf
+    s["components"] = [comp]
+    s["q"] = S.random_quaternions(rng, len(s["r"]))
+    s["j"] = S.angular_momenta(rng, s["q"], comp["inertia"], 1.0)
+    ctx, _ = check_step0(md, oracle_mod, s)
+    assert ctx.get_grid()["kernel"] == 1
+
+
 @pytest.mark.parametrize("n_cells,rho,rc", [(5, 0.75, 2.5), (6, 0.75, 2.5), (7, 0.8, 2.5), (6, 0.9, 1.6)])
 def test_step0_lj_boxes(md, oracle_mod, n_cells, rho, rc):
     """Single-site kernel on small boxes (3-6 cells per axis: sub-chunks
