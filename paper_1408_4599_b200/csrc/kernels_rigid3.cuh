@@ -49,6 +49,19 @@ using rig2::bcast;
 using rig2::pack;
 using rig2::dot;
 
+// LJ 12-6 of a site pair without the LJTS shift (added per partner by the caller), r = x_b - x_a
+__device__ __forceinline__ void lj_noshift(V3 r, float sig2, float eps24, float eps4, P2& u, V3& fa, V3& fh)
+{
+    const P2 r2 = dot(r, r);
+    const P2 ir2 = rig2::rcp2(r2);
+    const P2 s2 = sig2 * ir2;
+    const P2 s6 = s2 * s2 * s2;
+    const P2 fr = (eps24 * ir2) * s6 * fma(p2(2.f), s6, p2(-1.f));
+    u = fma(eps4 * s6, s6 - p2(1.f), u);
+    fa.x = fa.x - fr * r.x; fa.y = fa.y - fr * r.y; fa.z = fa.z - fr * r.z;
+    fh.x = fh.x - fr * r.x; fh.y = fh.y - fr * r.y; fh.z = fh.z - fr * r.z;
+}
+
 template <int NLJ, int NQ, int NMU, int NQQ>
 constexpr int smem_bytes()
 {
@@ -59,7 +72,7 @@ constexpr int smem_bytes()
 }
 
 template <int NLJ, int NQ, int NMU, int NQQ>
-__global__ void __launch_bounds__(WARPS * 32, 2) k_force_rigid3(ForceArgs a)
+__global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceArgs a)
 {
     using SH = Shape<NLJ, NQ, NMU, NQQ>;
     constexpr int NSLOT = SH::NSLOT;
@@ -202,54 +215,71 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_force_rigid3(ForceArgs a)
 #pragma unroll
                         for (int s = 0; s < NPOL; ++s) ts[s] = v3zero();
                         P2 uacc = p2(0.f), wacc = p2(0.f);
+                        int nval = 0;                          // real partners evaluated by this lane
                         const int cmax = max(__shfl_sync(FULL, cnt, 0), __shfl_sync(FULL, cnt, 16));
                         for (int k = 0; k < cmax; k += 32) {
                             const int e0 = k + gl, e1 = k + 16 + gl;
                             const bool v0 = e0 < cnt, v1 = e1 < cnt;
-                            // the molecule itself is on the list (r = 0): replaced by the dummy
+                            // Entries that are not partners -- past the list, the molecule itself (on the
+                            // list with r = 0), out of range in the guard band -- are the far dummy: its
+                            // site moments are 0 and its LJ terms vanish (~1e-26), so no mask is needed;
+                            // the LJTS shifts are subtracted per real partner at the end
                             const int h0 = v0 ? hl[e0] : DUMMY, h1 = v1 ? hl[e1] : DUMMY;
                             const bool s0 = v0 && h0 == self, s1 = v1 && h1 == self;
-                            const int j0 = s0 ? DUMMY : h0, j1 = s1 ? DUMMY : h1;
-                            const int q0 = 4 * (j0 >> 1) + (j0 & 1), q1 = 4 * (j1 >> 1) + (j1 & 1);
-                            const V3 d = V3{p2(cxf[q0] - xi.x, cxf[q1] - xi.x),
-                                            p2(cxf[q0 + 2] - xi.y, cxf[q1 + 2] - xi.y),
-                                            p2(czf[2 * (j0 >> 1) + (j0 & 1)] - xi.z, czf[2 * (j1 >> 1) + (j1 & 1)] - xi.z)};
-                            bool ok0 = v0 && !s0, ok1 = v1 && !s1;
+                            int j0 = s0 ? DUMMY : h0, j1 = s1 ? DUMMY : h1;
+                            auto com_of = [&](int j, float& X, float& Y, float& Z) {
+                                const int q = 4 * (j >> 1) + (j & 1);
+                                X = cxf[q] - xi.x;
+                                Y = cxf[q + 2] - xi.y;
+                                Z = czf[2 * (j >> 1) + (j & 1)] - xi.z;
+                            };
+                            V3 d;
+                            com_of(j0, d.x.v.x, d.y.v.x, d.z.v.x);
+                            com_of(j1, d.x.v.y, d.y.v.y, d.z.v.y);
                             nself += (s0 ? 1 : 0) + (s1 ? 1 : 0);
                             {
                                 // guard band (reading A12): the distance phase took r^2 < hi; a pair at
                                 // or above lo is decided exactly in integer quanta (rare)
                                 const P2 r2 = dot(d, d);
-                                const bool b0 = ok0 && r2.v.x >= g.cut2_lo, b1 = ok1 && r2.v.y >= g.cut2_lo;
+                                const bool b0 = j0 != DUMMY && r2.v.x >= g.cut2_lo, b1 = j1 != DUMMY && r2.v.y >= g.cut2_lo;
                                 if (b0 || b1) {
-                                    if (b0) ok0 = exact_in_range(d.x.v.x, d.y.v.x, d.z.v.x, g);
-                                    if (b1) ok1 = exact_in_range(d.x.v.y, d.y.v.y, d.z.v.y, g);
-                                    nrej += (b0 && !ok0 ? 1 : 0) + (b1 && !ok1 ? 1 : 0);
+                                    if (b0 && !exact_in_range(d.x.v.x, d.y.v.x, d.z.v.x, g)) {
+                                        j0 = DUMMY;
+                                        com_of(j0, d.x.v.x, d.y.v.x, d.z.v.x);
+                                        ++nrej;
+                                    }
+                                    if (b1 && !exact_in_range(d.x.v.y, d.y.v.y, d.z.v.y, g)) {
+                                        j1 = DUMMY;
+                                        com_of(j1, d.x.v.y, d.y.v.y, d.z.v.y);
+                                        ++nrej;
+                                    }
                                 }
                             }
-                            const P2 msk = p2(ok0 ? 1.f : 0.f, ok1 ? 1.f : 0.f);
+                            nval += (j0 != DUMMY ? 1 : 0) + (j1 != DUMMY ? 1 : 0);
                             V3 fh = v3zero();
 #pragma unroll
                             for (int ia = 0; ia < NLJ; ++ia) {
                                 const V3 sa = bcast(si[ia]);
+                                const V3 da = V3{d.x - sa.x, d.y - sa.y, d.z - sa.z};
 #pragma unroll
                                 for (int ibb = 0; ibb < NLJ; ++ibb) {
                                     const V3 sb = pack(ssw[ibb * STRIDE + j0], ssw[ibb * STRIDE + j1]);
-                                    const V3 rv = V3{d.x + sb.x - sa.x, d.y + sb.y - sa.y, d.z + sb.z - sa.z};
+                                    const V3 rv = V3{da.x + sb.x, da.y + sb.y, da.z + sb.z};
                                     const float4 pp = ljp[ia * NLJ + ibb];
-                                    rig2::lj2(rv, pp.x, pp.y * msk, pp.z * msk, pp.w * msk, uacc, fs[ia], fh);
+                                    lj_noshift(rv, pp.x, pp.y, pp.z, uacc, fs[ia], fh);
                                 }
                             }
 #pragma unroll
                             for (int ia = 0; ia < NQ; ++ia) {
                                 const float4 sa4 = si[SH::SQ + ia];
                                 const V3 sa = bcast(sa4);
+                                const V3 da = V3{d.x - sa.x, d.y - sa.y, d.z - sa.z};
 #pragma unroll
                                 for (int ibb = 0; ibb < NQ; ++ibb) {
                                     const float4 b0 = ssw[(SH::SQ + ibb) * STRIDE + j0], b1 = ssw[(SH::SQ + ibb) * STRIDE + j1];
                                     const V3 sb = pack(b0, b1);
-                                    const V3 rv = V3{d.x + sb.x - sa.x, d.y + sb.y - sa.y, d.z + sb.z - sa.z};
-                                    rig2::qq2(rv, sa4.w * p2(b0.w, b1.w) * msk, krf, crf, uacc, fs[NLJ + ia], fh);
+                                    const V3 rv = V3{da.x + sb.x, da.y + sb.y, da.z + sb.z};
+                                    rig2::qq2(rv, sa4.w * p2(b0.w, b1.w), krf, crf, uacc, fs[NLJ + ia], fh);
                                 }
                             }
 #define RIG3_POLAR(KA, KB, NA, NB, SLA, SLB, FIDX, TIDX, STA, STB)                                          \
@@ -267,7 +297,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_force_rigid3(ForceArgs a)
                                             ssw[((slb + 1) % NSLOT) * STRIDE + j1]) : v3zero();             \
             const V3 rv = V3{d.x + pb.x - pa.x, d.y + pb.y - pa.y, d.z + pb.z - pa.z};                     \
             V3 tdummy = v3zero();                                                                          \
-            rig2::polar2<KA, KB>(rv, ea, eb, pa4.w * p2(b0.w, b1.w) * msk, kmm, uacc, fs[FIDX + ia],       \
+            rig2::polar2<KA, KB>(rv, ea, eb, pa4.w * p2(b0.w, b1.w), kmm, uacc, fs[FIDX + ia],             \
                                  (TIDX) >= 0 ? ts[((TIDX) >= 0 ? (TIDX) : 0) + ia] : tdummy, fh);        \
         }                                                                                                  \
     }
@@ -324,7 +354,10 @@ __global__ void __launch_bounds__(WARPS * 32, 2) k_force_rigid3(ForceArgs a)
                                 F[q] += __shfl_xor_sync(FULL, F[q], o);
                                 T[q] += __shfl_xor_sync(FULL, T[q], o);
                             }
-                        Uw += (double)uacc.v.x + (double)uacc.v.y;
+                        float shsum = 0.f;                     // LJTS shifts of one molecule pair (A2)
+#pragma unroll
+                        for (int k = 0; k < NLJ * NLJ; ++k) shsum += ljp[k].w;
+                        Uw += (double)uacc.v.x + (double)uacc.v.y - (double)shsum * nval;
                         Ww += (double)wacc.v.x + (double)wacc.v.y;
                         npw += gl == 0 ? cnt : 0;
                         if (gact && gl == 0) {
