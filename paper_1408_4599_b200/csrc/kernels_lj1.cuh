@@ -97,23 +97,26 @@ struct Cfg {
     static constexpr int SMEM = WARPS * BYTES_PER_WARP;
 };
 
+// In terms of p = 1/r^6 (s6 = (sigma/r)^6 = c6 p, c6 = sigma^6): the force prefactor
+// s6 (s6 - 1/2) / r^2 = c6^2 p (p - 1/(2 c6)) / r^2, so the sigma^2 scaling of 1/r^2
+// costs nothing per pair (the powers of c6 are applied to the per-lane sums)
 struct Acc {
-    float2 gx, gy, gz;           // sum ir2 s6 (s6 - 1/2) d   (force = -48 eps g)
-    float2 a, b, h;              // sum s6^2, sum s6, sum ir2 r2 (= hit count)
+    float2 gx, gy, gz;           // sum ir2 p (p - hc) d   (force = -48 eps c6^2 g)
+    float2 a, b, h;              // sum p^2, sum p, sum ir2 r2 (= hit count)
     int hits_exact;              // hits found by the exact band pass / scalar paths
-    int band;                    // a pair fell into the guard band
+    float mb;                    // min |r^2 - mid| over the candidates (guard band iff <= hw)
 };
 
 __device__ __forceinline__ void acc_zero(Acc& A)
 {
     A.gx = A.gy = A.gz = A.a = A.b = A.h = make_float2(0.f, 0.f);
     A.hits_exact = 0;
-    A.band = 0;
+    A.mb = 1.0e30f;
 }
 
 // one candidate pair (j, j+1) against molecule (xi, yi, zi), fast pass
 __device__ __forceinline__ void pair2(const float4 xy, const float2 z, const float2 nxi, const float2 nyi,
-                                      const float2 nzi, const float2 sig2, const float lo, const float hi,
+                                      const float2 nzi, const float2 nhc, const float lo, const float2 nmid,
                                       Acc& A)
 {
     const float2 dx = __fadd2_rn(make_float2(xy.x, xy.y), nxi);
@@ -123,27 +126,28 @@ __device__ __forceinline__ void pair2(const float4 xy, const float2 z, const flo
     r2 = __ffma2_rn(dy, dy, r2);
     r2 = __ffma2_rn(dz, dz, r2);
     const bool h0 = r2.x < lo, h1 = r2.y < lo;
-    A.band |= (int)(((r2.x < hi) & !h0) | ((r2.y < hi) & !h1));
+    // guard band lo <= r^2 < hi  =>  |r^2 - mid| <= hw (the difference is exact there)
+    const float2 dm = __fadd2_rn(r2, nmid);
+    A.mb = fminf(A.mb, fminf(fabsf(dm.x), fabsf(dm.y)));
     float2 ir2;
     ir2.x = h0 ? rcp_approx(r2.x) : 0.f;
     ir2.y = h1 ? rcp_approx(r2.y) : 0.f;
-    const float2 s2 = __fmul2_rn(ir2, sig2);
-    const float2 s4 = __fmul2_rn(s2, s2);
-    const float2 s6 = __fmul2_rn(s4, s2);
-    const float2 t = __fadd2_rn(s6, make_float2(-0.5f, -0.5f));
-    const float2 fr = __fmul2_rn(__fmul2_rn(s6, ir2), t);
+    const float2 i4 = __fmul2_rn(ir2, ir2);
+    const float2 p6 = __fmul2_rn(i4, ir2);
+    const float2 t = __fadd2_rn(p6, nhc);
+    const float2 fr = __fmul2_rn(__fmul2_rn(p6, ir2), t);
     A.gx = __ffma2_rn(fr, dx, A.gx);
     A.gy = __ffma2_rn(fr, dy, A.gy);
     A.gz = __ffma2_rn(fr, dz, A.gz);
-    A.a = __ffma2_rn(s6, s6, A.a);
-    A.b = __fadd2_rn(s6, A.b);
+    A.a = __ffma2_rn(p6, p6, A.a);
+    A.b = __fadd2_rn(p6, A.b);
     A.h = __ffma2_rn(ir2, r2, A.h);
 }
 
 // one element in the exact (guard-band) pass or the scalar paths: the same
 // fp32 r^2 as the fast pass; BAND_ONLY: only band pairs, decided exactly
 template <bool BAND_ONLY>
-__device__ __forceinline__ void elem1(float X, float Y, float Z, float xi, float yi, float zi, float sig2,
+__device__ __forceinline__ void elem1(float X, float Y, float Z, float xi, float yi, float zi, float hc,
                                       float lo, float hi, const GridP& g, Acc& A)
 {
     const float dx = __fadd_rn(X, -xi), dy = __fadd_rn(Y, -yi), dz = __fadd_rn(Z, -zi);
@@ -157,14 +161,13 @@ __device__ __forceinline__ void elem1(float X, float Y, float Z, float xi, float
     }
     if (!hit) return;
     const float ir2 = rcp_approx(r2);
-    const float s2 = ir2 * sig2;
-    const float s6 = s2 * s2 * s2;
-    const float fr = s6 * ir2 * (s6 - 0.5f);
+    const float p6 = ir2 * ir2 * ir2;
+    const float fr = p6 * ir2 * (p6 - hc);
     A.gx.x += fr * dx;
     A.gy.x += fr * dy;
     A.gz.x += fr * dz;
-    A.a.x += s6 * s6;
-    A.b.x += s6;
+    A.a.x += p6 * p6;
+    A.b.x += p6;
     A.hits_exact += 1;
 }
 
@@ -203,7 +206,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
     const int nx = g.nc[0], ny = g.nc[1], nz = g.nc[2];
     const int kmax = min(KMAX, nx - 2);
     const float lo = g.cut2_lo, hi = g.cut2_hi;
-    const float2 sig2 = make_float2(a.sig2, a.sig2);
+    const float c6 = a.sig2 * a.sig2 * a.sig2, hc = 0.5f / c6;     // sigma^6, 1/(2 sigma^6)
+    const double c6d = (double)c6;
+    const float2 nhc = make_float2(-hc, -hc);
+    const float mid = 0.5f * (lo + hi), hw = 0.5f * (hi - lo) + 1e-6f * hi;   // band test (margin >> rounding of mid)
+    const float2 nmid = make_float2(-mid, -mid);
     const float rc2w = hi * (1.f + 1.f / 4096.f);       // generous window (necessary condition only)
     const float ex = g.edge[0], inv_ex = 1.f / g.edge[0];
     long long ncw = 0;
@@ -309,15 +316,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                                 for (int j = j0; j < j1; ++j) {
                                     if (j == mi) continue;
                                     const float4 xj = __ldg(a.xs + j);
-                                    elem1<false>(xj.x + ox, xj.y + oy, xj.z + oz, xsi.x, xsi.y, xsi.z, a.sig2, lo,
+                                    elem1<false>(xj.x + ox, xj.y + oy, xj.z + oz, xsi.x, xsi.y, xsi.z, hc, lo,
                                                  hi, g, A);
                                 }
                             }
                         }
-                    const float f = -2.f * a.eps24;
+                    const float f = -2.f * a.eps24 * c6 * c6;
                     Fown = make_float3(f * A.gx.x, f * A.gy.x, f * A.gz.x);
                     a.force[mi] = make_float4(Fown.x, Fown.y, Fown.z, 0.f);
-                    const double Ad = A.a.x, Bd = A.b.x;
+                    const double Ad = c6d * c6d * A.a.x, Bd = c6d * A.b.x;
                     ncw += ncand_l;
                     Uw += (double)a.eps4 * (Ad - Bd) - (double)a.shift * A.hits_exact;
                     Ww += (double)a.eps24 * (2.0 * Ad - Bd);
@@ -496,26 +503,26 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                         p = seg_b(sg);
                         e = seg_e(sg);
                     }
-                    pair2(xy0, z0, nxi, nyi, nzi, sig2, lo, hi, A);
-                    pair2(xy1, z1, nxi, nyi, nzi, sig2, lo, hi, A);
+                    pair2(xy0, z0, nxi, nyi, nzi, nhc, lo, nmid, A);
+                    pair2(xy1, z1, nxi, nyi, nzi, nhc, lo, nmid, A);
                 }
             }
             // the other element of the self pair
             if (act) {
                 const int eo = eself ^ 1;
                 elem1<false>(sxf[4 * pself + (eo & 1)], sxf[4 * pself + 2 + (eo & 1)], szf[2 * pself + (eo & 1)],
-                             xi, yi, zi, a.sig2, lo, hi, g, A);
+                             xi, yi, zi, hc, lo, hi, g, A);
             }
             // guard band (rare): exact re-decision of the band pairs of the lanes that saw one
-            if (__any_sync(0xffffffffu, A.band)) {
-                if (A.band) {
+            if (__any_sync(0xffffffffu, A.mb <= hw)) {
+                if (A.mb <= hw) {
                     for (int k = 0; k < nseg; ++k) {
                         const SegT sg = sseg[32 * k + lane];
                         for (int p = seg_b(sg); p < seg_e(sg); ++p) {
                             const float4 xy = sxy[p];
                             const float2 zz = sz[p];
-                            elem1<true>(xy.x, xy.z, zz.x, xi, yi, zi, a.sig2, lo, hi, g, A);
-                            elem1<true>(xy.y, xy.w, zz.y, xi, yi, zi, a.sig2, lo, hi, g, A);
+                            elem1<true>(xy.x, xy.z, zz.x, xi, yi, zi, hc, lo, hi, g, A);
+                            elem1<true>(xy.y, xy.w, zz.y, xi, yi, zi, hc, lo, hi, g, A);
                         }
                     }
                 }
@@ -526,12 +533,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
 #pragma unroll
                 for (int r = 0; r < 9; ++r) nc27 += scb[10 * r + kk + 3] - scb[10 * r + kk];
                 ncw += nc27;
-                const float f = -2.f * a.eps24;
+                const float f = -2.f * a.eps24 * c6 * c6;
                 const float gx = A.gx.x + A.gx.y, gy = A.gy.x + A.gy.y, gz = A.gz.x + A.gz.y;
                 Fown = make_float3(f * gx, f * gy, f * gz);
                 a.force[mi] = make_float4(Fown.x, Fown.y, Fown.z, 0.f);
                 const int hits = __float2int_rn(A.h.x + A.h.y) + A.hits_exact;
-                const double Ad = (double)A.a.x + (double)A.a.y, Bd = (double)A.b.x + (double)A.b.y;
+                const double Ad = c6d * c6d * ((double)A.a.x + (double)A.a.y), Bd = c6d * ((double)A.b.x + (double)A.b.y);
                 Uw += (double)a.eps4 * (Ad - Bd) - (double)a.shift * hits;
                 Ww += (double)a.eps24 * (2.0 * Ad - Bd);
                 npw += hits;
