@@ -67,7 +67,7 @@ constexpr int smem_bytes()
 {
     // COM pairs (CAP/2 + 1 pairs x 24 B, +1: the far dummy pair), NSLOT x (CAP + 1) site float4,
     // hit lists, accumulators, row table
-    return (CAP / 2 + 1) * 16 + ((CAP / 2 + 2) & ~1) * 8 + (NLJ + NQ + 2 * NMU + 2 * NQQ) * (CAP + 1) * 16 + WARPS * 2 * (HCAP + 2) * 2 +
+    return (CAP / 2 + 1) * 16 + ((CAP / 2 + 2) & ~1) * 8 + (NLJ + NQ + 2 * NMU + 2 * NQQ) * (CAP + 1) * 16 + WARPS * 2 * 2 * (HCAP + 2) * 2 +
            NHMAX * 8 * 4 + 16 * 8 * 4;
 }
 
@@ -90,12 +90,13 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
     float* czf = reinterpret_cast<float*>(pz);
     float4* ssw = reinterpret_cast<float4*>(pz + ((CAP / 2 + 2) & ~1));   // 16-byte aligned           // ssw[slot * STRIDE + j]
     uint16_t* hls = reinterpret_cast<uint16_t*>(ssw + NSLOT * STRIDE);     // [2 * WARPS][HCAP]
-    float* acc = reinterpret_cast<float*>(hls + 2 * WARPS * (HCAP + 2));         // [NHMAX][8]: F, tau
+    float* acc = reinterpret_cast<float*>(hls + 2 * WARPS * 2 * (HCAP + 2));         // [NHMAX][8]: F, tau
     int* rinfo = reinterpret_cast<int*>(acc + NHMAX * 8);                  // [9][8] row table + [72..]: totals
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
     const int half = lane >> 4, gl = lane & 15;
     const int grp = 2 * wib + half, NG = 2 * WARPS;
-    uint16_t* hl = hls + grp * (HCAP + 2);                                 // + spare slot for misses
+    uint16_t* hlA = hls + grp * 2 * (HCAP + 2);                            // two lists per group (+ spare slots)
+    uint16_t* hlB = hlA + (HCAP + 2);
     const unsigned gmask = 0xffffu << (16 * half);
     const GridP& g = a.g;
     const DevModel* __restrict__ M = a.model;
@@ -180,22 +181,24 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                     for (int s = 0; s < NSLOT; ++s) ssw[s * STRIDE + k] = sv[s];
                 }
                 __syncthreads();
-                // ---- home molecules of this batch, one per group (groups in lock-step per warp)
-                const int nrounds = (nb + NG - 1) / NG;
+                // ---- home molecules of this batch, two per group at a time (A, B): the distance
+                //      phase tests each staged molecule against both (one load, two tests)
+                const int nrounds = (nb + 2 * NG - 1) / (2 * NG);
                 for (int rr = 0; rr < nrounds; ++rr) {
-                    const int il = rr * NG + grp;          // batch-local home index of this group
-                    const bool gact = il < nb;
-                    if (!__any_sync(FULL, gact)) break;
-                    const int my = s_i + ib + (gact ? il : 0);
-                    const float4 xi = __ldg(a.xs + my);
-                    // this molecule's own element in the chunk (row 4 = the home row, after cell x - 1)
-                    const int self = rinfo[8 * 4 + 6] + rinfo[8 * 4 + 3] + ib + il - k0;
+                    const int ilA = rr * 2 * NG + grp, ilB = ilA + NG;   // batch-local home indices
+                    const bool gA = ilA < nb, gB = ilB < nb;
+                    if (!__any_sync(FULL, gA)) break;
+                    const int myA = s_i + ib + (gA ? ilA : 0), myB = s_i + ib + (gB ? ilB : 0);
+                    const float4 xiA = __ldg(a.xs + myA), xiB = __ldg(a.xs + myB);
+                    // the molecules' own elements in the chunk (row 4 = the home row, after cell x - 1)
+                    const int self0 = rinfo[8 * 4 + 6] + rinfo[8 * 4 + 3] + ib - k0;
+                    const int selfA = self0 + ilA, selfB = self0 + ilB;
 
                     // force phase over the group's list [0, cnt): entries (k + gl, k + 16 + gl) packed;
                     // then this lane's force and torque, group reduction, accumulation into acc[il].
                     // Self-contained (site offsets, accumulators and LJ table are loaded here), so
                     // that none of it is live during the distance phase
-                    auto flush = [&](int cnt) {
+                    auto flush = [&](int cnt, const uint16_t* hl, int my, float4 xi, int self, int il, bool gact) {
                         float4 si[NSLOT];
 #pragma unroll
                         for (int s = 0; s < NSLOT; ++s) si[s] = __ldg(a.site + (size_t)s * a.cap + my);
@@ -367,16 +370,25 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                         }
                     };
 
-                    // ---- distance phase: candidate pair p = base + gl (elements 2p, 2p + 1), ballot
-                    //      compaction; pairs in the guard band are flagged for the exact test
-                    int cnt = 0;
-                    const float2 nxi = make_float2(-xi.x, -xi.x), nyi = make_float2(-xi.y, -xi.y),
-                                 nzi = make_float2(-xi.z, -xi.z);
+                    // ---- distance phase: candidate pair p = base + gl (elements 2p, 2p + 1) against A
+                    //      and B, ballot compaction into the two lists (fixed order)
+                    int cntA = 0, cntB = 0;
+                    const float2 nxA = make_float2(-xiA.x, -xiA.x), nyA = make_float2(-xiA.y, -xiA.y),
+                                 nzA = make_float2(-xiA.z, -xiA.z);
+                    const float2 nxB = make_float2(-xiB.x, -xiB.x), nyB = make_float2(-xiB.y, -xiB.y),
+                                 nzB = make_float2(-xiB.z, -xiB.z);
                     const int npair = (mm + 1) >> 1;
-                    const float hi = gact ? g.cut2_hi : -1.f;      // idle group: no hits
+                    const float hiA = gA ? g.cut2_hi : -1.f, hiB = gB ? g.cut2_hi : -1.f;   // idle: no hits
                     unsigned below;
                     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(below));
-                    // two steps per iteration; the list (HCAP - 64 entries free) is evaluated when full
+                    auto append = [&](uint16_t* hl, int& cnt, bool h0, bool h1, int pp) {
+                        const unsigned b0 = __ballot_sync(FULL, h0) & gmask, b1 = __ballot_sync(FULL, h1) & gmask;
+                        const int n0 = __popc(b0);
+                        if (h0) hl[cnt + __popc(b0 & below)] = (uint16_t)(2 * pp);
+                        if (h1) hl[cnt + n0 + __popc(b1 & below)] = (uint16_t)(2 * pp + 1);
+                        cnt += n0 + __popc(b1);
+                    };
+                    // two steps per iteration; the lists (HCAP - 64 entries free) are evaluated when full
                     int base = 0;
                     for (;;) {
                         for (; base < npair; base += 32) {
@@ -386,29 +398,32 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                                 const int pp = p < npair ? p : CAP / 2;
                                 const float4 xy = cxy[pp];
                                 const float2 zz = pz[pp];
-                                const float2 dx = __fadd2_rn(make_float2(xy.x, xy.y), nxi);
-                                const float2 dy = __fadd2_rn(make_float2(xy.z, xy.w), nyi);
-                                const float2 dz = __fadd2_rn(zz, nzi);
+                                const float2 xx = make_float2(xy.x, xy.y), yy = make_float2(xy.z, xy.w);
+                                float2 dx = __fadd2_rn(xx, nxA), dy = __fadd2_rn(yy, nyA), dz = __fadd2_rn(zz, nzA);
                                 float2 r2 = __fmul2_rn(dx, dx);
                                 r2 = __ffma2_rn(dy, dy, r2);
                                 r2 = __ffma2_rn(dz, dz, r2);
-                                const bool h0 = r2.x < hi, h1 = r2.y < hi;
-                                const unsigned b0 = __ballot_sync(FULL, h0) & gmask, b1 = __ballot_sync(FULL, h1) & gmask;
-                                const int n0 = __popc(b0);
-                                if (h0) hl[cnt + __popc(b0 & below)] = (uint16_t)(2 * pp);
-                                if (h1) hl[cnt + n0 + __popc(b1 & below)] = (uint16_t)(2 * pp + 1);
-                                cnt += n0 + __popc(b1);
+                                const bool a0 = r2.x < hiA, a1 = r2.y < hiA;
+                                dx = __fadd2_rn(xx, nxB); dy = __fadd2_rn(yy, nyB); dz = __fadd2_rn(zz, nzB);
+                                r2 = __fmul2_rn(dx, dx);
+                                r2 = __ffma2_rn(dy, dy, r2);
+                                r2 = __ffma2_rn(dz, dz, r2);
+                                const bool c0 = r2.x < hiB, c1 = r2.y < hiB;
+                                append(hlA, cntA, a0, a1, pp);
+                                append(hlB, cntB, c0, c1, pp);
                             }
-                            if (__any_sync(FULL, cnt > HCAP - 64)) { base += 32; break; }
+                            if (__any_sync(FULL, cntA > HCAP - 64 || cntB > HCAP - 64)) { base += 32; break; }
                         }
                         if (base >= npair) break;
-                        __syncwarp();                               // list full: evaluate it now
-                        flush(cnt);
-                        cnt = 0;
+                        __syncwarp();                               // a list is full: evaluate both now
+                        flush(cntA, hlA, myA, xiA, selfA, ilA, gA);
+                        flush(cntB, hlB, myB, xiB, selfB, ilB, gB);
+                        cntA = cntB = 0;
                         __syncwarp();
                     }
                     __syncwarp();
-                    flush(cnt);
+                    flush(cntA, hlA, myA, xiA, selfA, ilA, gA);
+                    flush(cntB, hlB, myB, xiB, selfB, ilB, gB);
                     __syncwarp();
                 }
             }
