@@ -68,7 +68,7 @@ constexpr int smem_bytes()
     // COM pairs (CAP/2 + 1 pairs x 24 B, +1: the far dummy pair), NSLOT x (CAP + 1) site float4,
     // hit lists, accumulators, row table
     return (CAP / 2 + 1) * 16 + ((CAP / 2 + 2) & ~1) * 8 + (NLJ + NQ + 2 * NMU + 2 * NQQ) * (CAP + 1) * 16 + WARPS * 2 * 2 * (HCAP + 2) * 2 +
-           NHMAX * 8 * 4 + 16 * 8 * 4;
+           NHMAX * 8 * 4 + WARPS * 2 * 8 * 4 + 16 * 8 * 4;
 }
 
 template <int NLJ, int NQ, int NMU, int NQQ>
@@ -91,7 +91,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
     float4* ssw = reinterpret_cast<float4*>(pz + ((CAP / 2 + 2) & ~1));   // 16-byte aligned           // ssw[slot * STRIDE + j]
     uint16_t* hls = reinterpret_cast<uint16_t*>(ssw + NSLOT * STRIDE);     // [2 * WARPS][HCAP]
     float* acc = reinterpret_cast<float*>(hls + 2 * WARPS * 2 * (HCAP + 2));         // [NHMAX][8]: F, tau
-    int* rinfo = reinterpret_cast<int*>(acc + NHMAX * 8);                  // [9][8] row table + [72..]: totals
+    float* tacc = acc + NHMAX * 8;                                         // [NG][8]: tail slices (F, tau)
+    int* rinfo = reinterpret_cast<int*>(tacc + 2 * WARPS * 8);             // [9][8] row table + [72..]: totals
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
     const int half = lane >> 4, gl = lane & 15;
     const int grp = 2 * wib + half, NG = 2 * WARPS;
@@ -147,6 +148,14 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
             const int nb = min(NHMAX, n_all - ib);
             if (ib > 0) __syncthreads();          // previous batch written out
             for (int k = tid; k < nb * 8; k += WARPS * 32) acc[k] = 0.f;
+            for (int k = tid; k < NG * 8; k += WARPS * 32) tacc[k] = 0.f;
+            // work plan: full rounds of two molecules per group; a last round with at most NG
+            // molecules is split instead -- each of them over P = NG / rem groups, one slice of
+            // the neighbourhood per group (partials summed in slice order at the write-out)
+            const int npr = nb / (2 * NG), rem = nb - npr * 2 * NG;
+            const bool split = rem > 0 && rem <= NG;
+            const int P = split ? NG / rem : 1;
+            const int nrounds = npr + (rem > 0 ? 1 : 0);
             for (int k0 = 0; k0 < mtot; k0 += CAP) {
                 const int mm = min(CAP, mtot - k0);
                 __syncthreads();
@@ -183,10 +192,23 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                 __syncthreads();
                 // ---- home molecules of this batch, two per group at a time (A, B): the distance
                 //      phase tests each staged molecule against both (one load, two tests)
-                const int nrounds = (nb + 2 * NG - 1) / (2 * NG);
+                const int npair = (mm + 1) >> 1;
                 for (int rr = 0; rr < nrounds; ++rr) {
-                    const int ilA = rr * 2 * NG + grp, ilB = ilA + NG;   // batch-local home indices
-                    const bool gA = ilA < nb, gB = ilB < nb;
+                    const bool tail = split && rr == npr;
+                    int ilA, ilB, p0 = 0, p1 = npair;                    // batch-local home indices, slice
+                    bool gA, gB;
+                    float *tgtA, *tgtB;
+                    if (!tail) {
+                        ilA = rr * 2 * NG + grp; ilB = ilA + NG;
+                        gA = ilA < nb; gB = ilB < nb;
+                        tgtA = acc + 8 * ilA; tgtB = acc + 8 * ilB;
+                    } else {
+                        const int t = grp / P, sp = grp - t * P;
+                        ilA = npr * 2 * NG + t; ilB = 0;
+                        gA = t < rem; gB = false;
+                        p0 = sp * npair / P; p1 = (sp + 1) * npair / P;
+                        tgtA = tacc + 8 * grp; tgtB = acc;
+                    }
                     if (!__any_sync(FULL, gA)) break;
                     const int myA = s_i + ib + (gA ? ilA : 0), myB = s_i + ib + (gB ? ilB : 0);
                     const float4 xiA = __ldg(a.xs + myA), xiB = __ldg(a.xs + myB);
@@ -198,7 +220,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                     // then this lane's force and torque, group reduction, accumulation into acc[il].
                     // Self-contained (site offsets, accumulators and LJ table are loaded here), so
                     // that none of it is live during the distance phase
-                    auto flush = [&](int cnt, const uint16_t* hl, int my, float4 xi, int self, int il, bool gact) {
+                    auto flush = [&](int cnt, const uint16_t* hl, int my, float4 xi, int self, float* tgt, bool gact) {
                         float4 si[NSLOT];
 #pragma unroll
                         for (int s = 0; s < NSLOT; ++s) si[s] = __ldg(a.site + (size_t)s * a.cap + my);
@@ -364,9 +386,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                         Ww += (double)wacc.v.x + (double)wacc.v.y;
                         npw += gl == 0 ? cnt : 0;
                         if (gact && gl == 0) {
-                            float* A = acc + 8 * il;
-                            A[0] += F[0]; A[1] += F[1]; A[2] += F[2];
-                            A[4] += T[0]; A[5] += T[1]; A[6] += T[2];
+                            tgt[0] += F[0]; tgt[1] += F[1]; tgt[2] += F[2];
+                            tgt[4] += T[0]; tgt[5] += T[1]; tgt[6] += T[2];
                         }
                     };
 
@@ -377,8 +398,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                                  nzA = make_float2(-xiA.z, -xiA.z);
                     const float2 nxB = make_float2(-xiB.x, -xiB.x), nyB = make_float2(-xiB.y, -xiB.y),
                                  nzB = make_float2(-xiB.z, -xiB.z);
-                    const int npair = (mm + 1) >> 1;
                     const float hiA = gA ? g.cut2_hi : -1.f, hiB = gB ? g.cut2_hi : -1.f;   // idle: no hits
+                    const int span = max(__shfl_sync(FULL, p1 - p0, 0), __shfl_sync(FULL, p1 - p0, 16));
                     unsigned below;
                     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(below));
                     auto append = [&](uint16_t* hl, int& cnt, bool h0, bool h1, int pp) {
@@ -391,11 +412,11 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                     // two steps per iteration; the lists (HCAP - 64 entries free) are evaluated when full
                     int base = 0;
                     for (;;) {
-                        for (; base < npair; base += 32) {
+                        for (; base < span; base += 32) {
 #pragma unroll
                             for (int u = 0; u < 2; ++u) {
-                                const int p = base + 16 * u + gl;
-                                const int pp = p < npair ? p : CAP / 2;
+                                const int p = p0 + base + 16 * u + gl;
+                                const int pp = p < p1 ? p : CAP / 2;
                                 const float4 xy = cxy[pp];
                                 const float2 zz = pz[pp];
                                 const float2 xx = make_float2(xy.x, xy.y), yy = make_float2(xy.z, xy.w);
@@ -414,22 +435,29 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                             }
                             if (__any_sync(FULL, cntA > HCAP - 64 || cntB > HCAP - 64)) { base += 32; break; }
                         }
-                        if (base >= npair) break;
+                        if (base >= span) break;
                         __syncwarp();                               // a list is full: evaluate both now
-                        flush(cntA, hlA, myA, xiA, selfA, ilA, gA);
-                        flush(cntB, hlB, myB, xiB, selfB, ilB, gB);
+                        flush(cntA, hlA, myA, xiA, selfA, tgtA, gA);
+                        flush(cntB, hlB, myB, xiB, selfB, tgtB, gB);
                         cntA = cntB = 0;
                         __syncwarp();
                     }
                     __syncwarp();
-                    flush(cntA, hlA, myA, xiA, selfA, ilA, gA);
-                    flush(cntB, hlB, myB, xiB, selfB, ilB, gB);
+                    flush(cntA, hlA, myA, xiA, selfA, tgtA, gA);
+                    flush(cntB, hlB, myB, xiB, selfB, tgtB, gB);
                     __syncwarp();
                 }
             }
             __syncthreads();
             for (int k = tid; k < nb; k += WARPS * 32) {
-                const float* A = acc + 8 * k;
+                float A[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) A[q] = acc[8 * k + q];
+                const int t = k - npr * 2 * NG;
+                if (split && t >= 0)                          // tail molecule: its slices in order
+                    for (int sp = 0; sp < P; ++sp)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) A[q] += tacc[8 * (t * P + sp) + q];
                 a.force[s_i + ib + k] = make_float4(A[0], A[1], A[2], 0.f);
                 a.torque[s_i + ib + k] = make_float4(A[4], A[5], A[6], 0.f);
             }
