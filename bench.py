@@ -182,6 +182,48 @@ def cpu_baseline(system, seconds=12.0):
                       f"{system['name']} ({t_tot:.1f} s, OpenMP over molecules)"}
 
 
+def measure_e2e(args, system, ctx, run, world, dist, flush):
+    import torch
+    N = len(system["r"])
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    h_r, h_v = pin(system["r"]), pin(system["v"])
+    h_c, h_id = pin(system["comp"]), pin(system["id"])
+    rigid = ctx.get_grid()["kernel"] != 0
+    h_q = pin(system["q"]) if rigid else None
+    h_j = pin(system["j"]) if rigid else None
+    out = {"r": torch.empty((N, 3), dtype=torch.float64).pin_memory(),
+           "v": torch.empty((N, 3), dtype=torch.float64).pin_memory()}
+    if rigid:
+        out["q"] = torch.empty((N, 4), dtype=torch.float64).pin_memory()
+        out["j"] = torch.empty((N, 3), dtype=torch.float64).pin_memory()
+    stepper = run.step if run is not None else ctx.step
+    e_ms = []
+    for k in range(args.e2e_steps + 1):
+        flush.zero_()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        ctx.set_molecules(h_r, h_v, comp=h_c, q=h_q, j=h_j, id=h_id, half_step=1)
+        stepper(1)
+        ctx.get_observables()
+        ctx.get_molecules(out)
+        dt = time.perf_counter() - t0
+        if k > 0:
+            e_ms.append(dt * 1e3)
+    ms = float(np.mean(e_ms))
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    h2d = N * (3 * 8 + 3 * 8 + 4 + 8 + (7 * 8 if rigid else 0))
+    d2h = N * (3 * 8 + 3 * 8 + (7 * 8 if rigid else 0)) + 64
+    return {"value": N / (ms / 1e3) / 1e6, "unit": "MMUPS", "h2d_bytes_per_step": h2d * world,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms,
+            "what": "set_molecules(pinned host) + step(1) + get_observables + get_molecules(pinned host)"
+                    + (" on every rank (global arrays in, owned molecules out), max over ranks" if world > 1 else "")}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -275,37 +317,16 @@ def main():
                 "flop_model": "8 x half-shell COM candidates + per unique in-range pair: sum over site pairs of "
                               "(8 separation + kernel: LJ 20, q-q RF 23, Q-Q 110) (SURVEY 8(d)); single-site LJ: 20",
                 "peak_note": "FP32 CUDA cores: SMs x 128 x 2 x sm_max_mhz (MEASURED_PEAKS.json), derived"}
-    # ---- end to end through the C ABI with pinned host buffers
+    # ---- end to end through the C ABI with pinned host buffers: every step uploads the
+    #      molecules (set_molecules from pinned host arrays, exact resume) and reads back the
+    #      observables and the molecules (get_molecules into pinned host arrays); at N > 1 each
+    #      rank does this on its own context of the decomposed run, time = max over ranks
     e2e = None
-    if args.e2e_steps > 0 and world == 1:
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-        h_r, h_v = pin(system["r"]), pin(system["v"])
-        h_c, h_id = pin(system["comp"]), pin(system["id"])
-        rigid = ctx.get_grid()["kernel"] != 0
-        h_q = pin(system["q"]) if rigid else None
-        h_j = pin(system["j"]) if rigid else None
-        out = {"r": torch.empty((N, 3), dtype=torch.float64).pin_memory(),
-               "v": torch.empty((N, 3), dtype=torch.float64).pin_memory()}
-        if rigid:
-            out["q"] = torch.empty((N, 4), dtype=torch.float64).pin_memory()
-            out["j"] = torch.empty((N, 3), dtype=torch.float64).pin_memory()
-        e_ms = []
-        for k in range(args.e2e_steps + 1):
-            flush.zero_()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            ctx.set_molecules(h_r, h_v, comp=h_c, q=h_q, j=h_j, id=h_id, half_step=1)
-            ctx.step(1)
-            ctx.get_observables()
-            ctx.get_molecules(out)
-            dt = time.perf_counter() - t0
-            if k > 0:
-                e_ms.append(dt * 1e3)
-        h2d = N * (3 * 8 + 3 * 8 + 4 + 8 + (7 * 8 if rigid else 0))
-        d2h = N * (3 * 8 + 3 * 8 + (7 * 8 if rigid else 0)) + 64
-        e2e = {"value": N / (np.mean(e_ms) / 1e3) / 1e6, "unit": "MMUPS", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": float(np.mean(e_ms)),
-               "what": "set_molecules(pinned host) + step(1) + get_observables + get_molecules(pinned host)"}
+    if args.e2e_steps > 0:
+        try:
+            e2e = measure_e2e(args, system, ctx, run, world, dist, flush)
+        except Exception as ex:                     # the device-timed line must still print
+            e2e = {"error": repr(ex)[:300]}
     if rank != 0:
         return
     cpu = None if args.no_cpu_baseline or world > 1 else cpu_baseline(system)
