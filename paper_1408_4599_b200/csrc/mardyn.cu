@@ -811,7 +811,6 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
     double* dv = dr + 3 * n;
     double* dq = dv + 3 * n;
     double* dj = dq + 4 * n;
-    int* dc = (int*)(dj + 3 * n);
     CK(cudaMemcpyAsync(dr, r, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(dv, v, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, s));
     if (ctx->rigid) {
@@ -821,7 +820,6 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
     CK(cudaMemcpyAsync(ctx->comp_dev, comp, sizeof(int) * n, cudaMemcpyHostToDevice, s));
     if (id) CK(cudaMemcpyAsync(ctx->ids_dev, id, sizeof(int64_t) * n, cudaMemcpyHostToDevice, s));
     else k_iota64<<<nblk(n, 256), 256, 0, s>>>((int)n, ctx->ids_dev);
-    (void)dc;
     CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
     CK(cudaMemsetAsync(ctx->flag, 0, 4, s));
     const int src = 1, dst = 0;
