@@ -306,16 +306,6 @@ __device__ __forceinline__ void block_sum2_d(double a, double b, double* out_a, 
     }
 }
 
-// append one exchange record to destination `dst`'s send segment
-__device__ __forceinline__ void dd_push(const DDArgs& d, int dst, uint4 p, float4 v, float4 q, float4 j)
-{
-    const int k = atomicAdd(&d.send_cnt[dst], 1);
-    if (k >= d.seg_cap) { atomicOr(d.flag, 256); return; }
-    DDRec r;
-    r.pos = p; r.vel = v; r.quat = q; r.angm = j;
-    d.send[(size_t)dst * d.seg_cap + k] = r;
-}
-
 // DD = spatial decomposition: ghosts are skipped and
 // dropped; an owned molecule whose new cell belongs to another rank is
 // packed as a migrant for it (and dropped here); an owned molecule whose new
@@ -334,6 +324,10 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
     double ket = 0.0, ker = 0.0;
     int cl_bin = -1;
     bool ghost = false;
+    unsigned dmask = 0;                                // DD: ranks this molecule is sent to
+    int own = -1;
+    uint4 pn = make_uint4(0, 0, 0, 0);
+    float4 vn = make_float4(0.f, 0.f, 0.f, 0.f), qn = vn, jn = vn;
     if (DD && t < n) {
         ghost = md_ghost(vel[t].w);
         if (ghost) cell_of[t] = -1;
@@ -374,19 +368,16 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
         }
         int cl = c[0] + g.nc[0] * (c[1] + g.nc[1] * c[2]);
         if (DD) {
-            const uint4 pn = pos[t];
-            const float4 vn = vel[t];
-            const float4 qn = RIGID ? quat[t] : make_float4(1.f, 0.f, 0.f, 0.f);
-            const float4 jn = RIGID ? angm[t] : make_float4(0.f, 0.f, 0.f, 0.f);
-            const int own = dd.owner[cl];
-            unsigned gm = dd.gmask[cl] & ~(1u << dd.rank);
-            while (gm) {                                   // halo copies for the other ranks
-                const int r = __ffs(gm) - 1;
-                gm &= gm - 1u;
-                dd_push(dd, r, pn, make_float4(vn.x, vn.y, vn.z, __int_as_float(md_comp(vn.w) | 256)), qn, jn);
-            }
+            pn = pos[t];
+            vn = vel[t];
+            qn = RIGID ? quat[t] : make_float4(1.f, 0.f, 0.f, 0.f);
+            jn = RIGID ? angm[t] : make_float4(0.f, 0.f, 0.f, 0.f);
+            own = dd.owner[cl];
+            // halo copies for the other ranks whose halo holds the new cell; the record for the
+            // new owner (migrant) if that is another rank -- packed below, one atomic per warp
+            // and destination
+            dmask = (dd.gmask[cl] & ~(1u << dd.rank)) | (own != dd.rank ? 1u << own : 0u);
             if (own != dd.rank) {                          // migrant
-                dd_push(dd, own, pn, vn, qn, jn);
                 if ((dd.gmask[cl] >> dd.rank) & 1u) {      // its new cell is in my halo: keep a copy
                     vel[t] = make_float4(vn.x, vn.y, vn.z, __int_as_float(md_comp(vn.w) | 256));
                 } else {
@@ -397,6 +388,33 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
         }
         if (cl >= 0) cell_of[t] = cl;
         cl_bin = cl;
+    }
+    if (DD) {
+        // warp-aggregated packing: per destination rank one atomic reserves the warp's slots
+        const int lane = threadIdx.x & 31;
+        const unsigned below = (1u << lane) - 1u;
+        for (int r = 0; r < dd.nranks; ++r) {
+            const bool pr = (dmask >> r) & 1u;
+            const unsigned b = __ballot_sync(0xffffffffu, pr);
+            if (b == 0u) continue;
+            const int leader = __ffs(b) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&dd.send_cnt[r], __popc(b));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (pr) {
+                const int k = base + __popc(b & below);
+                if (k >= dd.seg_cap) {
+                    atomicOr(dd.flag, 256);
+                } else {
+                    DDRec rec;
+                    rec.pos = pn;
+                    rec.vel = r == own ? vn : make_float4(vn.x, vn.y, vn.z, __int_as_float(md_comp(vn.w) | 256));
+                    rec.quat = qn;
+                    rec.angm = jn;
+                    dd.send[(size_t)r * dd.seg_cap + k] = rec;
+                }
+            }
+        }
     }
     // next step's cell histogram + arrival rank: molecules are in cell order, so
     // the lanes of a warp share few cells; one atomic per distinct cell (the arrival
