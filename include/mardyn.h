@@ -269,6 +269,28 @@ int mardyn_dd_buffers(struct mardyn_ctx* ctx, void** send, int64_t* seg_cap, voi
                       int32_t* record_bytes);
 int mardyn_dd_end_step(struct mardyn_ctx* ctx, int64_t n_recv);
 
+/* Asynchronous decomposed step (same work, no host synchronisation; PAPER.md
+ * P:46, P:220-221 halo and migration, exchanged every step):
+ *     mardyn_dd_begin_step_async -> transport -> mardyn_dd_end_step_async
+ * The record counts stay in device memory: send_cnt[d] (int32, nranks) = records
+ * in send segment d after begin; the transport fills recv_cnt[r] (int32, nranks)
+ * with the count rank r sent here and copies rank r's send segment (seg_cap
+ * records, fixed size) to segment r of this rank's receive buffer (receive
+ * buffer = nranks segments of seg_cap records; e.g. two all-to-alls with equal
+ * splits).  A segment holding more than seg_cap records sets an error that the
+ * next synchronising call (get_observables, get_molecules, ...) reports as
+ * MARDYN_ECAPACITY; so does an import beyond the capacity.
+ *   mardyn_dd_set_segment: seg_cap (1 .. the workspace's segment stride; the
+ *     asynchronous step also needs seg_cap * nranks <= the receive capacity, else
+ *     MARDYN_ESTATE); returned by mardyn_dd_buffers.
+ *   mardyn_dd_device_counts: device addresses of send_cnt and recv_cnt (owned by
+ *     the context's workspace).
+ * Host-side calls that need the molecule count fetch it from the device. */
+int mardyn_dd_set_segment(struct mardyn_ctx* ctx, int64_t seg_cap);
+int mardyn_dd_device_counts(struct mardyn_ctx* ctx, void** send_cnt, void** recv_cnt);
+int mardyn_dd_begin_step_async(struct mardyn_ctx* ctx);
+int mardyn_dd_end_step_async(struct mardyn_ctx* ctx);
+
 const char* mardyn_last_error(const struct mardyn_ctx* ctx);
 void mardyn_destroy(struct mardyn_ctx* ctx);
 

@@ -104,6 +104,7 @@ struct DDArgs {
     int seg_cap;
     int* send_cnt;               // nranks counters
     int* flag;                   // bit 8: send segment overflow
+    const int* n_dev;            // asynchronous step: molecule count in device memory (else the kernel's n)
 };
 
 struct ObsRec {                  // one history entry (matches mardyn_observables order)

@@ -199,9 +199,11 @@ __global__ void __launch_bounds__(1024) k_scan(int ncell, int* __restrict__ coun
 // start[cell] + arrival rank
 __global__ void k_scatter(int n, const uint4* __restrict__ pos, const int* __restrict__ cell_of,
                           const int* __restrict__ rank, const int* __restrict__ start,
-                          unsigned long long* __restrict__ keys, int* __restrict__ oldidx)
+                          unsigned long long* __restrict__ keys, int* __restrict__ oldidx,
+                          const int* __restrict__ n_dev = nullptr)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n_dev) n = *n_dev;                  // asynchronous decomposed step: count on the device
     if (i >= n) return;
     const int cl = cell_of[i];
     if (cl < 0) return;                     // dropped ghost or migrant (spatial decomposition)
@@ -321,6 +323,7 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
                                                    int* __restrict__ flag, DDArgs dd = DDArgs())
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (DD && dd.n_dev) n = *dd.n_dev;      // asynchronous decomposed step: count on the device
     double ket = 0.0, ker = 0.0;
     int cl_bin = -1;
     bool ghost = false;
@@ -446,6 +449,41 @@ __global__ void k_import(int n, int base, GridP g, const DDRec* __restrict__ rec
     const int cl = cell_of_u(g, 0, r.pos.x) + g.nc[0] * (cell_of_u(g, 1, r.pos.y) + g.nc[1] * cell_of_u(g, 2, r.pos.z));
     cell_of[t] = cl;
     rank[t] = atomicAdd(&count[cl], 1);
+}
+
+// asynchronous decomposed step: import the records of the fixed receive
+// segments (segment r = records from rank r, recv_cnt[r] of them, at most
+// seg_cap) after the n_old = *n_old_dev molecules kept in place, bin them, and
+// write the unsorted count for the cell rebuild.  Nothing goes to the host.
+__global__ void k_import_seg(int nranks, int seg_cap, const int* __restrict__ recv_cnt,
+                             const int* __restrict__ n_old_dev, int cap, GridP g, const DDRec* __restrict__ recv,
+                             uint4* __restrict__ pos, float4* __restrict__ vel, float4* __restrict__ quat,
+                             float4* __restrict__ angm, int* __restrict__ cell_of, int* __restrict__ rank,
+                             int* __restrict__ count, int* __restrict__ n_unsorted, int* __restrict__ flag)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = t / seg_cap, k = t - r * seg_cap;
+    const int n_old = *n_old_dev;
+    int base = n_old, tot = n_old;
+    for (int q = 0; q < nranks; ++q) {
+        const int c = min(recv_cnt[q], seg_cap);
+        if (q < r) base += c;
+        tot += c;
+    }
+    if (t == 0) {
+        if (tot > cap) atomicOr(flag, 512);
+        *n_unsorted = min(tot, cap);
+    }
+    if (r >= nranks || k >= min(recv_cnt[r], seg_cap)) return;
+    const int slot = base + k;
+    if (slot >= cap) return;
+    const DDRec rec = recv[(size_t)r * seg_cap + k];
+    pos[slot] = rec.pos;
+    vel[slot] = rec.vel;
+    if (quat) { quat[slot] = rec.quat; angm[slot] = rec.angm; }
+    const int cl = cell_of_u(g, 0, rec.pos.x) + g.nc[0] * (cell_of_u(g, 1, rec.pos.y) + g.nc[1] * cell_of_u(g, 2, rec.pos.z));
+    cell_of[slot] = cl;
+    rank[slot] = atomicAdd(&count[cl], 1);
 }
 
 // kinetic energy at t without integrating (compute_forces, A9)

@@ -136,6 +136,10 @@ struct mardyn_ctx {
     int last_force_launches = 0;
     // spatial decomposition (§4): this rank's box, cell owners, halos
     int dd_rank = 0, nranks = 1;
+    bool n_stale = false;                  // asynchronous decomposed steps: host copy of n out of date
+    int* recv_cnt = nullptr;               // asynchronous exchange: records received per source rank (device)
+    int* n_aux = nullptr;                  // unsorted count after the import (device)
+    int64_t seg_max = 0;                   // send segment stride of the workspace layout
     std::vector<int32_t> boxes;
     std::vector<uint8_t> h_owner;
     std::vector<uint32_t> h_gmask;
@@ -323,6 +327,22 @@ static int occupancy_grid(mardyn_ctx* ctx, K kernel, int threads, size_t smem = 
     return per_sm * ctx->num_sms;
 }
 
+// after asynchronous decomposed steps the molecule count is only in device
+// memory (start[ncell] of the last cell rebuild): fetch it before host-side use
+static int refresh_n(mardyn_ctx* ctx)
+{
+    if (!ctx->n_stale) return MARDYN_OK;
+    int kept = 0, nf = 0;
+    CK(cudaMemcpyAsync(&kept, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&nf, ctx->n_aux + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->n = kept;
+    ctx->n_force = nf;
+    ctx->n_stale = false;
+    return MARDYN_OK;
+}
+
+
 // forces at the current state of buffer `buf`; step = true (single-site
 // kernel, one domain) also advances the molecules by one leapfrog step and
 // bins them for the next cell rebuild (count must be zeroed before)
@@ -404,15 +424,17 @@ static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 // counting sort of the unsorted buffer `src` (cell_of / rank / count
 // filled) into buffer `dst`, canonical in-cell order (A13)
-static int enqueue_sort(mardyn_ctx* ctx, int src, int dst, int64_t n_unsorted = -1)
+// n_dev: the unsorted count is in device memory (asynchronous decomposed step;
+// the grids then cover the capacity)
+static int enqueue_sort(mardyn_ctx* ctx, int src, int dst, int64_t n_unsorted = -1, const int* n_dev = nullptr)
 {
-    const int n = (int)(n_unsorted < 0 ? ctx->n : n_unsorted), ncell = ctx->g.ncell;
+    const int n = n_dev ? (int)ctx->cap : (int)(n_unsorted < 0 ? ctx->n : n_unsorted), ncell = ctx->g.ncell;
     cudaStream_t s = ctx->stream;
     // (look-back flags carry an epoch, counts are zeroed as read: no memsets per step)
     k_scan<<<ctx->ntiles, 1024, 0, s>>>(ncell, ctx->count, ctx->start, ctx->scan_flags,
                                         reinterpret_cast<unsigned*>(ctx->scan_flags + ctx->ntiles), ctx->blk_ctr);
     k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->pos[src], ctx->cell_of, ctx->rank, ctx->start, ctx->keys,
-                                            ctx->oldidx);
+                                            ctx->oldidx, n_dev);
     if (ctx->rigid)
         k_canon<true><<<nblk(n, 256), 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->oldidx, ctx->cell_of, ctx->start,
                                                    ctx->pos[src], ctx->vel[src], ctx->quat[src], ctx->angm[src],
@@ -690,6 +712,8 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     int8_t* owned = nullptr;
     DDRec *sendbuf = nullptr, *recvbuf = nullptr;
     int* send_cnt = nullptr;
+    int* recv_cnt = nullptr;
+    int* n_aux = nullptr;
     const int64_t seg_cap = ctx->nranks > 1 ? cap / ctx->nranks + 4096 : 0;
     const int64_t recv_cap = ctx->nranks > 1 ? cap : 0;
     if (ctx->nranks > 1) {
@@ -699,6 +723,8 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         sendbuf = (DDRec*)take(sizeof(DDRec) * (size_t)seg_cap * ctx->nranks);
         recvbuf = (DDRec*)take(sizeof(DDRec) * (size_t)recv_cap);
         send_cnt = (int*)take(4 * (size_t)ctx->nranks);
+        recv_cnt = (int*)take(4 * (size_t)ctx->nranks);
+        n_aux = (int*)take(8);                     // [0] unsorted count after import, [1] n at force time
     }
     if (assign) {
         ctx->pos[0] = pos0; ctx->pos[1] = pos1; ctx->vel[0] = vel0; ctx->vel[1] = vel1;
@@ -712,6 +738,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         ctx->ids_dev = ids_dev; ctx->comp_dev = comp_dev;
         ctx->owner = owner; ctx->gmask = gmask; ctx->owned = owned; ctx->sendbuf = sendbuf;
         ctx->recvbuf = recvbuf; ctx->send_cnt = send_cnt; ctx->seg_cap = seg_cap; ctx->recv_cap = recv_cap;
+        ctx->recv_cnt = recv_cnt; ctx->n_aux = n_aux; ctx->seg_max = seg_cap; ctx->n_stale = false;
         ctx->ncell_pad = ncell_pad; ctx->ntiles = ntiles; ctx->nkblocks = nk;
     }
     return off;
@@ -768,6 +795,7 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
     // per-molecule validation runs on the device (k_ingest); the host keeps copies of
     // ids and components only for the decomposed egress
     ctx->n = n;
+    ctx->n_stale = false;
     if (ctx->nranks > 1) {
         ctx->ids.resize(n);
         ctx->comp_host.assign(comp, comp + n);
@@ -873,6 +901,7 @@ int mardyn_compute_forces(mardyn_ctx* ctx)
     if (!ctx) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    if (int rc0 = refresh_n(ctx)) return rc0;
     cudaStream_t s = ctx->stream;
     const int n = (int)ctx->n, b = ctx->cur;
     launch_force(ctx, b);
@@ -980,6 +1009,8 @@ static int sync_check(mardyn_ctx* ctx)
     int flag = 0;
     CK(cudaMemcpy(&flag, ctx->flag, 4, cudaMemcpyDeviceToHost));
     if (flag & 4) return fail(ctx, MARDYN_ECAPACITY, "a row of three cells exceeds the force kernel's shared-memory slab");
+    if (flag & 256) return fail(ctx, MARDYN_ECAPACITY, "exchange segment overflow (raise the segment capacity)");
+    if (flag & 512) return fail(ctx, MARDYN_ECAPACITY, "owned + received molecules exceed the capacity");
     if (flag & 2) return fail(ctx, MARDYN_EOVERLAP, "two molecule centres coincide");
     if (flag) return fail(ctx, MARDYN_EUNSTABLE, "non-finite force/torque or a molecule moved more than one cell edge in a step");
     return MARDYN_OK;
@@ -1106,6 +1137,7 @@ int mardyn_get_molecules(mardyn_ctx* ctx, int64_t cap, int64_t* n, int64_t* id, 
     if (!ctx || !n) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    if (int rc0 = refresh_n(ctx)) return rc0;
     if (cap < ctx->n) return fail(ctx, MARDYN_EINVAL, "cap < number of molecules");
     if (ctx->nranks > 1)      // the rank's owned molecules, with their ids
         return egress(ctx, r, v, q, j, nullptr, nullptr, nullptr, nullptr, -1, n, id, comp);
@@ -1120,6 +1152,7 @@ int mardyn_get_forces(mardyn_ctx* ctx, int64_t cap, double* F, double* tau, int6
     if (!ctx) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    if (int rc0 = refresh_n(ctx)) return rc0;
     if (cap < ctx->n) return fail(ctx, MARDYN_EINVAL, "cap < number of molecules");
     // forces are indexed by the sorted slots of the buffer they were computed on
     int64_t* idp = nullptr;
@@ -1144,6 +1177,7 @@ int mardyn_get_raw(mardyn_ctx* ctx, int64_t cap, uint32_t* pos_fixed, int32_t* c
     if (!ctx) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    if (int rc0 = refresh_n(ctx)) return rc0;
     if (cap < ctx->n) return fail(ctx, MARDYN_EINVAL, "cap < number of molecules");
     int rc = egress(ctx, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, pos_fixed, cell);
     if (rc) return rc;
@@ -1257,6 +1291,7 @@ int mardyn_dd_begin_step(mardyn_ctx* ctx, int64_t* send_counts)
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
     if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "no decomposition: use mardyn_step");
+    if (int rc0 = refresh_n(ctx)) return rc0;
     cudaStream_t s = ctx->stream;
     const int b = ctx->cur, n = (int)ctx->n;
     long long step = ctx->host_step;
@@ -1269,6 +1304,7 @@ int mardyn_dd_begin_step(mardyn_ctx* ctx, int64_t* send_counts)
     DDArgs dd;
     dd.rank = ctx->dd_rank; dd.nranks = ctx->nranks; dd.owner = ctx->owner; dd.gmask = ctx->gmask;
     dd.send = ctx->sendbuf; dd.seg_cap = (int)ctx->seg_cap; dd.send_cnt = ctx->send_cnt; dd.flag = ctx->flag;
+    dd.n_dev = nullptr;
     const int nkb = nblk(n, 256);
     if (ctx->rigid)
         k_integrate<true, true><<<nkb, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b], ctx->quat[b],
@@ -1315,6 +1351,7 @@ int mardyn_dd_end_step(mardyn_ctx* ctx, int64_t n_recv)
     if (!ctx) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "no decomposition");
+    if (int rc0 = refresh_n(ctx)) return rc0;
     if (n_recv < 0 || n_recv > ctx->recv_cap || ctx->n + n_recv > ctx->cap)
         return fail(ctx, MARDYN_ECAPACITY, "received records exceed the capacity");
     cudaStream_t s = ctx->stream;
@@ -1333,6 +1370,90 @@ int mardyn_dd_end_step(mardyn_ctx* ctx, int64_t n_recv)
     CK(cudaMemcpyAsync(&kept, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     ctx->n = kept;
+    ctx->cur = 1 - b;
+    ctx->host_step += 1;
+    ctx->last_obs = ctx->host_step - 1;
+    return MARDYN_OK;
+}
+
+// ---- asynchronous decomposed step (no host synchronisation): the same work as
+// dd_begin_step / dd_end_step, with the record counts kept in device memory and
+// the receive buffer laid out in fixed segments of seg_cap records per source
+// rank (segment r of rank d's receive buffer = rank r's send segment d).
+int mardyn_dd_set_segment(mardyn_ctx* ctx, int64_t seg_cap)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (ctx->nranks < 2 || !ctx->ws) return fail(ctx, MARDYN_ESTATE, "no decomposition workspace");
+    if (seg_cap < 1 || seg_cap > ctx->seg_max) return fail(ctx, MARDYN_EINVAL, "segment capacity out of range");
+    ctx->seg_cap = seg_cap;
+    return MARDYN_OK;
+}
+
+int mardyn_dd_device_counts(mardyn_ctx* ctx, void** send_cnt, void** recv_cnt)
+{
+    if (!ctx || !send_cnt || !recv_cnt) return MARDYN_EINVAL;
+    if (ctx->nranks < 2 || !ctx->ws) return fail(ctx, MARDYN_ESTATE, "no decomposition workspace");
+    *send_cnt = ctx->send_cnt;
+    *recv_cnt = ctx->recv_cnt;
+    return MARDYN_OK;
+}
+
+int mardyn_dd_begin_step_async(mardyn_ctx* ctx)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "no decomposition: use mardyn_step");
+    cudaStream_t s = ctx->stream;
+    const int b = ctx->cur;
+    long long step = ctx->host_step;
+    CK(cudaMemcpyAsync(ctx->step_ctr, &step, 8, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ctx->n_aux + 1, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaEventRecord(ctx->ev_f0[b], s));
+    launch_force(ctx, b);
+    CK(cudaEventRecord(ctx->ev_f1[b], s));
+    CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
+    CK(cudaMemsetAsync(ctx->send_cnt, 0, sizeof(int) * ctx->nranks, s));
+    DDArgs dd;
+    dd.rank = ctx->dd_rank; dd.nranks = ctx->nranks; dd.owner = ctx->owner; dd.gmask = ctx->gmask;
+    dd.send = ctx->sendbuf; dd.seg_cap = (int)ctx->seg_cap; dd.send_cnt = ctx->send_cnt; dd.flag = ctx->flag;
+    dd.n_dev = ctx->start + ctx->g.ncell;             // the sorted count of the last cell rebuild
+    const int nkb = ctx->nkblocks;
+    if (ctx->rigid)
+        k_integrate<true, true><<<nkb, 256, 0, s>>>((int)ctx->cap, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
+                                                    ctx->quat[b], ctx->angm[b], ctx->force, ctx->torque, ctx->cell_of,
+                                                    ctx->rank, ctx->count, ctx->kpart, ctx->flag, dd);
+    else
+        k_integrate<false, true><<<nkb, 256, 0, s>>>((int)ctx->cap, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
+                                                     nullptr, nullptr, ctx->force, ctx->torque, ctx->cell_of,
+                                                     ctx->rank, ctx->count, ctx->kpart, ctx->flag, dd);
+    k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, nkb, ctx->kpart, ctx->ndof,
+                                                  ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket, 0);
+    ctx->launches += 3;
+    CK(cudaGetLastError());
+    ctx->last_parity = b;
+    return MARDYN_OK;
+}
+
+int mardyn_dd_end_step_async(mardyn_ctx* ctx)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "no decomposition");
+    if (ctx->seg_cap * ctx->nranks > ctx->recv_cap)
+        return fail(ctx, MARDYN_ESTATE, "segment capacity x ranks exceeds the receive buffer (mardyn_dd_set_segment)");
+    cudaStream_t s = ctx->stream;
+    const int b = ctx->cur;
+    const int seg = (int)ctx->seg_cap;
+    k_import_seg<<<nblk((int64_t)seg * ctx->nranks, 256), 256, 0, s>>>(
+        ctx->nranks, seg, ctx->recv_cnt, ctx->start + ctx->g.ncell, (int)ctx->cap, ctx->g, ctx->recvbuf, ctx->pos[b],
+        ctx->vel[b], ctx->rigid ? ctx->quat[b] : nullptr, ctx->rigid ? ctx->angm[b] : nullptr, ctx->cell_of,
+        ctx->rank, ctx->count, ctx->n_aux, ctx->flag);
+    ctx->launches += 1;
+    int rc = enqueue_sort(ctx, b, 1 - b, -1, ctx->n_aux);
+    if (rc) return rc;
+    CK(cudaGetLastError());
+    ctx->n_stale = true;
     ctx->cur = 1 - b;
     ctx->host_step += 1;
     ctx->last_obs = ctx->host_step - 1;

@@ -29,6 +29,8 @@ EXPORTS = ["mardyn_create", "mardyn_get_grid", "mardyn_workspace_bytes", "mardyn
            "mardyn_get_raw", "mardyn_last_step_timing", "mardyn_set_profiling",
            "mardyn_launch_count", "mardyn_cell_cost", "mardyn_kd_decompose",
            "mardyn_set_decomposition", "mardyn_dd_begin_step", "mardyn_dd_buffers", "mardyn_dd_end_step",
+           "mardyn_dd_set_segment", "mardyn_dd_device_counts", "mardyn_dd_begin_step_async",
+           "mardyn_dd_end_step_async",
            "mardyn_set_thermostat", "mardyn_lj_tail", "mardyn_get_tail_corrections",
            "mardyn_last_error", "mardyn_destroy"]
 
@@ -110,6 +112,10 @@ def load_library():
     lib.mardyn_dd_begin_step.argtypes = [vp, vp]
     lib.mardyn_dd_buffers.argtypes = [vp, P(vp), P(C.c_int64), P(vp), P(C.c_int64), P(C.c_int32)]
     lib.mardyn_dd_end_step.argtypes = [vp, C.c_int64]
+    lib.mardyn_dd_set_segment.argtypes = [vp, C.c_int64]
+    lib.mardyn_dd_device_counts.argtypes = [vp, P(vp), P(vp)]
+    lib.mardyn_dd_begin_step_async.argtypes = [vp]
+    lib.mardyn_dd_end_step_async.argtypes = [vp]
     lib.mardyn_get_raw.argtypes = [vp, C.c_int64, vp, vp, vp]
     lib.mardyn_last_step_timing.argtypes = [vp, P(C.c_double), P(C.c_double), P(C.c_int32)]
     lib.mardyn_set_profiling.argtypes = [vp, C.c_int32]
@@ -329,6 +335,24 @@ class Context:
     def dd_end_step(self, n_recv):
         self._check(self.lib.mardyn_dd_end_step(self.h, int(n_recv)))
 
+    # asynchronous decomposed step (include/mardyn.h): counts stay in device memory
+    def dd_set_segment(self, seg_cap):
+        self._check(self.lib.mardyn_dd_set_segment(self.h, int(seg_cap)))
+
+    def dd_device_counts(self):
+        """(send_cnt, recv_cnt): int32 [nranks] tensor views of the workspace (zero copy)."""
+        sc = C.c_void_p(); rc = C.c_void_p()
+        self._check(self.lib.mardyn_dd_device_counts(self.h, C.byref(sc), C.byref(rc)))
+        base = self.ws.data_ptr()
+        view = lambda ptr: self.ws[ptr - base: ptr - base + 4 * self.nranks].view(self.torch.int32)
+        return view(sc.value), view(rc.value)
+
+    def dd_begin_step_async(self):
+        self._check(self.lib.mardyn_dd_begin_step_async(self.h))
+
+    def dd_end_step_async(self):
+        self._check(self.lib.mardyn_dd_end_step_async(self.h))
+
     def _n(self):
         n = C.c_int64()
         self._check(self.lib.mardyn_get_molecules(self.h, self.capacity, C.byref(n), None, None, None,
@@ -460,9 +484,15 @@ class DecomposedRun:
     torch.distributed all_to_all over NCCL (NVLink)."""
 
     def __init__(self, system, nranks, transport="loopback", rank=None, eta=None, boxes=None, stream=None,
-                 rebalance_interval=0):
+                 rebalance_interval=0, async_exchange=True):
         import torch
         self.torch = torch
+        # one stream for every local context and the transport: the asynchronous step
+        # orders the exchange after the packing and before the import by the stream alone
+        self.stream = stream if stream is not None else torch.cuda.Stream()
+        stream = self.stream
+        self.async_exchange = bool(async_exchange)
+        self.seg_ready = False
         self.system = system
         self.nranks = nranks
         self.transport = transport
@@ -488,6 +518,7 @@ class DecomposedRun:
                               id=system["id"], half_step=0)
             self.ctxs.append(ctx)
         self.bufs = [c.dd_buffers() for c in self.ctxs]
+        self.seg_max = int(self.bufs[0][0].shape[1])
 
     def gather_molecules(self):
         """All owned molecules of all ranks (v, j at t - dt/2), ordered by id."""
@@ -516,7 +547,9 @@ class DecomposedRun:
         for r, ctx in zip(ranks, self.ctxs):
             ctx.set_decomposition(r, self.nranks, flat, self.ndof)
             ctx.set_molecules(m["r"], m["v"], comp=m["comp"], q=m["q"], j=m["j"], id=m["id"], half_step=1)
+            ctx.dd_set_segment(self.seg_max)
         self.bufs = [c.dd_buffers() for c in self.ctxs]
+        self.seg_ready = False                       # re-size the exchange segments for the new boxes
         return self.boxes
 
     def owned_counts(self):
@@ -529,23 +562,71 @@ class DecomposedRun:
         return parts
 
     def step(self, n=1):
-        for _ in range(n):
-            if self.rebalance_interval and self.nsteps and self.nsteps % self.rebalance_interval == 0:
-                self.rebalance()
-            self.nsteps += 1
-            counts = [c.dd_begin_step() for c in self.ctxs]
-            if self.transport == "loopback":
-                for dst, cd in enumerate(self.ctxs):
-                    recv = self.bufs[dst][1]
-                    off = 0
-                    for src in range(self.nranks):
-                        k = int(counts[src][dst])
-                        if k:
-                            recv[off: off + k].copy_(self.bufs[src][0][dst, :k])
-                            off += k
-                    cd.dd_end_step(off)
-            else:
-                self._nccl_exchange(counts[0])
+        """n time steps of all local ranks.  The first step after construction or a
+        rebalance runs with host-side record counts and sizes the exchange segments
+        (twice the largest count + 1024 records); the following steps run
+        asynchronously (no host synchronisation: counts and records move between
+        ranks as two all-to-alls with equal splits, see include/mardyn.h)."""
+        with self.torch.cuda.stream(self.stream):
+            for _ in range(n):
+                if self.rebalance_interval and self.nsteps and self.nsteps % self.rebalance_interval == 0:
+                    self.rebalance()
+                self.nsteps += 1
+                if self.async_exchange and self.seg_ready:
+                    self._step_async()
+                    continue
+                counts = [c.dd_begin_step() for c in self.ctxs]
+                if self.transport == "loopback":
+                    for dst, cd in enumerate(self.ctxs):
+                        recv = self.bufs[dst][1]
+                        off = 0
+                        for src in range(self.nranks):
+                            k = int(counts[src][dst])
+                            if k:
+                                recv[off: off + k].copy_(self.bufs[src][0][dst, :k])
+                                off += k
+                        cd.dd_end_step(off)
+                else:
+                    self._nccl_exchange(counts[0])
+                if self.async_exchange:
+                    self._size_segments(counts)
+
+    def _size_segments(self, counts):
+        torch = self.torch
+        big = max(int(np.max(c)) for c in counts)
+        if self.transport != "loopback":
+            import torch.distributed as dist
+            t = torch.tensor([big], dtype=torch.int64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            big = int(t.item())
+        recv_cap = int(self.bufs[0][1].shape[0])
+        seg = min(self.seg_max, recv_cap // self.nranks, ((2 * big + 1024 + 255) // 256) * 256)
+        for c in self.ctxs:
+            c.dd_set_segment(seg)
+        self.seg = seg
+        self.bufs = [c.dd_buffers() for c in self.ctxs]
+        self.cnts = [c.dd_device_counts() for c in self.ctxs]
+        self.seg_ready = True
+
+    def _step_async(self):
+        p, seg = self.nranks, self.seg
+        for c in self.ctxs:
+            c.dd_begin_step_async()
+        if self.transport == "loopback":
+            for dst in range(p):
+                recv = self.bufs[dst][1][: p * seg].view(p, seg, -1)
+                rcnt = self.cnts[dst][1]
+                for src in range(p):
+                    recv[src].copy_(self.bufs[src][0][dst])
+                    rcnt[src: src + 1].copy_(self.cnts[src][0][dst: dst + 1])
+        else:
+            import torch.distributed as dist
+            send, recv = self.bufs[0]
+            scnt, rcnt = self.cnts[0]
+            dist.all_to_all_single(rcnt, scnt)
+            dist.all_to_all_single(recv[: p * seg].reshape(-1), send.reshape(-1))
+        for c in self.ctxs:
+            c.dd_end_step_async()
 
     def _nccl_exchange(self, cnt):
         import torch.distributed as dist
