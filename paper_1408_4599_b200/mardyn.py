@@ -475,6 +475,16 @@ def exchange_records(send, cnt, recv, nranks, dist):
     return off
 
 
+def exchange_segments(send, send_cnt, recv, recv_cnt, nranks, dist):
+    """Transport of the asynchronous decomposed step (include/mardyn.h): rank r's
+    send segment d (seg_cap records, fixed size; send[d]) lands in segment r of
+    rank d's receive buffer, and its record count send_cnt[d] in recv_cnt[r] of
+    rank d.  Two all-to-alls with equal splits; nothing is read on the host
+    (NCCL over NVLink on GPUs, gloo on CPU)."""
+    dist.all_to_all_single(recv_cnt, send_cnt)
+    dist.all_to_all_single(recv[: send.numel() // send.shape[-1]].reshape(-1), send.reshape(-1))
+
+
 class DecomposedRun:
     """p spatial subdomains (k-d tree, §4) stepping together.
 
@@ -623,8 +633,7 @@ class DecomposedRun:
             import torch.distributed as dist
             send, recv = self.bufs[0]
             scnt, rcnt = self.cnts[0]
-            dist.all_to_all_single(rcnt, scnt)
-            dist.all_to_all_single(recv[: p * seg].reshape(-1), send.reshape(-1))
+            exchange_segments(send, scnt, recv, rcnt, p, dist)
         for c in self.ctxs:
             c.dd_end_step_async()
 

@@ -198,6 +198,47 @@ def test_gloo_exchange_records():
         assert n == len(expect) and rows == expect
 
 
+def _seg_main(rank, world, port, result):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rec, seg = 64, 8
+    send = torch.zeros((world, seg, rec), dtype=torch.uint8)
+    scnt = torch.tensor([(rank + 2 * d) % 5 + 1 for d in range(world)], dtype=torch.int32)
+    for d in range(world):
+        for k in range(int(scnt[d])):
+            send[d, k, :3] = torch.tensor([rank, d, k], dtype=torch.uint8)
+    recv = torch.full((world * seg + 5, rec), 255, dtype=torch.uint8)   # receive capacity > nranks x seg
+    rcnt = torch.zeros(world, dtype=torch.int32)
+    M.exchange_segments(send, scnt, recv, rcnt, world, dist)
+    result[rank] = (rcnt.tolist(), recv[: world * seg, :3].tolist(), recv[world * seg:, 0].tolist())
+    dist.destroy_process_group()
+
+
+def test_gloo_exchange_segments():
+    """The asynchronous step's transport (fixed segments + device counts, two
+    equal-split all-to-alls) on world_size 2 with gloo: segment r of rank d's
+    receive buffer is rank r's send segment d, counts alongside, the rest of the
+    receive buffer untouched."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_seg_main, args=(2, port, result), nprocs=2, join=True)
+    for dst in range(2):
+        rcnt, rows, tail = result[dst]
+        assert rcnt == [(src + 2 * dst) % 5 + 1 for src in range(2)]
+        for src in range(2):
+            for k in range(rcnt[src]):
+                assert rows[8 * src + k] == [src, dst, k]
+        assert tail == [255] * 5
+
+
 def test_droplet_kd_beats_static_split():
     """Heterogeneous workload (off-centre droplet; the
     direction of Fig. 7): the cost-weighted k-d tree balances the
