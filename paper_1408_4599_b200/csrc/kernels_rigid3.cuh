@@ -88,8 +88,10 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
     float2* pz = reinterpret_cast<float2*>(cxy + CAP / 2 + 1);
     float* cxf = reinterpret_cast<float*>(cxy);
     float* czf = reinterpret_cast<float*>(pz);
-    float4* ssw = reinterpret_cast<float4*>(pz + ((CAP / 2 + 2) & ~1));   // 16-byte aligned           // ssw[slot * STRIDE + j]
-    uint16_t* hls = reinterpret_cast<uint16_t*>(ssw + NSLOT * STRIDE);     // [2 * WARPS][HCAP]
+    // site slots as four component arrays per slot (x, y, z, w): the two partners of a
+    // packed operand are two scalar loads into a register pair, no moves
+    float* sws = reinterpret_cast<float*>(pz + ((CAP / 2 + 2) & ~1));    // sws[(4 slot + c) * STRIDE + j]
+    uint16_t* hls = reinterpret_cast<uint16_t*>(sws + 4 * NSLOT * STRIDE);  // [2 * WARPS][HCAP]
     float* acc = reinterpret_cast<float*>(hls + 2 * WARPS * 2 * (HCAP + 2));         // [NHMAX][8]: F, tau
     float* tacc = acc + NHMAX * 8;                                         // [NG][8]: tail slices (F, tau)
     int* rinfo = reinterpret_cast<int*>(tacc + 2 * WARPS * 8);             // [9][8] row table + [72..]: totals
@@ -106,7 +108,12 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
         cxy[CAP / 2] = make_float4(1.0e4f, 1.0e4f, 1.0e4f, 1.0e4f);
         pz[CAP / 2] = make_float2(1.0e4f, 1.0e4f);
 #pragma unroll
-        for (int s = 0; s < NSLOT; ++s) ssw[s * STRIDE + DUMMY] = make_float4(0.f, 0.f, 1.f, 0.f);
+        for (int s = 0; s < NSLOT; ++s) {
+            sws[(4 * s + 0) * STRIDE + DUMMY] = 0.f;
+            sws[(4 * s + 1) * STRIDE + DUMMY] = 0.f;
+            sws[(4 * s + 2) * STRIDE + DUMMY] = 1.f;
+            sws[(4 * s + 3) * STRIDE + DUMMY] = 0.f;
+        }
     }
     double Uw = 0.0, Ww = 0.0;             // per lane (fp32 per home molecule, then fp64)
     long long npw = 0, ncw = 0;
@@ -187,7 +194,12 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                         czf[2 * ph + 1] = 1.0e4f;
                     }
 #pragma unroll
-                    for (int s = 0; s < NSLOT; ++s) ssw[s * STRIDE + k] = sv[s];
+                    for (int s = 0; s < NSLOT; ++s) {
+                        sws[(4 * s + 0) * STRIDE + k] = sv[s].x;
+                        sws[(4 * s + 1) * STRIDE + k] = sv[s].y;
+                        sws[(4 * s + 2) * STRIDE + k] = sv[s].z;
+                        sws[(4 * s + 3) * STRIDE + k] = sv[s].w;
+                    }
                 }
                 __syncthreads();
                 // ---- home molecules of this batch, two per group at a time (A, B): the distance
@@ -241,6 +253,15 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                         for (int s = 0; s < NPOL; ++s) ts[s] = v3zero();
                         P2 uacc = p2(0.f), wacc = p2(0.f);
                         int nval = 0;                          // real partners evaluated by this lane
+                        auto slot3 = [&](int sl, int j0, int j1) {
+                            const float* b = sws + 4 * sl * STRIDE;
+                            return V3{p2(b[j0], b[j1]), p2(b[STRIDE + j0], b[STRIDE + j1]),
+                                      p2(b[2 * STRIDE + j0], b[2 * STRIDE + j1])};
+                        };
+                        auto slotw = [&](int sl, int j0, int j1) {
+                            const float* b = sws + (4 * sl + 3) * STRIDE;
+                            return p2(b[j0], b[j1]);
+                        };
                         const int cmax = max(__shfl_sync(FULL, cnt, 0), __shfl_sync(FULL, cnt, 16));
                         for (int k = 0; k < cmax; k += 32) {
                             const int e0 = k + gl, e1 = k + 16 + gl;
@@ -288,7 +309,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                                 const V3 da = V3{d.x - sa.x, d.y - sa.y, d.z - sa.z};
 #pragma unroll
                                 for (int ibb = 0; ibb < NLJ; ++ibb) {
-                                    const V3 sb = pack(ssw[ibb * STRIDE + j0], ssw[ibb * STRIDE + j1]);
+                                    const V3 sb = slot3(ibb, j0, j1);
                                     const V3 rv = V3{da.x + sb.x, da.y + sb.y, da.z + sb.z};
                                     const float4 pp = ljp[ia * NLJ + ibb];
                                     lj_noshift(rv, pp.x, pp.y, pp.z, uacc, fs[ia], fh);
@@ -301,10 +322,9 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                                 const V3 da = V3{d.x - sa.x, d.y - sa.y, d.z - sa.z};
 #pragma unroll
                                 for (int ibb = 0; ibb < NQ; ++ibb) {
-                                    const float4 b0 = ssw[(SH::SQ + ibb) * STRIDE + j0], b1 = ssw[(SH::SQ + ibb) * STRIDE + j1];
-                                    const V3 sb = pack(b0, b1);
+                                    const V3 sb = slot3(SH::SQ + ibb, j0, j1);
                                     const V3 rv = V3{da.x + sb.x, da.y + sb.y, da.z + sb.z};
-                                    rig2::qq2(rv, sa4.w * p2(b0.w, b1.w), krf, crf, uacc, fs[NLJ + ia], fh);
+                                    rig2::qq2(rv, sa4.w * slotw(SH::SQ + ibb, j0, j1), krf, crf, uacc, fs[NLJ + ia], fh);
                                 }
                             }
 #define RIG3_POLAR(KA, KB, NA, NB, SLA, SLB, FIDX, TIDX, STA, STB)                                          \
@@ -316,13 +336,11 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
         _Pragma("unroll") for (int ibb = 0; ibb < NB; ++ibb)                                               \
         {                                                                                                  \
             const int slb = (SLB) + ibb * STB;                                                             \
-            const float4 b0 = ssw[slb * STRIDE + j0], b1 = ssw[slb * STRIDE + j1];                         \
-            const V3 pb = pack(b0, b1);                                                                    \
-            const V3 eb = (STB == 2) ? pack(ssw[((slb + 1) % NSLOT) * STRIDE + j0],                          \
-                                            ssw[((slb + 1) % NSLOT) * STRIDE + j1]) : v3zero();             \
+            const V3 pb = slot3(slb, j0, j1);                                                              \
+            const V3 eb = (STB == 2) ? slot3((slb + 1) % NSLOT, j0, j1) : v3zero();                        \
             const V3 rv = V3{d.x + pb.x - pa.x, d.y + pb.y - pa.y, d.z + pb.z - pa.z};                     \
             V3 tdummy = v3zero();                                                                          \
-            rig2::polar2<KA, KB>(rv, ea, eb, pa4.w * p2(b0.w, b1.w), kmm, uacc, fs[FIDX + ia],             \
+            rig2::polar2<KA, KB>(rv, ea, eb, pa4.w * slotw(slb, j0, j1), kmm, uacc, fs[FIDX + ia],         \
                                  (TIDX) >= 0 ? ts[((TIDX) >= 0 ? (TIDX) : 0) + ia] : tdummy, fh);        \
         }                                                                                                  \
     }
