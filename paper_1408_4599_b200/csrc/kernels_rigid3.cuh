@@ -49,6 +49,19 @@ using rig2::bcast;
 using rig2::pack;
 using rig2::dot;
 
+// charge-charge with reaction field (A4) without the constant c_rf, which the caller
+// subtracts per partner as c_rf (sum_a q_a)(sum_b q_b) -- zero for neutral molecules
+__device__ __forceinline__ void qq_nocrf(V3 r, P2 qq, float krf, P2& u, V3& fa, V3& fh)
+{
+    const P2 r2 = dot(r, r);
+    const P2 ir = rig2::rsqrt2(r2);
+    const P2 ir2 = ir * ir;
+    u = fma(qq, fma(p2(krf), r2, ir), u);
+    const P2 fr = qq * fma(ir, ir2, p2(-2.f * krf));
+    fa.x = fa.x - fr * r.x; fa.y = fa.y - fr * r.y; fa.z = fa.z - fr * r.z;
+    fh.x = fh.x - fr * r.x; fh.y = fh.y - fr * r.y; fh.z = fh.z - fr * r.z;
+}
+
 // LJ 12-6 of a site pair without the LJTS shift (added per partner by the caller), r = x_b - x_a
 __device__ __forceinline__ void lj_noshift(V3 r, float sig2, float eps24, float eps4, P2& u, V3& fa, V3& fh)
 {
@@ -324,7 +337,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                                 for (int ibb = 0; ibb < NQ; ++ibb) {
                                     const V3 sb = slot3(SH::SQ + ibb, j0, j1);
                                     const V3 rv = V3{da.x + sb.x, da.y + sb.y, da.z + sb.z};
-                                    rig2::qq2(rv, sa4.w * slotw(SH::SQ + ibb, j0, j1), krf, crf, uacc, fs[NLJ + ia], fh);
+                                    qq_nocrf(rv, sa4.w * slotw(SH::SQ + ibb, j0, j1), krf, uacc, fs[NLJ + ia], fh);
                                 }
                             }
 #define RIG3_POLAR(KA, KB, NA, NB, SLA, SLB, FIDX, TIDX, STA, STB)                                          \
@@ -400,7 +413,10 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                         float shsum = 0.f;                     // LJTS shifts of one molecule pair (A2)
 #pragma unroll
                         for (int k = 0; k < NLJ * NLJ; ++k) shsum += ljp[k].w;
-                        Uw += (double)uacc.v.x + (double)uacc.v.y - (double)shsum * nval;
+                        float qtot = 0.f;                      // molecule charge (one component: partners alike)
+#pragma unroll
+                        for (int k = 0; k < NQ; ++k) qtot += si[SH::SQ + k].w;
+                        Uw += (double)uacc.v.x + (double)uacc.v.y - ((double)shsum + (double)crf * qtot * qtot) * nval;
                         Ww += (double)wacc.v.x + (double)wacc.v.y;
                         npw += gl == 0 ? cnt : 0;
                         if (gact && gl == 0) {
