@@ -633,7 +633,15 @@ class DecomposedRun:
             import torch.distributed as dist
             send, recv = self.bufs[0]
             scnt, rcnt = self.cnts[0]
-            exchange_segments(send, scnt, recv, rcnt, p, dist)
+            try:
+                exchange_segments(send, scnt, recv, rcnt, p, dist)
+            except RuntimeError:
+                # a backend without these all-to-alls: finish this step with host-side
+                # counts and point-to-point records, and stay on that path
+                self.async_exchange = False
+                n = exchange_records(send, scnt.cpu().tolist(), recv, p, dist)
+                self.ctxs[0].dd_end_step(n)
+                return
         for c in self.ctxs:
             c.dd_end_step_async()
 
