@@ -639,7 +639,8 @@ class DecomposedRun:
                 # a backend without these all-to-alls: finish this step with host-side
                 # counts and point-to-point records, and stay on that path
                 self.async_exchange = False
-                n = exchange_records(send, scnt.cpu().tolist(), recv, p, dist)
+                cnt = [min(int(x), seg) for x in scnt.cpu().tolist()]   # overflow: flagged by the library
+                n = exchange_records(send, cnt, recv, p, dist)
                 self.ctxs[0].dd_end_step(n)
                 return
         for c in self.ctxs:
