@@ -1406,8 +1406,9 @@ int mardyn_dd_begin_step_async(mardyn_ctx* ctx)
     if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "no decomposition: use mardyn_step");
     cudaStream_t s = ctx->stream;
     const int b = ctx->cur;
-    long long step = ctx->host_step;
-    CK(cudaMemcpyAsync(ctx->step_ctr, &step, 8, cudaMemcpyHostToDevice, s));
+    // (the device step counter already equals host_step: set_molecules / compute_forces set
+    // it, every finalize advances it; no host-to-device copy, which from pageable memory
+    // would synchronise the stream)
     CK(cudaMemcpyAsync(ctx->n_aux + 1, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToDevice, s));
     CK(cudaEventRecord(ctx->ev_f0[b], s));
     launch_force(ctx, b);
