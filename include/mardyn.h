@@ -287,6 +287,11 @@ int mardyn_dd_end_step(struct mardyn_ctx* ctx, int64_t n_recv);
  *     the context's workspace).
  * Host-side calls that need the molecule count fetch it from the device. */
 int mardyn_dd_set_segment(struct mardyn_ctx* ctx, int64_t seg_cap);
+/* Per-peer segments instead: send segment d holds send_caps[d] records and starts at the
+ * sum of the earlier send capacities; receive segment r likewise with recv_caps[r] (= rank
+ * r's send_caps[this rank]).  Host arrays of nranks int64, copied; the sums must fit the
+ * exchange buffers (MARDYN_EINVAL).  mardyn_dd_set_segment returns to uniform segments. */
+int mardyn_dd_set_peer_segments(struct mardyn_ctx* ctx, const int64_t* send_caps, const int64_t* recv_caps);
 int mardyn_dd_device_counts(struct mardyn_ctx* ctx, void** send_cnt, void** recv_cnt);
 int mardyn_dd_begin_step_async(struct mardyn_ctx* ctx);
 int mardyn_dd_end_step_async(struct mardyn_ctx* ctx);

@@ -105,6 +105,8 @@ struct DDArgs {
     int* send_cnt;               // nranks counters
     int* flag;                   // bit 8: send segment overflow
     const int* n_dev;            // asynchronous step: molecule count in device memory (else the kernel's n)
+    const int* seg_tab;          // per-peer segments: [0, nranks) offsets, [nranks, 2 nranks) capacities
+                                 // (records); nullptr: uniform segments r * seg_cap of seg_cap records
 };
 
 struct ObsRec {                  // one history entry (matches mardyn_observables order)

@@ -406,7 +406,9 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
             base = __shfl_sync(0xffffffffu, base, leader);
             if (pr) {
                 const int k = base + __popc(b & below);
-                if (k >= dd.seg_cap) {
+                const int cap_r = dd.seg_tab ? dd.seg_tab[dd.nranks + r] : dd.seg_cap;
+                const size_t off_r = dd.seg_tab ? (size_t)dd.seg_tab[r] : (size_t)r * dd.seg_cap;
+                if (k >= cap_r) {
                     atomicOr(dd.flag, 256);
                 } else {
                     DDRec rec;
@@ -414,7 +416,7 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
                     rec.vel = r == own ? vn : make_float4(vn.x, vn.y, vn.z, __int_as_float(md_comp(vn.w) | 256));
                     rec.quat = qn;
                     rec.angm = jn;
-                    dd.send[(size_t)r * dd.seg_cap + k] = rec;
+                    dd.send[off_r + k] = rec;
                 }
             }
         }
@@ -455,29 +457,35 @@ __global__ void k_import(int n, int base, GridP g, const DDRec* __restrict__ rec
 // segments (segment r = records from rank r, recv_cnt[r] of them, at most
 // seg_cap) after the n_old = *n_old_dev molecules kept in place, bin them, and
 // write the unsorted count for the cell rebuild.  Nothing goes to the host.
-__global__ void k_import_seg(int nranks, int seg_cap, const int* __restrict__ recv_cnt,
+// rtab: per-source segments ([0, nranks) offsets, [nranks, 2 nranks) capacities), or
+// nullptr for uniform segments r * seg_cap of seg_cap records; the grid covers the
+// sum of the capacities
+__global__ void k_import_seg(int nranks, int seg_cap, const int* __restrict__ rtab, const int* __restrict__ recv_cnt,
                              const int* __restrict__ n_old_dev, int cap, GridP g, const DDRec* __restrict__ recv,
                              uint4* __restrict__ pos, float4* __restrict__ vel, float4* __restrict__ quat,
                              float4* __restrict__ angm, int* __restrict__ cell_of, int* __restrict__ rank,
                              int* __restrict__ count, int* __restrict__ n_unsorted, int* __restrict__ flag)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int r = t / seg_cap, k = t - r * seg_cap;
     const int n_old = *n_old_dev;
-    int base = n_old, tot = n_old;
+    int r = nranks, k = 0, base = n_old, tot = n_old;
     for (int q = 0; q < nranks; ++q) {
-        const int c = min(recv_cnt[q], seg_cap);
-        if (q < r) base += c;
+        const int off = rtab ? rtab[q] : q * seg_cap, cq = rtab ? rtab[nranks + q] : seg_cap;
+        const int c = min(recv_cnt[q], cq);
+        if (t >= off && t < off + cq) { r = q; k = t - off; }
+        if (r == nranks) base += c;                       // sources before r
         tot += c;
     }
     if (t == 0) {
         if (tot > cap) atomicOr(flag, 512);
         *n_unsorted = min(tot, cap);
     }
-    if (r >= nranks || k >= min(recv_cnt[r], seg_cap)) return;
+    if (r >= nranks) return;
+    const int cr = rtab ? rtab[nranks + r] : seg_cap;
+    if (k >= min(recv_cnt[r], cr)) return;
     const int slot = base + k;
     if (slot >= cap) return;
-    const DDRec rec = recv[(size_t)r * seg_cap + k];
+    const DDRec rec = recv[(size_t)t];
     pos[slot] = rec.pos;
     vel[slot] = rec.vel;
     if (quat) { quat[slot] = rec.quat; angm[slot] = rec.angm; }

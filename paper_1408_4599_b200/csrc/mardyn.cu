@@ -140,6 +140,9 @@ struct mardyn_ctx {
     int* recv_cnt = nullptr;               // asynchronous exchange: records received per source rank (device)
     int* n_aux = nullptr;                  // unsorted count after the import (device)
     int64_t seg_max = 0;                   // send segment stride of the workspace layout
+    int* seg_tab = nullptr;                // per-peer segments (device): send offsets, send caps, recv offsets, recv caps
+    bool peer_segs = false;                // seg_tab in use (else uniform seg_cap segments)
+    int64_t recv_span = 0;                 // records of the receive buffer the segments cover
     std::vector<int32_t> boxes;
     std::vector<uint8_t> h_owner;
     std::vector<uint32_t> h_gmask;
@@ -714,6 +717,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     int* send_cnt = nullptr;
     int* recv_cnt = nullptr;
     int* n_aux = nullptr;
+    int* seg_tab = nullptr;
     const int64_t seg_cap = ctx->nranks > 1 ? cap / ctx->nranks + 4096 : 0;
     const int64_t recv_cap = ctx->nranks > 1 ? cap : 0;
     if (ctx->nranks > 1) {
@@ -725,6 +729,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         send_cnt = (int*)take(4 * (size_t)ctx->nranks);
         recv_cnt = (int*)take(4 * (size_t)ctx->nranks);
         n_aux = (int*)take(8);                     // [0] unsorted count after import, [1] n at force time
+        seg_tab = (int*)take(16 * (size_t)ctx->nranks);
     }
     if (assign) {
         ctx->pos[0] = pos0; ctx->pos[1] = pos1; ctx->vel[0] = vel0; ctx->vel[1] = vel1;
@@ -739,6 +744,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         ctx->owner = owner; ctx->gmask = gmask; ctx->owned = owned; ctx->sendbuf = sendbuf;
         ctx->recvbuf = recvbuf; ctx->send_cnt = send_cnt; ctx->seg_cap = seg_cap; ctx->recv_cap = recv_cap;
         ctx->recv_cnt = recv_cnt; ctx->n_aux = n_aux; ctx->seg_max = seg_cap; ctx->n_stale = false;
+        ctx->seg_tab = seg_tab; ctx->peer_segs = false;
         ctx->ncell_pad = ncell_pad; ctx->ntiles = ntiles; ctx->nkblocks = nk;
     }
     return off;
@@ -1305,6 +1311,7 @@ int mardyn_dd_begin_step(mardyn_ctx* ctx, int64_t* send_counts)
     dd.rank = ctx->dd_rank; dd.nranks = ctx->nranks; dd.owner = ctx->owner; dd.gmask = ctx->gmask;
     dd.send = ctx->sendbuf; dd.seg_cap = (int)ctx->seg_cap; dd.send_cnt = ctx->send_cnt; dd.flag = ctx->flag;
     dd.n_dev = nullptr;
+    dd.seg_tab = nullptr;                              // contiguous transport: uniform segments
     const int nkb = nblk(n, 256);
     if (ctx->rigid)
         k_integrate<true, true><<<nkb, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b], ctx->quat[b],
@@ -1386,6 +1393,33 @@ int mardyn_dd_set_segment(mardyn_ctx* ctx, int64_t seg_cap)
     if (ctx->nranks < 2 || !ctx->ws) return fail(ctx, MARDYN_ESTATE, "no decomposition workspace");
     if (seg_cap < 1 || seg_cap > ctx->seg_max) return fail(ctx, MARDYN_EINVAL, "segment capacity out of range");
     ctx->seg_cap = seg_cap;
+    ctx->peer_segs = false;
+    ctx->recv_span = seg_cap * ctx->nranks;
+    return MARDYN_OK;
+}
+
+// per-peer segments: send segment d (send_caps[d] records) at the sum of the earlier
+// send capacities, receive segment r (recv_caps[r]) likewise in the receive buffer
+int mardyn_dd_set_peer_segments(mardyn_ctx* ctx, const int64_t* send_caps, const int64_t* recv_caps)
+{
+    if (!ctx || !send_caps || !recv_caps) return MARDYN_EINVAL;
+    if (ctx->nranks < 2 || !ctx->ws) return fail(ctx, MARDYN_ESTATE, "no decomposition workspace");
+    const int p = ctx->nranks;
+    std::vector<int> tab(4 * (size_t)p);
+    int64_t so = 0, ro = 0;
+    for (int r = 0; r < p; ++r) {
+        if (send_caps[r] < 1 || recv_caps[r] < 1) return fail(ctx, MARDYN_EINVAL, "segment capacities must be >= 1");
+        tab[r] = (int)so; tab[p + r] = (int)send_caps[r];
+        tab[2 * p + r] = (int)ro; tab[3 * p + r] = (int)recv_caps[r];
+        so += send_caps[r];
+        ro += recv_caps[r];
+    }
+    if (so > ctx->seg_max * p || ro > ctx->recv_cap)
+        return fail(ctx, MARDYN_EINVAL, "segment capacities exceed the exchange buffers");
+    CK(cudaMemcpyAsync(ctx->seg_tab, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->peer_segs = true;
+    ctx->recv_span = ro;
     return MARDYN_OK;
 }
 
@@ -1419,6 +1453,7 @@ int mardyn_dd_begin_step_async(mardyn_ctx* ctx)
     dd.rank = ctx->dd_rank; dd.nranks = ctx->nranks; dd.owner = ctx->owner; dd.gmask = ctx->gmask;
     dd.send = ctx->sendbuf; dd.seg_cap = (int)ctx->seg_cap; dd.send_cnt = ctx->send_cnt; dd.flag = ctx->flag;
     dd.n_dev = ctx->start + ctx->g.ncell;             // the sorted count of the last cell rebuild
+    dd.seg_tab = ctx->peer_segs ? ctx->seg_tab : nullptr;
     const int nkb = ctx->nkblocks;
     if (ctx->rigid)
         k_integrate<true, true><<<nkb, 256, 0, s>>>((int)ctx->cap, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
@@ -1441,13 +1476,15 @@ int mardyn_dd_end_step_async(mardyn_ctx* ctx)
     if (!ctx) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "no decomposition");
-    if (ctx->seg_cap * ctx->nranks > ctx->recv_cap)
+    if (!ctx->peer_segs && ctx->seg_cap * ctx->nranks > ctx->recv_cap)
         return fail(ctx, MARDYN_ESTATE, "segment capacity x ranks exceeds the receive buffer (mardyn_dd_set_segment)");
     cudaStream_t s = ctx->stream;
     const int b = ctx->cur;
     const int seg = (int)ctx->seg_cap;
-    k_import_seg<<<nblk((int64_t)seg * ctx->nranks, 256), 256, 0, s>>>(
-        ctx->nranks, seg, ctx->recv_cnt, ctx->start + ctx->g.ncell, (int)ctx->cap, ctx->g, ctx->recvbuf, ctx->pos[b],
+    const int64_t span = ctx->peer_segs ? ctx->recv_span : (int64_t)seg * ctx->nranks;
+    k_import_seg<<<nblk(span, 256), 256, 0, s>>>(
+        ctx->nranks, seg, ctx->peer_segs ? ctx->seg_tab + 2 * ctx->nranks : nullptr, ctx->recv_cnt,
+        ctx->start + ctx->g.ncell, (int)ctx->cap, ctx->g, ctx->recvbuf, ctx->pos[b],
         ctx->vel[b], ctx->rigid ? ctx->quat[b] : nullptr, ctx->rigid ? ctx->angm[b] : nullptr, ctx->cell_of,
         ctx->rank, ctx->count, ctx->n_aux, ctx->flag);
     ctx->launches += 1;

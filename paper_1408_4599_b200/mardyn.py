@@ -29,7 +29,8 @@ EXPORTS = ["mardyn_create", "mardyn_get_grid", "mardyn_workspace_bytes", "mardyn
            "mardyn_get_raw", "mardyn_last_step_timing", "mardyn_set_profiling",
            "mardyn_launch_count", "mardyn_cell_cost", "mardyn_kd_decompose",
            "mardyn_set_decomposition", "mardyn_dd_begin_step", "mardyn_dd_buffers", "mardyn_dd_end_step",
-           "mardyn_dd_set_segment", "mardyn_dd_device_counts", "mardyn_dd_begin_step_async",
+           "mardyn_dd_set_segment", "mardyn_dd_set_peer_segments", "mardyn_dd_device_counts",
+           "mardyn_dd_begin_step_async",
            "mardyn_dd_end_step_async",
            "mardyn_set_thermostat", "mardyn_lj_tail", "mardyn_get_tail_corrections",
            "mardyn_last_error", "mardyn_destroy"]
@@ -113,6 +114,7 @@ def load_library():
     lib.mardyn_dd_buffers.argtypes = [vp, P(vp), P(C.c_int64), P(vp), P(C.c_int64), P(C.c_int32)]
     lib.mardyn_dd_end_step.argtypes = [vp, C.c_int64]
     lib.mardyn_dd_set_segment.argtypes = [vp, C.c_int64]
+    lib.mardyn_dd_set_peer_segments.argtypes = [vp, vp, vp]
     lib.mardyn_dd_device_counts.argtypes = [vp, P(vp), P(vp)]
     lib.mardyn_dd_begin_step_async.argtypes = [vp]
     lib.mardyn_dd_end_step_async.argtypes = [vp]
@@ -339,6 +341,12 @@ class Context:
     def dd_set_segment(self, seg_cap):
         self._check(self.lib.mardyn_dd_set_segment(self.h, int(seg_cap)))
 
+    def dd_set_peer_segments(self, send_caps, recv_caps):
+        sc = np.ascontiguousarray(np.asarray(send_caps, dtype=np.int64))
+        rc = np.ascontiguousarray(np.asarray(recv_caps, dtype=np.int64))
+        self._check(self.lib.mardyn_dd_set_peer_segments(self.h, sc.ctypes.data_as(C.c_void_p),
+                                                         rc.ctypes.data_as(C.c_void_p)))
+
     def dd_device_counts(self):
         """(send_cnt, recv_cnt): int32 [nranks] tensor views of the workspace (zero copy)."""
         sc = C.c_void_p(); rc = C.c_void_p()
@@ -463,10 +471,10 @@ def exchange_records(send, cnt, recv, nranks, dist):
     for d in range(nranks):
         if d == me:
             if int(cnt[d]):
-                outs[d].copy_(send[d, : int(cnt[d])])
+                outs[d].copy_(send[d][: int(cnt[d])])
             continue
         if int(cnt[d]):
-            ops.append(dist.P2POp(dist.isend, send[d, : int(cnt[d])].contiguous(), d))
+            ops.append(dist.P2POp(dist.isend, send[d][: int(cnt[d])].contiguous(), d))
         if rcounts[d]:
             ops.append(dist.P2POp(dist.irecv, outs[d], d))
     if ops:
@@ -475,14 +483,24 @@ def exchange_records(send, cnt, recv, nranks, dist):
     return off
 
 
-def exchange_segments(send, send_cnt, recv, recv_cnt, nranks, dist):
+def exchange_segments(send, send_cnt, recv, recv_cnt, nranks, dist, send_caps=None, recv_caps=None):
     """Transport of the asynchronous decomposed step (include/mardyn.h): rank r's
-    send segment d (seg_cap records, fixed size; send[d]) lands in segment r of
-    rank d's receive buffer, and its record count send_cnt[d] in recv_cnt[r] of
-    rank d.  Two all-to-alls with equal splits; nothing is read on the host
+    send segment d lands in segment r of rank d's receive buffer, and its record
+    count send_cnt[d] in recv_cnt[r] of rank d.  send / recv: [records, bytes]
+    views of the exchange buffers with the segments back to back -- all of size
+    seg = len(send) / nranks (uniform), or send_caps[d] / recv_caps[r] records
+    (per-peer, static split sizes).  Two all-to-alls; nothing is read on the host
     (NCCL over NVLink on GPUs, gloo on CPU)."""
     dist.all_to_all_single(recv_cnt, send_cnt)
-    dist.all_to_all_single(recv[: send.numel() // send.shape[-1]].reshape(-1), send.reshape(-1))
+    rb = send.shape[-1]
+    if send_caps is None:
+        n = send.shape[0]
+        dist.all_to_all_single(recv[:n].reshape(-1), send.reshape(-1))
+    else:
+        ns, nr = int(sum(send_caps)), int(sum(recv_caps))
+        dist.all_to_all_single(recv[:nr].reshape(-1), send[:ns].reshape(-1),
+                               output_split_sizes=[int(c) * rb for c in recv_caps],
+                               input_split_sizes=[int(c) * rb for c in send_caps])
 
 
 class DecomposedRun:
@@ -602,45 +620,78 @@ class DecomposedRun:
                     self._size_segments(counts)
 
     def _size_segments(self, counts):
-        torch = self.torch
-        big = max(int(np.max(c)) for c in counts)
+        """Per-peer exchange segments from the first step's record counts: twice the
+        count + 1024 records (face neighbours send far more than edge or corner ones);
+        uniform segments if the per-peer ones do not fit the buffers."""
+        torch, p = self.torch, self.nranks
+        cap = lambda c: ((2 * int(c) + 1024 + 255) // 256) * 256
+        send_caps = [[cap(c) for c in cnt] for cnt in counts]          # per local rank, per destination
+        if self.transport == "loopback":
+            ranks = list(range(p))
+            recv_caps = [[send_caps[src][dst] for src in range(p)] for dst in range(p)]
+        else:
+            import torch.distributed as dist
+            ranks = [self.rank]
+            t = torch.tensor(send_caps[0], dtype=torch.int64, device="cuda")
+            r = torch.empty_like(t)
+            dist.all_to_all_single(r, t)
+            recv_caps = [r.tolist()]
+        recv_cap = int(self.bufs[0][1].shape[0])
+        fits = all(sum(sc) <= self.seg_max * p and sum(rc) <= recv_cap for sc, rc in zip(send_caps, recv_caps))
         if self.transport != "loopback":
             import torch.distributed as dist
-            t = torch.tensor([big], dtype=torch.int64, device="cuda")
+            t = torch.tensor([0 if fits else 1], dtype=torch.int32, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            big = int(t.item())
-        recv_cap = int(self.bufs[0][1].shape[0])
-        seg = min(self.seg_max, recv_cap // self.nranks, ((2 * big + 1024 + 255) // 256) * 256)
-        for c in self.ctxs:
-            c.dd_set_segment(seg)
-        self.seg = seg
+            fits = int(t.item()) == 0
+        if fits:
+            for c, sc, rc in zip(self.ctxs, send_caps, recv_caps):
+                c.dd_set_peer_segments(sc, rc)
+            self.send_caps, self.recv_caps = send_caps, recv_caps
+        else:
+            big = max(max(sc) for sc in send_caps)
+            if self.transport != "loopback":
+                t = torch.tensor([big], dtype=torch.int64, device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                big = int(t.item())
+            seg = min(self.seg_max, recv_cap // p, big)
+            for c in self.ctxs:
+                c.dd_set_segment(seg)
+            self.send_caps = [[seg] * p for _ in self.ctxs]
+            self.recv_caps = [[seg] * p for _ in self.ctxs]
         self.bufs = [c.dd_buffers() for c in self.ctxs]
+        self.flat = [(sb.reshape(-1, sb.shape[-1]), rv) for sb, rv in self.bufs]   # [records, bytes] views
         self.cnts = [c.dd_device_counts() for c in self.ctxs]
         self.seg_ready = True
 
     def _step_async(self):
-        p, seg = self.nranks, self.seg
+        p = self.nranks
         for c in self.ctxs:
             c.dd_begin_step_async()
         if self.transport == "loopback":
+            soff = [np.concatenate([[0], np.cumsum(sc)[:-1]]) for sc in self.send_caps]
+            roff = [np.concatenate([[0], np.cumsum(rc)[:-1]]) for rc in self.recv_caps]
             for dst in range(p):
-                recv = self.bufs[dst][1][: p * seg].view(p, seg, -1)
                 rcnt = self.cnts[dst][1]
                 for src in range(p):
-                    recv[src].copy_(self.bufs[src][0][dst])
+                    c = int(self.send_caps[src][dst])
+                    a, b = int(roff[dst][src]), int(soff[src][dst])
+                    self.flat[dst][1][a: a + c].copy_(self.flat[src][0][b: b + c])
                     rcnt[src: src + 1].copy_(self.cnts[src][0][dst: dst + 1])
         else:
             import torch.distributed as dist
-            send, recv = self.bufs[0]
+            send, recv = self.flat[0]
             scnt, rcnt = self.cnts[0]
             try:
-                exchange_segments(send, scnt, recv, rcnt, p, dist)
+                exchange_segments(send, scnt, recv, rcnt, p, dist, self.send_caps[0], self.recv_caps[0])
             except RuntimeError:
                 # a backend without these all-to-alls: finish this step with host-side
                 # counts and point-to-point records, and stay on that path
                 self.async_exchange = False
-                cnt = [min(int(x), seg) for x in scnt.cpu().tolist()]   # overflow: flagged by the library
-                n = exchange_records(send, cnt, recv, p, dist)
+                sc = self.send_caps[0]
+                off = np.concatenate([[0], np.cumsum(sc)[:-1]])
+                segs = [send[int(off[d]): int(off[d]) + int(sc[d])] for d in range(p)]
+                cnt = [min(int(x), int(sc[d])) for d, x in enumerate(scnt.cpu().tolist())]   # overflow: flagged
+                n = exchange_records(segs, cnt, recv, p, dist)
                 self.ctxs[0].dd_end_step(n)
                 return
         for c in self.ctxs:

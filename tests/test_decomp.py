@@ -212,8 +212,22 @@ def _seg_main(rank, world, port, result):
             send[d, k, :3] = torch.tensor([rank, d, k], dtype=torch.uint8)
     recv = torch.full((world * seg + 5, rec), 255, dtype=torch.uint8)   # receive capacity > nranks x seg
     rcnt = torch.zeros(world, dtype=torch.int32)
-    M.exchange_segments(send, scnt, recv, rcnt, world, dist)
-    result[rank] = (rcnt.tolist(), recv[: world * seg, :3].tolist(), recv[world * seg:, 0].tolist())
+    M.exchange_segments(send.reshape(-1, rec), scnt, recv, rcnt, world, dist)
+    uniform = (rcnt.tolist(), recv[: world * seg, :3].tolist(), recv[world * seg:, 0].tolist())
+    # per-peer segments: rank r sends caps[r][d] records to d (back to back), d receives them
+    # back to back in source order
+    caps = [[6, 3], [2, 7]]
+    sc, rc = caps[rank], [caps[0][rank], caps[1][rank]]
+    flat = torch.zeros((sum(sc), rec), dtype=torch.uint8)
+    off = 0
+    for d in range(world):
+        for k in range(min(int(scnt[d]), sc[d])):
+            flat[off + k, :3] = torch.tensor([rank, d, k], dtype=torch.uint8)
+        off += sc[d]
+    recv2 = torch.full((sum(rc) + 3, rec), 255, dtype=torch.uint8)
+    rcnt2 = torch.zeros(world, dtype=torch.int32)
+    M.exchange_segments(flat, scnt, recv2, rcnt2, world, dist, sc, rc)
+    result[rank] = (uniform, (rcnt2.tolist(), recv2[:, :3].tolist(), rc))
     dist.destroy_process_group()
 
 
@@ -231,12 +245,19 @@ def test_gloo_exchange_segments():
     result = mgr.dict()
     mp.spawn(_seg_main, args=(2, port, result), nprocs=2, join=True)
     for dst in range(2):
-        rcnt, rows, tail = result[dst]
+        (rcnt, rows, tail), (rcnt2, rows2, rc) = result[dst]
         assert rcnt == [(src + 2 * dst) % 5 + 1 for src in range(2)]
         for src in range(2):
             for k in range(rcnt[src]):
                 assert rows[8 * src + k] == [src, dst, k]
         assert tail == [255] * 5
+        assert rcnt2 == rcnt
+        off = 0
+        for src in range(2):
+            for k in range(min(rcnt2[src], rc[src])):
+                assert rows2[off + k] == [src, dst, k]
+            off += rc[src]
+        assert rows2[off:] == [[255, 255, 255]] * 3
 
 
 def test_droplet_kd_beats_static_split():
