@@ -109,6 +109,42 @@ struct DDArgs {
                                  // (records); nullptr: uniform segments r * seg_cap of seg_cap records
 };
 
+// Pack this lane's exchange records (spatial decomposition): one record for every rank in
+// dmask -- a halo copy (ghost flag, bit 8 of the component word) for the ranks whose halo
+// holds the molecule's new cell, the molecule itself for its new owner `own`.  Warp-collective
+// (every lane calls it, dmask = 0 for none): per destination one atomic reserves the warp's
+// slots of that segment.  Overflow sets bit 8 of the flag.
+__device__ __forceinline__ void dd_pack_warp(const DDArgs& dd, unsigned dmask, int own, uint4 pn, float4 vn,
+                                             float4 qn, float4 jn)
+{
+    const int lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
+    for (int r = 0; r < dd.nranks; ++r) {
+        const bool pr = (dmask >> r) & 1u;
+        const unsigned b = __ballot_sync(0xffffffffu, pr);
+        if (b == 0u) continue;
+        const int leader = __ffs(b) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&dd.send_cnt[r], __popc(b));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (pr) {
+            const int k = base + __popc(b & below);
+            const int cap_r = dd.seg_tab ? dd.seg_tab[dd.nranks + r] : dd.seg_cap;
+            const size_t off_r = dd.seg_tab ? (size_t)dd.seg_tab[r] : (size_t)r * dd.seg_cap;
+            if (k >= cap_r) {
+                atomicOr(dd.flag, 256);
+            } else {
+                DDRec rec;
+                rec.pos = pn;
+                rec.vel = r == own ? vn : make_float4(vn.x, vn.y, vn.z, __int_as_float((__float_as_int(vn.w) & 0xff) | 256));
+                rec.quat = qn;
+                rec.angm = jn;
+                dd.send[off_r + k] = rec;
+            }
+        }
+    }
+}
+
 struct ObsRec {                  // one history entry (matches mardyn_observables order)
     long long step;
     double U, W, T, KEt, KEr;

@@ -73,6 +73,7 @@ struct Args {
     int* count;
     int* flag;
     float mass, inv_mass;
+    DDArgs dd;                   // STEP with DD: exchange packing of the decomposed step
 };
 
 // origin (in quanta, mod 2^32) to subtract from the stored u of a molecule
@@ -186,7 +187,12 @@ __device__ __forceinline__ int find_from(const float* __restrict__ sxf, int rb, 
     return g;
 }
 
-template <int WARPS, int CAPP, int MINB, bool STEP>
+// STEP: the leapfrog step of the block's home molecules is fused in (one domain: every
+// molecule is home).  DD (with STEP, spatial decomposition): the molecules of halo cells are
+// dropped and every home molecule's exchange records -- migrant for its new owner, halo
+// copies for the ranks whose halo holds its new cell -- are packed here too (reading the
+// force kernel's own results: no separate integrator pass over the state)
+template <int WARPS, int CAPP, int MINB, bool STEP, bool DD = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
 {
     using C = Cfg<WARPS, CAPP>;
@@ -553,15 +559,33 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
             // fused leapfrog (Eqs. 2-3): this block's molecules are only read by this warp
             // (neighbours are staged from xs), so they are advanced in place
             int clb = -1;
+            unsigned dmask = 0;
+            int own = -1;
+            uint4 pn = make_uint4(0, 0, 0, 0);
+            float4 vn = make_float4(0.f, 0.f, 0.f, 0.f);
             if (home) {
                 const LeapOut o = md_leapfrog(g, pi, vi, Fown.x, Fown.y, Fown.z, a.mass, a.inv_mass);
                 if (o.bad) atomicOr(a.flag, 1);
                 a.pos[mi] = o.p;
                 a.vel[mi] = o.v;
                 clb = o.c[0] + nx * (o.c[1] + ny * o.c[2]);
+                if (DD) {
+                    pn = o.p;
+                    vn = o.v;
+                    own = a.dd.owner[clb];
+                    const uint32_t gm = a.dd.gmask[clb];
+                    dmask = (gm & ~(1u << a.dd.rank)) | (own != a.dd.rank ? 1u << own : 0u);
+                    if (own != a.dd.rank) {                // migrant: kept as a ghost if in my halo
+                        if ((gm >> a.dd.rank) & 1u) a.vel[mi] = make_float4(vn.x, vn.y, vn.z, __int_as_float(md_comp(vn.w) | 256));
+                        else clb = -1;
+                    }
+                }
                 a.cell_of[mi] = clb;
                 Kw = o.ket;
+            } else if (DD && valid) {
+                a.cell_of[mi] = -1;                        // last step's halo copies are dropped
             }
+            if (DD) dd_pack_warp(a.dd, dmask, own, pn, vn, make_float4(1.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f));
             // arrival ranks: one atomic per distinct cell; the rank store waits for the
             // atomic's reply, so it is deferred to after the next block's forces
             if (pend_mi >= 0) a.rank[pend_mi] = __shfl_sync(pend_m, pend_b, __ffs(pend_m) - 1) + pend_r;

@@ -392,35 +392,7 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
         if (cl >= 0) cell_of[t] = cl;
         cl_bin = cl;
     }
-    if (DD) {
-        // warp-aggregated packing: per destination rank one atomic reserves the warp's slots
-        const int lane = threadIdx.x & 31;
-        const unsigned below = (1u << lane) - 1u;
-        for (int r = 0; r < dd.nranks; ++r) {
-            const bool pr = (dmask >> r) & 1u;
-            const unsigned b = __ballot_sync(0xffffffffu, pr);
-            if (b == 0u) continue;
-            const int leader = __ffs(b) - 1;
-            int base = 0;
-            if (lane == leader) base = atomicAdd(&dd.send_cnt[r], __popc(b));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (pr) {
-                const int k = base + __popc(b & below);
-                const int cap_r = dd.seg_tab ? dd.seg_tab[dd.nranks + r] : dd.seg_cap;
-                const size_t off_r = dd.seg_tab ? (size_t)dd.seg_tab[r] : (size_t)r * dd.seg_cap;
-                if (k >= cap_r) {
-                    atomicOr(dd.flag, 256);
-                } else {
-                    DDRec rec;
-                    rec.pos = pn;
-                    rec.vel = r == own ? vn : make_float4(vn.x, vn.y, vn.z, __int_as_float(md_comp(vn.w) | 256));
-                    rec.quat = qn;
-                    rec.angm = jn;
-                    dd.send[off_r + k] = rec;
-                }
-            }
-        }
-    }
+    if (DD) dd_pack_warp(dd, dmask, own, pn, vn, qn, jn);   // warp-aggregated (one atomic per destination)
     // next step's cell histogram + arrival rank: molecules are in cell order, so
     // the lanes of a warp share few cells; one atomic per distinct cell (the arrival
     // order only places molecules before the canonical in-cell ordering)

@@ -45,6 +45,7 @@ constexpr int LJ1_CAPP = MD_LJ1_CAPP;
 using LJ1 = lj1::Cfg<LJ1_WARPS, LJ1_CAPP>;
 #define K_LJ1 lj1::k_force_lj1<LJ1_WARPS, LJ1_CAPP, MD_LJ1_MINB, false>
 #define K_LJ1_STEP lj1::k_force_lj1<LJ1_WARPS, LJ1_CAPP, MD_LJ1_MINB, true>
+#define K_LJ1_STEP_DD lj1::k_force_lj1<LJ1_WARPS, LJ1_CAPP, MD_LJ1_MINB, true, true>
 #ifndef MD_RIGID3
 #define MD_RIGID3 1                       // load-balanced rigid kernel (kernels_rigid3.cuh) for configs 2, 3
 #endif
@@ -349,7 +350,8 @@ static int refresh_n(mardyn_ctx* ctx)
 // forces at the current state of buffer `buf`; step = true (single-site
 // kernel, one domain) also advances the molecules by one leapfrog step and
 // bins them for the next cell rebuild (count must be zeroed before)
-static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_graph = false)
+static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_graph = false,
+                        const DDArgs* dd = nullptr)
 {
     ctx->n_force = ctx->n;
     ForceArgs a;
@@ -414,8 +416,14 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_gra
         b.flag = ctx->flag;
         b.mass = ctx->model.comp[0].mass;
         b.inv_mass = ctx->model.comp[0].inv_mass;
-        if (step) K_LJ1_STEP<<<ctx->force_grid, threads, LJ1::SMEM, ctx->stream>>>(b);
-        else K_LJ1<<<ctx->force_grid, threads, LJ1::SMEM, ctx->stream>>>(b);
+        if (step && dd) {
+            b.dd = *dd;
+            K_LJ1_STEP_DD<<<ctx->force_grid, threads, LJ1::SMEM, ctx->stream>>>(b);
+        } else if (step) {
+            K_LJ1_STEP<<<ctx->force_grid, threads, LJ1::SMEM, ctx->stream>>>(b);
+        } else {
+            K_LJ1<<<ctx->force_grid, threads, LJ1::SMEM, ctx->stream>>>(b);
+        }
         if (!in_graph) CK(cudaMemsetAsync(ctx->blk_ctr, 0, sizeof(int), ctx->stream));
     }
     }
@@ -631,6 +639,7 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
     default:
         CK(cudaFuncSetAttribute(K_LJ1, cudaFuncAttributeMaxDynamicSharedMemorySize, LJ1::SMEM));
         CK(cudaFuncSetAttribute(K_LJ1_STEP, cudaFuncAttributeMaxDynamicSharedMemorySize, LJ1::SMEM));
+        CK(cudaFuncSetAttribute(K_LJ1_STEP_DD, cudaFuncAttributeMaxDynamicSharedMemorySize, LJ1::SMEM));
         ctx->force_blocks = occupancy_grid(ctx, K_LJ1, threads, LJ1::SMEM);
     }
     for (int b = 0; b < 2; ++b) {
@@ -1444,16 +1453,29 @@ int mardyn_dd_begin_step_async(mardyn_ctx* ctx)
     // it, every finalize advances it; no host-to-device copy, which from pageable memory
     // would synchronise the stream)
     CK(cudaMemcpyAsync(ctx->n_aux + 1, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToDevice, s));
-    CK(cudaEventRecord(ctx->ev_f0[b], s));
-    launch_force(ctx, b);
-    CK(cudaEventRecord(ctx->ev_f1[b], s));
-    CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
-    CK(cudaMemsetAsync(ctx->send_cnt, 0, sizeof(int) * ctx->nranks, s));
     DDArgs dd;
     dd.rank = ctx->dd_rank; dd.nranks = ctx->nranks; dd.owner = ctx->owner; dd.gmask = ctx->gmask;
     dd.send = ctx->sendbuf; dd.seg_cap = (int)ctx->seg_cap; dd.send_cnt = ctx->send_cnt; dd.flag = ctx->flag;
     dd.n_dev = ctx->start + ctx->g.ncell;             // the sorted count of the last cell rebuild
     dd.seg_tab = ctx->peer_segs ? ctx->seg_tab : nullptr;
+    CK(cudaMemsetAsync(ctx->send_cnt, 0, sizeof(int) * ctx->nranks, s));
+    if (ctx->kernel == KER_LJ1) {
+        // single-site kernel with the leapfrog, binning and exchange packing fused in (the
+        // cell counts are zero: the last rebuild's scan cleared them)
+        CK(cudaEventRecord(ctx->ev_f0[b], s));
+        launch_force(ctx, b, true, false, &dd);
+        CK(cudaEventRecord(ctx->ev_f1[b], s));
+        k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, 0, ctx->kpart, ctx->ndof,
+                                                      ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket, 0);
+        ctx->launches += 1;
+        CK(cudaGetLastError());
+        ctx->last_parity = b;
+        return MARDYN_OK;
+    }
+    CK(cudaEventRecord(ctx->ev_f0[b], s));
+    launch_force(ctx, b);
+    CK(cudaEventRecord(ctx->ev_f1[b], s));
+    CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
     const int nkb = ctx->nkblocks;
     if (ctx->rigid)
         k_integrate<true, true><<<nkb, 256, 0, s>>>((int)ctx->cap, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
