@@ -294,7 +294,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
         dist.barrier()
-    value = world * N * args.steps / (tot_ms / 1e3) / 1e6
+    # whole job: the N molecules of the system are updated once per step, shared among the
+    # ranks of the spatial decomposition (strong scaling: N is fixed as the GPU count grows)
+    value = N * args.steps / (tot_ms / 1e3) / 1e6
     # ---- roofline of the dominant kernel (force): algorithmic flops
     ncand_half = obs["n_candidates"] / 2.0
     flops = FLOP_COM_TEST * ncand_half + pair_flops(system) * obs["n_pairs"]
@@ -302,7 +304,8 @@ def main():
     pk = peaks()
     props = torch.cuda.get_device_properties(local)
     peak = fp32_peak_tflops(props.multi_processor_count, pk.get("sm_max_mhz", 1965.0))
-    achieved = flops / (f_ms / 1e3) / 1e12 if f_ms else None
+    # per GPU: the method's work of the whole system shared by the ranks, over one rank's force time
+    achieved = flops / world / (f_ms / 1e3) / 1e12 if f_ms else None
     traffic = None
     try:
         prof = json.load(open(os.path.join(ROOT, "profiles", "force_traffic.json")))
@@ -313,7 +316,7 @@ def main():
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": {0: "k_force_lj1", 1: "k_force_rigid3"}.get(ctx.get_grid()["kernel"], "k_force_rigid"),
                 "force_ms": f_ms, "force_share": (f_ms * args.steps / tot_ms) if f_ms else None,
-                "algorithmic_gflop_per_launch": flops / 1e9,
+                "algorithmic_gflop_per_launch": flops / world / 1e9,
                 "flop_model": "8 x half-shell COM candidates + per unique in-range pair: sum over site pairs of "
                               "(8 separation + kernel: LJ 20, q-q RF 23, Q-Q 110) (SURVEY 8(d)); single-site LJ: 20",
                 "peak_note": "FP32 CUDA cores: SMs x 128 x 2 x sm_max_mhz (MEASURED_PEAKS.json), derived"}
