@@ -42,7 +42,7 @@ REF_SAMPLE = 32768     # molecules per --impl reference step
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=100)     # BASELINE configs[1]: 100 steps NVE
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--config", default="c1")
     p.add_argument("--impl", default="mardyn", choices=["mardyn", "reference"])
@@ -78,7 +78,9 @@ def fp32_peak_tflops(num_sms, mhz):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line): an NVML thread polling every 5 ms (the timed
+    region of a step is well under a millisecond), nvidia-smi as the fallback."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -86,10 +88,45 @@ class Clocks:
 
     def __init__(self, device):
         self.device = device
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.samples, self.reasons, self.smax = [], set(), 0.0
+        self.thread = None
+        self.stop_flag = False
         self.p = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            idx = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(device)).split(",")[device]) \
+                if os.environ.get("CUDA_VISIBLE_DEVICES", "").replace(",", "").isdigit() else device
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self.nv = None
+
+    def _poll(self):
+        nv = self.nv
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        while not self.stop_flag:
+            try:
+                self.samples.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, b in bits.items():
+                    if r & b:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def start(self):
+        if self.nv is not None:
+            import threading
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
                                        "--format=csv,noheader,nounits", "-lms", "200"],
@@ -98,6 +135,13 @@ class Clocks:
             self.p = None
 
     def stop(self):
+        if self.thread is not None:
+            self.stop_flag = True
+            self.thread.join()
+            if not self.samples:
+                return None
+            return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.smax,
+                    "reasons": sorted(self.reasons), "samples": len(self.samples), "source": "nvml, 5 ms"}
         if self.p is None:
             return None
         time.sleep(0.25)
@@ -123,7 +167,7 @@ class Clocks:
         if not sm:
             return None
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi, 200 ms"}
 
 
 def run_reference(args, system, rank, world):
