@@ -172,6 +172,35 @@ def test_trajectory(md, oracle_mod, name, nsteps):
         assert dq.max() < 1e-4
 
 
+@pytest.mark.parametrize("name,nsteps", [("c2s", 60), ("c3s", 60)])
+def test_rigid_long_run(md, oracle_mod, name, nsteps):
+    """Longer rigid-body runs (Fincham rotation, reading A7).  Independent fp32 and
+    fp64 trajectories part chaotically (c2s starts from close random-orientation
+    contacts), so the per-step protocol is a snapshot: after the run the oracle
+    evaluates the GPU's own state (positions, quaternions) -- forces and torques
+    within A15, U and W within 1e-5 -- and the GPU conserves total energy as well
+    as the oracle's own trajectory does (its drift + 1e-5 of the kinetic energy)."""
+    s = S.config(name)
+    ctx, hist, mol, o, u, v, q, j, obs = run_both(md, oracle_mod, s, nsteps)
+    Eg = np.array([x["U_pot"] + x["E_kin_trans"] + x["E_kin_rot"] for x in hist])
+    ekin = np.array([x["E_kin_trans"] + x["E_kin_rot"] for x in hist])
+    Eo = np.asarray(obs["U"]) + np.asarray(obs["KEt"]) + np.asarray(obs["KEr"])
+    drift, drift_o = np.abs(Eg - Eg[0]).max(), np.abs(Eo - Eo[0]).max()
+    assert drift <= drift_o + 1e-5 * ekin.mean(), (drift, drift_o)
+    # snapshot parity on the GPU's state at t_n
+    ctx.compute_forces()
+    og = ctx.get_observables()
+    Fg, tg = ctx.get_forces()
+    ug, _, _ = ctx.get_raw()
+    m = ctx.get_molecules()
+    Fo, to, tot = o.forces(s["comp"], ug, m["q"], mode="full")
+    assert og["n_pairs"] == tot["npairs"]
+    assert_forces_close(Fg, Fo, "force")
+    assert_forces_close(tg, to, "torque")
+    assert_rel(og["U_pot"], tot["U"], "U_pot")
+    assert_rel(og["virial"], tot["W"], "virial")
+
+
 def test_initial_temperature_and_nve(md):
     """A8 pin on the GPU: T(0) = generator T; NVE over 400 steps of config 0
     within 2.5e-4 eps per particle (the oracle's own bound)."""
