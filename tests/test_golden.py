@@ -95,3 +95,35 @@ def test_site_pair_golden(oracle_mod):
     u_inf = _sys(oracle_mod, rc=2.5, eps_rf=math.inf).site_pair(d, z, d, z, [1.0, 0, 0])[0]
     u_one = _sys(oracle_mod, rc=2.5, eps_rf=1.0).site_pair(d, z, d, z, [1.0, 0, 0])[0]
     assert u_inf - u_one == pytest.approx(c["delta_u"], rel=1e-13), c["cite"]
+
+
+def pair_system(which):
+    """Two rigid molecules of the config-2 or config-3 model as in the SURVEY 8(c)
+    pair pins: molecule 1 at the box centre, unrotated; molecule 2 displaced and
+    rotated (periodic box of >= 3 cells per axis)."""
+    g = load("survey_pair_values.json")[which]
+    comp = S.c2_component() if which == "clj2q" else S.c3_component()
+    box = 20.0 if which == "clj2q" else 60.0
+    c = box / 2
+    s = {"name": f"pair-{which}", "box": (box, box, box), "rc": g["rc"], "dt": 0.001, "steps": 1, "T": 1.0,
+         "eps_rf": math.inf, "lj_shift": 1, "components": [comp], "id": np.arange(2, dtype=np.int64),
+         "comp": np.zeros(2, np.int32),
+         "r": np.array([[c, c, c], [c + g["r2"][0], c + g["r2"][1], c + g["r2"][2]]]),
+         "v": np.zeros((2, 3)), "q": np.array([[1.0, 0.0, 0.0, 0.0], g["q2"]]), "j": np.zeros((2, 3))}
+    return s, g
+
+
+@pytest.mark.parametrize("which", ["clj2q", "tip4p"])
+def test_rigid_pair_golden_oracle(oracle_mod, which):
+    """The oracle's whole rigid-pair assembly against the SURVEY 8(c) pair pins
+    (positions snapped to the fixed-point lattice: relative changes ~1e-6)."""
+    s, g = pair_system(which)
+    o = oracle_mod.System(s)
+    F, tau, tot = o.forces(s["comp"], o.quantize(s["r"]), s["q"], mode="brute")
+    scale = np.abs(g["F2"]).max()
+    assert tot["npairs"] == 1
+    assert tot["U"] == pytest.approx(g["U"], rel=2e-5), g["cite"]
+    assert tot["W"] == pytest.approx(g["W"], rel=2e-5), g["cite"]
+    assert np.abs(F[1] - g["F2"]).max() <= 2e-5 * scale, (F[1], g["F2"])
+    assert np.abs(F[0] + F[1]).max() <= 1e-12 * scale
+    assert np.abs(tau[1] - g["tau2"]).max() <= 2e-5 * np.abs(g["tau2"]).max(), (tau[1], g["tau2"])

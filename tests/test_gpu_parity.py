@@ -314,3 +314,23 @@ def test_nvt_trajectory_and_tail(md, oracle_mod):
     assert U == pytest.approx(Uo, rel=1e-12) and W == pytest.approx(Wo, rel=1e-12)
     with pytest.raises(md.MardynError):
         ctx.set_thermostat(-1.0, 5)
+
+
+@pytest.mark.parametrize("which", ["clj2q", "tip4p"])
+def test_rigid_pair_golden_gpu(md, which):
+    """The CUDA path on the SURVEY 8(c) pair pins (two molecules: rigid kernel,
+    quaternion convention, lever-arm torque, reaction field, virial sign) --
+    fp32 against the printed 8-digit values."""
+    from test_golden import pair_system
+    s, g = pair_system(which)
+    ctx = md.from_system(s)
+    F, tau = ctx.get_forces()
+    ctx.compute_forces()
+    obs = ctx.get_observables()
+    assert ctx.get_grid()["kernel"] == 1
+    assert obs["n_pairs"] == 1
+    assert_rel(obs["U_pot"], g["U"], "U_pot", tol=5e-5)
+    assert_rel(obs["virial"], g["W"], "virial", tol=5e-5)
+    scale = np.abs(g["F2"]).max()
+    assert np.abs(F[1] - g["F2"]).max() <= 5e-5 * scale, (F[1], g["F2"])
+    assert np.abs(tau[1] - g["tau2"]).max() <= 5e-5 * np.abs(g["tau2"]).max(), (tau[1], g["tau2"])
