@@ -127,3 +127,28 @@ def test_rigid_pair_golden_oracle(oracle_mod, which):
     assert np.abs(F[1] - g["F2"]).max() <= 2e-5 * scale, (F[1], g["F2"])
     assert np.abs(F[0] + F[1]).max() <= 1e-12 * scale
     assert np.abs(tau[1] - g["tau2"]).max() <= 2e-5 * np.abs(g["tau2"]).max(), (tau[1], g["tau2"])
+
+
+def test_c0_reference_run_golden(oracle_mod):
+    """Generator + oracle against the survey's independent fp64 c0 run (t = 0 state
+    and per-step U, W, T of the first 10 leapfrog steps).  The box snap of reading A12
+    (-1.5e-7 relative) accounts for the ~1e-6 differences in U and W; T, which does not
+    depend on the box, agrees to 1e-8."""
+    g = load("survey_state_values.json")["c0"]
+    s = S.config("c0")
+    N = len(s["r"])
+    assert N == g["N"]
+    o = oracle_mod.System(s)
+    u = o.quantize(s["r"])
+    F, _, tot = o.forces(s["comp"], u, s["q"], mode="full")
+    assert tot["npairs"] == g["npairs"]
+    assert tot["U"] / N == pytest.approx(g["U_per_N"], rel=2e-6)
+    assert tot["W"] / N == pytest.approx(g["W_per_N"], rel=2e-6)
+    assert np.sqrt((F ** 2).sum(1).mean()) == pytest.approx(g["rms_F"], rel=1e-5)
+    *_, obs = o.run(s["dt"], s["comp"], u, s["v"], s["q"], s["j"], 10, half_step=0, mode="full")
+    for k, (U, W, T) in g["steps"].items():
+        k = int(k)
+        assert obs["npairs"][k] == g["npairs"]
+        assert obs["U"][k] == pytest.approx(U, rel=2e-6), k
+        assert obs["W"][k] == pytest.approx(W, rel=2e-6), k
+        assert obs["T"][k] == pytest.approx(T, rel=1e-8), k
