@@ -31,6 +31,9 @@
 
 namespace lj1 {
 
+#ifndef MD_LJ1_PREFETCH
+#define MD_LJ1_PREFETCH 1
+#endif
 constexpr int KMAX = 6;          // home cells per sub-chunk: staged |x| < 4 E (A12 quantum)
 constexpr int BLOCKS_PER_FETCH = 1;
 
@@ -499,6 +502,26 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                 const int siend = 32 * nseg + lane;
                 SegT sg = sseg[si];
                 int p = seg_b(sg), e = seg_e(sg);
+#if MD_LJ1_PREFETCH
+                // software pipelined: the next step's pairs are loaded before this step's
+                // arithmetic (past the last step the loads fall on the sentinel's far pads)
+                float4 xy0 = sxy[p], xy1 = sxy[p + 1];
+                float2 z0 = sz[p], z1 = sz[p + 1];
+                for (int it = 0; it < tmax; it += 2) {
+                    p += 2;
+                    if (p == e) {
+                        si = min(si + 32, siend);
+                        sg = sseg[si];
+                        p = seg_b(sg);
+                        e = seg_e(sg);
+                    }
+                    const float4 nxy0 = sxy[p], nxy1 = sxy[p + 1];
+                    const float2 nz0 = sz[p], nz1 = sz[p + 1];
+                    pair2(xy0, z0, nxi, nyi, nzi, nhc, lo, nmid, A);
+                    pair2(xy1, z1, nxi, nyi, nzi, nhc, lo, nmid, A);
+                    xy0 = nxy0; xy1 = nxy1; z0 = nz0; z1 = nz1;
+                }
+#else
                 for (int it = 0; it < tmax; it += 2) {
                     const float4 xy0 = sxy[p], xy1 = sxy[p + 1];
                     const float2 z0 = sz[p], z1 = sz[p + 1];
@@ -512,6 +535,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                     pair2(xy0, z0, nxi, nyi, nzi, nhc, lo, nmid, A);
                     pair2(xy1, z1, nxi, nyi, nzi, nhc, lo, nmid, A);
                 }
+#endif
             }
             // the other element of the self pair
             if (act) {
