@@ -276,6 +276,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                             return p2(b[j0], b[j1]);
                         };
                         const int cmax = max(__shfl_sync(FULL, cnt, 0), __shfl_sync(FULL, cnt, 16));
+                        // list entries of the next round are read one round ahead
+                        int hn0 = gl < cnt ? hl[gl] : DUMMY, hn1 = 16 + gl < cnt ? hl[16 + gl] : DUMMY;
                         for (int k = 0; k < cmax; k += 32) {
                             const int e0 = k + gl, e1 = k + 16 + gl;
                             const bool v0 = e0 < cnt, v1 = e1 < cnt;
@@ -283,7 +285,9 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                             // list with r = 0), out of range in the guard band -- are the far dummy: its
                             // site moments are 0 and its LJ terms vanish (~1e-26), so no mask is needed;
                             // the LJTS shifts are subtracted per real partner at the end
-                            const int h0 = v0 ? hl[e0] : DUMMY, h1 = v1 ? hl[e1] : DUMMY;
+                            const int h0 = hn0, h1 = hn1;
+                            hn0 = e0 + 32 < cnt ? hl[e0 + 32] : DUMMY;
+                            hn1 = e1 + 32 < cnt ? hl[e1 + 32] : DUMMY;
                             const bool s0 = v0 && h0 == self, s1 = v1 && h1 == self;
                             int j0 = s0 ? DUMMY : h0, j1 = s1 ? DUMMY : h1;
                             auto com_of = [&](int j, float& X, float& Y, float& Z) {
