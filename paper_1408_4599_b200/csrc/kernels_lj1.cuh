@@ -31,6 +31,9 @@
 
 namespace lj1 {
 
+#ifndef MD_LJ1_UP
+#define MD_LJ1_UP 4
+#endif
 #ifndef MD_LJ1_PREFETCH
 #define MD_LJ1_PREFETCH 1
 #endif
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                         c = ee < n1 ? cm1 : (ee < n12 ? cm2 : cm3);
                         v = __ldg(a.xs + gi);
                     };
-                    constexpr int UP = 4;                         // pairs per lane per round: 8 loads in flight
+                    constexpr int UP = MD_LJ1_UP;                 // pairs per lane per round: 2 UP loads in flight
                     for (int q0 = lane - 3 * r3; q0 < np; q0 += 3 * UP) {
                         float4 v[2 * UP];
                         float c[2 * UP];
