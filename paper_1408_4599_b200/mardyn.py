@@ -450,22 +450,6 @@ def global_costs(system):
     return cell_cost(counts)
 
 
-def rank_loads(system, boxes):
-    """Molecules each rank holds (owned + one halo cell layer, periodic) for the given
-    k-d boxes (cells of the grid n_k = floor(L_k / rc)): sizes the rank's capacity."""
-    box = np.asarray(system["box"], float)
-    n = np.floor(box / system["rc"]).astype(int)
-    c = np.minimum((np.asarray(system["r"]) % box / box * n).astype(int), n - 1)
-    counts = np.zeros((n[2], n[1], n[0]), np.int64)
-    np.add.at(counts, (c[:, 2], c[:, 1], c[:, 0]), 1)
-    out = []
-    for lo, hi in np.asarray(boxes).reshape(-1, 2, 3):
-        ix = [np.arange(lo[k] - 1, hi[k] + 1) % n[k] for k in range(3)]
-        ix = [np.unique(a) for a in ix]
-        out.append(int(counts[np.ix_(ix[2], ix[1], ix[0])].sum()))
-    return out
-
-
 def exchange_records(send, cnt, recv, nranks, dist):
     """Halo/migration transport between ranks:
     send[d, :cnt[d]] goes to rank d; records from all ranks land contiguously
@@ -551,25 +535,23 @@ class DecomposedRun:
         ndof = system_ndof(system)
         self.ndof = ndof
         ranks = range(nranks) if transport == "loopback" else [rank]
-        loads = rank_loads(system, self.boxes)
         self.ctxs = []
         for r in ranks:
             ctx = Context(system["box"], system["rc"], system["components"], system["dt"],
                           eps_rf=system.get("eps_rf", math.inf), lj_shift=system.get("lj_shift", 1), eta=eta,
                           stream=stream)
             ctx.set_decomposition(r, nranks, flat, ndof)
-            # owned + halo + received records, with room for density changes; the step
-            # kernels' grids cover the capacity
-            ctx.reserve(min(2 * len(system["r"]), self._capacity(loads[r])))
+            # every rank takes the GLOBAL arrays in set_molecules (the library keeps the owned
+            # and halo molecules), so the capacity -- which also sizes the input staging -- is
+            # at least the global count; twice that holds owned + halo + received records of
+            # small boxes whose halo is as large as the box; the asynchronous step's
+            # capacity-wide grids exit early past the rank's molecules
+            ctx.reserve(2 * len(system["r"]))
             ctx.set_molecules(system["r"], system["v"], comp=system["comp"], q=system["q"], j=system["j"],
                               id=system["id"], half_step=0)
             self.ctxs.append(ctx)
         self.bufs = [c.dd_buffers() for c in self.ctxs]
         self.seg_max = int(self.bufs[0][0].shape[1])
-
-    @staticmethod
-    def _capacity(load):
-        return int(1.75 * load) + 16384
 
     def gather_molecules(self):
         """All owned molecules of all ranks (v, j at t - dt/2), ordered by id."""
@@ -595,12 +577,8 @@ class DecomposedRun:
         self.boxes = np.asarray(boxes).reshape(self.nranks, 2, 3)
         flat = np.concatenate([self.boxes[:, 0, :], self.boxes[:, 1, :]], axis=1)
         ranks = range(self.nranks) if self.transport == "loopback" else [self.rank]
-        loads = rank_loads(now, self.boxes)
         for r, ctx in zip(ranks, self.ctxs):
             ctx.set_decomposition(r, self.nranks, flat, self.ndof)
-            need = min(2 * len(m["r"]), self._capacity(loads[r]))
-            if need > ctx.capacity:                      # the new box holds more molecules
-                ctx.reserve(need)
             ctx.set_molecules(m["r"], m["v"], comp=m["comp"], q=m["q"], j=m["j"], id=m["id"], half_step=1)
             ctx.dd_set_segment(int(ctx.dd_buffers()[0].shape[1]))
         self.bufs = [c.dd_buffers() for c in self.ctxs]
