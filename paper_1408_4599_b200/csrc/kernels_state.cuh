@@ -202,15 +202,15 @@ __global__ void k_scatter(int n, const uint4* __restrict__ pos, const int* __res
                           unsigned long long* __restrict__ keys, int* __restrict__ oldidx,
                           const int* __restrict__ n_dev = nullptr)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (n_dev) n = *n_dev;                  // asynchronous decomposed step: count on the device
-    if (i >= n) return;
-    const int cl = cell_of[i];
-    if (cl < 0) return;                     // dropped ghost or migrant (spatial decomposition)
-    int slot = start[cl] + rank[i];
-    const uint4 p = pos[i];
-    keys[slot] = ((unsigned long long)p.x << 32) | p.w;
-    oldidx[slot] = i;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int cl = cell_of[i];
+        if (cl < 0) continue;               // dropped ghost or migrant (spatial decomposition)
+        int slot = start[cl] + rank[i];
+        const uint4 p = pos[i];
+        keys[slot] = ((unsigned long long)p.x << 32) | p.w;
+        oldidx[slot] = i;
+    }
 }
 
 // canonical gather: each sorted slot finds its rank inside its cell in the
@@ -220,7 +220,7 @@ __global__ void k_scatter(int n, const uint4* __restrict__ pos, const int* __res
 // and writes the staging copy (cell-relative coordinates, exact) and, for
 // rigid models, the world-frame site offsets s = R(q) d.
 template <bool RIGID>
-__global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __restrict__ keys,
+__device__ __forceinline__ void canon_one(int t, int cap, const GridP& g, const unsigned long long* __restrict__ keys,
                         const int* __restrict__ oldidx, const int* __restrict__ cell_of,
                         const int* __restrict__ start,
                         const uint4* __restrict__ pos_s, const float4* __restrict__ vel_s,
@@ -230,8 +230,6 @@ __global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __res
                         float4* __restrict__ xs, float4* __restrict__ site,
                         const DevModel* __restrict__ model)
 {
-    int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n || t >= start[g.ncell]) return;
     const unsigned long long key = keys[t];
     const int old = oldidx[t];
     int c = cell_of[old];
@@ -273,6 +271,25 @@ __global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __res
             site[(size_t)(ns + 2 * k + 1) * cap + dst] = make_float4(e.x, e.y, e.z, 0.f);
         }
     }
+}
+
+// grid-stride over the sorted slots (the asynchronous decomposed step launches a
+// capacity-independent grid)
+template <bool RIGID>
+__global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __restrict__ keys,
+                        const int* __restrict__ oldidx, const int* __restrict__ cell_of,
+                        const int* __restrict__ start,
+                        const uint4* __restrict__ pos_s, const float4* __restrict__ vel_s,
+                        const float4* __restrict__ quat_s, const float4* __restrict__ angm_s,
+                        uint4* __restrict__ pos_d, float4* __restrict__ vel_d,
+                        float4* __restrict__ quat_d, float4* __restrict__ angm_d,
+                        float4* __restrict__ xs, float4* __restrict__ site,
+                        const DevModel* __restrict__ model)
+{
+    const int lim = min(n, start[g.ncell]);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < lim; t += gridDim.x * blockDim.x)
+        canon_one<RIGID>(t, cap, g, keys, oldidx, cell_of, start, pos_s, vel_s, quat_s, angm_s, pos_d, vel_d,
+                         quat_d, angm_d, xs, site, model);
 }
 
 // ------------------------------------------------------------------------

@@ -440,19 +440,22 @@ static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 static int enqueue_sort(mardyn_ctx* ctx, int src, int dst, int64_t n_unsorted = -1, const int* n_dev = nullptr)
 {
     const int n = n_dev ? (int)ctx->cap : (int)(n_unsorted < 0 ? ctx->n : n_unsorted), ncell = ctx->g.ncell;
+    // count known on the host: one thread per molecule; in device memory only: a grid-stride
+    // grid of 8 blocks per SM (independent of the capacity)
+    const int gb = n_dev ? std::min(nblk(n, 256), 8 * ctx->num_sms) : nblk(n, 256);
     cudaStream_t s = ctx->stream;
     // (look-back flags carry an epoch, counts are zeroed as read: no memsets per step)
     k_scan<<<ctx->ntiles, 1024, 0, s>>>(ncell, ctx->count, ctx->start, ctx->scan_flags,
                                         reinterpret_cast<unsigned*>(ctx->scan_flags + ctx->ntiles), ctx->blk_ctr);
-    k_scatter<<<nblk(n, 256), 256, 0, s>>>(n, ctx->pos[src], ctx->cell_of, ctx->rank, ctx->start, ctx->keys,
+    k_scatter<<<gb, 256, 0, s>>>(n, ctx->pos[src], ctx->cell_of, ctx->rank, ctx->start, ctx->keys,
                                             ctx->oldidx, n_dev);
     if (ctx->rigid)
-        k_canon<true><<<nblk(n, 256), 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->oldidx, ctx->cell_of, ctx->start,
+        k_canon<true><<<gb, 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->oldidx, ctx->cell_of, ctx->start,
                                                    ctx->pos[src], ctx->vel[src], ctx->quat[src], ctx->angm[src],
                                                    ctx->pos[dst], ctx->vel[dst], ctx->quat[dst], ctx->angm[dst],
                                                    ctx->xs, ctx->site, ctx->dmodel);
     else
-        k_canon<false><<<nblk(n, 256), 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->oldidx, ctx->cell_of, ctx->start,
+        k_canon<false><<<gb, 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->oldidx, ctx->cell_of, ctx->start,
                                                     ctx->pos[src], ctx->vel[src], nullptr, nullptr,
                                                     ctx->pos[dst], ctx->vel[dst], nullptr, nullptr, ctx->xs,
                                                     nullptr, ctx->dmodel);
