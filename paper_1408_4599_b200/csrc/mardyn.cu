@@ -138,6 +138,7 @@ struct mardyn_ctx {
     // spatial decomposition (§4): this rank's box, cell owners, halos
     int dd_rank = 0, nranks = 1;
     bool n_stale = false;                  // asynchronous decomposed steps: host copy of n out of date
+    bool side_join = false;                // the step's finalize runs on the side stream until end_step
     int* recv_cnt = nullptr;               // asynchronous exchange: records received per source rank (device)
     int* n_aux = nullptr;                  // unsorted count after the import (device)
     int64_t seg_max = 0;                   // send segment stride of the workspace layout
@@ -1023,6 +1024,7 @@ int mardyn_step(mardyn_ctx* ctx, int32_t nsteps)
 
 static int sync_check(mardyn_ctx* ctx)
 {
+    if (ctx->side_join) CK(cudaStreamSynchronize(ctx->side_stream));
     CK(cudaStreamSynchronize(ctx->stream));
     int flag = 0;
     CK(cudaMemcpy(&flag, ctx->flag, 4, cudaMemcpyDeviceToHost));
@@ -1468,8 +1470,14 @@ int mardyn_dd_begin_step_async(mardyn_ctx* ctx)
         CK(cudaEventRecord(ctx->ev_f0[b], s));
         launch_force(ctx, b, true, false, &dd);
         CK(cudaEventRecord(ctx->ev_f1[b], s));
-        k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, 0, ctx->kpart, ctx->ndof,
+        // the observables of the step on a side stream, concurrent with the exchange and the
+        // cell rebuild (joined at the end of mardyn_dd_end_step_async)
+        CK(cudaEventRecord(ctx->ev_s0, s));
+        CK(cudaStreamWaitEvent(ctx->side_stream, ctx->ev_s0, 0));
+        k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, ctx->side_stream>>>(ctx->nfpart, ctx->fpart, 0, ctx->kpart, ctx->ndof,
                                                       ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket, 0);
+        CK(cudaEventRecord(ctx->ev_s1, ctx->side_stream));
+        ctx->side_join = true;
         ctx->launches += 1;
         CK(cudaGetLastError());
         ctx->last_parity = b;
@@ -1515,6 +1523,10 @@ int mardyn_dd_end_step_async(mardyn_ctx* ctx)
     ctx->launches += 1;
     int rc = enqueue_sort(ctx, b, 1 - b, -1, ctx->n_aux);
     if (rc) return rc;
+    if (ctx->side_join) {                              // the next step's force rewrites the partials
+        CK(cudaStreamWaitEvent(s, ctx->ev_s1, 0));
+        ctx->side_join = false;
+    }
     CK(cudaGetLastError());
     ctx->n_stale = true;
     ctx->cur = 1 - b;
