@@ -48,6 +48,9 @@ def parse():
     p.add_argument("--impl", default="mardyn", choices=["mardyn", "reference"])
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    # test hook: gloo instead of NCCL (ranks may then share a GPU; exercises the N > 1
+    # orchestration on a one-GPU box -- not a performance configuration)
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     return p.parse_args()
 
 
@@ -279,11 +282,16 @@ def main():
         return run_reference(args, system, rank, world)
 
     import torch
+    if args.dist_backend == "gloo":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1408_4599_b200 import build as b
     from paper_1408_4599_b200 import mardyn
     if rank == 0 or world == 1:
@@ -386,7 +394,8 @@ def main():
         "data": "synthetic (seeded generator of BASELINE configs, no checkpoints)",
         "config": {"workload": system["name"], "n_molecules": N, "steps_per_run": args.steps,
                    "parallelism": (f"k-d tree spatial decomposition over {world} GPUs, halo exchange + "
-                                   "migration with NCCL send/recv every step") if world > 1 else "single GPU",
+                                   f"migration with {'NCCL' if args.dist_backend == 'nccl' else 'gloo (test transport)'} "
+                                   "all-to-alls every step") if world > 1 else "single GPU",
                    "l2": "flushed between timed steps (256 MB write)",
                    "arithmetic": "fp32 forces (packed fp32x2), u32 fixed-point positions, fp64 sums",
                    "pair_interactions_per_s": obs["n_pairs"] * args.steps / (tot_ms / 1e3)},

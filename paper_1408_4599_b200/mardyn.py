@@ -467,19 +467,27 @@ def exchange_records(send, cnt, recv, nranks, dist):
         outs.append(recv[off: off + k])
         off += k
     me = dist.get_rank()
-    ops = []
+    # gloo moves device tensors in its collectives but not point to point: stage through host
+    host = dev.type == "cuda" and dist.get_backend() != "nccl"
+    ops, land = [], []
     for d in range(nranks):
         if d == me:
             if int(cnt[d]):
                 outs[d].copy_(send[d][: int(cnt[d])])
             continue
         if int(cnt[d]):
-            ops.append(dist.P2POp(dist.isend, send[d][: int(cnt[d])].contiguous(), d))
+            t = send[d][: int(cnt[d])].contiguous()
+            ops.append(dist.P2POp(dist.isend, t.cpu() if host else t, d))
         if rcounts[d]:
-            ops.append(dist.P2POp(dist.irecv, outs[d], d))
+            t = torch.empty(outs[d].shape, dtype=outs[d].dtype) if host else outs[d]
+            land.append((outs[d], t))
+            ops.append(dist.P2POp(dist.irecv, t, d))
     if ops:
         for w in dist.batch_isend_irecv(ops):
             w.wait()
+    if host:
+        for o, t in land:
+            o.copy_(t)
     return off
 
 
