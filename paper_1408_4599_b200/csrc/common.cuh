@@ -61,6 +61,7 @@ struct GridP {
     float edge[3];               // E * s
     float cut2;                  // rc^2 (fp32)
     float cut2_lo, cut2_hi;      // guard band around rc^2 for the exact test
+    float band_mid, band_hw;     // 0.5 (lo + hi), 0.5 (hi - lo) + 1e-6 hi (fp32, set with lo / hi)
     long long cut2_q;            // exact threshold in quanta^2: in range iff r2q < cut2_q
     float dt;
     int hlo[3], hdim[3];         // home cells of this rank: box [hlo, hlo + hdim) (whole grid if 1 rank)

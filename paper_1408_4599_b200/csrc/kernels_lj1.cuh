@@ -221,7 +221,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
     const float c6 = a.sig2 * a.sig2 * a.sig2, hc = 0.5f / c6;     // sigma^6, 1/(2 sigma^6)
     const double c6d = (double)c6;
     const float2 nhc = make_float2(-hc, -hc);
-    const float mid = 0.5f * (lo + hi), hw = 0.5f * (hi - lo) + 1e-6f * hi;   // band test (margin >> rounding of mid)
+    // band test |r^2 - mid| <= hw (margin >> rounding of mid); host-computed kernel parameters, so
+    // that the main loop takes them as constant operands instead of holding or recomputing them
+    const float mid = g.band_mid, hw = g.band_hw;
     const float2 nmid = make_float2(-mid, -mid);
     const float rc2w = hi * (1.f + 1.f / 4096.f);       // generous window (necessary condition only)
     const float ex = g.edge[0], inv_ex = 1.f / g.edge[0];

@@ -225,6 +225,8 @@ static int setup_grid(mardyn_ctx* ctx)
     g.cut2 = (float)rc2;
     g.cut2_lo = std::nextafterf((float)(rc2 * (1.0 - std::ldexp(1.0, -20))), 0.f);
     g.cut2_hi = std::nextafterf((float)(rc2 * (1.0 + std::ldexp(1.0, -20))), INFINITY);
+    g.band_mid = 0.5f * (g.cut2_lo + g.cut2_hi);
+    g.band_hw = 0.5f * (g.cut2_hi - g.cut2_lo) + 1e-6f * g.cut2_hi;
     g.cut2_q = (long long)std::ceil(rc2 / (s * s));
     g.dt = (float)ctx->dt;
     for (int k = 0; k < 3; ++k) { g.hlo[k] = 0; g.hdim[k] = g.nc[k]; }
