@@ -334,3 +334,44 @@ def test_rigid_pair_golden_gpu(md, which):
     scale = np.abs(g["F2"]).max()
     assert np.abs(F[1] - g["F2"]).max() <= 5e-5 * scale, (F[1], g["F2"])
     assert np.abs(tau[1] - g["tau2"]).max() <= 5e-5 * np.abs(g["tau2"]).max(), (tau[1], g["tau2"])
+
+
+@pytest.mark.parametrize("model", ["lj", "2cljq"])
+@pytest.mark.parametrize("shift", [0, 1, -1])
+def test_guard_band_exact(md, oracle_mod, model, shift):
+    """Pairs exactly at the cutoff and one position quantum inside / outside it
+    (reading A12: in range iff the exact r^2 < rc^2, decided in integer quanta).
+    Simple cubic lattice of spacing rc/2: the second axis neighbours sit at r = rc
+    exactly, so the fp32 fast passes of both force kernels see them in the guard band
+    and the exact pass decides them.  shift = +-1: the molecules of x-columns
+    i mod 4 in {0, 1} move by +-1 quantum along x, so half of the x-axis second
+    neighbours come one quantum inside rc.  n_pairs is pinned in closed form
+    (26 neighbours with r^2 / a^2 in {1, 2, 3} per molecule, + N/2 for the shifted
+    lattice) and forces / U / W against the oracle."""
+    rc = 2.5 if model == "lj" else 4.0
+    a, n = rc / 2, 8
+    idx = np.stack(np.meshgrid(*[np.arange(n)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    r = (idx + 0.5) * a
+    N = len(r)
+    rng = np.random.default_rng(77)
+    if model == "lj":
+        comps, q = [S.lj1_component()], None
+    else:
+        comps, q = [S.c2_component()], S.random_quaternions(rng, N)
+    s = S._system(f"band_{model}", (n * a,) * 3, rc, 0.001, 1, 1.0, comps, r, np.zeros((N, 3)), q=q)
+    quantum = oracle_mod.System(s).quantum
+    s["r"] = np.ascontiguousarray(r + np.outer(shift * quantum * (idx[:, 0] % 4 < 2), [1.0, 0.0, 0.0]))
+    ctx, Fg, tg, obs, ug, cg, ng = gpu_state(md, s)
+    o, uo, co, no, Fo, to, tot = oracle_state(oracle_mod, s)
+    assert np.array_equal(ug, uo) and np.array_equal(cg, co) and np.array_equal(ng, no)
+    expect = N * 26 // 2 + (N // 2 if shift else 0)
+    assert tot["npairs"] == expect
+    assert obs["n_pairs"] == expect
+    assert_rel(obs["U_pot"], tot["U"], "U_pot")
+    assert_rel(obs["virial"], tot["W"], "virial")
+    # the LJ lattice is (nearly) force-free by symmetry: the force tolerance is taken
+    # relative to the nearest-neighbour pair force instead of the RMS molecular force
+    scale = max(rms(Fo), abs(24 * (2 * a ** -13 - a ** -7)))
+    assert np.abs(Fg - Fo).max() <= 1e-4 * scale
+    if model != "lj":
+        assert_forces_close(tg, to, "torque")

@@ -211,3 +211,38 @@ def test_hit_rate_ideal_gas(oracle_mod):
     assert ratio == pytest.approx(4 * math.pi / 3 * 2.5 ** 3 / (27 * edge ** 3), rel=0.02)
     assert edge == pytest.approx(2.5)
     assert ratio == pytest.approx(0.155, abs=0.005)
+
+
+@pytest.mark.parametrize("shift", [0, 1, -1])
+def test_cutoff_boundary_closed_form(oracle_mod, shift):
+    """Reading A12 at the cutoff itself: in range iff the exact r^2 < rc^2.  Simple
+    cubic lattice of spacing a = rc/2 (8^3 sites): the second axis neighbours sit at
+    r = rc exactly and are out; with the x-columns i mod 4 in {0, 1} moved by
+    shift = +-1 position quantum, half of the x-axis second neighbours come one
+    quantum inside (N/2 more pairs).  Unshifted: every site has 6 + 12 + 8 neighbours
+    at a, a sqrt2, a sqrt3, U/N and W/N are the LJTS shell sums, F = 0; brute force
+    and linked cells agree."""
+    rc = 2.5
+    a, n = rc / 2, 8
+    idx = np.stack(np.meshgrid(*[np.arange(n)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    r = (idx + 0.5) * a
+    N = len(r)
+    s = S._system("band", (n * a,) * 3, rc, 0.001, 1, 1.0, [S.lj1_component()], r, np.zeros((N, 3)))
+    o = oracle_mod.System(s)
+    s["r"] = r + np.outer(shift * o.quantum * (idx[:, 0] % 4 < 2), [1.0, 0.0, 0.0])
+    u = o.quantize(s["r"])
+    assert np.array_equal(u[:, 0].astype(np.int64) - o.quantize(r)[:, 0].astype(np.int64),
+                          shift * (idx[:, 0] % 4 < 2))      # exactly one quantum
+    res = [o.forces(s["comp"], u, s["q"], mode=m) for m in ("cells", "brute")]
+    expect = N * 26 // 2 + (N // 2 if shift else 0)
+    for F, _, tot in res:
+        assert tot["npairs"] == expect
+    if shift == 0:
+        d = np.array([1.0] * 6 + [math.sqrt(2)] * 12 + [math.sqrt(3)] * 8) * a
+        uu = 4 * (d ** -12 - d ** -6) - 4 * (rc ** -12 - rc ** -6)
+        ww = 24 * (2 * d ** -12 - d ** -6)
+        F, _, tot = res[0]
+        assert tot["U"] / N == pytest.approx(0.5 * uu.sum(), rel=1e-12)
+        assert tot["W"] / N == pytest.approx(0.5 * ww.sum(), rel=1e-12)
+        assert np.abs(F).max() < 1e-9
+    assert res[0][2]["U"] == pytest.approx(res[1][2]["U"], rel=1e-12)
