@@ -39,6 +39,14 @@ namespace lj1 {
 #endif
 constexpr int KMAX = 6;          // home cells per sub-chunk: staged |x| < 4 E (A12 quantum)
 constexpr int BLOCKS_PER_FETCH = 1;
+// small systems (at most MD_LJ1_HALF blocks of 32 per warp of the grid) are taken as half
+// blocks of 16 molecules with two lanes per molecule (each lane one half of the neighbour
+// rows): a block's latency sets the time of such a launch.  (Half blocks for the last wave
+// of a large system only -- the tail -- measured 1 % slower on c1: staging and window
+// searches cost a half block as much as a full one.)
+#ifndef MD_LJ1_HALF
+#define MD_LJ1_HALF 1
+#endif
 
 // per-lane segment [begin, end) of staged pairs: packed 16-bit halves (smaller
 // shared memory per warp -> more resident warps) or two ints
@@ -113,6 +121,20 @@ struct Acc {
     int hits_exact;              // hits found by the exact band pass / scalar paths
     float mb;                    // min |r^2 - mid| over the candidates (guard band iff <= hw)
 };
+
+// two lanes of one molecule (half blocks): sum their partial accumulators (commutative
+// adds: both lanes hold the same bits afterwards)
+__device__ __forceinline__ void acc_pair_sum(Acc& A, unsigned m)
+{
+    A.gx.x += __shfl_xor_sync(m, A.gx.x, 1); A.gx.y += __shfl_xor_sync(m, A.gx.y, 1);
+    A.gy.x += __shfl_xor_sync(m, A.gy.x, 1); A.gy.y += __shfl_xor_sync(m, A.gy.y, 1);
+    A.gz.x += __shfl_xor_sync(m, A.gz.x, 1); A.gz.y += __shfl_xor_sync(m, A.gz.y, 1);
+    A.a.x += __shfl_xor_sync(m, A.a.x, 1); A.a.y += __shfl_xor_sync(m, A.a.y, 1);
+    A.b.x += __shfl_xor_sync(m, A.b.x, 1); A.b.y += __shfl_xor_sync(m, A.b.y, 1);
+    A.h.x += __shfl_xor_sync(m, A.h.x, 1); A.h.y += __shfl_xor_sync(m, A.h.y, 1);
+    A.hits_exact += __shfl_xor_sync(m, A.hits_exact, 1);
+    A.mb = fminf(A.mb, __shfl_xor_sync(m, A.mb, 1));
+}
 
 __device__ __forceinline__ void acc_zero(Acc& A)
 {
@@ -232,7 +254,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
     // n_candidates (27-cell full-shell count, reported observable): each home lane
     // adds sum_27 N_c' - 1 for its molecule (from the staged cell table or start[])
     const int nsorted = __ldg(a.start + g.ncell);
-    const int nblocks = (nsorted + 31) >> 5;
+    const int nb32 = (nsorted + 31) >> 5;
+    const int B1 = nb32 <= MD_LJ1_HALF * nw ? 0 : nb32;       // blocks of 32, or half blocks of 16
+    const int nblocks = B1 + max(0, (nsorted - 32 * B1 + 15) >> 4);
     for (int b = nblocks + gw * 32 + lane; b < a.nbcap; b += nw * 32)     // unused block partials
         a.bpart[b] = ForcePartial{0.0, 0.0, 0, 0, 0.0};
     // blocks are handed out in sorted order by an atomic counter (load balance);
@@ -251,7 +275,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
         double Uw = 0.0, Ww = 0.0;
         long long npw = 0;
         float3 Fown = make_float3(0.f, 0.f, 0.f);  // this lane's molecule (STEP)
-        const int mi = blk * 32 + lane;
+        const bool lp2 = blk >= B1;                // half block: lanes 2k, 2k+1 share molecule k
+        const int sub = lp2 ? (lane & 1) : 0;      // which half of the neighbour rows (parity of r)
+        const bool own_lane = sub == 0;            // the lane that writes the molecule's results
+        const int mi = lp2 ? 32 * B1 + 16 * (blk - B1) + (lane >> 1) : blk * 32 + lane;
         bool valid = mi < nsorted;
         uint4 pi = valid ? a.pos[mi] : make_uint4(0, 0, 0, 0);
         const float4 vi = (STEP && valid) ? a.vel[mi] : make_float4(0.f, 0.f, 0.f, 0.f);   // in flight during the forces
@@ -314,12 +341,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                 Acc A;
                 acc_zero(A);
                 if ((todo >> lane) & 1u) {
-                    int ncand_l = -1;                      // the molecule itself is no candidate
+                    int ncand_l = own_lane ? -1 : 0;       // the molecule itself is no candidate
                     // cell-relative coordinates of the staging copy (read-only while the fused
                     // step advances pos in place): neighbour cell (dx, dy, dz) adds its offset, exact
                     const float4 xsi = __ldg(a.xs + mi);
                     for (int dz = -1; dz <= 1; ++dz)
                         for (int dy = -1; dy <= 1; ++dy) {
+                            if (((dy + 1 + 3 * (dz + 1)) & 1) != sub && lp2) continue;   // the partner lane's row
                             const int rowc = nx * (wrapi(cy + dy, ny) + ny * wrapi(cz + dz, nz));
                             const float oy = (float)dy * g.edge[1], oz = (float)dz * g.edge[2];
                             for (int dx = -1; dx <= 1; ++dx) {
@@ -335,14 +363,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                                 }
                             }
                         }
+                    if (lp2) acc_pair_sum(A, todo);
                     const float f = -2.f * a.eps24 * c6 * c6;
                     Fown = make_float3(f * A.gx.x, f * A.gy.x, f * A.gz.x);
-                    a.force[mi] = make_float4(Fown.x, Fown.y, Fown.z, 0.f);
-                    const double Ad = c6d * c6d * A.a.x, Bd = c6d * A.b.x;
                     ncw += ncand_l;
-                    Uw += (double)a.eps4 * (Ad - Bd) - (double)a.shift * A.hits_exact;
-                    Ww += (double)a.eps24 * (2.0 * Ad - Bd);
-                    npw += A.hits_exact;
+                    if (own_lane) {
+                        a.force[mi] = make_float4(Fown.x, Fown.y, Fown.z, 0.f);
+                        const double Ad = c6d * c6d * A.a.x, Bd = c6d * A.b.x;
+                        Uw += (double)a.eps4 * (Ad - Bd) - (double)a.shift * A.hits_exact;
+                        Ww += (double)a.eps24 * (2.0 * Ad - Bd);
+                        npw += A.hits_exact;
+                    }
                 }
                 break;
             }
@@ -435,7 +466,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                     const float w2 = rc2w - Dy * Dy - Dz * Dz;
                     float w;                                     // approximate: rc2w is generous by 2^-12
                     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(w) : "f"(fmaxf(w2, 0.f)));
-                    const bool on = act && w2 > 0.f;
+                    const bool on = act && w2 > 0.f && (!lp2 || (r & 1) == sub);
                     const float xl = on ? xi - w : FAR, xh = on ? xi + w : -FAR;   // off: empty window
                     // cell of each bound, rounded outward by 1e-3 cell (>> the 1e-6 rounding of the
                     // product): a lower cell for xl / a higher cell for xh only widens the window
@@ -480,7 +511,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                 for (int r = 0; r < 9; ++r) {
                     int pa = la[r];
                     const int pb = ua[r];
-                    if (r == 4 && act) {
+                    if (r == 4 && act && own_lane) {
                         if (pself > pa) {
                             const int qa = pa - ((pself - pa) & 1);
                             sseg[32 * nseg + lane] = seg_make(qa, pself); ++nseg; ttot += pself - qa;
@@ -543,7 +574,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
 #endif
             }
             // the other element of the self pair
-            if (act) {
+            if (act && own_lane) {
                 const int eo = eself ^ 1;
                 elem1<false>(sxf[4 * pself + (eo & 1)], sxf[4 * pself + 2 + (eo & 1)], szf[2 * pself + (eo & 1)],
                              xi, yi, zi, hc, lo, hi, g, A);
@@ -562,7 +593,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                     }
                 }
             }
-            if (act) {
+            if (lp2) acc_pair_sum(A, 0xffffffffu);
+            if (act && own_lane) {
                 int nc27 = -1;                             // the molecule itself is no candidate
                 const int kk = cx - cA;                    // staged cells kk, kk+1, kk+2 hold its 27-cell rows
 #pragma unroll
@@ -592,7 +624,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
             int own = -1;
             uint4 pn = make_uint4(0, 0, 0, 0);
             float4 vn = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (home) {
+            if (home && own_lane) {
                 const LeapOut o = md_leapfrog(g, pi, vi, Fown.x, Fown.y, Fown.z, a.mass, a.inv_mass);
                 if (o.bad) atomicOr(a.flag, 1);
                 a.pos[mi] = o.p;
@@ -611,7 +643,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                 }
                 a.cell_of[mi] = clb;
                 Kw = o.ket;
-            } else if (DD && valid) {
+            } else if (DD && valid && own_lane) {
                 a.cell_of[mi] = -1;                        // last step's halo copies are dropped
             }
             if (DD) dd_pack_warp(a.dd, dmask, own, pn, vn, make_float4(1.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f));

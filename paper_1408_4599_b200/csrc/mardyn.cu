@@ -691,7 +691,9 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     const int ntiles = ncell_pad / SCAN_TILE;
     const int nk = std::max(1, nblk(cap, 256));
     const int nfw = std::max(1, ctx->force_blocks * ctx->force_warps_per_block);
-    const int nbc = ctx->kernel == KER_LJ1 ? nblk(cap, 32) + 1 : 0;
+    // single-site kernel: one partial per block -- blocks of 32, or (small systems) half blocks
+    // of 16 (k_force_lj1: MD_LJ1_HALF)
+    const int nbc = ctx->kernel == KER_LJ1 ? nblk(cap, 32) + 1 + MD_LJ1_HALF * nfw : 0;
     uint4* pos0 = (uint4*)take(16 * cap);
     uint4* pos1 = (uint4*)take(16 * cap);
     float4* vel0 = (float4*)take(16 * cap);
@@ -843,7 +845,8 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
     {
         int grid = ctx->force_blocks;
         if (ctx->nranks == 1) {
-            const int64_t units = ctx->kernel == KER_LJ1 ? (n + 31) / 32 : (int64_t)ctx->g.nhome;
+            // (single-site: half blocks of 16 when there are fewer 32-blocks than warps)
+            const int64_t units = ctx->kernel == KER_LJ1 ? (n + 15) / 16 : (int64_t)ctx->g.nhome;
             const int upb = (ctx->kernel == KER_RIGID && MD_RIGID3) ? 1 : ctx->force_warps_per_block;   // rig3: CTA per cell
             const int64_t need = (units + upb - 1) / upb;
             grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, need));
