@@ -293,6 +293,17 @@ int mardyn_dd_set_segment(struct mardyn_ctx* ctx, int64_t seg_cap);
  * exchange buffers (MARDYN_EINVAL).  mardyn_dd_set_segment returns to uniform segments. */
 int mardyn_dd_set_peer_segments(struct mardyn_ctx* ctx, const int64_t* send_caps, const int64_t* recv_caps);
 int mardyn_dd_device_counts(struct mardyn_ctx* ctx, void** send_cnt, void** recv_cnt);
+/* Direct puts (device-initiated exchange, no transport step): with the segments set
+ * (uniform or per-peer; setting them again clears the targets), the packing kernel of mardyn_dd_begin_step_async writes the records for rank d straight
+ * to rec_addr[d] -- the device address of this rank's receive segment in rank d's receive
+ * buffer (peer memory over NVLink, or another context's buffer on the same device) -- and
+ * a one-warp kernel then stores this rank's count for d at cnt_addr[d] (the entry for this
+ * rank in d's recv_cnt).  Host arrays of nranks device addresses (records 16-byte, counts
+ * 4-byte aligned; MARDYN_EINVAL otherwise), copied.  The caller orders every rank's begin
+ * before any rank's end, and every rank's end before any rank's next begin (one stream, or
+ * a cross-device barrier).  rec_addr = NULL switches back to the transport; so do
+ * mardyn_dd_set_segment and mardyn_dd_set_peer_segments. */
+int mardyn_dd_set_peer_targets(struct mardyn_ctx* ctx, const uint64_t* rec_addr, const uint64_t* cnt_addr);
 int mardyn_dd_begin_step_async(struct mardyn_ctx* ctx);
 int mardyn_dd_end_step_async(struct mardyn_ctx* ctx);
 

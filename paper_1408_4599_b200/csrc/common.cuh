@@ -108,6 +108,8 @@ struct DDArgs {
     const int* n_dev;            // asynchronous step: molecule count in device memory (else the kernel's n)
     const int* seg_tab;          // per-peer segments: [0, nranks) offsets, [nranks, 2 nranks) capacities
                                  // (records); nullptr: uniform segments r * seg_cap of seg_cap records
+    DDRec* const* put_rec = nullptr;   // direct puts: record k for rank r goes to put_rec[r][k] (this rank's
+                                 // segment in r's receive buffer; peer memory), nullptr: own send buffer
 };
 
 // Pack this lane's exchange records (spatial decomposition): one record for every rank in
@@ -140,7 +142,8 @@ __device__ __forceinline__ void dd_pack_warp(const DDArgs& dd, unsigned dmask, i
                 rec.vel = r == own ? vn : make_float4(vn.x, vn.y, vn.z, __int_as_float((__float_as_int(vn.w) & 0xff) | 256));
                 rec.quat = qn;
                 rec.angm = jn;
-                dd.send[off_r + k] = rec;
+                if (dd.put_rec) dd.put_rec[r][k] = rec;
+                else dd.send[off_r + k] = rec;
             }
         }
     }

@@ -449,6 +449,13 @@ __global__ void k_import(int n, int base, GridP g, const DDRec* __restrict__ rec
 // rtab: per-source segments ([0, nranks) offsets, [nranks, 2 nranks) capacities), or
 // nullptr for uniform segments r * seg_cap of seg_cap records; the grid covers the
 // sum of the capacities
+// direct puts: this rank's record counts into the receiving ranks' count arrays (peer memory)
+__global__ void k_put_counts(int nranks, const int* __restrict__ send_cnt, int* const* __restrict__ put_cnt)
+{
+    const int r = threadIdx.x;
+    if (r < nranks) *put_cnt[r] = send_cnt[r];
+}
+
 __global__ void k_import_seg(int nranks, int seg_cap, const int* __restrict__ rtab, const int* __restrict__ recv_cnt,
                              const int* __restrict__ n_old_dev, int cap, GridP g, const DDRec* __restrict__ recv,
                              uint4* __restrict__ pos, float4* __restrict__ vel, float4* __restrict__ quat,

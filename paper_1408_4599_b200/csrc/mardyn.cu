@@ -140,6 +140,9 @@ struct mardyn_ctx {
     bool n_stale = false;                  // asynchronous decomposed steps: host copy of n out of date
     bool side_join = false;                // the step's finalize runs on the side stream until end_step
     int* recv_cnt = nullptr;               // asynchronous exchange: records received per source rank (device)
+    DDRec** put_rec = nullptr;             // direct puts: per destination rank, where this rank's records go
+    int** put_cnt = nullptr;               //   and where its record count goes (device arrays of addresses)
+    bool direct = false;
     int* n_aux = nullptr;                  // unsorted count after the import (device)
     int64_t seg_max = 0;                   // send segment stride of the workspace layout
     int* seg_tab = nullptr;                // per-peer segments (device): send offsets, send caps, recv offsets, recv caps
@@ -735,6 +738,8 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     int* recv_cnt = nullptr;
     int* n_aux = nullptr;
     int* seg_tab = nullptr;
+    DDRec** put_rec = nullptr;
+    int** put_cnt = nullptr;
     const int64_t seg_cap = ctx->nranks > 1 ? cap / ctx->nranks + 4096 : 0;
     const int64_t recv_cap = ctx->nranks > 1 ? cap : 0;
     if (ctx->nranks > 1) {
@@ -747,6 +752,8 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         recv_cnt = (int*)take(4 * (size_t)ctx->nranks);
         n_aux = (int*)take(8);                     // [0] unsorted count after import, [1] n at force time
         seg_tab = (int*)take(16 * (size_t)ctx->nranks);
+        put_rec = (DDRec**)take(sizeof(void*) * (size_t)ctx->nranks);
+        put_cnt = (int**)take(sizeof(void*) * (size_t)ctx->nranks);
     }
     if (assign) {
         ctx->pos[0] = pos0; ctx->pos[1] = pos1; ctx->vel[0] = vel0; ctx->vel[1] = vel1;
@@ -762,6 +769,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         ctx->recvbuf = recvbuf; ctx->send_cnt = send_cnt; ctx->seg_cap = seg_cap; ctx->recv_cap = recv_cap;
         ctx->recv_cnt = recv_cnt; ctx->n_aux = n_aux; ctx->seg_max = seg_cap; ctx->n_stale = false;
         ctx->seg_tab = seg_tab; ctx->peer_segs = false;
+        ctx->put_rec = put_rec; ctx->put_cnt = put_cnt; ctx->direct = false;
         ctx->ncell_pad = ncell_pad; ctx->ntiles = ntiles; ctx->nkblocks = nk;
     }
     return off;
@@ -1413,6 +1421,7 @@ int mardyn_dd_set_segment(mardyn_ctx* ctx, int64_t seg_cap)
     if (seg_cap < 1 || seg_cap > ctx->seg_max) return fail(ctx, MARDYN_EINVAL, "segment capacity out of range");
     ctx->seg_cap = seg_cap;
     ctx->peer_segs = false;
+    ctx->direct = false;                   // peer targets were laid out for the per-peer segments
     ctx->recv_span = seg_cap * ctx->nranks;
     return MARDYN_OK;
 }
@@ -1438,7 +1447,31 @@ int mardyn_dd_set_peer_segments(mardyn_ctx* ctx, const int64_t* send_caps, const
     CK(cudaMemcpyAsync(ctx->seg_tab, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->peer_segs = true;
+    ctx->direct = false;                   // new offsets: the peer targets must be set again
     ctx->recv_span = ro;
+    return MARDYN_OK;
+}
+
+int mardyn_dd_set_peer_targets(mardyn_ctx* ctx, const uint64_t* rec_addr, const uint64_t* cnt_addr)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (ctx->nranks < 2 || !ctx->ws) return fail(ctx, MARDYN_ESTATE, "no decomposition workspace");
+    if (!rec_addr || !cnt_addr) {
+        ctx->direct = false;
+        return MARDYN_OK;
+    }
+    const int p = ctx->nranks;
+    std::vector<uint64_t> tab(2 * (size_t)p);
+    for (int r = 0; r < p; ++r) {
+        if (!rec_addr[r] || rec_addr[r] % 16 || !cnt_addr[r] || cnt_addr[r] % 4)
+            return fail(ctx, MARDYN_EINVAL, "peer target addresses must be non-null and aligned (16 B records, 4 B counts)");
+        tab[r] = rec_addr[r];
+        tab[p + r] = cnt_addr[r];
+    }
+    CK(cudaMemcpyAsync(ctx->put_rec, tab.data(), sizeof(uint64_t) * p, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->put_cnt, tab.data() + p, sizeof(uint64_t) * p, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->direct = true;
     return MARDYN_OK;
 }
 
@@ -1468,6 +1501,7 @@ int mardyn_dd_begin_step_async(mardyn_ctx* ctx)
     dd.send = ctx->sendbuf; dd.seg_cap = (int)ctx->seg_cap; dd.send_cnt = ctx->send_cnt; dd.flag = ctx->flag;
     dd.n_dev = ctx->start + ctx->g.ncell;             // the sorted count of the last cell rebuild
     dd.seg_tab = ctx->peer_segs ? ctx->seg_tab : nullptr;
+    dd.put_rec = ctx->direct ? ctx->put_rec : nullptr;
     CK(cudaMemsetAsync(ctx->send_cnt, 0, sizeof(int) * ctx->nranks, s));
     if (ctx->kernel == KER_LJ1) {
         // single-site kernel with the leapfrog, binning and exchange packing fused in (the
@@ -1475,6 +1509,10 @@ int mardyn_dd_begin_step_async(mardyn_ctx* ctx)
         CK(cudaEventRecord(ctx->ev_f0[b], s));
         launch_force(ctx, b, true, false, &dd);
         CK(cudaEventRecord(ctx->ev_f1[b], s));
+        if (ctx->direct) {
+            k_put_counts<<<1, 32, 0, s>>>(ctx->nranks, ctx->send_cnt, ctx->put_cnt);
+            ctx->launches += 1;
+        }
         // the observables of the step on a side stream, concurrent with the exchange and the
         // cell rebuild (joined at the end of mardyn_dd_end_step_async)
         CK(cudaEventRecord(ctx->ev_s0, s));
@@ -1501,6 +1539,10 @@ int mardyn_dd_begin_step_async(mardyn_ctx* ctx)
         k_integrate<false, true><<<nkb, 256, 0, s>>>((int)ctx->cap, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
                                                      nullptr, nullptr, ctx->force, ctx->torque, ctx->cell_of,
                                                      ctx->rank, ctx->count, ctx->kpart, ctx->flag, dd);
+    if (ctx->direct) {
+        k_put_counts<<<1, 32, 0, s>>>(ctx->nranks, ctx->send_cnt, ctx->put_cnt);
+        ctx->launches += 1;
+    }
     k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, nkb, ctx->kpart, ctx->ndof,
                                                   ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket, 0);
     ctx->launches += 3;

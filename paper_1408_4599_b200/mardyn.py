@@ -30,6 +30,7 @@ EXPORTS = ["mardyn_create", "mardyn_get_grid", "mardyn_workspace_bytes", "mardyn
            "mardyn_launch_count", "mardyn_cell_cost", "mardyn_kd_decompose",
            "mardyn_set_decomposition", "mardyn_dd_begin_step", "mardyn_dd_buffers", "mardyn_dd_end_step",
            "mardyn_dd_set_segment", "mardyn_dd_set_peer_segments", "mardyn_dd_device_counts",
+           "mardyn_dd_set_peer_targets",
            "mardyn_dd_begin_step_async",
            "mardyn_dd_end_step_async",
            "mardyn_set_thermostat", "mardyn_lj_tail", "mardyn_get_tail_corrections",
@@ -116,6 +117,7 @@ def load_library():
     lib.mardyn_dd_set_segment.argtypes = [vp, C.c_int64]
     lib.mardyn_dd_set_peer_segments.argtypes = [vp, vp, vp]
     lib.mardyn_dd_device_counts.argtypes = [vp, P(vp), P(vp)]
+    lib.mardyn_dd_set_peer_targets.argtypes = [vp, vp, vp]
     lib.mardyn_dd_begin_step_async.argtypes = [vp]
     lib.mardyn_dd_end_step_async.argtypes = [vp]
     lib.mardyn_get_raw.argtypes = [vp, C.c_int64, vp, vp, vp]
@@ -347,6 +349,17 @@ class Context:
         self._check(self.lib.mardyn_dd_set_peer_segments(self.h, sc.ctypes.data_as(C.c_void_p),
                                                          rc.ctypes.data_as(C.c_void_p)))
 
+    def dd_set_peer_targets(self, rec_addrs, cnt_addrs):
+        """Direct puts (include/mardyn.h): device addresses, per destination rank, of this
+        rank's receive segment and count entry in that rank's buffers; None: transport."""
+        if rec_addrs is None:
+            self._check(self.lib.mardyn_dd_set_peer_targets(self.h, None, None))
+            return
+        ra = np.ascontiguousarray(np.asarray(rec_addrs, dtype=np.uint64))
+        ca = np.ascontiguousarray(np.asarray(cnt_addrs, dtype=np.uint64))
+        self._check(self.lib.mardyn_dd_set_peer_targets(self.h, ra.ctypes.data_as(C.c_void_p),
+                                                        ca.ctypes.data_as(C.c_void_p)))
+
     def dd_device_counts(self):
         """(send_cnt, recv_cnt): int32 [nranks] tensor views of the workspace (zero copy)."""
         sc = C.c_void_p(); rc = C.c_void_p()
@@ -520,7 +533,7 @@ class DecomposedRun:
     torch.distributed all_to_all over NCCL (NVLink)."""
 
     def __init__(self, system, nranks, transport="loopback", rank=None, eta=None, boxes=None, stream=None,
-                 rebalance_interval=0, async_exchange=True):
+                 rebalance_interval=0, async_exchange=True, direct=False):
         import torch
         self.torch = torch
         # one stream for every local context and the transport: the asynchronous step
@@ -528,6 +541,12 @@ class DecomposedRun:
         self.stream = stream if stream is not None else torch.cuda.Stream()
         stream = self.stream
         self.async_exchange = bool(async_exchange)
+        # device-initiated exchange: the packing kernels store the records straight into the
+        # receiving contexts' buffers (loopback: same device; across GPUs this needs peer
+        # pointers, e.g. symmetric memory, and a cross-device barrier -- not built)
+        if direct and transport != "loopback":
+            raise ValueError("direct puts are implemented for the loopback transport only")
+        self.direct = bool(direct) and self.async_exchange
         self.seg_ready = False
         self.system = system
         self.nranks = nranks
@@ -675,13 +694,23 @@ class DecomposedRun:
         self.bufs = [c.dd_buffers() for c in self.ctxs]
         self.flat = [(sb.reshape(-1, sb.shape[-1]), rv) for sb, rv in self.bufs]   # [records, bytes] views
         self.cnts = [c.dd_device_counts() for c in self.ctxs]
+        self.puts = False
+        if self.direct:
+            rb = int(self.flat[0][1].shape[-1])
+            for src, c in enumerate(self.ctxs):
+                rec = [self.flat[dst][1].data_ptr() + rb * int(sum(self.recv_caps[dst][:src])) for dst in range(p)]
+                cnt = [self.cnts[dst][1].data_ptr() + 4 * src for dst in range(p)]
+                c.dd_set_peer_targets(rec, cnt)
+            self.puts = True
         self.seg_ready = True
 
     def _step_async(self):
         p = self.nranks
         for c in self.ctxs:
             c.dd_begin_step_async()
-        if self.transport == "loopback":
+        if self.puts:
+            pass                       # records and counts already stored by the packing kernels
+        elif self.transport == "loopback":
             soff = [np.concatenate([[0], np.cumsum(sc)[:-1]]) for sc in self.send_caps]
             roff = [np.concatenate([[0], np.cumsum(rc)[:-1]]) for rc in self.recv_caps]
             for dst in range(p):

@@ -94,3 +94,22 @@ def test_rebalance_droplet(md):
     d = m["r"] - m1["r"]
     d -= np.asarray(ctx1.get_grid()["box"]) * np.round(d / np.asarray(ctx1.get_grid()["box"]))
     assert np.abs(d).max() <= 1e-5
+
+
+@pytest.mark.parametrize("name,p", [("c1s", 4), ("c2s", 3), ("c4s", 8)])
+def test_direct_puts_equal_transport(md, name, p):
+    """Device-initiated exchange: the packing kernels store each record straight into
+    the receiving context's segment and the counts into its count array (no transport
+    step); the records land where the transport would put them, so the run is bitwise
+    the one with the segment copies."""
+    s = S.config(name)
+    out = []
+    for direct in (False, True):
+        run = md.DecomposedRun(s, p, transport="loopback", direct=direct)
+        run.step(8)
+        assert run.puts == direct
+        m = run.molecules()
+        out.append((m["r"].copy(), m["v"].copy(), m["q"].copy(), run.observables()))
+    for a, b in zip(out[0][:3], out[1][:3]):
+        assert np.array_equal(a, b)
+    assert out[0][3] == out[1][3]
