@@ -51,6 +51,9 @@ def parse():
     # test hook: gloo instead of NCCL (ranks may then share a GPU; exercises the N > 1
     # orchestration on a one-GPU box -- not a performance configuration)
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    # N > 1: device-initiated exchange (records stored into the peers' symmetric-memory
+    # buffers by the packing kernels, device barriers) instead of the NCCL all-to-alls
+    p.add_argument("--direct", action="store_true")
     return p.parse_args()
 
 
@@ -304,7 +307,8 @@ def main():
         # spatial k-d decomposition (§4) with halo exchange and
         # migration over NCCL every step; one rank per GPU
         with torch.cuda.stream(stream):
-            run = mardyn.DecomposedRun(system, world, transport="nccl", rank=rank, stream=stream)
+            run = mardyn.DecomposedRun(system, world, transport="nccl", rank=rank, stream=stream,
+                                       direct=args.direct)
         ctx = run.ctxs[0]
         stepper = run.step
     else:

@@ -219,11 +219,15 @@ class Context:
             msg = self.lib.mardyn_last_error(self.h).decode() if self.h else ""
             raise MardynError(rc, msg)
 
-    def reserve(self, capacity):
-        """Allocate the device workspace through PyTorch (caching allocator)."""
+    def reserve(self, capacity, alloc=None):
+        """Allocate the device workspace through PyTorch (caching allocator, or alloc(nbytes),
+        e.g. symmetric memory that peers can address)."""
         nbytes = C.c_size_t()
         self._check(self.lib.mardyn_workspace_bytes(self.h, int(capacity), C.byref(nbytes)))
-        self.ws = self.torch.empty(nbytes.value + 256, dtype=self.torch.uint8, device="cuda")
+        if alloc is not None:
+            self.ws = alloc(nbytes.value + 256)
+        else:
+            self.ws = self.torch.empty(nbytes.value + 256, dtype=self.torch.uint8, device="cuda")
         ptr = self.ws.data_ptr()
         ptr += (-ptr) % 256
         self._check(self.lib.mardyn_set_workspace(self.h, C.c_void_p(ptr), nbytes.value, int(capacity)))
@@ -463,6 +467,18 @@ def global_costs(system):
     return cell_cost(counts)
 
 
+def peer_target_addrs(me, bases, rows, record_bytes):
+    """Direct puts (include/mardyn.h mardyn_dd_set_peer_targets): device addresses, per
+    destination rank d, of rank me's receive segment and count entry in d's buffers.
+    bases[d]: base address of d's (symmetric) allocation; rows[d] = [receive buffer offset,
+    count array offset (bytes, from bases[d]), then d's receive segment offsets (records)
+    per source rank].  Loopback: bases = 0 and absolute addresses."""
+    p = len(bases)
+    rec = [int(bases[d]) + int(rows[d][0]) + record_bytes * int(rows[d][2 + me]) for d in range(p)]
+    cnt = [int(bases[d]) + int(rows[d][1]) + 4 * me for d in range(p)]
+    return rec, cnt
+
+
 def exchange_records(send, cnt, recv, nranks, dist):
     """Halo/migration transport between ranks:
     send[d, :cnt[d]] goes to rank d; records from all ranks land contiguously
@@ -542,11 +558,21 @@ class DecomposedRun:
         stream = self.stream
         self.async_exchange = bool(async_exchange)
         # device-initiated exchange: the packing kernels store the records straight into the
-        # receiving contexts' buffers (loopback: same device; across GPUs this needs peer
-        # pointers, e.g. symmetric memory, and a cross-device barrier -- not built)
-        if direct and transport != "loopback":
-            raise ValueError("direct puts are implemented for the loopback transport only")
+        # receiving contexts' buffers -- loopback: same device, ordered by the stream; NCCL
+        # ranks: workspaces in symmetric memory (peer pointers over NVLink) and a device
+        # barrier before the puts and before the import of every step
         self.direct = bool(direct) and self.async_exchange
+        self.symm = None
+        alloc = None
+        if self.direct and transport != "loopback":
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm
+            try:
+                symm.enable_symm_mem_for_group(dist.group.WORLD.group_name)
+            except Exception:
+                pass
+            dev = torch.device("cuda", torch.cuda.current_device())
+            alloc = lambda nb: symm.empty(nb, dtype=torch.uint8, device=dev)
         self.seg_ready = False
         self.system = system
         self.nranks = nranks
@@ -573,7 +599,11 @@ class DecomposedRun:
             # at least the global count; twice that holds owned + halo + received records of
             # small boxes whose halo is as large as the box; the asynchronous step's
             # capacity-wide grids exit early past the rank's molecules
-            ctx.reserve(2 * len(system["r"]))
+            ctx.reserve(2 * len(system["r"]), alloc=alloc)
+            if alloc is not None:
+                import torch.distributed as dist
+                import torch.distributed._symmetric_memory as symm
+                self.symm = symm.rendezvous(ctx.ws, dist.group.WORLD)
             ctx.set_molecules(system["r"], system["v"], comp=system["comp"], q=system["q"], j=system["j"],
                               id=system["id"], half_step=0)
             self.ctxs.append(ctx)
@@ -697,19 +727,35 @@ class DecomposedRun:
         self.puts = False
         if self.direct:
             rb = int(self.flat[0][1].shape[-1])
-            for src, c in enumerate(self.ctxs):
-                rec = [self.flat[dst][1].data_ptr() + rb * int(sum(self.recv_caps[dst][:src])) for dst in range(p)]
-                cnt = [self.cnts[dst][1].data_ptr() + 4 * src for dst in range(p)]
-                c.dd_set_peer_targets(rec, cnt)
+            offs = lambda caps: [int(sum(caps[:r])) for r in range(p)]
+            if self.transport == "loopback":
+                rows = [[self.flat[d][1].data_ptr(), self.cnts[d][1].data_ptr()] + offs(self.recv_caps[d])
+                        for d in range(p)]
+                for src, c in enumerate(self.ctxs):
+                    c.dd_set_peer_targets(*peer_target_addrs(src, [0] * p, rows, rb))
+            else:
+                import torch.distributed as dist
+                bases = list(self.symm.buffer_ptrs)
+                mine = [self.flat[0][1].data_ptr() - bases[self.rank],
+                        self.cnts[0][1].data_ptr() - bases[self.rank]] + offs(self.recv_caps[0])
+                t = torch.tensor(mine, dtype=torch.int64, device="cuda")
+                allt = [torch.empty_like(t) for _ in range(p)]
+                dist.all_gather(allt, t)
+                rows = [x.tolist() for x in allt]
+                self.ctxs[0].dd_set_peer_targets(*peer_target_addrs(self.rank, bases, rows, rb))
             self.puts = True
         self.seg_ready = True
 
     def _step_async(self):
         p = self.nranks
+        if self.puts and self.symm is not None:
+            self.symm.barrier(channel=0)       # every rank's last import done: its buffers are free
         for c in self.ctxs:
             c.dd_begin_step_async()
         if self.puts:
-            pass                       # records and counts already stored by the packing kernels
+            # records and counts already stored by the packing kernels (peers: after the barrier)
+            if self.symm is not None:
+                self.symm.barrier(channel=0)
         elif self.transport == "loopback":
             soff = [np.concatenate([[0], np.cumsum(sc)[:-1]]) for sc in self.send_caps]
             roff = [np.concatenate([[0], np.cumsum(rc)[:-1]]) for rc in self.recv_caps]

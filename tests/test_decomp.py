@@ -278,3 +278,51 @@ def test_droplet_kd_beats_static_split():
               for z0, z1 in zip(cuts[2], cuts[2][1:])]
         static = max(st) / np.mean(st)
         assert kd < 1.25 and static > 1.5 * kd, (p, kd, static)
+
+
+def _puts_main(rank, world, port, result):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rb = 64
+    caps = [[6, 3, 5], [2, 7, 4], [9, 1, 8]]                 # caps[src][dst]: per-peer segments
+    recv_caps = [caps[s][rank] for s in range(world)]
+    bases = [(d + 1) << 40 for d in range(world)]            # each rank's symmetric allocation
+    recv_off, cnt_off = 4096 * (rank + 1), 256 * (rank + 3)  # layouts may differ per rank
+    mine = [recv_off, cnt_off] + [sum(recv_caps[:s]) for s in range(world)]
+    t = torch.tensor(mine, dtype=torch.int64)
+    allt = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(allt, t)
+    rec, cnt = M.peer_target_addrs(rank, bases, [x.tolist() for x in allt], rb)
+    got = [torch.empty(2 * world, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(got, torch.tensor(rec + cnt, dtype=torch.int64))
+    # where every source's records and count land in this rank's buffers
+    result[rank] = (mine, [g.tolist() for g in got])
+    dist.destroy_process_group()
+
+
+def test_gloo_direct_put_targets():
+    """Direct puts across ranks (DecomposedRun(direct=True) over NCCL, peer pointers of
+    symmetric memory): the addresses rank src stores to for rank d -- its base plus d's
+    receive-buffer offset plus d's segment offset for src, and d's count entry src -- are
+    exactly where d's import reads source src (world_size 3, gloo, per-peer segments,
+    different layouts per rank)."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    mgr = mp.Manager()
+    result = mgr.dict()
+    mp.spawn(_puts_main, args=(3, port, result), nprocs=3, join=True)
+    caps = [[6, 3, 5], [2, 7, 4], [9, 1, 8]]
+    for d in range(3):
+        mine, got = result[d]
+        base = (d + 1) << 40
+        assert mine[0] == 4096 * (d + 1) and mine[1] == 256 * (d + 3)
+        for src in range(3):
+            seg_off = sum(caps[s][d] for s in range(src))
+            assert got[src][d] == base + mine[0] + 64 * seg_off
+            assert got[src][3 + d] == base + mine[1] + 4 * src
