@@ -113,3 +113,40 @@ def test_direct_puts_equal_transport(md, name, p):
     for a, b in zip(out[0][:3], out[1][:3]):
         assert np.array_equal(a, b)
     assert out[0][3] == out[1][3]
+
+
+_SYMM_SCRIPT = r'''
+import os, torch, torch.distributed as dist
+import torch.distributed._symmetric_memory as symm
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+try:
+    symm.enable_symm_mem_for_group(dist.group.WORLD.group_name)
+except Exception:
+    pass
+t = symm.empty(1 << 20, dtype=torch.uint8, device=torch.device("cuda", 0))
+h = symm.rendezvous(t, dist.group.WORLD)
+base = list(h.buffer_ptrs)[0]
+assert 0 <= t.data_ptr() - base < (1 << 20), (t.data_ptr(), base)
+t.fill_(7)
+h.barrier(channel=0)
+torch.cuda.synchronize()
+print("SYMM_OK", t.data_ptr() - base)
+dist.destroy_process_group()
+'''
+
+
+def test_symmetric_memory_plumbing():
+    """The calls the multi-GPU direct puts rely on (DecomposedRun(direct=True) over NCCL):
+    a symmetric allocation, its rendezvous, the peer base pointers and the device barrier --
+    on one rank (a barrier that waits on no other rank)."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    out = subprocess.run([sys.executable, "-c", _SYMM_SCRIPT], capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0 and "SYMM_OK" in out.stdout, (out.stdout[-1000:], out.stderr[-2000:])
