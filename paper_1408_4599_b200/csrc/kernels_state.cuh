@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(1024) k_scan(int ncell, int* __restrict__ coun
 __global__ void k_scatter(int n, const uint4* __restrict__ pos, const int* __restrict__ cell_of,
                           const int* __restrict__ rank, const int* __restrict__ start,
                           unsigned long long* __restrict__ keys, int* __restrict__ oldidx,
+                          int* __restrict__ slot_cell,
                           const int* __restrict__ n_dev = nullptr)
 {
     if (n_dev) n = *n_dev;                  // asynchronous decomposed step: count on the device
@@ -210,6 +211,7 @@ __global__ void k_scatter(int n, const uint4* __restrict__ pos, const int* __res
         const uint4 p = pos[i];
         keys[slot] = ((unsigned long long)p.x << 32) | p.w;
         oldidx[slot] = i;
+        slot_cell[slot] = cl;               // the gather reads it coalesced (no dependent load)
     }
 }
 
@@ -221,7 +223,7 @@ __global__ void k_scatter(int n, const uint4* __restrict__ pos, const int* __res
 // rigid models, the world-frame site offsets s = R(q) d.
 template <bool RIGID>
 __device__ __forceinline__ void canon_one(int t, int cap, const GridP& g, const unsigned long long* __restrict__ keys,
-                        const int* __restrict__ oldidx, const int* __restrict__ cell_of,
+                        const int* __restrict__ oldidx, const int* __restrict__ slot_cell,
                         const int* __restrict__ start,
                         const uint4* __restrict__ pos_s, const float4* __restrict__ vel_s,
                         const float4* __restrict__ quat_s, const float4* __restrict__ angm_s,
@@ -232,7 +234,7 @@ __device__ __forceinline__ void canon_one(int t, int cap, const GridP& g, const 
 {
     const unsigned long long key = keys[t];
     const int old = oldidx[t];
-    int c = cell_of[old];
+    int c = slot_cell[t];
     int s0 = start[c], s1 = start[c + 1];
     int r = 0;
     for (int m = s0; m < s1; ++m) r += keys[m] < key;
@@ -277,7 +279,7 @@ __device__ __forceinline__ void canon_one(int t, int cap, const GridP& g, const 
 // capacity-independent grid)
 template <bool RIGID>
 __global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __restrict__ keys,
-                        const int* __restrict__ oldidx, const int* __restrict__ cell_of,
+                        const int* __restrict__ oldidx, const int* __restrict__ slot_cell,
                         const int* __restrict__ start,
                         const uint4* __restrict__ pos_s, const float4* __restrict__ vel_s,
                         const float4* __restrict__ quat_s, const float4* __restrict__ angm_s,
@@ -288,7 +290,7 @@ __global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __res
 {
     const int lim = min(n, start[g.ncell]);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < lim; t += gridDim.x * blockDim.x)
-        canon_one<RIGID>(t, cap, g, keys, oldidx, cell_of, start, pos_s, vel_s, quat_s, angm_s, pos_d, vel_d,
+        canon_one<RIGID>(t, cap, g, keys, oldidx, slot_cell, start, pos_s, vel_s, quat_s, angm_s, pos_d, vel_d,
                          quat_d, angm_d, xs, site, model);
 }
 

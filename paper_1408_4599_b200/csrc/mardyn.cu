@@ -454,14 +454,14 @@ static int enqueue_sort(mardyn_ctx* ctx, int src, int dst, int64_t n_unsorted = 
     k_scan<<<ctx->ntiles, 1024, 0, s>>>(ncell, ctx->count, ctx->start, ctx->scan_flags,
                                         reinterpret_cast<unsigned*>(ctx->scan_flags + ctx->ntiles), ctx->blk_ctr);
     k_scatter<<<gb, 256, 0, s>>>(n, ctx->pos[src], ctx->cell_of, ctx->rank, ctx->start, ctx->keys,
-                                            ctx->oldidx, n_dev);
+                                            ctx->oldidx, ctx->oldidx + ctx->cap, n_dev);
     if (ctx->rigid)
-        k_canon<true><<<gb, 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->oldidx, ctx->cell_of, ctx->start,
+        k_canon<true><<<gb, 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->oldidx, ctx->oldidx + ctx->cap, ctx->start,
                                                    ctx->pos[src], ctx->vel[src], ctx->quat[src], ctx->angm[src],
                                                    ctx->pos[dst], ctx->vel[dst], ctx->quat[dst], ctx->angm[dst],
                                                    ctx->xs, ctx->site, ctx->dmodel);
     else
-        k_canon<false><<<gb, 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->oldidx, ctx->cell_of, ctx->start,
+        k_canon<false><<<gb, 256, 0, s>>>(n, (int)ctx->cap, ctx->g, ctx->keys, ctx->oldidx, ctx->oldidx + ctx->cap, ctx->start,
                                                     ctx->pos[src], ctx->vel[src], nullptr, nullptr,
                                                     ctx->pos[dst], ctx->vel[dst], nullptr, nullptr, ctx->xs,
                                                     nullptr, ctx->dmodel);
@@ -713,7 +713,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     int* cell_of = (int*)take(4 * cap);
     int* rank = (int*)take(4 * cap);
     unsigned long long* keys = (unsigned long long*)take(8 * cap);
-    int* oldidx = (int*)take(4 * cap);
+    int* oldidx = (int*)take(8 * cap);               // [0, cap) unsorted index, [cap, 2 cap) cell of the slot
     int* count = (int*)take(4 * (size_t)ncell_pad);
     int* start = (int*)take(4 * ((size_t)ncell + 1));
     unsigned long long* scan_flags = (unsigned long long*)take(8 * (size_t)(std::max(ntiles, 1) + 1));
