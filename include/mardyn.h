@@ -124,7 +124,7 @@ int mardyn_get_grid(const struct mardyn_ctx* ctx, mardyn_grid* out);
 /* Device bytes needed for up to n_capacity molecules.                      */
 int mardyn_workspace_bytes(struct mardyn_ctx* ctx, int64_t n_capacity, size_t* bytes);
 
-/* Hand the context a device buffer (16-byte aligned) of at least
+/* Hand the context a device buffer (256-byte aligned; MARDYN_EINVAL otherwise) of at least
  * mardyn_workspace_bytes(n_capacity) bytes; must precede set_molecules.     */
 int mardyn_set_workspace(struct mardyn_ctx* ctx, void* device_ptr, size_t bytes,
                          int64_t n_capacity);

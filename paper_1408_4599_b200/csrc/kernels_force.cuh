@@ -2,7 +2,7 @@
 // every site kind, runtime site counts; hot loop of the method: "the largest
 // part of the computational cost is caused by the force and distance
 // calculations"; linked cells P:134-155), and the row helpers
-// it shares with the packed single-component kernel (kernels_rigid.cuh).  The
+// it shares with the packed single-component kernel (kernels_rigid3.cuh, packed2.cuh).  The
 // single-site LJ kernel is in kernels_lj1.cuh.
 //
 // Work decomposition.  Persistent grid; each warp owns a

@@ -26,7 +26,7 @@
 #pragma once
 #include "common.cuh"
 #include "kernels_force.cuh"
-#include "kernels_rigid.cuh"
+#include "packed2.cuh"
 
 namespace rig3 {
 
@@ -40,28 +40,21 @@ constexpr int CAP = MD_RIG3_CAP;      // staged molecules per chunk of the neigh
 constexpr int WARPS = MD_RIG3_WARPS;
 constexpr int HCAP = 256;             // hit-list entries per group
 constexpr int NHMAX = 64;             // home molecules per batch (force/torque accumulators)
-#ifndef MD_RIG3_WIN
-// x-windows in the distance phase (1), or every staged molecule (0, default): the windows cut the
-// tested pairs by 45 % (c2 412 -> 226 per round) but measured 6 % (c2) / 3 % (c3) slower -- the
-// walk over nine ranges adds 30 % to the distance step and more spills
-#define MD_RIG3_WIN 0
-#endif
-constexpr int WB = 32;                // x-buckets per staged row (window bounds by table lookup)
 
-using rig2::P2;
-using rig2::V3;
-using rig2::p2;
-using rig2::v3zero;
-using rig2::bcast;
-using rig2::pack;
-using rig2::dot;
+using pk2::P2;
+using pk2::V3;
+using pk2::p2;
+using pk2::v3zero;
+using pk2::bcast;
+using pk2::pack;
+using pk2::dot;
 
 // charge-charge with reaction field (A4) without the constant c_rf, which the caller
 // subtracts per partner as c_rf (sum_a q_a)(sum_b q_b) -- zero for neutral molecules
 __device__ __forceinline__ void qq_nocrf(V3 r, P2 qq, float krf, P2& u, V3& fa, V3& fh)
 {
     const P2 r2 = dot(r, r);
-    const P2 ir = rig2::rsqrt2(r2);
+    const P2 ir = pk2::rsqrt2(r2);
     const P2 ir2 = ir * ir;
     u = fma(qq, fma(p2(krf), r2, ir), u);
     const P2 fr = qq * fma(ir, ir2, p2(-2.f * krf));
@@ -73,7 +66,7 @@ __device__ __forceinline__ void qq_nocrf(V3 r, P2 qq, float krf, P2& u, V3& fa, 
 __device__ __forceinline__ void lj_noshift(V3 r, float sig2, float eps24, float eps4, P2& u, V3& fa, V3& fh)
 {
     const P2 r2 = dot(r, r);
-    const P2 ir2 = rig2::rcp2(r2);
+    const P2 ir2 = pk2::rcp2(r2);
     const P2 s2 = sig2 * ir2;
     const P2 s6 = s2 * s2 * s2;
     const P2 fr = (eps24 * ir2) * s6 * fma(p2(2.f), s6, p2(-1.f));
@@ -88,7 +81,7 @@ constexpr int smem_bytes()
     // COM pairs (CAP/2 + 1 pairs x 24 B, +1: the far dummy pair), NSLOT x (CAP + 1) site float4,
     // hit lists, accumulators, row table
     return (CAP / 2 + 1) * 16 + ((CAP / 2 + 2) & ~1) * 8 + (NLJ + NQ + 2 * NMU + 2 * NQQ) * (CAP + 1) * 16 + WARPS * 2 * 2 * (HCAP + 2) * 2 +
-           NHMAX * 8 * 4 + WARPS * 2 * 8 * 4 + 16 * 8 * 4 + (MD_RIG3_WIN ? WARPS * 2 * 9 * 8 + 9 * (WB + 1) * 2 + 16 : 0);
+           NHMAX * 8 * 4 + WARPS * 2 * 8 * 4 + 16 * 8 * 4;
 }
 
 template <int NLJ, int NQ, int NMU, int NQQ>
@@ -115,10 +108,6 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
     float* acc = reinterpret_cast<float*>(hls + 2 * WARPS * 2 * (HCAP + 2));         // [NHMAX][8]: F, tau
     float* tacc = acc + NHMAX * 8;                                         // [NG][8]: tail slices (F, tau)
     int* rinfo = reinterpret_cast<int*>(tacc + 2 * WARPS * 8);             // [9][8] row table + [72..]: totals
-#if MD_RIG3_WIN
-    int2* wtab = reinterpret_cast<int2*>(rinfo + 16 * 8);                  // [NG][9] window pair ranges
-    uint16_t* btab = reinterpret_cast<uint16_t*>(wtab + 2 * WARPS * 9);    // [9][WB + 1] bucket starts
-#endif
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
     const int half = lane >> 4, gl = lane & 15;
     const int grp = 2 * wib + half, NG = 2 * WARPS;
@@ -226,26 +215,6 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                     }
                 }
                 __syncthreads();
-#if MD_RIG3_WIN
-                // ---- x-bucket table of the staged rows: btab[r][b] = first element of row r (in this
-                //      chunk) with X >= -edge + b * 3 edge / WB (rows are x-sorted; X in [-edge, 2 edge))
-                for (int q = tid; q < 9 * (WB + 1); q += WARPS * 32) {
-                    const int r = q / (WB + 1), b = q - r * (WB + 1);
-                    const int rg = rinfo[8 * r + 6];
-                    const int rs = min(max(rg - k0, 0), mm);
-                    const int re = min(max(rg + rinfo[8 * r + 3] + rinfo[8 * r + 4] + rinfo[8 * r + 5] - k0, 0), mm);
-                    const float xb = -g.edge[0] + (float)b * (3.f / WB) * g.edge[0];
-                    int b0 = rs, n = re - rs;
-                    if (b == 0) n = 0;
-                    if (b == WB) { b0 = re; n = 0; }
-                    while (n > 0) {
-                        const int h = n >> 1, k = b0 + h;
-                        if (cxf[4 * (k >> 1) + (k & 1)] < xb) { b0 = k + 1; n -= h + 1; } else n = h;
-                    }
-                    btab[q] = (uint16_t)b0;
-                }
-                __syncthreads();
-#endif
                 // ---- home molecules of this batch, two per group at a time (A, B): the distance
                 //      phase tests each staged molecule against both (one load, two tests)
                 const int npair = (mm + 1) >> 1;
@@ -388,7 +357,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
             const V3 eb = (STB == 2) ? slot3((slb + 1) % NSLOT, j0, j1) : v3zero();                        \
             const V3 rv = V3{d.x + pb.x - pa.x, d.y + pb.y - pa.y, d.z + pb.z - pa.z};                     \
             V3 tdummy = v3zero();                                                                          \
-            rig2::polar2<KA, KB>(rv, ea, eb, pa4.w * slotw(slb, j0, j1), kmm, uacc, fs[FIDX + ia],         \
+            pk2::polar2<KA, KB>(rv, ea, eb, pa4.w * slotw(slb, j0, j1), kmm, uacc, fs[FIDX + ia],         \
                                  (TIDX) >= 0 ? ts[((TIDX) >= 0 ? (TIDX) : 0) + ia] : tdummy, fh);        \
         }                                                                                                  \
     }
@@ -468,78 +437,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                     const float2 nxB = make_float2(-xiB.x, -xiB.x), nyB = make_float2(-xiB.y, -xiB.y),
                                  nzB = make_float2(-xiB.z, -xiB.z);
                     const float hiA = gA ? g.cut2_hi : -1.f, hiB = gB ? g.cut2_hi : -1.f;   // idle: no hits
-#if MD_RIG3_WIN
-                    // ---- x-windows.  A staged row (cells x-1, x, x+1 of one (dy, dz), canonical order)
-                    //      is sorted by x, so a partner of A or B in row r lies in |X - x| < w_r,
-                    //      w_r^2 = rc^2 - Dy^2 - Dz^2 (Dy, Dz: distance to the row's y / z extent; a
-                    //      necessary condition, taken with a generous rc^2).  Lanes 0..8 of a group bound
-                    //      row gl's elements by two binary searches; the rows' pair ranges (elements 2p,
-                    //      2p + 1) are made disjoint (a pair spanning two rows stays with the first) and
-                    //      walked as one virtual sequence [0, T).
-                    int2* wt = wtab + 9 * grp;
-                    {
-                        int wlo = 0, whi = 0;
-                        if (gl < 9) {
-                            const int dy = gl % 3 - 1, dz = gl / 3 - 1;
-                            const float rc2w = g.cut2_hi * (1.f + 1.f / 4096.f);
-                            float xl = 3.0e38f, xh = -3.0e38f;
-                            auto widen = [&](bool on, float4 xi) {
-                                const float Dy = dy == 0 ? 0.f : (dy > 0 ? g.edge[1] - xi.y : xi.y);
-                                const float Dz = dz == 0 ? 0.f : (dz > 0 ? g.edge[2] - xi.z : xi.z);
-                                const float w2 = rc2w - Dy * Dy - Dz * Dz;
-                                if (on && w2 > 0.f) {
-                                    const float w = sqrtf(w2);
-                                    xl = fminf(xl, xi.x - w);
-                                    xh = fmaxf(xh, xi.x + w);
-                                }
-                            };
-                            widen(gA, xiA);
-                            widen(gB, xiB);
-                            // buckets holding the bounds, rounded outward by 1e-3 bucket (>> rounding)
-                            const float sc = (float)WB / (3.f * g.edge[0]);
-                            const uint16_t* bt = btab + gl * (WB + 1);
-                            if (xl <= xh) {
-                                const int bl = min(max(__float2int_rd(fmaf(xl + g.edge[0], sc, -1e-3f)), 0), WB);
-                                const int bh = min(max(__float2int_rd(fmaf(xh + g.edge[0], sc, 1e-3f)) + 1, 0), WB);
-                                wlo = bt[bl];
-                                whi = max((int)bt[bh], wlo);
-                            } else {
-                                wlo = whi = bt[0];
-                            }
-                        }
-                        int plo = wlo >> 1, phi = whi > wlo ? (whi + 1) >> 1 : plo;
-                        int m = gl < 9 ? phi : 0;                         // exclusive max-scan of phi over rows
-#pragma unroll
-                        for (int o = 1; o < 16; o <<= 1) {
-                            const int t = __shfl_up_sync(FULL, m, o, 16);
-                            if (gl >= o) m = max(m, t);
-                        }
-                        const int mprev = __shfl_up_sync(FULL, m, 1, 16);
-                        if (gl > 0) plo = max(plo, mprev);
-                        phi = max(phi, plo);
-                        if (gl < 9) wt[gl] = make_int2(plo, phi);
-                    }
-                    __syncwarp();
-                    int tot = gl < 9 ? wt[gl].y - wt[gl].x : 0;
-#pragma unroll
-                    for (int o = 1; o < 16; o <<= 1) tot += __shfl_xor_sync(FULL, tot, o, 16);
-                    // this group's slice [v0, v1) of the virtual sequence; the lane's walk (row wr, pair wp
-                    // of the row's range ending at we) starts at v0 + gl and advances by 16
-                    const int v0 = tail ? (int)((long long)(grp - (grp / P) * P) * tot / P) : 0;
-                    const int v1 = tail ? (int)((long long)(grp - (grp / P) * P + 1) * tot / P) : tot;
-                    int wr = 0, wp, we;
-                    {
-                        int v = v0 + gl;
-                        int2 t = wt[0];
-                        while (wr < 8 && v >= t.y - t.x) { v -= t.y - t.x; t = wt[++wr]; }
-                        wp = t.x + v;
-                        we = t.y;
-                    }
-                    int vc = v0 + gl;
-                    const int span = max(__shfl_sync(FULL, v1 - v0, 0), __shfl_sync(FULL, v1 - v0, 16));
-#else
                     const int span = max(__shfl_sync(FULL, p1 - p0, 0), __shfl_sync(FULL, p1 - p0, 16));
-#endif
                     unsigned below;
                     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(below));
                     auto append = [&](uint16_t* hl, int& cnt, bool h0, bool h1, int pp) {
@@ -555,20 +453,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                         for (; base < span; base += 32) {
 #pragma unroll
                             for (int u = 0; u < 2; ++u) {
-#if MD_RIG3_WIN
-                                const int pp = vc < v1 ? wp : CAP / 2;
-                                vc += 16;
-                                wp += 16;
-                                while (wp >= we && wr < 8) {
-                                    const int over = wp - we;
-                                    const int2 t = wt[++wr];
-                                    wp = t.x + over;
-                                    we = t.y;
-                                }
-#else
                                 const int p = p0 + base + 16 * u + gl;
                                 const int pp = p < p1 ? p : CAP / 2;
-#endif
                                 const float4 xy = cxy[pp];
                                 const float2 zz = pz[pp];
                                 const float2 xx = make_float2(xy.x, xy.y), yy = make_float2(xy.z, xy.w);

@@ -14,7 +14,6 @@
 #include "decomp.hpp"
 #include "kernels_force.cuh"
 #include "kernels_lj1.cuh"
-#include "kernels_rigid.cuh"
 #include "kernels_rigid3.cuh"
 #include "kernels_state.cuh"
 
@@ -46,10 +45,7 @@ using LJ1 = lj1::Cfg<LJ1_WARPS, LJ1_CAPP>;
 #define K_LJ1 lj1::k_force_lj1<LJ1_WARPS, LJ1_CAPP, MD_LJ1_MINB, false>
 #define K_LJ1_STEP lj1::k_force_lj1<LJ1_WARPS, LJ1_CAPP, MD_LJ1_MINB, true>
 #define K_LJ1_STEP_DD lj1::k_force_lj1<LJ1_WARPS, LJ1_CAPP, MD_LJ1_MINB, true, true>
-#ifndef MD_RIGID3
-#define MD_RIGID3 1                       // load-balanced rigid kernel (kernels_rigid3.cuh) for configs 2, 3
-#endif
-constexpr int RIG_WARPS = MD_RIGID3 ? rig3::WARPS : 4;
+constexpr int RIG_WARPS = rig3::WARPS;   // load-balanced rigid kernel (kernels_rigid3.cuh), configs 2, 3
 constexpr int GEN_WARPS = 1;
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -341,6 +337,10 @@ static int occupancy_grid(mardyn_ctx* ctx, K kernel, int threads, size_t smem = 
 // memory (start[ncell] of the last cell rebuild): fetch it before host-side use
 static int refresh_n(mardyn_ctx* ctx)
 {
+    if (ctx->side_join) {              // an asynchronous step's finalize still runs on the side stream
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_s1, 0));
+        ctx->side_join = false;
+    }
     if (!ctx->n_stale) return MARDYN_OK;
     int kept = 0, nf = 0;
     CK(cudaMemcpyAsync(&kept, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -381,20 +381,10 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_gra
     const int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ:
-        if (MD_RIGID3)
-            rig3::k_force_rigid3<2, 0, 0, 1>
-                <<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
-        else
-            rig2::k_force_rigid2<2, 0, 0, 1, RIG_WARPS>
-                <<<ctx->force_grid, threads, rig2::smem_bytes<2, 0, 0, 1, RIG_WARPS>(), ctx->stream>>>(a);
+        rig3::k_force_rigid3<2, 0, 0, 1><<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
         break;
     case SHAPE_TIP4P:
-        if (MD_RIGID3)
-            rig3::k_force_rigid3<1, 3, 0, 0>
-                <<<ctx->force_grid, threads, rig3::smem_bytes<1, 3, 0, 0>(), ctx->stream>>>(a);
-        else
-            rig2::k_force_rigid2<1, 3, 0, 0, RIG_WARPS>
-                <<<ctx->force_grid, threads, rig2::smem_bytes<1, 3, 0, 0, RIG_WARPS>(), ctx->stream>>>(a);
+        rig3::k_force_rigid3<1, 3, 0, 0><<<ctx->force_grid, threads, rig3::smem_bytes<1, 3, 0, 0>(), ctx->stream>>>(a);
         break;
     case SHAPE_GEN:
         k_force_rigid<4, 4, 2, 2, true, GEN_WARPS>
@@ -625,15 +615,15 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
     int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ: {
-        auto k = MD_RIGID3 ? rig3::k_force_rigid3<2, 0, 0, 1> : rig2::k_force_rigid2<2, 0, 0, 1, RIG_WARPS>;
-        const int sm = MD_RIGID3 ? rig3::smem_bytes<2, 0, 0, 1>() : rig2::smem_bytes<2, 0, 0, 1, RIG_WARPS>();
+        auto k = rig3::k_force_rigid3<2, 0, 0, 1>;
+        const int sm = rig3::smem_bytes<2, 0, 0, 1>();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         ctx->force_blocks = occupancy_grid(ctx, k, threads, sm);
         break;
     }
     case SHAPE_TIP4P: {
-        auto k = MD_RIGID3 ? rig3::k_force_rigid3<1, 3, 0, 0> : rig2::k_force_rigid2<1, 3, 0, 0, RIG_WARPS>;
-        const int sm = MD_RIGID3 ? rig3::smem_bytes<1, 3, 0, 0>() : rig2::smem_bytes<1, 3, 0, 0, RIG_WARPS>();
+        auto k = rig3::k_force_rigid3<1, 3, 0, 0>;
+        const int sm = rig3::smem_bytes<1, 3, 0, 0>();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         ctx->force_blocks = occupancy_grid(ctx, k, threads, sm);
         break;
@@ -855,16 +845,18 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
         if (ctx->nranks == 1) {
             // (single-site: half blocks of 16 when there are fewer 32-blocks than warps)
             const int64_t units = ctx->kernel == KER_LJ1 ? (n + 15) / 16 : (int64_t)ctx->g.nhome;
-            const int upb = (ctx->kernel == KER_RIGID && MD_RIGID3) ? 1 : ctx->force_warps_per_block;   // rig3: CTA per cell
+            const int upb = ctx->kernel == KER_RIGID ? 1 : ctx->force_warps_per_block;   // rig3: CTA per cell
             const int64_t need = (units + upb - 1) / upb;
             grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, need));
         }
         if (grid != ctx->force_grid) {
             ctx->force_grid = grid;
             CK(cudaMemsetAsync(ctx->fpart, 0, sizeof(ForcePartial) * ctx->nfpart, s));
-            for (int b = 0; b < 2; ++b)                   // the step graphs hold the launch shape
-                if (ctx->gexec[b]) { cudaGraphExecDestroy(ctx->gexec[b]); ctx->gexec[b] = nullptr; }
         }
+        // the step graphs hold the launch shape, the molecule count n and N_dof: rebuilt after
+        // every reload (a graph of the previous n would scatter stale or too few molecules)
+        for (int b = 0; b < 2; ++b)
+            if (ctx->gexec[b]) { cudaGraphExecDestroy(ctx->gexec[b]); ctx->gexec[b] = nullptr; }
     }
     // host -> device (the caller's buffers; pinned ones are DMA'd directly)
     double* dr = (double*)ctx->stage;
@@ -903,14 +895,15 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
     }
     long long step = ctx->host_step;
     CK(cudaMemcpyAsync(ctx->step_ctr, &step, 8, cudaMemcpyHostToDevice, s));
-    if (!half_step) {   // A8: backward half kick with F(t0), tau(t0)
+    if (!half_step) {   // A8: backward half kick with F(t0), tau(t0) of the molecules kept (ctx->n)
         launch_force(ctx, ctx->cur);
+        const int nk = (int)ctx->n;
         if (ctx->rigid)
-            k_half_kick<true><<<nblk(n, 256), 256, 0, s>>>((int)n, ctx->g, ctx->dmodel, ctx->vel[ctx->cur],
-                                                           ctx->angm[ctx->cur], ctx->force, ctx->torque);
+            k_half_kick<true><<<nblk(nk, 256), 256, 0, s>>>(nk, ctx->g, ctx->dmodel, ctx->vel[ctx->cur],
+                                                            ctx->angm[ctx->cur], ctx->force, ctx->torque);
         else
-            k_half_kick<false><<<nblk(n, 256), 256, 0, s>>>((int)n, ctx->g, ctx->dmodel, ctx->vel[ctx->cur],
-                                                            nullptr, ctx->force, nullptr);
+            k_half_kick<false><<<nblk(nk, 256), 256, 0, s>>>(nk, ctx->g, ctx->dmodel, ctx->vel[ctx->cur],
+                                                             nullptr, ctx->force, nullptr);
         ctx->launches += 1;
     }
     CK(cudaGetLastError());
