@@ -94,6 +94,8 @@ def lib():
         _lib.or_run_nvt.argtypes = [P(Sys), C.c_double, C.c_int64, C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int,
                                     C.c_int, C.c_int, C.c_double, C.c_int, P(Obs)]
+        _lib.or_run_cont.argtypes = [P(Sys), C.c_double, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, P(Obs)]
         _lib.or_lj_tail.argtypes = [P(Sys), C.c_void_p, C.c_double, C.c_void_p, C.c_void_p]
     return _lib
 
@@ -243,6 +245,25 @@ class System:
                        dtype=[("U", "f8"), ("W", "f8"), ("KEt", "f8"), ("KEr", "f8"),
                               ("T", "f8"), ("npairs", "i8")])
         return u, v, q, j, out
+
+    def run_continuous(self, dt, comp, r, v, q, j, nsteps, half_step=0, nthreads=0):
+        """The same steps on unquantised fp64 positions (no A12 lattice; brute-force
+        full shell, fp64 minimum image): the reference that bounds the effect of the
+        position quantum.  Returns (r, v, q, j, obs) like run()."""
+        comp = np.ascontiguousarray(comp, np.int32)
+        r = np.array(r, dtype=np.float64, order="C") % self.box
+        v = np.array(v, dtype=np.float64, order="C")
+        q = np.array(q, dtype=np.float64, order="C")
+        j = np.array(j, dtype=np.float64, order="C")
+        obs = (Obs * max(nsteps, 1))()
+        rc = lib().or_run_cont(C.byref(self.s), float(dt), len(r), _ptr(comp), _ptr(r), _ptr(v), _ptr(q),
+                               _ptr(j), int(nsteps), int(half_step), int(nthreads), obs)
+        if rc:
+            raise RuntimeError(f"or_run_cont failed ({rc})")
+        out = np.array([(o.U, o.W, o.KEt, o.KEr, o.T, o.npairs) for o in obs[:nsteps]],
+                       dtype=[("U", "f8"), ("W", "f8"), ("KEt", "f8"), ("KEr", "f8"),
+                              ("T", "f8"), ("npairs", "i8")])
+        return r, v, q, j, out
 
     def site_pair(self, a, ea, b, eb, rv, eta=1.0):
         """One site pair (Site structs, world axes, rv = x_b - x_a):

@@ -350,11 +350,10 @@ static void state_free(or_state* X) { free(X->sp); free(X->se); }
  *   *U, and returns the molecular virial term -rij.F_i in *w.
  * The force on j is -Fi.
  */
-static int mol_pair(const or_state* X, int64_t i, int64_t j, const int64_t dq[3],
-                    double* U, double* Fi, double* ti, double* tj, double* w)
+static int mol_pair_r(const or_state* X, int64_t i, int64_t j, const double rij[3],
+                      double* U, double* Fi, double* ti, double* tj, double* w)
 {
     const or_sys* S = X->S;
-    double rij[3] = {dq[0] * S->s, dq[1] * S->s, dq[2] * S->s};   /* exact */
     double r2 = dot(rij, rij);           /* exact when near rc (A12) */
     if (!(r2 < S->rc * S->rc)) return 0;
     const or_comp* Ci = &S->comp[X->comp[i]];
@@ -383,6 +382,15 @@ static int mol_pair(const or_state* X, int64_t i, int64_t j, const int64_t dq[3]
     for (int k = 0; k < 3; ++k) Fi[k] += Fsum[k];
     *w = -dot(rij, Fsum);                /* molecular virial, A6 */
     return 1;
+}
+
+/* the same for a separation given in quanta (A12): rij = dq s, exact        */
+static int mol_pair(const or_state* X, int64_t i, int64_t j, const int64_t dq[3],
+                    double* U, double* Fi, double* ti, double* tj, double* w)
+{
+    const or_sys* S = X->S;
+    double rij[3] = {dq[0] * S->s, dq[1] * S->s, dq[2] * S->s};   /* exact */
+    return mol_pair_r(X, i, j, rij, U, Fi, ti, tj, w);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -698,6 +706,118 @@ int or_run(const or_sys* S, double dt, int64_t n, const int32_t* comp, uint32_t*
            int nthreads, or_obs* obs)
 {
     return or_run_nvt(S, dt, n, comp, u, v, q, j, nsteps, half_step, mode, nthreads, 0.0, 0, obs);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Unquantised reference run (pin of reading A12): the same    */
+/* leapfrog + Fincham steps as or_run_nvt, but positions are plain doubles   */
+/* r in [0, box) (no fixed-point lattice): r += dt v, wrapped mod box, and   */
+/* the forces come from a brute-force full shell with the fp64 minimum image  */
+/* d = r_j - r_i - box rint((r_j - r_i)/box) (A1 strict r < rc).      */
+/* Used only to bound the effect of the position quantum s on U, W, T.       */
+static int forces_cont(const or_sys* S, int64_t n, const int32_t* comp, const double* r, const double* q,
+                       double* F, double* tau, double* ui, double* wi, int64_t* npi, int nthreads)
+{
+    or_state X;
+    if (state_init(&X, S, n, comp, NULL, q)) return -2;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 64)
+#endif
+    for (int64_t i = 0; i < n; ++i) {
+        double Fi[3] = {0, 0, 0}, ti[3] = {0, 0, 0}, U = 0, W = 0;
+        int64_t np = 0;
+        for (int64_t j = 0; j < n; ++j) {
+            if (j == i) continue;
+            double d[3];
+            for (int k = 0; k < 3; ++k) {
+                d[k] = r[3 * j + k] - r[3 * i + k];
+                d[k] -= S->box[k] * rint(d[k] / S->box[k]);
+            }
+            double tj[3] = {0, 0, 0}, w = 0;
+            if (mol_pair_r(&X, i, j, d, &U, Fi, ti, tj, &w)) { W += w; np += 1; }
+        }
+        for (int k = 0; k < 3; ++k) { F[3 * i + k] = Fi[k]; tau[3 * i + k] = ti[k]; }
+        ui[i] = 0.5 * U; wi[i] = 0.5 * W; npi[i] = np;
+    }
+    state_free(&X);
+    return 0;
+}
+
+int or_run_cont(const or_sys* S, double dt, int64_t n, const int32_t* comp, double* r,
+                double* v, double* q, double* j, int nsteps, int half_step, int nthreads, or_obs* obs)
+{
+    double* F = (double*)malloc(sizeof(double) * 3 * (n ? n : 1));
+    double* tau = (double*)malloc(sizeof(double) * 3 * (n ? n : 1));
+    double* ui = (double*)malloc(sizeof(double) * (n ? n : 1));
+    double* wi = (double*)malloc(sizeof(double) * (n ? n : 1));
+    int64_t* npi = (int64_t*)malloc(sizeof(int64_t) * (n ? n : 1));
+    if (!F || !tau || !ui || !wi || !npi) return -2;
+    int64_t ndof = 3 * n;
+    for (int64_t i = 0; i < n; ++i) ndof += rot_dof(&S->comp[comp[i]]);
+    int rc = 0;
+    for (int step = 0; step < nsteps; ++step) {
+        rc = forces_cont(S, n, comp, r, q, F, tau, ui, wi, npi, nthreads);
+        if (rc) break;
+        double U = 0, W = 0;
+        int64_t np = 0;
+        for (int64_t i = 0; i < n; ++i) { U += ui[i]; W += wi[i]; np += npi[i]; }
+        if (step == 0 && !half_step) {           /* A8: backward half kick */
+            for (int64_t i = 0; i < n; ++i) {
+                const or_comp* C = &S->comp[comp[i]];
+                for (int k = 0; k < 3; ++k) {
+                    v[3 * i + k] -= 0.5 * dt * F[3 * i + k] / C->mass;
+                    j[3 * i + k] -= 0.5 * dt * tau[3 * i + k];
+                }
+            }
+        }
+        double KEt = 0, KEr = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            const or_comp* C = &S->comp[comp[i]];
+            double* vi = v + 3 * i;
+            double* ji = j + 3 * i;
+            double* qi = q + 4 * i;
+            const double* Fi = F + 3 * i;
+            const double* ti = tau + 3 * i;
+            double vt[3];
+            for (int k = 0; k < 3; ++k) vt[k] = vi[k] + 0.5 * dt * Fi[k] / C->mass;
+            KEt += 0.5 * C->mass * dot(vt, vt);
+            for (int k = 0; k < 3; ++k) {                 /* Eqs. 2-3, no lattice */
+                vi[k] += dt * Fi[k] / C->mass;
+                double x = r[3 * i + k] + dt * vi[k];
+                x -= S->box[k] * floor(x / S->box[k]);
+                r[3 * i + k] = x;
+            }
+            if (rot_dof(C) == 0) continue;
+            double jt[3], wb[3], wq[4], dq[4], qh[4], jb[3];   /* A7, as in or_run_nvt */
+            for (int k = 0; k < 3; ++k) jt[k] = ji[k] + 0.5 * dt * ti[k];
+            body_omega(C, qi, jt, wb);
+            {
+                double R[3][3];
+                quat_to_R(qi, R);
+                matTvec(R, jt, jb);
+                KEr += 0.5 * dot(jb, wb);
+            }
+            wq[0] = 0; wq[1] = wb[0]; wq[2] = wb[1]; wq[3] = wb[2];
+            quat_mul(qi, wq, dq);
+            for (int k = 0; k < 4; ++k) qh[k] = qi[k] + 0.5 * dt * 0.5 * dq[k];
+            quat_normalize(qh);
+            for (int k = 0; k < 3; ++k) ji[k] += dt * ti[k];
+            body_omega(C, qh, ji, wb);
+            wq[1] = wb[0]; wq[2] = wb[1]; wq[3] = wb[2];
+            quat_mul(qh, wq, dq);
+            for (int k = 0; k < 4; ++k) qi[k] += dt * 0.5 * dq[k];
+            quat_normalize(qi);
+        }
+        obs[step].U = U;
+        obs[step].W = W;
+        obs[step].KEt = KEt;
+        obs[step].KEr = KEr;
+        obs[step].T = 2.0 * (KEt + KEr) / (double)ndof;
+        obs[step].npairs = np / 2;
+    }
+    free(F); free(tau); free(ui); free(wi); free(npi);
+    return rc;
 }
 
 /* ------------------------------------------------------------------------ */
