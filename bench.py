@@ -48,12 +48,9 @@ def parse():
     p.add_argument("--impl", default="mardyn", choices=["mardyn", "reference"])
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    # test hook: gloo instead of NCCL (ranks may then share a GPU; exercises the N > 1
-    # orchestration on a one-GPU box -- not a performance configuration)
-    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
-    # N > 1: device-initiated exchange (records stored into the peers' symmetric-memory
-    # buffers by the packing kernels, device barriers) instead of the NCCL all-to-alls
-    p.add_argument("--direct", action="store_true")
+    # N > 1: steps between k-d re-partitions from the measured cell loads;
+    # default: 100 for the heterogeneous slab c4 (BASELINE configs[4]), else static
+    p.add_argument("--rebalance-interval", type=int, default=None)
     return p.parse_args()
 
 
@@ -285,16 +282,14 @@ def main():
         return run_reference(args, system, rank, world)
 
     import torch
-    if args.dist_backend == "gloo":
-        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
+        # torch.distributed launches the ranks and broadcasts the library's NCCL unique id;
+        # the halo exchange, migration, rebalance and observable reductions run on the
+        # library's own communicator (include/mardyn.h)
         import torch.distributed as dist
-        if args.dist_backend == "gloo":
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1408_4599_b200 import build as b
     from paper_1408_4599_b200 import mardyn
     if rank == 0 or world == 1:
@@ -303,12 +298,13 @@ def main():
         dist.barrier()
     N = len(system["r"])
     stream = torch.cuda.Stream()
+    rebalance = args.rebalance_interval if args.rebalance_interval is not None else (100 if args.config == "c4" else 0)
     if world > 1:
         # spatial k-d decomposition (§4) with halo exchange and
         # migration over NCCL every step; one rank per GPU
         with torch.cuda.stream(stream):
             run = mardyn.DecomposedRun(system, world, transport="nccl", rank=rank, stream=stream,
-                                       direct=args.direct)
+                                       rebalance_interval=rebalance)
         ctx = run.ctxs[0]
         stepper = run.step
     else:
@@ -398,8 +394,9 @@ def main():
         "data": "synthetic (seeded generator of BASELINE configs, no checkpoints)",
         "config": {"workload": system["name"], "n_molecules": N, "steps_per_run": args.steps,
                    "parallelism": (f"k-d tree spatial decomposition over {world} GPUs, halo exchange + "
-                                   f"migration with {'NCCL' if args.dist_backend == 'nccl' else 'gloo (test transport)'} "
-                                   "all-to-alls every step") if world > 1 else "single GPU",
+                                   "migration by NCCL send/recv every step (library-owned communicator), "
+                                   f"rebalance every {rebalance} steps" if rebalance else "static partition")
+                                  if world > 1 else "single GPU",
                    "l2": "flushed between timed steps (256 MB write)",
                    "arithmetic": "fp32 forces (packed fp32x2), u32 fixed-point positions, fp64 sums",
                    "pair_interactions_per_s": obs["n_pairs"] * args.steps / (tot_ms / 1e3)},

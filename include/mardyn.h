@@ -54,7 +54,7 @@ enum {
                                than one cell edge in one step    */
     MARDYN_ECAPACITY = -4,  /* workspace too small for the requested capacity   */
     MARDYN_ECUDA = -5,      /* CUDA runtime error (context poisoned)            */
-    MARDYN_ENCCL = -6,      /* reserved: multi-GPU transport error              */
+    MARDYN_ENCCL = -6,      /* NCCL error (multi-GPU transport; context poisoned) */
     MARDYN_ESTATE = -7      /* call order, e.g. step before set_molecules       */
 };
 
@@ -84,6 +84,9 @@ typedef struct {
     int32_t lj_shift;           /* 1 = truncated and shifted LJ (LJTS, A2)       */
     const double* eta;          /* n_comps*n_comps binary parameters or
                                    NULL (all 1); copied                           */
+    int32_t rebalance_interval; /* decomposed contexts: re-partition from the
+                                   measured cell loads every this many steps
+                                   (P:197); 0 = static partition          */
     void* cuda_stream;          /* cudaStream_t or NULL                          */
 } mardyn_options;
 
@@ -242,70 +245,83 @@ int mardyn_kd_decompose(const double* cost, int32_t nx, int32_t ny, int32_t nz, 
                         int32_t* boxes, double* loads);
 
 /*
- * Spatial decomposition across GPUs (§4; one context per
- * rank, same box/cutoff/components on every rank).  boxes = nranks * 6 cell
- * ranges (from mardyn_kd_decompose, tiling the grid); this rank owns the
- * molecules in boxes[rank] and holds halo copies of the molecules in the
- * cells within one cell (>= rc) of its box.  ndof_global: the
- * degrees of freedom of the whole system (T of the rank-local observables
- * then sums to the global T).  The first call must precede
- * mardyn_workspace_bytes; a later call with the same nranks re-partitions
- * (rebalancing): the context then holds no molecules until
- * the next set_molecules (half_step = 1 resumes exactly).
- * set_molecules then takes the GLOBAL arrays on every rank and keeps owned
- * and halo molecules.  A time step is
- *     mardyn_dd_begin_step -> transport -> mardyn_dd_end_step
- * where the transport delivers, for every pair of ranks (src, dst), the
- * send_counts[dst] records of src's send segment dst into dst's receive
- * buffer (contiguous, any order: the cell rebuild sorts canonically).
- * Observables and get_* report rank-local values (owned molecules); there
- * n_pairs counts ordered pairs (i owned by the rank), so the global unique
- * pair count is the sum over ranks divided by 2.
+ * Spatial decomposition across GPUs (§4).
+ * A decomposed run is a group of ranks with the same box, cutoff, components
+ * and options, each rank one context on its own GPU:
+ *
+ *   rank 0:  mardyn_nccl_unique_id(id)     -- 128 bytes, broadcast by the caller
+ *   every rank: mardyn_create_distributed(..., id, rank, world, device, &ctx)
+ *               mardyn_partition(ctx, N, r_global)          -- k-d tree (below)
+ *               mardyn_dd_counts -> size the workspace       -- owned + halo
+ *               mardyn_workspace_bytes / set_workspace
+ *               mardyn_set_molecules(ctx, N, GLOBAL arrays)  -- keeps owned + halo
+ *               mardyn_step(ctx, n) ...                      -- collective
+ *               mardyn_get_observables(ctx, &o)              -- collective, global
+ *
+ * The library owns the NCCL communicator (NCCL is loaded at run time,
+ * dlopen("libnccl.so.2"): the copy a host process already loaded, else the
+ * system one).  Each step: forces on the rank's home box (its k-d box; the
+ * halo holds copies of every molecule within one cell layer of edge >= rc,
+ * P:220-221), kick / drift / rotation of the owned molecules, then every
+ * molecule whose new cell lies in another rank's box (migrant) or halo
+ * (halo copy) is packed as a 64-byte record (position, v, q, j) by the same
+ * kernel, the records move by NCCL send / recv over NVLink (fixed per-peer
+ * segments with device-side counts: no host synchronisation after the first
+ * step), and the receiver imports them and rebuilds its cells.  Every
+ * rebalance_interval steps the measured per-cell loads of the last cell
+ * rebuild are summed over the ranks (ncclAllReduce), the Eq. 6 cost and the
+ * k-d tree are recomputed on every rank (identical host code), and the
+ * molecules are re-distributed through the same records.
+ * mardyn_get_observables / _history return GLOBAL values (rank-ordered sums
+ * of the ranks' partials; ncclAllGather) and are collective calls;
+ * mardyn_get_molecules / get_forces / get_raw return the rank's owned
+ * molecules (compacted, ordered by input index) with their ids.  NVT
+ * rescaling is not available on decomposed contexts (MARDYN_ESTATE).
+ * world = 1 is allowed: a one-domain context whose observables travel
+ * through the communicator.  Errors: MARDYN_ENCCL (NCCL missing or failed;
+ * the context is poisoned), MARDYN_ECAPACITY (a rank's owned + halo +
+ * received molecules exceed its capacity, or an exchange segment overflows).
  */
-int mardyn_set_decomposition(struct mardyn_ctx* ctx, int32_t rank, int32_t nranks, const int32_t* boxes,
-                             double ndof_global);
-int mardyn_dd_begin_step(struct mardyn_ctx* ctx, int64_t* send_counts);
-int mardyn_dd_buffers(struct mardyn_ctx* ctx, void** send, int64_t* seg_cap, void** recv, int64_t* recv_cap,
-                      int32_t* record_bytes);
-int mardyn_dd_end_step(struct mardyn_ctx* ctx, int64_t n_recv);
+int mardyn_nccl_unique_id(void* out128);
+int mardyn_create_distributed(const double box[3], double cutoff, const mardyn_component* comps,
+                              int32_t n_comps, const mardyn_options* opt, const void* nccl_unique_id,
+                              int32_t rank, int32_t world, int32_t device, struct mardyn_ctx** out);
 
-/* Asynchronous decomposed step (same work, no host synchronisation; PAPER.md
- * P:46, P:220-221 halo and migration, exchanged every step):
- *     mardyn_dd_begin_step_async -> transport -> mardyn_dd_end_step_async
- * The record counts stay in device memory: send_cnt[d] (int32, nranks) = records
- * in send segment d after begin; the transport fills recv_cnt[r] (int32, nranks)
- * with the count rank r sent here and copies rank r's send segment (seg_cap
- * records, fixed size) to segment r of this rank's receive buffer (receive
- * buffer = nranks segments of seg_cap records; e.g. two all-to-alls with equal
- * splits).  A segment holding more than seg_cap records sets an error that the
- * next synchronising call (get_observables, get_molecules, ...) reports as
- * MARDYN_ECAPACITY; so does an import beyond the capacity.
- *   mardyn_dd_set_segment: seg_cap (1 .. the workspace's segment stride; the
- *     asynchronous step also needs seg_cap * nranks <= the receive capacity, else
- *     MARDYN_ESTATE); returned by mardyn_dd_buffers.
- *   mardyn_dd_device_counts: device addresses of send_cnt and recv_cnt (owned by
- *     the context's workspace).
- * Host-side calls that need the molecule count fetch it from the device. */
-int mardyn_dd_set_segment(struct mardyn_ctx* ctx, int64_t seg_cap);
-/* Per-peer segments instead: send segment d holds send_caps[d] records and starts at the
- * sum of the earlier send capacities; receive segment r likewise with recv_caps[r] (= rank
- * r's send_caps[this rank]).  Host arrays of nranks int64, copied; the sums must fit the
- * exchange buffers (MARDYN_EINVAL).  mardyn_dd_set_segment returns to uniform segments. */
-int mardyn_dd_set_peer_segments(struct mardyn_ctx* ctx, const int64_t* send_caps, const int64_t* recv_caps);
-int mardyn_dd_device_counts(struct mardyn_ctx* ctx, void** send_cnt, void** recv_cnt);
-/* Direct puts (device-initiated exchange, no transport step): with the segments set
- * (uniform or per-peer; setting them again clears the targets), the packing kernel of mardyn_dd_begin_step_async writes the records for rank d straight
- * to rec_addr[d] -- the device address of this rank's receive segment in rank d's receive
- * buffer (peer memory over NVLink, or another context's buffer on the same device) -- and
- * a one-warp kernel then stores this rank's count for d at cnt_addr[d] (the entry for this
- * rank in d's recv_cnt).  Host arrays of nranks device addresses (records 16-byte, counts
- * 4-byte aligned; MARDYN_EINVAL otherwise), copied.  The caller orders every rank's begin
- * before any rank's end, and every rank's end before any rank's next begin (one stream, or
- * a cross-device barrier).  rec_addr = NULL switches back to the transport; so do
- * mardyn_dd_set_segment and mardyn_dd_set_peer_segments. */
-int mardyn_dd_set_peer_targets(struct mardyn_ctx* ctx, const uint64_t* rec_addr, const uint64_t* cnt_addr);
-int mardyn_dd_begin_step_async(struct mardyn_ctx* ctx);
-int mardyn_dd_end_step_async(struct mardyn_ctx* ctx);
+/* p ranks of one decomposition inside this process, on the current device, all
+ * enqueued on one stream (opt->cuda_stream, or one the group creates): the
+ * single-GPU correctness path.  out[p] receives the ranks' contexts (rank r =
+ * out[r]); each needs its own workspace and set_molecules with the global arrays;
+ * step / compute_forces / rebalance go through out[0] and advance every rank
+ * (records are stored straight into the receiving rank's buffer); get_observables
+ * on any rank returns the global values.                                       */
+int mardyn_create_loopback(const double box[3], double cutoff, const mardyn_component* comps,
+                           int32_t n_comps, const mardyn_options* opt, int32_t p, struct mardyn_ctx** out);
+
+/* k-d partition from the GLOBAL positions r (n*3, any order; host arrays):
+ * per-cell molecule counts on the A12 lattice, the Eq. 6 cost, the k-d tree
+ * (mardyn_kd_decompose); every rank computes the same boxes.  Before
+ * set_molecules.  mardyn_set_partition: explicit boxes (p*6, as
+ * mardyn_kd_decompose returns; e.g. static equal-volume boxes), the context then
+ * holds no molecules until the next set_molecules.  mardyn_get_partition: the
+ * current boxes (p*6).  mardyn_dd_counts: owned + halo molecules of every rank
+ * (p int64) for the current partition (host; to size the workspaces).          */
+int mardyn_partition(struct mardyn_ctx* ctx, int64_t n, const double* r);
+int mardyn_set_partition(struct mardyn_ctx* ctx, const int32_t* boxes);
+int mardyn_get_partition(const struct mardyn_ctx* ctx, int32_t* boxes);
+int mardyn_dd_counts(struct mardyn_ctx* ctx, int64_t n, const double* r, int64_t* counts);
+
+/* Host-only (no context, no GPU): cells per axis of the A12 lattice for box and
+ * cutoff (ncell[3]) and, if counts != NULL, the molecules per cell (x fastest) of
+ * the n positions r (n*3); and the k-d partition of those positions into p boxes
+ * (Eq. 6 cost + mardyn_kd_decompose), as mardyn_partition computes it.         */
+int mardyn_grid_counts(const double box[3], double cutoff, int64_t n, const double* r, int32_t ncell[3],
+                       int32_t* counts);
+int mardyn_kd_partition(const double box[3], double cutoff, int64_t n, const double* r, int32_t p,
+                        int32_t* boxes, double* loads);
+
+/* Re-partition now (collective; loopback: through rank 0), as the periodic
+ * rebalance of options.rebalance_interval does.                               */
+int mardyn_rebalance(struct mardyn_ctx* ctx);
 
 const char* mardyn_last_error(const struct mardyn_ctx* ctx);
 void mardyn_destroy(struct mardyn_ctx* ctx);

@@ -492,6 +492,173 @@ __global__ void k_import_seg(int nranks, int seg_cap, const int* __restrict__ rt
     rank[slot] = atomicAdd(&count[cl], 1);
 }
 
+// ------------------------------------------------------------------------
+// spatial decomposition (§4)
+
+// decomposed ingest of one chunk of the GLOBAL arrays (molecules base .. base + m - 1,
+// already on the device): the molecules of this rank's box and halo are kept at compacted
+// slots (one atomic per warp), quantised and binned; iid = global index.  Invalid input
+// sets bit 512 of the flag, more kept molecules than the capacity bit 1024.
+__global__ void k_ingest_dd(int m, int base, const double* __restrict__ r, const double* __restrict__ v,
+                            const double* __restrict__ q, const double* __restrict__ j,
+                            const int* __restrict__ comp, GridP g, uint4* __restrict__ pos,
+                            float4* __restrict__ vel, float4* __restrict__ quat, float4* __restrict__ angm,
+                            int* __restrict__ cell_of, int* __restrict__ rank, int* __restrict__ count,
+                            int ncomp, int* __restrict__ flag, const uint8_t* __restrict__ owner,
+                            const uint32_t* __restrict__ gmask, int me, int* __restrict__ n_kept, int cap)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    bool keep = false, ghost = false;
+    uint32_t u[3] = {0, 0, 0};
+    int cl = -1;
+    if (i < m) {
+        bool ok = comp[i] >= 0 && comp[i] < ncomp;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) ok = ok && isfinite(r[3 * i + k]) && isfinite(v[3 * i + k]);
+        if (q) {
+            const double qn = q[4 * i] * q[4 * i] + q[4 * i + 1] * q[4 * i + 1] + q[4 * i + 2] * q[4 * i + 2] +
+                              q[4 * i + 3] * q[4 * i + 3];
+            ok = ok && fabs(qn - 1.0) < 1e-5;
+        }
+        if (!ok) {
+            atomicOr(flag, 512);
+        } else {
+            int c[3];
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const long long P = (long long)g.P64[k];
+                long long x = __double2ll_rn(r[3 * i + k] / (double)g.s);
+                x %= P;
+                if (x < 0) x += P;
+                u[k] = (uint32_t)x;
+                c[k] = cell_of_u(g, k, u[k]);
+            }
+            cl = c[0] + g.nc[0] * (c[1] + g.nc[1] * c[2]);
+            ghost = (gmask[cl] >> me) & 1u;
+            keep = owner[cl] == me || ghost;
+        }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    int slot0 = 0;
+    if (b && lane == __ffs(b) - 1) slot0 = atomicAdd(n_kept, __popc(b));
+    slot0 = __shfl_sync(0xffffffffu, slot0, __ffs(b ? b : 1u) - 1);
+    if (!keep) return;
+    const int slot = slot0 + __popc(b & ((1u << lane) - 1u));
+    if (slot >= cap) { atomicOr(flag, 1024); return; }
+    pos[slot] = make_uint4(u[0], u[1], u[2], (uint32_t)(base + i));
+    vel[slot] = make_float4((float)v[3 * i], (float)v[3 * i + 1], (float)v[3 * i + 2],
+                            __int_as_float(comp[i] | (ghost ? 256 : 0)));
+    if (quat) {
+        quat[slot] = q ? make_float4((float)q[4 * i], (float)q[4 * i + 1], (float)q[4 * i + 2], (float)q[4 * i + 3])
+                       : make_float4(1.f, 0.f, 0.f, 0.f);
+        angm[slot] = j ? make_float4((float)j[3 * i], (float)j[3 * i + 1], (float)j[3 * i + 2], 0.f)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    cell_of[slot] = cl;
+    rank[slot] = atomicAdd(&count[cl], 1);
+}
+
+// per-cell molecule counts of the cells this rank owns (0 elsewhere) from the last cell
+// rebuild: the measured load of the rebalance (Eq. 6 input, reading A19)
+__global__ void k_owned_counts(int ncell, const int* __restrict__ start, const uint8_t* __restrict__ owner,
+                               int me, int* __restrict__ out)
+{
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < ncell) out[c] = owner[c] == me ? start[c + 1] - start[c] : 0;
+}
+
+// Rebalance: re-distribute the sorted state under the new cell
+// owners / halo masks.  Every molecule this rank owned is sent to its new owner (if
+// another rank) and as a halo copy to every rank whose new halo holds its cell; it stays
+// here as an owned molecule or a halo copy, or leaves.  The old halo copies are dropped
+// (their owners send the new ones).  COUNT: records per destination only (send_cnt);
+// else the records are packed at the per-destination offsets of dd.seg_tab and the kept
+// molecules binned for the cell rebuild.  No time passes (v, j stay at t - dt/2).
+template <bool COUNT>
+__global__ void k_repartition(int n, GridP g, DDArgs dd, const uint4* __restrict__ pos, float4* __restrict__ vel,
+                              const float4* __restrict__ quat, const float4* __restrict__ angm,
+                              int* __restrict__ cell_of, int* __restrict__ rank, int* __restrict__ count)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    unsigned dmask = 0;
+    int own = -1, cl = -1;
+    uint4 p = make_uint4(0, 0, 0, 0);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f), qn = make_float4(1.f, 0.f, 0.f, 0.f), jn = v;
+    if (t < n) {
+        v = vel[t];
+        if (!md_ghost(v.w)) {
+            p = pos[t];
+            cl = cell_of_u(g, 0, p.x) + g.nc[0] * (cell_of_u(g, 1, p.y) + g.nc[1] * cell_of_u(g, 2, p.z));
+            own = dd.owner[cl];
+            const uint32_t gm = dd.gmask[cl];
+            dmask = (gm & ~(1u << dd.rank)) | (own != dd.rank ? 1u << own : 0u);
+            if (quat) { qn = quat[t]; jn = angm[t]; }
+            if (!COUNT) {
+                if (own == dd.rank) {
+                    vel[t] = make_float4(v.x, v.y, v.z, __int_as_float(md_comp(v.w)));
+                } else if ((gm >> dd.rank) & 1u) {
+                    vel[t] = make_float4(v.x, v.y, v.z, __int_as_float(md_comp(v.w) | 256));
+                } else {
+                    cl = -1;
+                }
+            }
+        }
+    }
+    if (COUNT) {
+        for (int r = 0; r < dd.nranks; ++r) {
+            const unsigned b = __ballot_sync(0xffffffffu, (dmask >> r) & 1u);
+            if (b && lane == 0) atomicAdd(&dd.send_cnt[r], __popc(b));
+        }
+        return;
+    }
+    if (t < n) cell_of[t] = cl;
+    const float4 vn = make_float4(v.x, v.y, v.z, __int_as_float(md_comp(v.w)));
+    dd_pack_warp(dd, dmask, own, p, vn, qn, jn);
+    const unsigned m = __match_any_sync(0xffffffffu, cl);
+    if (cl >= 0) {
+        const int leader = __ffs(m) - 1;
+        int b = 0;
+        if (lane == leader) b = atomicAdd(&count[cl], __popc(m));
+        b = __shfl_sync(m, b, leader);
+        rank[t] = b + __popc(m & ((1u << lane) - 1u));
+    }
+}
+
+// decomposed egress: this rank's owned molecules, compacted (one atomic per warp) into
+// records of rec_words doubles: iid, then the requested fields (the host orders by iid)
+__global__ void k_egress_dd(int n, GridP g, const uint4* __restrict__ pos, const float4* __restrict__ vel,
+                            const float4* __restrict__ quat, const float4* __restrict__ angm,
+                            const float4* __restrict__ force, const float4* __restrict__ torque,
+                            unsigned fields, int rec_words, double* __restrict__ out, int* __restrict__ ctr)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const bool on = t < n && !md_ghost(vel[t].w);
+    const unsigned b = __ballot_sync(0xffffffffu, on);
+    int k0 = 0;
+    if (b && lane == __ffs(b) - 1) k0 = atomicAdd(ctr, __popc(b));
+    k0 = __shfl_sync(0xffffffffu, k0, __ffs(b ? b : 1u) - 1);
+    if (!on) return;
+    double* o = out + (size_t)(k0 + __popc(b & ((1u << lane) - 1u))) * rec_words;
+    const uint4 p = pos[t];
+    int w = 0;
+    o[w++] = (double)p.w;
+    if (fields & 1) { o[w++] = (double)p.x * g.s; o[w++] = (double)p.y * g.s; o[w++] = (double)p.z * g.s; }
+    if (fields & 2) { const float4 x = vel[t]; o[w++] = x.x; o[w++] = x.y; o[w++] = x.z; }
+    if (fields & 4) {
+        const float4 x = quat ? quat[t] : make_float4(1.f, 0.f, 0.f, 0.f);
+        o[w++] = x.x; o[w++] = x.y; o[w++] = x.z; o[w++] = x.w;
+    }
+    if (fields & 8) { const float4 x = angm ? angm[t] : make_float4(0.f, 0.f, 0.f, 0.f); o[w++] = x.x; o[w++] = x.y; o[w++] = x.z; }
+    if (fields & 16) { const float4 x = force[t]; o[w++] = x.x; o[w++] = x.y; o[w++] = x.z; }
+    if (fields & 32) { const float4 x = torque ? torque[t] : make_float4(0.f, 0.f, 0.f, 0.f); o[w++] = x.x; o[w++] = x.y; o[w++] = x.z; }
+    if (fields & 64) { o[w++] = (double)p.x; o[w++] = (double)p.y; o[w++] = (double)p.z; }
+    if (fields & 128)
+        o[w++] = (double)(cell_of_u(g, 0, p.x) + g.nc[0] * (cell_of_u(g, 1, p.y) + g.nc[1] * cell_of_u(g, 2, p.z)));
+}
+
 // kinetic energy at t without integrating (compute_forces, A9)
 template <bool RIGID>
 __global__ void __launch_bounds__(256) k_kinetic(int n, GridP g, const DevModel* __restrict__ model,
@@ -656,14 +823,12 @@ __global__ void k_egress(int n, GridP g, const uint4* __restrict__ pos, const fl
                          const float4* __restrict__ force, const float4* __restrict__ torque,
                          double* __restrict__ r, double* __restrict__ v, double* __restrict__ q,
                          double* __restrict__ j, double* __restrict__ F, double* __restrict__ tau,
-                         uint32_t* __restrict__ ufix, int* __restrict__ cell, int8_t* __restrict__ owned = nullptr)
+                         uint32_t* __restrict__ ufix, int* __restrict__ cell)
 {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
-    if (md_ghost(vel[t].w)) return;          // halo copies are reported by their owner
     uint4 p = pos[t];
     int i = (int)p.w;
-    if (owned) owned[i] = 1;
     if (r) { r[3 * i] = (double)p.x * g.s; r[3 * i + 1] = (double)p.y * g.s; r[3 * i + 2] = (double)p.z * g.s; }
     if (ufix) { ufix[3 * i] = p.x; ufix[3 * i + 1] = p.y; ufix[3 * i + 2] = p.z; }
     if (cell) {

@@ -3,6 +3,7 @@
 // kernels_state.cuh / kernels_force.cuh; this file validates inputs, lays
 // out the caller-provided workspace, builds the per-component tables,
 // captures one time step per buffer parity as a CUDA graph and replays it.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -12,6 +13,7 @@
 #include "../../include/mardyn.h"
 #include "common.cuh"
 #include "decomp.hpp"
+#include "nccl_api.hpp"
 #include "kernels_force.cuh"
 #include "kernels_lj1.cuh"
 #include "kernels_rigid3.cuh"
@@ -51,6 +53,20 @@ constexpr int GEN_WARPS = 1;
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace
+
+struct Group;                            // ranks that step together (dist_engine.cuh)
+struct mardyn_ctx;
+static bool group_is_nccl(const Group* g);
+static int set_molecules_dd(mardyn_ctx* ctx, int64_t n, const int64_t* id, const int32_t* comp, const double* r,
+                            const double* v, const double* q, const double* j, int32_t half_step);
+static int egress_dd(mardyn_ctx* ctx, double* r, double* v, double* q, double* j, double* F, double* tau,
+                     uint32_t* ufix, int32_t* cell, int64_t n_slots, int64_t* n_out, int64_t* ids_out,
+                     int32_t* comp_out);
+static int group_observables(mardyn_ctx* ctx, std::vector<ObsRec>& ring);
+static int group_step(mardyn_ctx* ctx, int32_t nsteps);
+static int group_compute_forces(mardyn_ctx* ctx);
+static void group_release(mardyn_ctx* ctx);
+static int compute_forces_local(mardyn_ctx* ctx);
 
 struct mardyn_ctx {
     std::string err;
@@ -132,25 +148,33 @@ struct mardyn_ctx {
     double last_total_ms = 0, last_force_ms = 0;
     int last_force_launches = 0;
     // spatial decomposition (§4): this rank's box, cell owners, halos
+    Group* grp = nullptr;                  // distributed / loopback group (nullptr: one domain)
     int dd_rank = 0, nranks = 1;
+    int rebalance_interval = 0;            // steps between re-partitions (0: static)
+    long long last_rebalance = -1;         // host_step of the last re-partition
+    bool seg_ready = false;                // exchange segments sized (else the next step is synchronous)
     bool n_stale = false;                  // asynchronous decomposed steps: host copy of n out of date
     bool side_join = false;                // the step's finalize runs on the side stream until end_step
     int* recv_cnt = nullptr;               // asynchronous exchange: records received per source rank (device)
     DDRec** put_rec = nullptr;             // direct puts: per destination rank, where this rank's records go
     int** put_cnt = nullptr;               //   and where its record count goes (device arrays of addresses)
     bool direct = false;
-    int* n_aux = nullptr;                  // unsorted count after the import (device)
+    int* n_aux = nullptr;                  // [0] unsorted count after the import, [1] n at force time, [2] egress counter
     int64_t seg_max = 0;                   // send segment stride of the workspace layout
     int* seg_tab = nullptr;                // per-peer segments (device): send offsets, send caps, recv offsets, recv caps
     bool peer_segs = false;                // seg_tab in use (else uniform seg_cap segments)
     int64_t recv_span = 0;                 // records of the receive buffer the segments cover
+    std::vector<int64_t> send_off, send_caps, recv_off, recv_caps;   // host copies of the segment layout
     std::vector<int32_t> boxes;
     std::vector<uint8_t> h_owner;
     std::vector<uint32_t> h_gmask;
     double ndof_global = -1.0;
+    int64_t n_global = 0;                  // molecules of the whole system (decomposed contexts)
     uint8_t* owner = nullptr;
     uint32_t* gmask = nullptr;
-    int8_t* owned = nullptr;
+    int* gcount = nullptr;                 // per-cell owned counts (rebalance)
+    int64_t* cmat = nullptr;               // record-count matrix staging (NCCL allgather)
+    ObsRec* obs_all = nullptr;             // allgathered observable rings (NCCL)
     DDRec* sendbuf = nullptr;
     DDRec* recvbuf = nullptr;
     int* send_cnt = nullptr;
@@ -179,29 +203,28 @@ static int fail(mardyn_ctx* c, int code, const std::string& msg)
     } while (0)
 
 // grid and fixed-point lattice, reading A12
-static int setup_grid(mardyn_ctx* ctx)
+static int grid_setup(const double L[3], double rc, double dt, GridP& g, std::string& err)
 {
     int nc[3];
     for (int k = 0; k < 3; ++k) {
-        nc[k] = (int)std::floor(ctx->L[k] / ctx->rc);
-        if (nc[k] < 3) return fail(ctx, MARDYN_EINVAL, "box must hold >= 3 cells of edge >= rc per axis");
+        nc[k] = (int)std::floor(L[k] / rc);
+        if (nc[k] < 3) { err = "box must hold >= 3 cells of edge >= rc per axis"; return MARDYN_EINVAL; }
     }
     double s = 0;
     long long E[3];
     for (int it = 0; it < 4; ++it) {
         double emax = 0;
-        for (int k = 0; k < 3; ++k) emax = std::fmax(emax, ctx->L[k] / nc[k]);
+        for (int k = 0; k < 3; ++k) emax = std::fmax(emax, L[k] / nc[k]);
         int ex = (int)std::ceil(std::log2(emax));
         s = std::ldexp(1.0, ex - 22);
         bool again = false;
         for (int k = 0; k < 3; ++k) {
-            E[k] = std::llround(ctx->L[k] / (nc[k] * s));
-            if ((double)E[k] * s < ctx->rc) { nc[k] -= 1; again = true; }
-            if (nc[k] < 3) return fail(ctx, MARDYN_EINVAL, "box must hold >= 3 cells of edge >= rc per axis");
+            E[k] = std::llround(L[k] / (nc[k] * s));
+            if ((double)E[k] * s < rc) { nc[k] -= 1; again = true; }
+            if (nc[k] < 3) { err = "box must hold >= 3 cells of edge >= rc per axis"; return MARDYN_EINVAL; }
         }
         if (!again) break;
     }
-    GridP& g = ctx->g;
     std::memset(&g, 0, sizeof(g));
     long long ncell = 1;
     for (int k = 0; k < 3; ++k) {
@@ -210,27 +233,34 @@ static int setup_grid(mardyn_ctx* ctx)
         // ceil(2^64 / E) for the multiply-high division (E >= 2, so no overflow)
         g.Einv[k] = (uint64_t)(~0ull / (uint64_t)E[k]) + 1ull;
         uint64_t P = (uint64_t)E[k] * (uint64_t)nc[k];
-        if (P > (1ull << 32)) return fail(ctx, MARDYN_EINVAL, "box too large for 32-bit fixed point");
+        if (P > (1ull << 32)) { err = "box too large for 32-bit fixed point"; return MARDYN_EINVAL; }
         g.P64[k] = P;
         g.P[k] = (uint32_t)(P & 0xffffffffu);
         g.edge[k] = (float)((double)E[k] * s);
         ncell *= nc[k];
     }
-    if (ncell > (1ll << 30)) return fail(ctx, MARDYN_EINVAL, "too many cells");
+    if (ncell > (1ll << 30)) { err = "too many cells"; return MARDYN_EINVAL; }
     g.ncell = (int)ncell;
     g.s = (float)s;
     g.inv_s = (float)(1.0 / s);
-    double rc2 = ctx->rc * ctx->rc;
+    double rc2 = rc * rc;
     g.cut2 = (float)rc2;
     g.cut2_lo = std::nextafterf((float)(rc2 * (1.0 - std::ldexp(1.0, -20))), 0.f);
     g.cut2_hi = std::nextafterf((float)(rc2 * (1.0 + std::ldexp(1.0, -20))), INFINITY);
     g.band_mid = 0.5f * (g.cut2_lo + g.cut2_hi);
     g.band_hw = 0.5f * (g.cut2_hi - g.cut2_lo) + 1e-6f * g.cut2_hi;
     g.cut2_q = (long long)std::ceil(rc2 / (s * s));
-    g.dt = (float)ctx->dt;
+    g.dt = (float)dt;
     for (int k = 0; k < 3; ++k) { g.hlo[k] = 0; g.hdim[k] = g.nc[k]; }
     g.nhome = g.ncell;
     return MARDYN_OK;
+}
+
+static int setup_grid(mardyn_ctx* ctx)
+{
+    std::string err;
+    int rc = grid_setup(ctx->L, ctx->rc, ctx->dt, ctx->g, err);
+    return rc ? fail(ctx, rc, err) : MARDYN_OK;
 }
 
 static int build_model(mardyn_ctx* ctx)
@@ -569,6 +599,8 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
     ctx->dt = opt->dt;
     ctx->eps_rf = opt->eps_rf;
     ctx->lj_shift = opt->lj_shift;
+    if (opt->rebalance_interval < 0) return bad("rebalance_interval must be >= 0");
+    ctx->rebalance_interval = opt->rebalance_interval;
     int lj_total = 0;
     for (int c = 0; c < n_comps; ++c) {
         const mardyn_component& C = comps[c];
@@ -716,13 +748,15 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     long long* step_ctr = (long long*)take(8);
     int* flag = (int*)take(4);
     DevModel* dmodel = (DevModel*)take(sizeof(DevModel));
-    const size_t stage_bytes = (size_t)cap * (19 * 8 + 3 * 4 + 4 + 4);
+    const size_t stage_bytes = (size_t)cap * (24 * 8);   // ingest chunks (108 B), egress (<= 184 B)
     char* stage = take(stage_bytes);
     int64_t* ids_dev = (int64_t*)take(8 * (size_t)cap);
     int32_t* comp_dev = (int32_t*)take(4 * (size_t)cap);
     uint8_t* owner = nullptr;
     uint32_t* gmask = nullptr;
-    int8_t* owned = nullptr;
+    int* gcount = nullptr;
+    int64_t* cmat = nullptr;
+    ObsRec* obs_all = nullptr;
     DDRec *sendbuf = nullptr, *recvbuf = nullptr;
     int* send_cnt = nullptr;
     int* recv_cnt = nullptr;
@@ -735,16 +769,19 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     if (ctx->nranks > 1) {
         owner = (uint8_t*)take((size_t)ncell);
         gmask = (uint32_t*)take(4 * (size_t)ncell);
-        owned = (int8_t*)take((size_t)cap);
+        gcount = (int*)take(4 * (size_t)ncell);
+        cmat = (int64_t*)take(8 * (size_t)ctx->nranks * (ctx->nranks + 1));
         sendbuf = (DDRec*)take(sizeof(DDRec) * (size_t)seg_cap * ctx->nranks);
         recvbuf = (DDRec*)take(sizeof(DDRec) * (size_t)recv_cap);
         send_cnt = (int*)take(4 * (size_t)ctx->nranks);
         recv_cnt = (int*)take(4 * (size_t)ctx->nranks);
-        n_aux = (int*)take(8);                     // [0] unsorted count after import, [1] n at force time
+        n_aux = (int*)take(16);                    // [0] unsorted count after import, [1] n at force time, [2] egress
         seg_tab = (int*)take(16 * (size_t)ctx->nranks);
         put_rec = (DDRec**)take(sizeof(void*) * (size_t)ctx->nranks);
         put_cnt = (int**)take(sizeof(void*) * (size_t)ctx->nranks);
     }
+    if (ctx->grp && group_is_nccl(ctx->grp))
+        obs_all = (ObsRec*)take(sizeof(ObsRec) * MD_HISTORY * (size_t)ctx->nranks);
     if (assign) {
         ctx->pos[0] = pos0; ctx->pos[1] = pos1; ctx->vel[0] = vel0; ctx->vel[1] = vel1;
         ctx->quat[0] = q0; ctx->quat[1] = q1; ctx->angm[0] = j0; ctx->angm[1] = j1;
@@ -755,9 +792,11 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         ctx->hist = hist; ctx->step_ctr = step_ctr; ctx->flag = flag; ctx->dmodel = dmodel;
         ctx->stage = stage; ctx->stage_bytes = stage_bytes;
         ctx->ids_dev = ids_dev; ctx->comp_dev = comp_dev;
-        ctx->owner = owner; ctx->gmask = gmask; ctx->owned = owned; ctx->sendbuf = sendbuf;
+        ctx->owner = owner; ctx->gmask = gmask; ctx->gcount = gcount; ctx->cmat = cmat; ctx->obs_all = obs_all;
+        ctx->sendbuf = sendbuf;
         ctx->recvbuf = recvbuf; ctx->send_cnt = send_cnt; ctx->seg_cap = seg_cap; ctx->recv_cap = recv_cap;
         ctx->recv_cnt = recv_cnt; ctx->n_aux = n_aux; ctx->seg_max = seg_cap; ctx->n_stale = false;
+        ctx->seg_ready = false;
         ctx->seg_tab = seg_tab; ctx->peer_segs = false;
         ctx->put_rec = put_rec; ctx->put_cnt = put_cnt; ctx->direct = false;
         ctx->ncell_pad = ncell_pad; ctx->ntiles = ntiles; ctx->nkblocks = nk;
@@ -792,7 +831,7 @@ int mardyn_set_workspace(mardyn_ctx* ctx, void* device_ptr, size_t bytes, int64_
     CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, ctx->stream));
     if (ctx->blk_ctr) CK(cudaMemsetAsync(ctx->blk_ctr, 0, sizeof(int), ctx->stream));
     CK(cudaMemsetAsync(ctx->hist, 0, sizeof(ObsRec) * MD_HISTORY, ctx->stream));
-    if (ctx->nranks > 1) {
+    if (ctx->nranks > 1 && !ctx->h_owner.empty()) {
         CK(cudaMemcpyAsync(ctx->owner, ctx->h_owner.data(), ctx->g.ncell, cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemcpyAsync(ctx->gmask, ctx->h_gmask.data(), 4 * (size_t)ctx->g.ncell, cudaMemcpyHostToDevice,
                            ctx->stream));
@@ -809,6 +848,7 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
     if (!ctx) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->ws) return fail(ctx, MARDYN_ESTATE, "set_workspace must precede set_molecules");
+    if (ctx->nranks > 1) return set_molecules_dd(ctx, n, id, comp, r, v, q, j, half_step);
     if (n < 1 || n > ctx->cap) return fail(ctx, MARDYN_EINVAL, "n must be in [1, capacity]");
     if (!comp || !r || !v) return fail(ctx, MARDYN_EINVAL, "comp, r, v are required");
     if (ctx->rigid && (!q || !j)) return fail(ctx, MARDYN_EINVAL, "q and j are required for rigid molecules");
@@ -817,11 +857,6 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
     // ids and components only for the decomposed egress
     ctx->n = n;
     ctx->n_stale = false;
-    if (ctx->nranks > 1) {
-        ctx->ids.resize(n);
-        ctx->comp_host.assign(comp, comp + n);
-        for (int64_t i = 0; i < n; ++i) ctx->ids[i] = id ? id[i] : i;
-    }
     ctx->comp_counts.assign(ncomp, 0);
     if (ncomp == 1) ctx->comp_counts[0] = n;
     else
@@ -834,7 +869,7 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
             for (int64_t i = 0; i < n; ++i)
                 if (comp[i] >= 0 && comp[i] < ncomp) ndof += ctx->model.comp[comp[i]].rot;
     }
-    ctx->ndof = ctx->ndof_global > 0 ? ctx->ndof_global : ndof;
+    ctx->ndof = ndof;
     ctx->n_input = n;
     cudaStream_t s = ctx->stream;
     // launched force grid: the occupancy grid, or (one domain) just enough CTAs for a
@@ -879,20 +914,12 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
                                            ctx->comp_dev, ctx->g, ctx->pos[src], ctx->vel[src],
                                            ctx->rigid ? ctx->quat[src] : nullptr,
                                            ctx->rigid ? ctx->angm[src] : nullptr, ctx->cell_of, ctx->rank, ctx->count,
-                                           ncomp, ctx->flag,
-                                           ctx->nranks > 1 ? ctx->owner : nullptr,
-                                           ctx->nranks > 1 ? ctx->gmask : nullptr, ctx->rank_id());
+                                           ncomp, ctx->flag);
     ctx->launches += 1;
     int rc = enqueue_sort(ctx, src, dst, n);
     if (rc) return rc;
     CK(cudaGetLastError());
     ctx->cur = dst;
-    if (ctx->nranks > 1) {        // owned + halo molecules kept by this rank
-        int kept = 0;
-        CK(cudaMemcpyAsync(&kept, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        ctx->n = kept;
-    }
     long long step = ctx->host_step;
     CK(cudaMemcpyAsync(ctx->step_ctr, &step, 8, cudaMemcpyHostToDevice, s));
     if (!half_step) {   // A8: backward half kick with F(t0), tau(t0) of the molecules kept (ctx->n)
@@ -925,7 +952,15 @@ int mardyn_compute_forces(mardyn_ctx* ctx)
 {
     if (!ctx) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
+    if (ctx->grp && ctx->nranks > 1) return group_compute_forces(ctx);
     if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
+    return compute_forces_local(ctx);
+}
+
+}  // extern "C"
+
+static int compute_forces_local(mardyn_ctx* ctx)
+{
     if (int rc0 = refresh_n(ctx)) return rc0;
     cudaStream_t s = ctx->stream;
     const int n = (int)ctx->n, b = ctx->cur;
@@ -938,12 +973,15 @@ int mardyn_compute_forces(mardyn_ctx* ctx)
                                                        ctx->force, nullptr, ctx->kpart);
     // kpart beyond the used blocks stays from earlier steps: same block count
     k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, ctx->nkblocks, ctx->kpart, ctx->ndof,
-                                                  ctx->step_ctr, 0, ctx->hist, ctx->fin_scratch, ctx->fin_ticket);
+                                                  ctx->step_ctr, 0, ctx->hist, ctx->fin_scratch, ctx->fin_ticket,
+                                                  ctx->nranks > 1 ? 0 : 1);
     ctx->launches += 3;
     CK(cudaGetLastError());
     ctx->last_obs = ctx->host_step;
     return MARDYN_OK;
 }
+
+extern "C" {
 
 int mardyn_set_thermostat(mardyn_ctx* ctx, double T_target, int32_t interval)
 {
@@ -1010,8 +1048,8 @@ int mardyn_step(mardyn_ctx* ctx, int32_t nsteps)
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
     if (nsteps < 0) return fail(ctx, MARDYN_EINVAL, "n must be >= 0");
-    if (ctx->nranks > 1) return fail(ctx, MARDYN_ESTATE, "decomposed context: use mardyn_dd_begin_step / dd_end_step");
     if (nsteps == 0) return MARDYN_OK;
+    if (ctx->nranks > 1) return group_step(ctx, nsteps);
     if (!ctx->gexec[0]) {
         int rc = build_graphs(ctx);
         if (rc) return rc;
@@ -1059,6 +1097,13 @@ int mardyn_get_observables(mardyn_ctx* ctx, mardyn_observables* out)
     if (!ctx || !out) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (ctx->last_obs < 0) return fail(ctx, MARDYN_ESTATE, "no force evaluation yet (step or compute_forces)");
+    if (ctx->grp) {                           // global values: rank-ordered sums over the group (A23)
+        std::vector<ObsRec> ring;
+        int rc = group_observables(ctx, ring);
+        if (rc) return rc;
+        to_obs(ring[ctx->last_obs % MD_HISTORY], out);
+        return MARDYN_OK;
+    }
     int rc = sync_check(ctx);
     if (rc) return rc;
     ObsRec o;
@@ -1071,13 +1116,18 @@ int mardyn_get_observable_history(mardyn_ctx* ctx, int32_t cap, int32_t* n, mard
 {
     if (!ctx || !n || (cap > 0 && !out)) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
-    int rc = sync_check(ctx);
-    if (rc) return rc;
     long long last = ctx->last_obs;
     long long avail = std::min<long long>(last + 1, MD_HISTORY);
     long long m = std::min<long long>(avail, cap);
     std::vector<ObsRec> h(MD_HISTORY);
-    CK(cudaMemcpy(h.data(), ctx->hist, sizeof(ObsRec) * MD_HISTORY, cudaMemcpyDeviceToHost));
+    if (ctx->grp) {
+        int rc = group_observables(ctx, h);
+        if (rc) return rc;
+    } else {
+        int rc = sync_check(ctx);
+        if (rc) return rc;
+        CK(cudaMemcpy(h.data(), ctx->hist, sizeof(ObsRec) * MD_HISTORY, cudaMemcpyDeviceToHost));
+    }
     for (long long k = 0; k < m; ++k) to_obs(h[(last - m + 1 + k) % MD_HISTORY], out + k);
     *n = (int32_t)m;
     return MARDYN_OK;
@@ -1090,71 +1140,42 @@ static int egress(mardyn_ctx* ctx, double* r, double* v, double* q, double* j, d
                   uint32_t* ufix, int32_t* cell, int64_t n_slots = -1, int64_t* n_out = nullptr,
                   int64_t* ids_out = nullptr, int32_t* comp_out = nullptr)
 {
-    const bool dd = ctx->nranks > 1;
-    const int64_t n = n_slots < 0 ? ctx->n : n_slots;          // sorted slots to read
-    const int64_t N = dd ? ctx->n_input : ctx->n;               // index space of the output
+    if (ctx->nranks > 1)      // the rank's owned molecules, compacted, with their ids
+        return egress_dd(ctx, r, v, q, j, F, tau, ufix, cell, n_slots, n_out, ids_out, comp_out);
+    const int64_t n = n_slots < 0 ? ctx->n : n_slots;          // sorted slots to read = molecules
     cudaStream_t s = ctx->stream;
     double* d_r = (double*)ctx->stage;
-    double* d_v = d_r + 3 * N;
-    double* d_q = d_v + 3 * N;
-    double* d_j = d_q + 4 * N;
-    double* d_F = d_j + 3 * N;
-    double* d_t = d_F + 3 * N;
-    uint32_t* d_u = (uint32_t*)(d_t + 3 * N);
-    int* d_c = (int*)(d_u + 3 * N);
+    double* d_v = d_r + 3 * n;
+    double* d_q = d_v + 3 * n;
+    double* d_j = d_q + 4 * n;
+    double* d_F = d_j + 3 * n;
+    double* d_t = d_F + 3 * n;
+    uint32_t* d_u = (uint32_t*)(d_t + 3 * n);
+    int* d_c = (int*)(d_u + 3 * n);
     const int b = ctx->cur;
-    if (dd) CK(cudaMemsetAsync(ctx->owned, 0, (size_t)N, s));
     if (ctx->rigid)
         k_egress<true><<<nblk(n, 256), 256, 0, s>>>((int)n, ctx->g, ctx->pos[b], ctx->vel[b], ctx->quat[b],
                                                     ctx->angm[b], ctx->force, ctx->torque, r ? d_r : nullptr,
                                                     v ? d_v : nullptr, q ? d_q : nullptr, j ? d_j : nullptr,
                                                     F ? d_F : nullptr, tau ? d_t : nullptr, ufix ? d_u : nullptr,
-                                                    cell ? d_c : nullptr, dd ? ctx->owned : nullptr);
+                                                    cell ? d_c : nullptr);
     else
         k_egress<false><<<nblk(n, 256), 256, 0, s>>>((int)n, ctx->g, ctx->pos[b], ctx->vel[b], nullptr, nullptr,
                                                      ctx->force, nullptr, r ? d_r : nullptr, v ? d_v : nullptr,
                                                      q ? d_q : nullptr, j ? d_j : nullptr, F ? d_F : nullptr,
-                                                     tau ? d_t : nullptr, ufix ? d_u : nullptr, cell ? d_c : nullptr,
-                                                     dd ? ctx->owned : nullptr);
+                                                     tau ? d_t : nullptr, ufix ? d_u : nullptr, cell ? d_c : nullptr);
     ctx->launches += 1;
     CK(cudaGetLastError());
-    if (!dd) {
-        if (r) CK(cudaMemcpyAsync(r, d_r, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
-        if (v) CK(cudaMemcpyAsync(v, d_v, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
-        if (q) CK(cudaMemcpyAsync(q, d_q, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, s));
-        if (j) CK(cudaMemcpyAsync(j, d_j, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
-        if (F) CK(cudaMemcpyAsync(F, d_F, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
-        if (tau) CK(cudaMemcpyAsync(tau, d_t, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
-        if (ufix) CK(cudaMemcpyAsync(ufix, d_u, sizeof(uint32_t) * 3 * n, cudaMemcpyDeviceToHost, s));
-        if (cell) CK(cudaMemcpyAsync(cell, d_c, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
-        if (n_out) *n_out = n;
-        return sync_check(ctx);
-    }
-    std::vector<int8_t> mask((size_t)N);
-    CK(cudaMemcpyAsync(mask.data(), ctx->owned, (size_t)N, cudaMemcpyDeviceToHost, s));
-    struct Out { void* host; void* dev; size_t width; };
-    const Out outs[] = {{r, d_r, 24}, {v, d_v, 24}, {q, d_q, 32}, {j, d_j, 24}, {F, d_F, 24}, {tau, d_t, 24},
-                        {ufix, d_u, 12}, {cell, d_c, 4}};
-    std::vector<std::vector<char>> tmp(8);
-    for (int k = 0; k < 8; ++k)
-        if (outs[k].host) {
-            tmp[k].resize(outs[k].width * (size_t)N);
-            CK(cudaMemcpyAsync(tmp[k].data(), outs[k].dev, outs[k].width * (size_t)N, cudaMemcpyDeviceToHost, s));
-        }
-    int rc = sync_check(ctx);
-    if (rc) return rc;
-    int64_t m = 0;
-    for (int64_t i = 0; i < N; ++i) {
-        if (!mask[i]) continue;
-        for (int k = 0; k < 8; ++k)
-            if (outs[k].host)
-                std::memcpy((char*)outs[k].host + outs[k].width * m, tmp[k].data() + outs[k].width * i, outs[k].width);
-        if (ids_out) ids_out[m] = ctx->ids[i];
-        if (comp_out) comp_out[m] = ctx->comp_host[i];
-        ++m;
-    }
-    if (n_out) *n_out = m;
-    return MARDYN_OK;
+    if (r) CK(cudaMemcpyAsync(r, d_r, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if (v) CK(cudaMemcpyAsync(v, d_v, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if (q) CK(cudaMemcpyAsync(q, d_q, sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, s));
+    if (j) CK(cudaMemcpyAsync(j, d_j, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if (F) CK(cudaMemcpyAsync(F, d_F, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if (tau) CK(cudaMemcpyAsync(tau, d_t, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if (ufix) CK(cudaMemcpyAsync(ufix, d_u, sizeof(uint32_t) * 3 * n, cudaMemcpyDeviceToHost, s));
+    if (cell) CK(cudaMemcpyAsync(cell, d_c, sizeof(int) * n, cudaMemcpyDeviceToHost, s));
+    if (n_out) *n_out = n;
+    return sync_check(ctx);
 }
 
 int mardyn_get_molecules(mardyn_ctx* ctx, int64_t cap, int64_t* n, int64_t* id, int32_t* comp, double* r,
@@ -1244,336 +1265,12 @@ int mardyn_set_profiling(mardyn_ctx* ctx, int32_t on)
 
 int64_t mardyn_launch_count(const mardyn_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
-// ---------------------------------------------------------------------------
-// spatial decomposition (§4)
+}  // extern "C"
 
-int mardyn_set_decomposition(mardyn_ctx* ctx, int32_t rank, int32_t nranks, const int32_t* boxes,
-                             double ndof_global)
-{
-    if (!ctx) return MARDYN_EINVAL;
-    // first call before the workspace (its layout depends on nranks); later calls
-    // (rebalancing) keep nranks and re-upload the cell maps
-    if (ctx->ws && nranks != ctx->nranks)
-        return fail(ctx, MARDYN_ESTATE, "set_decomposition after set_workspace must keep nranks");
-    if (nranks < 1 || nranks > 32 || rank < 0 || rank >= nranks || !boxes)
-        return fail(ctx, MARDYN_EINVAL, "bad rank / nranks (1..32) / boxes");
-    const GridP& g0 = ctx->g;
-    const int nx = g0.nc[0], ny = g0.nc[1], nz = g0.nc[2];
-    std::vector<uint8_t> owner((size_t)g0.ncell, 255);
-    for (int r = 0; r < nranks; ++r) {
-        const int32_t* b = boxes + 6 * r;
-        for (int k = 0; k < 3; ++k)
-            if (b[k] < 0 || b[3 + k] > g0.nc[k] || b[3 + k] - b[k] < 2)
-                return fail(ctx, MARDYN_EINVAL, "every box needs >= 2 cells per axis inside the grid (P:213)");
-        for (int z = b[2]; z < b[5]; ++z)
-            for (int y = b[1]; y < b[4]; ++y)
-                for (int x = b[0]; x < b[3]; ++x) {
-                    uint8_t& o = owner[x + (size_t)nx * (y + (size_t)ny * z)];
-                    if (o != 255) return fail(ctx, MARDYN_EINVAL, "boxes overlap");
-                    o = (uint8_t)r;
-                }
-    }
-    for (uint8_t o : owner)
-        if (o == 255) return fail(ctx, MARDYN_EINVAL, "boxes do not tile the grid");
-    // halo of rank r: cells within one cell (periodic) of its box, owned by another rank
-    std::vector<uint32_t> gmask((size_t)g0.ncell, 0u);
-    for (int r = 0; r < nranks; ++r) {
-        const int32_t* b = boxes + 6 * r;
-        for (int z = b[2] - 1; z <= b[5]; ++z)
-            for (int y = b[1] - 1; y <= b[4]; ++y)
-                for (int x = b[0] - 1; x <= b[3]; ++x) {
-                    const size_t c = (size_t)((x + nx) % nx) + (size_t)nx * (((y + ny) % ny) + (size_t)ny * ((z + nz) % nz));
-                    if (owner[c] != r) gmask[c] |= 1u << r;
-                }
-    }
-    ctx->dd_rank = rank;
-    ctx->nranks = nranks;
-    ctx->boxes.assign(boxes, boxes + 6 * nranks);
-    ctx->h_owner.swap(owner);
-    ctx->h_gmask.swap(gmask);
-    ctx->ndof_global = ndof_global;
-    const int32_t* b = boxes + 6 * rank;
-    GridP& g = ctx->g;
-    for (int k = 0; k < 3; ++k) { g.hlo[k] = b[k]; g.hdim[k] = b[3 + k] - b[k]; }
-    g.nhome = g.hdim[0] * g.hdim[1] * g.hdim[2];
-    if (ctx->ws) {          // rebalance: new maps; the caller reloads the molecules (set_molecules)
-        CK(cudaMemcpyAsync(ctx->owner, ctx->h_owner.data(), ctx->g.ncell, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync(ctx->gmask, ctx->h_gmask.data(), 4 * (size_t)ctx->g.ncell, cudaMemcpyHostToDevice,
-                           ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        ctx->loaded = false;
-    }
-    return MARDYN_OK;
-}
+// spatial decomposition across GPUs: the distributed engine and its C ABI
+#include "dist_engine.cuh"
 
-// forces at t_k on the home box, observables (rank-local partials), kick /
-// drift / rotation of the owned molecules, binning, and packing of the
-// exchange records: migrants for their new owners, halo copies for the
-// ranks whose halo holds the molecule's new cell.  Returns the records per
-// destination rank.
-int mardyn_dd_begin_step(mardyn_ctx* ctx, int64_t* send_counts)
-{
-    if (!ctx || !send_counts) return MARDYN_EINVAL;
-    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
-    if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
-    if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "no decomposition: use mardyn_step");
-    if (int rc0 = refresh_n(ctx)) return rc0;
-    cudaStream_t s = ctx->stream;
-    const int b = ctx->cur, n = (int)ctx->n;
-    long long step = ctx->host_step;
-    CK(cudaMemcpyAsync(ctx->step_ctr, &step, 8, cudaMemcpyHostToDevice, s));
-    CK(cudaEventRecord(ctx->ev_f0[b], s));
-    launch_force(ctx, b);
-    CK(cudaEventRecord(ctx->ev_f1[b], s));
-    CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
-    CK(cudaMemsetAsync(ctx->send_cnt, 0, sizeof(int) * ctx->nranks, s));
-    DDArgs dd;
-    dd.rank = ctx->dd_rank; dd.nranks = ctx->nranks; dd.owner = ctx->owner; dd.gmask = ctx->gmask;
-    dd.send = ctx->sendbuf; dd.seg_cap = (int)ctx->seg_cap; dd.send_cnt = ctx->send_cnt; dd.flag = ctx->flag;
-    dd.n_dev = nullptr;
-    dd.seg_tab = nullptr;                              // contiguous transport: uniform segments
-    const int nkb = nblk(n, 256);
-    if (ctx->rigid)
-        k_integrate<true, true><<<nkb, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b], ctx->quat[b],
-                                                    ctx->angm[b], ctx->force, ctx->torque, ctx->cell_of, ctx->rank,
-                                                    ctx->count, ctx->kpart, ctx->flag, dd);
-    else
-        k_integrate<false, true><<<nkb, 256, 0, s>>>(n, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b], nullptr,
-                                                     nullptr, ctx->force, ctx->torque, ctx->cell_of, ctx->rank,
-                                                     ctx->count, ctx->kpart, ctx->flag, dd);
-    k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, nkb, ctx->kpart, ctx->ndof,
-                                                  ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket, 0);
-    ctx->launches += 3;
-    CK(cudaGetLastError());
-    std::vector<int> cnt(ctx->nranks);
-    CK(cudaMemcpyAsync(cnt.data(), ctx->send_cnt, 4 * ctx->nranks, cudaMemcpyDeviceToHost, s));
-    int flag = 0;
-    CK(cudaMemcpyAsync(&flag, ctx->flag, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (flag & 256) return fail(ctx, MARDYN_ECAPACITY, "exchange segment overflow");
-    for (int r = 0; r < ctx->nranks; ++r) send_counts[r] = cnt[r];
-    ctx->last_parity = b;
-    return MARDYN_OK;
-}
-
-// device addresses of the exchange buffers: send segment r at
-// send + r * seg_cap records; the receive buffer holds records contiguously
-int mardyn_dd_buffers(mardyn_ctx* ctx, void** send, int64_t* seg_cap, void** recv, int64_t* recv_cap,
-                      int32_t* record_bytes)
-{
-    if (!ctx || !send || !seg_cap || !recv || !recv_cap || !record_bytes) return MARDYN_EINVAL;
-    if (ctx->nranks < 2 || !ctx->ws) return fail(ctx, MARDYN_ESTATE, "no decomposition workspace");
-    *send = ctx->sendbuf;
-    *seg_cap = ctx->seg_cap;
-    *recv = ctx->recvbuf;
-    *recv_cap = ctx->recv_cap;
-    *record_bytes = (int32_t)sizeof(DDRec);
-    return MARDYN_OK;
-}
-
-// import the n_recv records placed in the receive buffer, then rebuild the
-// cells (counting sort of owned + halo molecules) for the next step
-int mardyn_dd_end_step(mardyn_ctx* ctx, int64_t n_recv)
-{
-    if (!ctx) return MARDYN_EINVAL;
-    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
-    if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "no decomposition");
-    if (int rc0 = refresh_n(ctx)) return rc0;
-    if (n_recv < 0 || n_recv > ctx->recv_cap || ctx->n + n_recv > ctx->cap)
-        return fail(ctx, MARDYN_ECAPACITY, "received records exceed the capacity");
-    cudaStream_t s = ctx->stream;
-    const int b = ctx->cur;
-    if (n_recv > 0) {
-        k_import<<<nblk(n_recv, 256), 256, 0, s>>>((int)n_recv, (int)ctx->n, ctx->g, ctx->recvbuf, ctx->pos[b],
-                                                   ctx->vel[b], ctx->rigid ? ctx->quat[b] : nullptr,
-                                                   ctx->rigid ? ctx->angm[b] : nullptr, ctx->cell_of, ctx->rank,
-                                                   ctx->count);
-        ctx->launches += 1;
-    }
-    int rc = enqueue_sort(ctx, b, 1 - b, ctx->n + n_recv);
-    if (rc) return rc;
-    CK(cudaGetLastError());
-    int kept = 0;
-    CK(cudaMemcpyAsync(&kept, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    ctx->n = kept;
-    ctx->cur = 1 - b;
-    ctx->host_step += 1;
-    ctx->last_obs = ctx->host_step - 1;
-    return MARDYN_OK;
-}
-
-// ---- asynchronous decomposed step (no host synchronisation): the same work as
-// dd_begin_step / dd_end_step, with the record counts kept in device memory and
-// the receive buffer laid out in fixed segments of seg_cap records per source
-// rank (segment r of rank d's receive buffer = rank r's send segment d).
-int mardyn_dd_set_segment(mardyn_ctx* ctx, int64_t seg_cap)
-{
-    if (!ctx) return MARDYN_EINVAL;
-    if (ctx->nranks < 2 || !ctx->ws) return fail(ctx, MARDYN_ESTATE, "no decomposition workspace");
-    if (seg_cap < 1 || seg_cap > ctx->seg_max) return fail(ctx, MARDYN_EINVAL, "segment capacity out of range");
-    ctx->seg_cap = seg_cap;
-    ctx->peer_segs = false;
-    ctx->direct = false;                   // peer targets were laid out for the per-peer segments
-    ctx->recv_span = seg_cap * ctx->nranks;
-    return MARDYN_OK;
-}
-
-// per-peer segments: send segment d (send_caps[d] records) at the sum of the earlier
-// send capacities, receive segment r (recv_caps[r]) likewise in the receive buffer
-int mardyn_dd_set_peer_segments(mardyn_ctx* ctx, const int64_t* send_caps, const int64_t* recv_caps)
-{
-    if (!ctx || !send_caps || !recv_caps) return MARDYN_EINVAL;
-    if (ctx->nranks < 2 || !ctx->ws) return fail(ctx, MARDYN_ESTATE, "no decomposition workspace");
-    const int p = ctx->nranks;
-    std::vector<int> tab(4 * (size_t)p);
-    int64_t so = 0, ro = 0;
-    for (int r = 0; r < p; ++r) {
-        if (send_caps[r] < 1 || recv_caps[r] < 1) return fail(ctx, MARDYN_EINVAL, "segment capacities must be >= 1");
-        tab[r] = (int)so; tab[p + r] = (int)send_caps[r];
-        tab[2 * p + r] = (int)ro; tab[3 * p + r] = (int)recv_caps[r];
-        so += send_caps[r];
-        ro += recv_caps[r];
-    }
-    if (so > ctx->seg_max * p || ro > ctx->recv_cap)
-        return fail(ctx, MARDYN_EINVAL, "segment capacities exceed the exchange buffers");
-    CK(cudaMemcpyAsync(ctx->seg_tab, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    ctx->peer_segs = true;
-    ctx->direct = false;                   // new offsets: the peer targets must be set again
-    ctx->recv_span = ro;
-    return MARDYN_OK;
-}
-
-int mardyn_dd_set_peer_targets(mardyn_ctx* ctx, const uint64_t* rec_addr, const uint64_t* cnt_addr)
-{
-    if (!ctx) return MARDYN_EINVAL;
-    if (ctx->nranks < 2 || !ctx->ws) return fail(ctx, MARDYN_ESTATE, "no decomposition workspace");
-    if (!rec_addr || !cnt_addr) {
-        ctx->direct = false;
-        return MARDYN_OK;
-    }
-    const int p = ctx->nranks;
-    std::vector<uint64_t> tab(2 * (size_t)p);
-    for (int r = 0; r < p; ++r) {
-        if (!rec_addr[r] || rec_addr[r] % 16 || !cnt_addr[r] || cnt_addr[r] % 4)
-            return fail(ctx, MARDYN_EINVAL, "peer target addresses must be non-null and aligned (16 B records, 4 B counts)");
-        tab[r] = rec_addr[r];
-        tab[p + r] = cnt_addr[r];
-    }
-    CK(cudaMemcpyAsync(ctx->put_rec, tab.data(), sizeof(uint64_t) * p, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->put_cnt, tab.data() + p, sizeof(uint64_t) * p, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    ctx->direct = true;
-    return MARDYN_OK;
-}
-
-int mardyn_dd_device_counts(mardyn_ctx* ctx, void** send_cnt, void** recv_cnt)
-{
-    if (!ctx || !send_cnt || !recv_cnt) return MARDYN_EINVAL;
-    if (ctx->nranks < 2 || !ctx->ws) return fail(ctx, MARDYN_ESTATE, "no decomposition workspace");
-    *send_cnt = ctx->send_cnt;
-    *recv_cnt = ctx->recv_cnt;
-    return MARDYN_OK;
-}
-
-int mardyn_dd_begin_step_async(mardyn_ctx* ctx)
-{
-    if (!ctx) return MARDYN_EINVAL;
-    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
-    if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
-    if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "no decomposition: use mardyn_step");
-    cudaStream_t s = ctx->stream;
-    const int b = ctx->cur;
-    // (the device step counter already equals host_step: set_molecules / compute_forces set
-    // it, every finalize advances it; no host-to-device copy, which from pageable memory
-    // would synchronise the stream)
-    CK(cudaMemcpyAsync(ctx->n_aux + 1, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToDevice, s));
-    DDArgs dd;
-    dd.rank = ctx->dd_rank; dd.nranks = ctx->nranks; dd.owner = ctx->owner; dd.gmask = ctx->gmask;
-    dd.send = ctx->sendbuf; dd.seg_cap = (int)ctx->seg_cap; dd.send_cnt = ctx->send_cnt; dd.flag = ctx->flag;
-    dd.n_dev = ctx->start + ctx->g.ncell;             // the sorted count of the last cell rebuild
-    dd.seg_tab = ctx->peer_segs ? ctx->seg_tab : nullptr;
-    dd.put_rec = ctx->direct ? ctx->put_rec : nullptr;
-    CK(cudaMemsetAsync(ctx->send_cnt, 0, sizeof(int) * ctx->nranks, s));
-    if (ctx->kernel == KER_LJ1) {
-        // single-site kernel with the leapfrog, binning and exchange packing fused in (the
-        // cell counts are zero: the last rebuild's scan cleared them)
-        CK(cudaEventRecord(ctx->ev_f0[b], s));
-        launch_force(ctx, b, true, false, &dd);
-        CK(cudaEventRecord(ctx->ev_f1[b], s));
-        if (ctx->direct) {
-            k_put_counts<<<1, 32, 0, s>>>(ctx->nranks, ctx->send_cnt, ctx->put_cnt);
-            ctx->launches += 1;
-        }
-        // the observables of the step on a side stream, concurrent with the exchange and the
-        // cell rebuild (joined at the end of mardyn_dd_end_step_async)
-        CK(cudaEventRecord(ctx->ev_s0, s));
-        CK(cudaStreamWaitEvent(ctx->side_stream, ctx->ev_s0, 0));
-        k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, ctx->side_stream>>>(ctx->nfpart, ctx->fpart, 0, ctx->kpart, ctx->ndof,
-                                                      ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket, 0);
-        CK(cudaEventRecord(ctx->ev_s1, ctx->side_stream));
-        ctx->side_join = true;
-        ctx->launches += 1;
-        CK(cudaGetLastError());
-        ctx->last_parity = b;
-        return MARDYN_OK;
-    }
-    CK(cudaEventRecord(ctx->ev_f0[b], s));
-    launch_force(ctx, b);
-    CK(cudaEventRecord(ctx->ev_f1[b], s));
-    CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
-    const int nkb = ctx->nkblocks;
-    if (ctx->rigid)
-        k_integrate<true, true><<<nkb, 256, 0, s>>>((int)ctx->cap, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
-                                                    ctx->quat[b], ctx->angm[b], ctx->force, ctx->torque, ctx->cell_of,
-                                                    ctx->rank, ctx->count, ctx->kpart, ctx->flag, dd);
-    else
-        k_integrate<false, true><<<nkb, 256, 0, s>>>((int)ctx->cap, ctx->g, ctx->dmodel, ctx->pos[b], ctx->vel[b],
-                                                     nullptr, nullptr, ctx->force, ctx->torque, ctx->cell_of,
-                                                     ctx->rank, ctx->count, ctx->kpart, ctx->flag, dd);
-    if (ctx->direct) {
-        k_put_counts<<<1, 32, 0, s>>>(ctx->nranks, ctx->send_cnt, ctx->put_cnt);
-        ctx->launches += 1;
-    }
-    k_finalize<<<FIN_BLOCKS, FIN_THREADS, 0, s>>>(ctx->nfpart, ctx->fpart, nkb, ctx->kpart, ctx->ndof,
-                                                  ctx->step_ctr, 1, ctx->hist, ctx->fin_scratch, ctx->fin_ticket, 0);
-    ctx->launches += 3;
-    CK(cudaGetLastError());
-    ctx->last_parity = b;
-    return MARDYN_OK;
-}
-
-int mardyn_dd_end_step_async(mardyn_ctx* ctx)
-{
-    if (!ctx) return MARDYN_EINVAL;
-    if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
-    if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "no decomposition");
-    if (!ctx->peer_segs && ctx->seg_cap * ctx->nranks > ctx->recv_cap)
-        return fail(ctx, MARDYN_ESTATE, "segment capacity x ranks exceeds the receive buffer (mardyn_dd_set_segment)");
-    cudaStream_t s = ctx->stream;
-    const int b = ctx->cur;
-    const int seg = (int)ctx->seg_cap;
-    const int64_t span = ctx->peer_segs ? ctx->recv_span : (int64_t)seg * ctx->nranks;
-    k_import_seg<<<nblk(span, 256), 256, 0, s>>>(
-        ctx->nranks, seg, ctx->peer_segs ? ctx->seg_tab + 2 * ctx->nranks : nullptr, ctx->recv_cnt,
-        ctx->start + ctx->g.ncell, (int)ctx->cap, ctx->g, ctx->recvbuf, ctx->pos[b],
-        ctx->vel[b], ctx->rigid ? ctx->quat[b] : nullptr, ctx->rigid ? ctx->angm[b] : nullptr, ctx->cell_of,
-        ctx->rank, ctx->count, ctx->n_aux, ctx->flag);
-    ctx->launches += 1;
-    int rc = enqueue_sort(ctx, b, 1 - b, -1, ctx->n_aux);
-    if (rc) return rc;
-    if (ctx->side_join) {                              // the next step's force rewrites the partials
-        CK(cudaStreamWaitEvent(s, ctx->ev_s1, 0));
-        ctx->side_join = false;
-    }
-    CK(cudaGetLastError());
-    ctx->n_stale = true;
-    ctx->cur = 1 - b;
-    ctx->host_step += 1;
-    ctx->last_obs = ctx->host_step - 1;
-    return MARDYN_OK;
-}
+extern "C" {
 
 int mardyn_cell_cost(const int32_t* counts, int32_t nx, int32_t ny, int32_t nz, double* cost)
 {
@@ -1608,6 +1305,7 @@ const char* mardyn_last_error(const mardyn_ctx* ctx) { return ctx ? ctx->err.c_s
 void mardyn_destroy(mardyn_ctx* ctx)
 {
     if (!ctx) return;
+    group_release(ctx);
     for (int b = 0; b < 2; ++b) {
         if (ctx->gexec[b]) cudaGraphExecDestroy(ctx->gexec[b]);
         if (ctx->ev_f0[b]) cudaEventDestroy(ctx->ev_f0[b]);

@@ -28,11 +28,9 @@ EXPORTS = ["mardyn_create", "mardyn_get_grid", "mardyn_workspace_bytes", "mardyn
            "mardyn_get_observable_history", "mardyn_get_molecules", "mardyn_get_forces",
            "mardyn_get_raw", "mardyn_last_step_timing", "mardyn_set_profiling",
            "mardyn_launch_count", "mardyn_cell_cost", "mardyn_kd_decompose",
-           "mardyn_set_decomposition", "mardyn_dd_begin_step", "mardyn_dd_buffers", "mardyn_dd_end_step",
-           "mardyn_dd_set_segment", "mardyn_dd_set_peer_segments", "mardyn_dd_device_counts",
-           "mardyn_dd_set_peer_targets",
-           "mardyn_dd_begin_step_async",
-           "mardyn_dd_end_step_async",
+           "mardyn_nccl_unique_id", "mardyn_create_distributed", "mardyn_create_loopback",
+           "mardyn_partition", "mardyn_set_partition", "mardyn_get_partition", "mardyn_dd_counts",
+           "mardyn_rebalance", "mardyn_grid_counts", "mardyn_kd_partition",
            "mardyn_set_thermostat", "mardyn_lj_tail", "mardyn_get_tail_corrections",
            "mardyn_last_error", "mardyn_destroy"]
 
@@ -63,7 +61,8 @@ class Component(C.Structure):
 
 class Options(C.Structure):
     _fields_ = [("dt", C.c_double), ("eps_rf", C.c_double), ("lj_shift", C.c_int32),
-                ("eta", C.POINTER(C.c_double)), ("cuda_stream", C.c_void_p)]
+                ("eta", C.POINTER(C.c_double)), ("rebalance_interval", C.c_int32),
+                ("cuda_stream", C.c_void_p)]
 
 
 class Observables(C.Structure):
@@ -106,20 +105,22 @@ def load_library():
     lib.mardyn_get_observable_history.argtypes = [vp, C.c_int32, P(C.c_int32), P(Observables)]
     lib.mardyn_get_molecules.argtypes = [vp, C.c_int64, P(C.c_int64), vp, vp, vp, vp, vp, vp]
     lib.mardyn_get_forces.argtypes = [vp, C.c_int64, vp, vp, P(C.c_int64), vp]
-    lib.mardyn_set_decomposition.argtypes = [vp, C.c_int32, C.c_int32, vp, C.c_double]
+    lib.mardyn_nccl_unique_id.argtypes = [vp]
+    lib.mardyn_create_distributed.argtypes = [P(C.c_double), C.c_double, P(Component), C.c_int32, P(Options), vp,
+                                              C.c_int32, C.c_int32, C.c_int32, P(vp)]
+    lib.mardyn_create_loopback.argtypes = [P(C.c_double), C.c_double, P(Component), C.c_int32, P(Options),
+                                           C.c_int32, P(vp)]
+    lib.mardyn_partition.argtypes = [vp, C.c_int64, vp]
+    lib.mardyn_set_partition.argtypes = [vp, vp]
+    lib.mardyn_get_partition.argtypes = [vp, vp]
+    lib.mardyn_dd_counts.argtypes = [vp, C.c_int64, vp, vp]
+    lib.mardyn_rebalance.argtypes = [vp]
+    lib.mardyn_grid_counts.argtypes = [P(C.c_double), C.c_double, C.c_int64, vp, vp, vp]
+    lib.mardyn_kd_partition.argtypes = [P(C.c_double), C.c_double, C.c_int64, vp, C.c_int32, vp, vp]
     lib.mardyn_set_thermostat.argtypes = [vp, C.c_double, C.c_int32]
     lib.mardyn_lj_tail.argtypes = [P(Component), C.c_int32, vp, vp, C.c_double, C.c_double, P(C.c_double),
                                    P(C.c_double)]
     lib.mardyn_get_tail_corrections.argtypes = [vp, P(C.c_double), P(C.c_double)]
-    lib.mardyn_dd_begin_step.argtypes = [vp, vp]
-    lib.mardyn_dd_buffers.argtypes = [vp, P(vp), P(C.c_int64), P(vp), P(C.c_int64), P(C.c_int32)]
-    lib.mardyn_dd_end_step.argtypes = [vp, C.c_int64]
-    lib.mardyn_dd_set_segment.argtypes = [vp, C.c_int64]
-    lib.mardyn_dd_set_peer_segments.argtypes = [vp, vp, vp]
-    lib.mardyn_dd_device_counts.argtypes = [vp, P(vp), P(vp)]
-    lib.mardyn_dd_set_peer_targets.argtypes = [vp, vp, vp]
-    lib.mardyn_dd_begin_step_async.argtypes = [vp]
-    lib.mardyn_dd_end_step_async.argtypes = [vp]
     lib.mardyn_get_raw.argtypes = [vp, C.c_int64, vp, vp, vp]
     lib.mardyn_last_step_timing.argtypes = [vp, P(C.c_double), P(C.c_double), P(C.c_int32)]
     lib.mardyn_set_profiling.argtypes = [vp, C.c_int32]
@@ -188,13 +189,29 @@ class Context:
     """One simulation box on the current CUDA device (mardyn_ctx)."""
 
     def __init__(self, box, cutoff, components, dt, eps_rf=math.inf, lj_shift=1, eta=None,
-                 capacity=None, stream=None):
+                 capacity=None, stream=None, rebalance_interval=0, _handle=None, _keep=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("mardyn needs a CUDA device (there is no CPU fallback)")
         self.lib = load_library()
         self.torch = torch
         self.stream = stream if stream is not None else torch.cuda.Stream()
+        self.ws = None
+        self.capacity = 0
+        self.rank, self.nranks = 0, 1
+        if _handle is not None:                  # a rank of a group made by create_loopback
+            self.h, self._keep = _handle, _keep
+            return
+        self.h = None
+        opt, box_a, comps, n = self._options(box, components, dt, eps_rf, lj_shift, eta, rebalance_interval)
+        h = C.c_void_p()
+        rc = self.lib.mardyn_create(box_a, float(cutoff), comps, n, C.byref(opt), C.byref(h))
+        self.h = h
+        self._check(rc)
+        if capacity is not None:
+            self.reserve(capacity)
+
+    def _options(self, box, components, dt, eps_rf, lj_shift, eta, rebalance_interval):
         comps, self._keep = _components(components)
         self._eta = None if eta is None else np.ascontiguousarray(eta, dtype=np.float64)
         opt = Options()
@@ -202,16 +219,55 @@ class Context:
         opt.eps_rf = float(eps_rf)
         opt.lj_shift = int(lj_shift)
         opt.eta = None if self._eta is None else self._eta.ctypes.data_as(C.POINTER(C.c_double))
+        opt.rebalance_interval = int(rebalance_interval)
         opt.cuda_stream = C.c_void_p(self.stream.cuda_stream)
         box_a = (C.c_double * 3)(*[float(x) for x in box])
+        return opt, box_a, comps, len(components)
+
+    @classmethod
+    def distributed(cls, box, cutoff, components, dt, nccl_id, rank, world, device=None, eps_rf=math.inf,
+                    lj_shift=1, eta=None, stream=None, rebalance_interval=0):
+        """One rank of a decomposed run over NCCL (mardyn_create_distributed); nccl_id:
+        the 128 bytes of rank 0's nccl_unique_id(), broadcast by the caller."""
+        import torch
+        self = cls.__new__(cls)
+        self.lib = load_library()
+        self.torch = torch
+        dev = torch.cuda.current_device() if device is None else int(device)
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=dev)
+        self.ws, self.capacity, self.h = None, 0, None
+        opt, box_a, comps, n = self._options(box, components, dt, eps_rf, lj_shift, eta, rebalance_interval)
+        uid = C.create_string_buffer(bytes(nccl_id), 128)
         h = C.c_void_p()
-        rc = self.lib.mardyn_create(box_a, float(cutoff), comps, len(components), C.byref(opt), C.byref(h))
+        rc = self.lib.mardyn_create_distributed(box_a, float(cutoff), comps, n, C.byref(opt), uid, int(rank),
+                                                int(world), dev, C.byref(h))
         self.h = h
-        self.ws = None
-        self.capacity = 0
         self._check(rc)
-        if capacity is not None:
-            self.reserve(capacity)
+        self.rank, self.nranks = int(rank), int(world)
+        return self
+
+    @classmethod
+    def loopback(cls, box, cutoff, components, dt, p, eps_rf=math.inf, lj_shift=1, eta=None, stream=None,
+                 rebalance_interval=0):
+        """p ranks of a decomposed run in this process on the current device, one
+        stream (mardyn_create_loopback): returns their contexts in rank order."""
+        import torch
+        lead = cls.__new__(cls)
+        lead.lib = load_library()
+        lead.torch = torch
+        lead.stream = stream if stream is not None else torch.cuda.Stream()
+        lead.ws, lead.capacity, lead.h = None, 0, None
+        opt, box_a, comps, n = lead._options(box, components, dt, eps_rf, lj_shift, eta, rebalance_interval)
+        hs = (C.c_void_p * p)()
+        rc = lead.lib.mardyn_create_loopback(box_a, float(cutoff), comps, n, C.byref(opt), int(p), hs)
+        out = [cls(None, None, None, None, stream=lead.stream, _handle=C.c_void_p(hs[r]), _keep=lead._keep)
+               for r in range(p)]
+        for r, c in enumerate(out):
+            c.rank, c.nranks = r, p
+        if rc != MARDYN_OK:
+            msg = lead.lib.mardyn_last_error(out[0].h).decode() if hs[0] else ""
+            raise MardynError(rc, msg)
+        return out
 
     # -- plumbing ---------------------------------------------------------
     def _check(self, rc):
@@ -305,7 +361,6 @@ class Context:
             return F[:m], tau[:m], ids[:m]
         return F[:m], tau[:m]
 
-    # -- spatial decomposition (one context per rank) ----------------------
     def set_thermostat(self, T_target, interval=1):
         """NVT velocity rescaling every `interval` steps (reading A24); T_target = 0: NVE."""
         self._check(self.lib.mardyn_set_thermostat(self.h, float(T_target), int(interval)))
@@ -316,67 +371,32 @@ class Context:
         self._check(self.lib.mardyn_get_tail_corrections(self.h, C.byref(U), C.byref(W)))
         return U.value, W.value
 
-    def set_decomposition(self, rank, nranks, boxes, ndof_global):
-        b = np.ascontiguousarray(np.asarray(boxes, dtype=np.int32).reshape(nranks, 6))
-        self._dd_boxes = b
-        self._check(self.lib.mardyn_set_decomposition(self.h, int(rank), int(nranks),
-                                                      b.ctypes.data_as(C.c_void_p), float(ndof_global)))
-        self.rank, self.nranks = int(rank), int(nranks)
+    # -- spatial decomposition (one context per rank; include/mardyn.h) -----
+    def partition(self, r):
+        """k-d partition from the global positions (mardyn_partition)."""
+        ra = np.ascontiguousarray(r, dtype=np.float64)
+        self._check(self.lib.mardyn_partition(self.h, len(ra), ra.ctypes.data_as(C.c_void_p)))
 
-    def dd_begin_step(self):
-        cnt = np.zeros(self.nranks, np.int64)
-        self._check(self.lib.mardyn_dd_begin_step(self.h, cnt.ctypes.data_as(C.c_void_p)))
-        return cnt
+    def set_partition(self, boxes):
+        b = np.ascontiguousarray(np.asarray(boxes, dtype=np.int32).reshape(self.nranks, 6))
+        self._check(self.lib.mardyn_set_partition(self.h, b.ctypes.data_as(C.c_void_p)))
 
-    def dd_buffers(self):
-        """(send tensor view [nranks, seg_cap, rec], recv tensor view [recv_cap, rec])
-        as uint8 slices of the workspace tensor (zero copy)."""
-        send = C.c_void_p(); seg = C.c_int64(); recv = C.c_void_p(); rcap = C.c_int64(); rb = C.c_int32()
-        self._check(self.lib.mardyn_dd_buffers(self.h, C.byref(send), C.byref(seg), C.byref(recv),
-                                               C.byref(rcap), C.byref(rb)))
-        base = self.ws.data_ptr()
-        so, ro = send.value - base, recv.value - base
-        sb = self.ws[so: so + self.nranks * seg.value * rb.value].view(self.nranks, seg.value, rb.value)
-        rv = self.ws[ro: ro + rcap.value * rb.value].view(rcap.value, rb.value)
-        return sb, rv
+    def get_partition(self):
+        """Current boxes (p, 2, 3): [lo, hi] cell ranges in (x, y, z)."""
+        b = np.empty((self.nranks, 6), dtype=np.int32)
+        self._check(self.lib.mardyn_get_partition(self.h, b.ctypes.data_as(C.c_void_p)))
+        return b.reshape(self.nranks, 2, 3)
 
-    def dd_end_step(self, n_recv):
-        self._check(self.lib.mardyn_dd_end_step(self.h, int(n_recv)))
+    def dd_counts(self, r):
+        """Owned + halo molecules of every rank under the current partition."""
+        ra = np.ascontiguousarray(r, dtype=np.float64)
+        out = np.zeros(max(self.nranks, 1), dtype=np.int64)
+        self._check(self.lib.mardyn_dd_counts(self.h, len(ra), ra.ctypes.data_as(C.c_void_p),
+                                              out.ctypes.data_as(C.c_void_p)))
+        return out
 
-    # asynchronous decomposed step (include/mardyn.h): counts stay in device memory
-    def dd_set_segment(self, seg_cap):
-        self._check(self.lib.mardyn_dd_set_segment(self.h, int(seg_cap)))
-
-    def dd_set_peer_segments(self, send_caps, recv_caps):
-        sc = np.ascontiguousarray(np.asarray(send_caps, dtype=np.int64))
-        rc = np.ascontiguousarray(np.asarray(recv_caps, dtype=np.int64))
-        self._check(self.lib.mardyn_dd_set_peer_segments(self.h, sc.ctypes.data_as(C.c_void_p),
-                                                         rc.ctypes.data_as(C.c_void_p)))
-
-    def dd_set_peer_targets(self, rec_addrs, cnt_addrs):
-        """Direct puts (include/mardyn.h): device addresses, per destination rank, of this
-        rank's receive segment and count entry in that rank's buffers; None: transport."""
-        if rec_addrs is None:
-            self._check(self.lib.mardyn_dd_set_peer_targets(self.h, None, None))
-            return
-        ra = np.ascontiguousarray(np.asarray(rec_addrs, dtype=np.uint64))
-        ca = np.ascontiguousarray(np.asarray(cnt_addrs, dtype=np.uint64))
-        self._check(self.lib.mardyn_dd_set_peer_targets(self.h, ra.ctypes.data_as(C.c_void_p),
-                                                        ca.ctypes.data_as(C.c_void_p)))
-
-    def dd_device_counts(self):
-        """(send_cnt, recv_cnt): int32 [nranks] tensor views of the workspace (zero copy)."""
-        sc = C.c_void_p(); rc = C.c_void_p()
-        self._check(self.lib.mardyn_dd_device_counts(self.h, C.byref(sc), C.byref(rc)))
-        base = self.ws.data_ptr()
-        view = lambda ptr: self.ws[ptr - base: ptr - base + 4 * self.nranks].view(self.torch.int32)
-        return view(sc.value), view(rc.value)
-
-    def dd_begin_step_async(self):
-        self._check(self.lib.mardyn_dd_begin_step_async(self.h))
-
-    def dd_end_step_async(self):
-        self._check(self.lib.mardyn_dd_end_step_async(self.h))
+    def rebalance(self):
+        self._check(self.lib.mardyn_rebalance(self.h))
 
     def _n(self):
         n = C.c_int64()
@@ -450,362 +470,123 @@ def kd_decompose(cost, p):
     return boxes.reshape(p, 2, 3), loads
 
 
-def system_ndof(system):
-    """3 N + rotational degrees of freedom (nonzero principal moments), A9."""
-    rot = np.array([sum(1 for x in c["inertia"] if x > 0) for c in system["components"]])
-    return float(3 * len(system["r"]) + rot[np.asarray(system["comp"])].sum())
+def grid_counts(box, cutoff, r):
+    """Molecules per cell (nz, ny, nx) of the A12 lattice (mardyn_grid_counts; host)."""
+    lib = load_library()
+    b = (C.c_double * 3)(*[float(x) for x in box])
+    ra = np.ascontiguousarray(r, dtype=np.float64).reshape(-1, 3)
+    nc = np.zeros(3, np.int32)
+    rc = lib.mardyn_grid_counts(b, float(cutoff), len(ra), ra.ctypes.data_as(C.c_void_p),
+                                nc.ctypes.data_as(C.c_void_p), None)
+    if rc:
+        raise MardynError(rc, "grid_counts")
+    out = np.zeros(int(np.prod(nc)), np.int32)
+    lib.mardyn_grid_counts(b, float(cutoff), len(ra), ra.ctypes.data_as(C.c_void_p), nc.ctypes.data_as(C.c_void_p),
+                           out.ctypes.data_as(C.c_void_p))
+    return out.reshape(nc[2], nc[1], nc[0])
 
 
-def global_costs(system):
-    """Eq. 6 per cell of the global grid (x fastest) for the k-d tree, from
-    the molecule counts per cell of edge >= rc (every rank computes the same)."""
-    box = np.asarray(system["box"], float)
-    n = np.floor(box / system["rc"]).astype(int)
-    c = np.minimum((np.asarray(system["r"]) % box / box * n).astype(int), n - 1)
-    counts = np.zeros((n[2], n[1], n[0]), np.int32)
-    np.add.at(counts, (c[:, 2], c[:, 1], c[:, 0]), 1)
-    return cell_cost(counts)
+def kd_partition(box, cutoff, r, p):
+    """k-d partition of positions r into p boxes (mardyn_kd_partition; host):
+    (boxes (p, 2, 3), loads (p,))."""
+    lib = load_library()
+    b = (C.c_double * 3)(*[float(x) for x in box])
+    ra = np.ascontiguousarray(r, dtype=np.float64).reshape(-1, 3)
+    boxes = np.empty((p, 6), np.int32)
+    loads = np.empty(p)
+    rc = lib.mardyn_kd_partition(b, float(cutoff), len(ra), ra.ctypes.data_as(C.c_void_p), int(p),
+                                 boxes.ctypes.data_as(C.c_void_p), loads.ctypes.data_as(C.c_void_p))
+    if rc:
+        raise MardynError(rc, "kd_partition")
+    return boxes.reshape(p, 2, 3), loads
 
 
-def peer_target_addrs(me, bases, rows, record_bytes):
-    """Direct puts (include/mardyn.h mardyn_dd_set_peer_targets): device addresses, per
-    destination rank d, of rank me's receive segment and count entry in d's buffers.
-    bases[d]: base address of d's (symmetric) allocation; rows[d] = [receive buffer offset,
-    count array offset (bytes, from bases[d]), then d's receive segment offsets (records)
-    per source rank].  Loopback: bases = 0 and absolute addresses."""
-    p = len(bases)
-    rec = [int(bases[d]) + int(rows[d][0]) + record_bytes * int(rows[d][2 + me]) for d in range(p)]
-    cnt = [int(bases[d]) + int(rows[d][1]) + 4 * me for d in range(p)]
-    return rec, cnt
+def broadcast_unique_id(dist):
+    """Rank 0's NCCL unique id (mardyn_nccl_unique_id) on every rank of the default
+    torch.distributed group (the 128 bytes SURVEY §8(b) has the caller broadcast)."""
+    obj = [nccl_unique_id() if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
 
 
-def exchange_records(send, cnt, recv, nranks, dist):
-    """Halo/migration transport between ranks:
-    send[d, :cnt[d]] goes to rank d; records from all ranks land contiguously
-    in recv in source-rank order.  Counts travel first (all_to_all_single),
-    then the records as grouped point-to-point send/recv (NCCL over NVLink on
-    GPUs, gloo on CPU).  Returns the number of records received."""
-    import torch
-    dev = recv.device
-    sc = torch.tensor([int(x) for x in cnt], dtype=torch.int64, device=dev)
-    rc = torch.empty_like(sc)
-    dist.all_to_all_single(rc, sc)
-    rcounts = rc.cpu().tolist()
-    outs, off = [], 0
-    for k in rcounts:
-        outs.append(recv[off: off + k])
-        off += k
-    me = dist.get_rank()
-    # gloo moves device tensors in its collectives but not point to point: stage through host
-    host = dev.type == "cuda" and dist.get_backend() != "nccl"
-    ops, land = [], []
-    for d in range(nranks):
-        if d == me:
-            if int(cnt[d]):
-                outs[d].copy_(send[d][: int(cnt[d])])
-            continue
-        if int(cnt[d]):
-            t = send[d][: int(cnt[d])].contiguous()
-            ops.append(dist.P2POp(dist.isend, t.cpu() if host else t, d))
-        if rcounts[d]:
-            t = torch.empty(outs[d].shape, dtype=outs[d].dtype) if host else outs[d]
-            land.append((outs[d], t))
-            ops.append(dist.P2POp(dist.irecv, t, d))
-    if ops:
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
-    if host:
-        for o, t in land:
-            o.copy_(t)
-    return off
-
-
-def exchange_segments(send, send_cnt, recv, recv_cnt, nranks, dist, send_caps=None, recv_caps=None):
-    """Transport of the asynchronous decomposed step (include/mardyn.h): rank r's
-    send segment d lands in segment r of rank d's receive buffer, and its record
-    count send_cnt[d] in recv_cnt[r] of rank d.  send / recv: [records, bytes]
-    views of the exchange buffers with the segments back to back -- all of size
-    seg = len(send) / nranks (uniform), or send_caps[d] / recv_caps[r] records
-    (per-peer, static split sizes).  Two all-to-alls; nothing is read on the host
-    (NCCL over NVLink on GPUs, gloo on CPU)."""
-    dist.all_to_all_single(recv_cnt, send_cnt)
-    rb = send.shape[-1]
-    if send_caps is None:
-        n = send.shape[0]
-        dist.all_to_all_single(recv[:n].reshape(-1), send.reshape(-1))
-    else:
-        ns, nr = int(sum(send_caps)), int(sum(recv_caps))
-        dist.all_to_all_single(recv[:nr].reshape(-1), send[:ns].reshape(-1),
-                               output_split_sizes=[int(c) * rb for c in recv_caps],
-                               input_split_sizes=[int(c) * rb for c in send_caps])
+def nccl_unique_id():
+    """128-byte NCCL unique id (mardyn_nccl_unique_id; rank 0 calls it, the caller
+    broadcasts it)."""
+    lib = load_library()
+    buf = C.create_string_buffer(128)
+    rc = lib.mardyn_nccl_unique_id(buf)
+    if rc:
+        raise MardynError(rc, "nccl_unique_id: NCCL unavailable")
+    return bytes(buf.raw)
 
 
 class DecomposedRun:
-    """p spatial subdomains (k-d tree, §4) stepping together.
+    """p spatial subdomains (k-d tree, §4) stepping together.  All of the
+    method runs in the library (include/mardyn.h): the partition, the per-step halo
+    exchange and migration, the periodic rebalance and the global observables;
+    this class only creates the ranks, sizes their workspaces and steps them.
 
-    transport = "loopback": all ranks' contexts live in this process on one
-    device and records move by device copies (correctness path, 1 GPU).
-    transport = "nccl": one rank per process/GPU, records move with
-    torch.distributed all_to_all over NCCL (NVLink)."""
+    transport = "loopback": all ranks in this process on one device
+    (mardyn_create_loopback; the single-GPU correctness path).
+    transport = "nccl": one rank per process / GPU (mardyn_create_distributed;
+    the NCCL unique id travels by torch.distributed.broadcast_object_list)."""
 
     def __init__(self, system, nranks, transport="loopback", rank=None, eta=None, boxes=None, stream=None,
-                 rebalance_interval=0, async_exchange=True, direct=False):
+                 rebalance_interval=0, headroom=1.5):
         import torch
         self.torch = torch
-        # one stream for every local context and the transport: the asynchronous step
-        # orders the exchange after the packing and before the import by the stream alone
-        self.stream = stream if stream is not None else torch.cuda.Stream()
-        stream = self.stream
-        self.async_exchange = bool(async_exchange)
-        # device-initiated exchange: the packing kernels store the records straight into the
-        # receiving contexts' buffers -- loopback: same device, ordered by the stream; NCCL
-        # ranks: workspaces in symmetric memory (peer pointers over NVLink) and a device
-        # barrier before the puts and before the import of every step
-        self.direct = bool(direct) and self.async_exchange
-        self.symm = None
-        alloc = None
-        if self.direct and transport != "loopback":
+        self.system, self.nranks, self.transport = system, int(nranks), transport
+        args = (system["box"], system["rc"], system["components"], system["dt"])
+        kw = dict(eps_rf=system.get("eps_rf", math.inf), lj_shift=system.get("lj_shift", 1), eta=eta,
+                  stream=stream, rebalance_interval=rebalance_interval)
+        if transport == "loopback":
+            self.ctxs = Context.loopback(*args, self.nranks, **kw)
+            self.rank = None
+        else:
             import torch.distributed as dist
-            import torch.distributed._symmetric_memory as symm
-            try:
-                symm.enable_symm_mem_for_group(dist.group.WORLD.group_name)
-            except Exception:
-                pass
-            dev = torch.device("cuda", torch.cuda.current_device())
-            alloc = lambda nb: symm.empty(nb, dtype=torch.uint8, device=dev)
-        self.seg_ready = False
-        self.system = system
-        self.nranks = nranks
-        self.transport = transport
-        self.rank = rank
-        self.rebalance_interval = int(rebalance_interval)   # steps between re-partitions (0: static)
-        self.nsteps = 0
-        cost = global_costs(system)
-        if boxes is None:
-            boxes, loads = kd_decompose(cost, nranks)
-        self.boxes = np.asarray(boxes).reshape(nranks, 2, 3)
-        flat = np.concatenate([self.boxes[:, 0, :], self.boxes[:, 1, :]], axis=1)
-        ndof = system_ndof(system)
-        self.ndof = ndof
-        ranks = range(nranks) if transport == "loopback" else [rank]
-        self.ctxs = []
-        for r in ranks:
-            ctx = Context(system["box"], system["rc"], system["components"], system["dt"],
-                          eps_rf=system.get("eps_rf", math.inf), lj_shift=system.get("lj_shift", 1), eta=eta,
-                          stream=stream)
-            ctx.set_decomposition(r, nranks, flat, ndof)
-            # every rank takes the GLOBAL arrays in set_molecules (the library keeps the owned
-            # and halo molecules), so the capacity -- which also sizes the input staging -- is
-            # at least the global count; twice that holds owned + halo + received records of
-            # small boxes whose halo is as large as the box; the asynchronous step's
-            # capacity-wide grids exit early past the rank's molecules
-            ctx.reserve(2 * len(system["r"]), alloc=alloc)
-            if alloc is not None:
-                import torch.distributed as dist
-                import torch.distributed._symmetric_memory as symm
-                self.symm = symm.rendezvous(ctx.ws, dist.group.WORLD)
-            ctx.set_molecules(system["r"], system["v"], comp=system["comp"], q=system["q"], j=system["j"],
-                              id=system["id"], half_step=0)
-            self.ctxs.append(ctx)
-        self.bufs = [c.dd_buffers() for c in self.ctxs]
-        self.seg_max = int(self.bufs[0][0].shape[1])
+            uid = broadcast_unique_id(dist)
+            self.ctxs = [Context.distributed(*args, uid, rank, self.nranks, **kw)]
+            self.rank = int(rank)
+        self.lead = self.ctxs[0]
+        self.stream = self.lead.stream
+        r = system["r"]
+        for c in self.ctxs:
+            if boxes is None:
+                c.partition(r)
+            else:
+                c.set_partition(np.asarray(boxes).reshape(self.nranks, 6) if np.asarray(boxes).ndim != 2
+                                else boxes)
+        # workspace: owned + halo of the most loaded rank (the library counts them), with
+        # headroom for migration and for a rebalance that moves load between ranks
+        cap = int(headroom * int(self.lead.dd_counts(r).max())) + 4096
+        for c in self.ctxs:
+            c.reserve(cap)
+            c.set_molecules(r, system["v"], comp=system["comp"], q=system["q"], j=system["j"], id=system["id"],
+                            half_step=0)
 
-    def gather_molecules(self):
-        """All owned molecules of all ranks (v, j at t - dt/2), ordered by id."""
-        if self.transport == "loopback":
-            return self.molecules()
-        import torch.distributed as dist
-        parts = [None] * self.nranks
-        dist.all_gather_object(parts, self.ctxs[0].get_molecules())
-        ids = np.concatenate([p["id"] for p in parts])
-        order = np.argsort(ids)
-        return {k: np.concatenate([p[k] for p in parts])[order] for k in parts[0]}
-
-    def rebalance(self, boxes=None):
-        """Re-partition from the current cell counts (Eq. 6 cost of reading A19,
-        k-d tree with alternating axes and minimum-imbalance planes)
-        and reload every rank's owned + halo molecules (exact resume).  Returns
-        the new boxes."""
-        m = self.gather_molecules()
-        now = dict(self.system)
-        now["r"], now["comp"] = m["r"], m["comp"]
-        if boxes is None:
-            boxes, _ = kd_decompose(global_costs(now), self.nranks)
-        self.boxes = np.asarray(boxes).reshape(self.nranks, 2, 3)
-        flat = np.concatenate([self.boxes[:, 0, :], self.boxes[:, 1, :]], axis=1)
-        ranks = range(self.nranks) if self.transport == "loopback" else [self.rank]
-        for r, ctx in zip(ranks, self.ctxs):
-            ctx.set_decomposition(r, self.nranks, flat, self.ndof)
-            ctx.set_molecules(m["r"], m["v"], comp=m["comp"], q=m["q"], j=m["j"], id=m["id"], half_step=1)
-            ctx.dd_set_segment(int(ctx.dd_buffers()[0].shape[1]))
-        self.bufs = [c.dd_buffers() for c in self.ctxs]
-        self.seg_max = min(int(b[0].shape[1]) for b in self.bufs)
-        self.seg_ready = False                       # re-size the exchange segments for the new boxes
-        return self.boxes
-
-    def owned_counts(self):
-        """Owned molecules per rank (load balance check)."""
-        if self.transport == "loopback":
-            return [len(c.get_molecules()["id"]) for c in self.ctxs]
-        import torch.distributed as dist
-        parts = [None] * self.nranks
-        dist.all_gather_object(parts, len(self.ctxs[0].get_molecules()["id"]))
-        return parts
+    @property
+    def boxes(self):
+        return self.lead.get_partition()
 
     def step(self, n=1):
-        """n time steps of all local ranks.  The first step after construction or a
-        rebalance runs with host-side record counts and sizes the exchange segments
-        (twice the largest count + 1024 records); the following steps run
-        asynchronously (no host synchronisation: counts and records move between
-        ranks as two all-to-alls with equal splits, see include/mardyn.h)."""
-        with self.torch.cuda.stream(self.stream):
-            for _ in range(n):
-                if self.rebalance_interval and self.nsteps and self.nsteps % self.rebalance_interval == 0:
-                    self.rebalance()
-                self.nsteps += 1
-                if self.async_exchange and self.seg_ready:
-                    self._step_async()
-                    continue
-                counts = [c.dd_begin_step() for c in self.ctxs]
-                if self.transport == "loopback":
-                    for dst, cd in enumerate(self.ctxs):
-                        recv = self.bufs[dst][1]
-                        off = 0
-                        for src in range(self.nranks):
-                            k = int(counts[src][dst])
-                            if k:
-                                recv[off: off + k].copy_(self.bufs[src][0][dst, :k])
-                                off += k
-                        cd.dd_end_step(off)
-                else:
-                    self._nccl_exchange(counts[0])
-                if self.async_exchange:
-                    self._size_segments(counts)
+        self.lead.step(n)
 
-    def _size_segments(self, counts):
-        """Per-peer exchange segments from the first step's record counts: twice the
-        count + 1024 records (face neighbours send far more than edge or corner ones);
-        uniform segments if the per-peer ones do not fit the buffers."""
-        torch, p = self.torch, self.nranks
-        cap = lambda c: ((2 * int(c) + 1024 + 255) // 256) * 256
-        send_caps = [[cap(c) for c in cnt] for cnt in counts]          # per local rank, per destination
-        if self.transport == "loopback":
-            ranks = list(range(p))
-            recv_caps = [[send_caps[src][dst] for src in range(p)] for dst in range(p)]
-        else:
-            import torch.distributed as dist
-            ranks = [self.rank]
-            t = torch.tensor(send_caps[0], dtype=torch.int64, device="cuda")
-            r = torch.empty_like(t)
-            dist.all_to_all_single(r, t)
-            recv_caps = [r.tolist()]
-        recv_cap = int(self.bufs[0][1].shape[0])
-        fits = all(sum(sc) <= self.seg_max * p and sum(rc) <= recv_cap for sc, rc in zip(send_caps, recv_caps))
-        if self.transport != "loopback":
-            import torch.distributed as dist
-            t = torch.tensor([0 if fits else 1], dtype=torch.int32, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            fits = int(t.item()) == 0
-        if fits:
-            for c, sc, rc in zip(self.ctxs, send_caps, recv_caps):
-                c.dd_set_peer_segments(sc, rc)
-            self.send_caps, self.recv_caps = send_caps, recv_caps
-        else:
-            big = max(max(sc) for sc in send_caps)
-            if self.transport != "loopback":
-                t = torch.tensor([big], dtype=torch.int64, device="cuda")
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
-                big = int(t.item())
-            seg = min(self.seg_max, recv_cap // p, big)
-            for c in self.ctxs:
-                c.dd_set_segment(seg)
-            self.send_caps = [[seg] * p for _ in self.ctxs]
-            self.recv_caps = [[seg] * p for _ in self.ctxs]
-        self.bufs = [c.dd_buffers() for c in self.ctxs]
-        self.flat = [(sb.reshape(-1, sb.shape[-1]), rv) for sb, rv in self.bufs]   # [records, bytes] views
-        self.cnts = [c.dd_device_counts() for c in self.ctxs]
-        self.puts = False
-        if self.direct:
-            rb = int(self.flat[0][1].shape[-1])
-            offs = lambda caps: [int(sum(caps[:r])) for r in range(p)]
-            if self.transport == "loopback":
-                rows = [[self.flat[d][1].data_ptr(), self.cnts[d][1].data_ptr()] + offs(self.recv_caps[d])
-                        for d in range(p)]
-                for src, c in enumerate(self.ctxs):
-                    c.dd_set_peer_targets(*peer_target_addrs(src, [0] * p, rows, rb))
-            else:
-                import torch.distributed as dist
-                bases = list(self.symm.buffer_ptrs)
-                mine = [self.flat[0][1].data_ptr() - bases[self.rank],
-                        self.cnts[0][1].data_ptr() - bases[self.rank]] + offs(self.recv_caps[0])
-                t = torch.tensor(mine, dtype=torch.int64, device="cuda")
-                allt = [torch.empty_like(t) for _ in range(p)]
-                dist.all_gather(allt, t)
-                rows = [x.tolist() for x in allt]
-                self.ctxs[0].dd_set_peer_targets(*peer_target_addrs(self.rank, bases, rows, rb))
-            self.puts = True
-        self.seg_ready = True
-
-    def _step_async(self):
-        p = self.nranks
-        if self.puts and self.symm is not None:
-            self.symm.barrier(channel=0)       # every rank's last import done: its buffers are free
-        for c in self.ctxs:
-            c.dd_begin_step_async()
-        if self.puts:
-            # records and counts already stored by the packing kernels (peers: after the barrier)
-            if self.symm is not None:
-                self.symm.barrier(channel=0)
-        elif self.transport == "loopback":
-            soff = [np.concatenate([[0], np.cumsum(sc)[:-1]]) for sc in self.send_caps]
-            roff = [np.concatenate([[0], np.cumsum(rc)[:-1]]) for rc in self.recv_caps]
-            for dst in range(p):
-                rcnt = self.cnts[dst][1]
-                for src in range(p):
-                    c = int(self.send_caps[src][dst])
-                    a, b = int(roff[dst][src]), int(soff[src][dst])
-                    self.flat[dst][1][a: a + c].copy_(self.flat[src][0][b: b + c])
-                    rcnt[src: src + 1].copy_(self.cnts[src][0][dst: dst + 1])
-        else:
-            import torch.distributed as dist
-            send, recv = self.flat[0]
-            scnt, rcnt = self.cnts[0]
-            try:
-                exchange_segments(send, scnt, recv, rcnt, p, dist, self.send_caps[0], self.recv_caps[0])
-            except RuntimeError:
-                # a backend without these all-to-alls: finish this step with host-side
-                # counts and point-to-point records, and stay on that path
-                self.async_exchange = False
-                sc = self.send_caps[0]
-                off = np.concatenate([[0], np.cumsum(sc)[:-1]])
-                segs = [send[int(off[d]): int(off[d]) + int(sc[d])] for d in range(p)]
-                cnt = [min(int(x), int(sc[d])) for d, x in enumerate(scnt.cpu().tolist())]   # overflow: flagged
-                n = exchange_records(segs, cnt, recv, p, dist)
-                self.ctxs[0].dd_end_step(n)
-                return
-        for c in self.ctxs:
-            c.dd_end_step_async()
-
-    def _nccl_exchange(self, cnt):
-        import torch.distributed as dist
-        ctx = self.ctxs[0]
-        send, recv = self.bufs[0]
-        n = exchange_records(send, cnt, recv, self.nranks, dist)
-        ctx.dd_end_step(n)
+    def rebalance(self):
+        self.lead.rebalance()
+        return self.boxes
 
     def observables(self):
-        keys = ("U_pot", "virial", "T", "E_kin_trans", "E_kin_rot", "n_pairs", "n_candidates")
-        if self.transport == "loopback":
-            parts = [c.get_observables() for c in self.ctxs]
-        else:
-            import torch.distributed as dist
-            parts = [None] * self.nranks
-            dist.all_gather_object(parts, self.ctxs[0].get_observables())
-        out = dict(parts[0])
-        for k in keys:
-            out[k] = sum(p[k] for p in parts)        # rank order: deterministic
-        out["n_pairs"] //= 2                         # ranks report ordered pairs of owned molecules
-        return out
+        return self.lead.get_observables()
+
+    def observable_history(self, cap=4096):
+        return self.lead.get_observable_history(cap)
+
+    def compute_forces(self):
+        self.lead.compute_forces()
+
+    def owned_counts(self):
+        """Owned molecules per local rank."""
+        return [c._n() for c in self.ctxs]
 
     def molecules(self):
         """Owned molecules of the local ranks, merged and ordered by id."""

@@ -121,143 +121,66 @@ def test_slab_and_droplet_balance():
     assert loads.max() / loads.mean() < 1.1
 
 
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
 def _rank_main(rank, world, port, result):
+    """One rank of the distributed rebalance's host side: the rank bins the molecules it
+    owns on the A12 lattice (mardyn_grid_counts, the library's binning), the per-cell
+    counts are summed over the ranks (the engine's ncclAllReduce; gloo here), and every
+    rank computes Eq. 6 + the k-d tree through the C ABI."""
+    import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    import torch
     s = S.config("c4s")
-    # each rank owns half of the molecules and bins them (cells of edge >= rc)
-    n = np.floor(s["box"] / s["rc"]).astype(int)
     mine = np.arange(len(s["r"]))[rank::world]
-    c = np.minimum((s["r"][mine] / s["box"] * n).astype(int), n - 1)
-    counts = np.zeros((n[2], n[1], n[0]), np.int64)
-    np.add.at(counts, (c[:, 2], c[:, 1], c[:, 0]), 1)
+    counts = M.grid_counts(s["box"], s["rc"], s["r"][mine]).astype(np.int64)
     t = torch.from_numpy(counts)
     dist.all_reduce(t)                                # per-cell counts of all ranks
     cost = M.cell_cost(t.numpy().astype(np.int32))
     boxes, loads = M.kd_decompose(cost, 4)
     gathered = [None] * world
     dist.all_gather_object(gathered, boxes.tolist())
-    result[rank] = (gathered, int(t.sum()), float(loads.max() / loads.mean()))
+    uid = M.broadcast_unique_id(dist)                 # the NCCL id every rank creates its context with
+    ids = [None] * world
+    dist.all_gather_object(ids, uid)
+    result[rank] = (gathered, int(t.sum()), float(loads.max() / loads.mean()), ids)
     dist.destroy_process_group()
 
 
 def test_gloo_two_ranks_agree():
+    """world_size 2: the reduced per-cell loads give every rank the same k-d tree, equal to
+    the partition of the whole system (mardyn_kd_partition), and every rank receives rank
+    0's NCCL unique id."""
     import torch.multiprocessing as mp
-    import socket
-    with socket.socket() as so:
-        so.bind(("127.0.0.1", 0))
-        port = so.getsockname()[1]
     mgr = mp.Manager()
     result = mgr.dict()
-    mp.spawn(_rank_main, args=(2, port, result), nprocs=2, join=True)
-    g0, n0, imb0 = result[0]
-    g1, n1, imb1 = result[1]
-    assert g0[0] == g0[1] == g1[0] == g1[1]          # every rank builds the same tree
-    assert n0 == n1 == len(S.config("c4s")["r"])
+    mp.spawn(_rank_main, args=(2, _free_port(), result), nprocs=2, join=True)
+    g0, n0, imb0, ids0 = result[0]
+    g1, n1, imb1, ids1 = result[1]
+    s = S.config("c4s")
+    whole, _ = M.kd_partition(s["box"], s["rc"], s["r"], 4)
+    assert g0[0] == g0[1] == g1[0] == g1[1] == whole.tolist()   # every rank builds the same tree
+    assert n0 == n1 == len(s["r"])
     assert imb0 == imb1 and imb0 < 1.2
+    assert ids0[0] == ids0[1] == ids1[0] and len(ids0[0]) == 128
 
 
-def _xchg_main(rank, world, port, result):
-    import torch
-    import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    rec = 64
-    seg = 8
-    send = torch.zeros((world, seg, rec), dtype=torch.uint8)
-    cnt = [(rank + d) % 3 + 1 for d in range(world)]          # records for rank d
-    for d in range(world):
-        for k in range(cnt[d]):
-            send[d, k, 0] = rank
-            send[d, k, 1] = d
-            send[d, k, 2] = k
-    recv = torch.zeros((world * seg, rec), dtype=torch.uint8)
-    n = M.exchange_records(send, cnt, recv, world, dist)
-    result[rank] = (n, recv[:n, :3].tolist())
-    dist.destroy_process_group()
-
-
-def test_gloo_exchange_records():
-    """The multi-rank record transport (counts, then records in source-rank
-    order) on world_size 2 with gloo."""
-    import socket
-    import torch.multiprocessing as mp
-    with socket.socket() as so:
-        so.bind(("127.0.0.1", 0))
-        port = so.getsockname()[1]
-    mgr = mp.Manager()
-    result = mgr.dict()
-    mp.spawn(_xchg_main, args=(2, port, result), nprocs=2, join=True)
-    for dst in range(2):
-        n, rows = result[dst]
-        expect = [[src, dst, k] for src in range(2) for k in range((src + dst) % 3 + 1)]
-        assert n == len(expect) and rows == expect
-
-
-def _seg_main(rank, world, port, result):
-    import torch
-    import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    rec, seg = 64, 8
-    send = torch.zeros((world, seg, rec), dtype=torch.uint8)
-    scnt = torch.tensor([(rank + 2 * d) % 5 + 1 for d in range(world)], dtype=torch.int32)
-    for d in range(world):
-        for k in range(int(scnt[d])):
-            send[d, k, :3] = torch.tensor([rank, d, k], dtype=torch.uint8)
-    recv = torch.full((world * seg + 5, rec), 255, dtype=torch.uint8)   # receive capacity > nranks x seg
-    rcnt = torch.zeros(world, dtype=torch.int32)
-    M.exchange_segments(send.reshape(-1, rec), scnt, recv, rcnt, world, dist)
-    uniform = (rcnt.tolist(), recv[: world * seg, :3].tolist(), recv[world * seg:, 0].tolist())
-    # per-peer segments: rank r sends caps[r][d] records to d (back to back), d receives them
-    # back to back in source order
-    caps = [[6, 3], [2, 7]]
-    sc, rc = caps[rank], [caps[0][rank], caps[1][rank]]
-    flat = torch.zeros((sum(sc), rec), dtype=torch.uint8)
-    off = 0
-    for d in range(world):
-        for k in range(min(int(scnt[d]), sc[d])):
-            flat[off + k, :3] = torch.tensor([rank, d, k], dtype=torch.uint8)
-        off += sc[d]
-    recv2 = torch.full((sum(rc) + 3, rec), 255, dtype=torch.uint8)
-    rcnt2 = torch.zeros(world, dtype=torch.int32)
-    M.exchange_segments(flat, scnt, recv2, rcnt2, world, dist, sc, rc)
-    result[rank] = (uniform, (rcnt2.tolist(), recv2[:, :3].tolist(), rc))
-    dist.destroy_process_group()
-
-
-def test_gloo_exchange_segments():
-    """The asynchronous step's transport (fixed segments + device counts, two
-    equal-split all-to-alls) on world_size 2 with gloo: segment r of rank d's
-    receive buffer is rank r's send segment d, counts alongside, the rest of the
-    receive buffer untouched."""
-    import socket
-    import torch.multiprocessing as mp
-    with socket.socket() as so:
-        so.bind(("127.0.0.1", 0))
-        port = so.getsockname()[1]
-    mgr = mp.Manager()
-    result = mgr.dict()
-    mp.spawn(_seg_main, args=(2, port, result), nprocs=2, join=True)
-    for dst in range(2):
-        (rcnt, rows, tail), (rcnt2, rows2, rc) = result[dst]
-        assert rcnt == [(src + 2 * dst) % 5 + 1 for src in range(2)]
-        for src in range(2):
-            for k in range(rcnt[src]):
-                assert rows[8 * src + k] == [src, dst, k]
-        assert tail == [255] * 5
-        assert rcnt2 == rcnt
-        off = 0
-        for src in range(2):
-            for k in range(min(rcnt2[src], rc[src])):
-                assert rows2[off + k] == [src, dst, k]
-            off += rc[src]
-        assert rows2[off:] == [[255, 255, 255]] * 3
+def test_grid_counts_are_the_oracle_cells(oracle_mod):
+    """The library's host binning (used by mardyn_partition and the rebalance) is the
+    A12 cell rule: counts equal the oracle's on the same positions."""
+    for name in ("c1s", "c2s", "c4s"):
+        s = S.config(name)
+        o = oracle_mod.System(s)
+        _, cnt = o.cells(o.quantize(s["r"]))
+        nc = o.ncell
+        assert np.array_equal(M.grid_counts(s["box"], s["rc"], s["r"]), cnt.reshape(nc[2], nc[1], nc[0]))
 
 
 def test_droplet_kd_beats_static_split():
@@ -265,7 +188,7 @@ def test_droplet_kd_beats_static_split():
     direction of Fig. 7): the cost-weighted k-d tree balances the
     Eq. 6 load far better than equal-volume boxes."""
     s = S.droplet(L=50.0, R=13.0)                # 20 cells per axis
-    cost = M.global_costs(s)
+    cost = M.cell_cost(M.grid_counts(s["box"], s["rc"], s["r"]))
     nz, ny, nx = cost.shape
     for p in (2, 4, 8):
         boxes, loads = M.kd_decompose(cost, p)
@@ -278,51 +201,3 @@ def test_droplet_kd_beats_static_split():
               for z0, z1 in zip(cuts[2], cuts[2][1:])]
         static = max(st) / np.mean(st)
         assert kd < 1.25 and static > 1.5 * kd, (p, kd, static)
-
-
-def _puts_main(rank, world, port, result):
-    import torch
-    import torch.distributed as dist
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    rb = 64
-    caps = [[6, 3, 5], [2, 7, 4], [9, 1, 8]]                 # caps[src][dst]: per-peer segments
-    recv_caps = [caps[s][rank] for s in range(world)]
-    bases = [(d + 1) << 40 for d in range(world)]            # each rank's symmetric allocation
-    recv_off, cnt_off = 4096 * (rank + 1), 256 * (rank + 3)  # layouts may differ per rank
-    mine = [recv_off, cnt_off] + [sum(recv_caps[:s]) for s in range(world)]
-    t = torch.tensor(mine, dtype=torch.int64)
-    allt = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(allt, t)
-    rec, cnt = M.peer_target_addrs(rank, bases, [x.tolist() for x in allt], rb)
-    got = [torch.empty(2 * world, dtype=torch.int64) for _ in range(world)]
-    dist.all_gather(got, torch.tensor(rec + cnt, dtype=torch.int64))
-    # where every source's records and count land in this rank's buffers
-    result[rank] = (mine, [g.tolist() for g in got])
-    dist.destroy_process_group()
-
-
-def test_gloo_direct_put_targets():
-    """Direct puts across ranks (DecomposedRun(direct=True) over NCCL, peer pointers of
-    symmetric memory): the addresses rank src stores to for rank d -- its base plus d's
-    receive-buffer offset plus d's segment offset for src, and d's count entry src -- are
-    exactly where d's import reads source src (world_size 3, gloo, per-peer segments,
-    different layouts per rank)."""
-    import socket
-    import torch.multiprocessing as mp
-    with socket.socket() as so:
-        so.bind(("127.0.0.1", 0))
-        port = so.getsockname()[1]
-    mgr = mp.Manager()
-    result = mgr.dict()
-    mp.spawn(_puts_main, args=(3, port, result), nprocs=3, join=True)
-    caps = [[6, 3, 5], [2, 7, 4], [9, 1, 8]]
-    for d in range(3):
-        mine, got = result[d]
-        base = (d + 1) << 40
-        assert mine[0] == 4096 * (d + 1) and mine[1] == 256 * (d + 3)
-        for src in range(3):
-            seg_off = sum(caps[s][d] for s in range(src))
-            assert got[src][d] == base + mine[0] + 64 * seg_off
-            assert got[src][3 + d] == base + mine[1] + 4 * src
