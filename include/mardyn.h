@@ -213,8 +213,10 @@ int mardyn_get_forces(struct mardyn_ctx* ctx, int64_t cap, double* F, double* ta
 int mardyn_get_raw(struct mardyn_ctx* ctx, int64_t cap, uint32_t* pos_fixed,
                    int32_t* cell, int32_t* cell_count);
 
-/* Device timing of the last mardyn_step call: total ms and ms in the force
- * kernel (CUDA events on the context stream; 0 if not recorded).           */
+/* Device timing of the last step: force_ms = the force kernel (CUDA events on
+ * the context stream; 0 if not recorded); total_ms = on a decomposed context
+ * after an asynchronous step, this rank's own kernels of the step (its
+ * begin and end halves; the exchange wait excluded), else 0.               */
 int mardyn_last_step_timing(struct mardyn_ctx* ctx, double* total_ms, double* force_ms,
                             int32_t* force_launches);
 

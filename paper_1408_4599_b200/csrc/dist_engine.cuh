@@ -539,6 +539,7 @@ static int exchange_exact(Group* G, const std::vector<std::vector<int64_t>>& C, 
 static int group_sync_step(Group* G)
 {
     const int p = G->p;
+    for (mardyn_ctx* c : G->m) c->rank_timed = false;
     std::vector<std::vector<int64_t>> C(p, std::vector<int64_t>(p, 0));
     for (mardyn_ctx* c : G->m) {
         if (int rc = dd_begin_sync(c, C[c->dd_rank].data())) return rc;
@@ -597,8 +598,12 @@ static int group_sync_step(Group* G)
 // grouped send / recv on the context stream; loopback: the packing kernels already stored them
 static int group_async_step(Group* G)
 {
-    for (mardyn_ctx* c : G->m)
+    for (mardyn_ctx* c : G->m) {
+        mardyn_ctx* ctx = c;
+        if (c->profiling) CK(cudaEventRecord(c->ev_r[0], c->stream));
         if (int rc = dd_begin_async(c)) return rc;
+        if (c->profiling) CK(cudaEventRecord(c->ev_r[1], c->stream));
+    }
     if (G->nccl) {
         mardyn_ctx* ctx = G->m[0];
         const int p = G->p, me = ctx->dd_rank;
@@ -613,8 +618,13 @@ static int group_async_step(Group* G)
         }
         NCK(mdn::api().GroupEnd());
     }
-    for (mardyn_ctx* c : G->m)
+    for (mardyn_ctx* c : G->m) {
+        mardyn_ctx* ctx = c;
+        if (c->profiling) CK(cudaEventRecord(c->ev_r[2], c->stream));
         if (int rc = dd_end_async(c)) return rc;
+        if (c->profiling) CK(cudaEventRecord(c->ev_r[3], c->stream));
+        c->rank_timed = c->profiling;
+    }
     return MARDYN_OK;
 }
 

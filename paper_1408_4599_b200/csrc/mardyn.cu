@@ -102,6 +102,8 @@ struct mardyn_ctx {
     float4* site = nullptr;
     float4* force = nullptr;
     float4* torque = nullptr;
+    unsigned long long* rfix = nullptr;  // half-shell reactions, fixed point (6 x int64 per molecule)
+    float fscale = 1.f, tscale = 1.f;    // force / torque -> fixed point
     int* cell_of = nullptr;
     int* rank = nullptr;
     int* count = nullptr;
@@ -139,8 +141,12 @@ struct mardyn_ctx {
     int32_t* comp_dev = nullptr;       // components, input order
     // graphs: one time step starting from buffer parity 0 / 1
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    int64_t graph_n = -1;              // molecule count and N_dof the step graphs were built for
+    double graph_ndof = -1.0;
     cudaEvent_t ev_f0[2] = {nullptr, nullptr}, ev_f1[2] = {nullptr, nullptr};
     cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;      // fork / join of the graph's side branch
+    cudaEvent_t ev_r[4] = {nullptr, nullptr, nullptr, nullptr};   // decomposed step: this rank's begin / end
+    bool rank_timed = false;
     cudaStream_t side_stream = nullptr;
     int last_parity = 0;
     bool profiling = true;
@@ -337,6 +343,27 @@ static int build_model(mardyn_ctx* ctx)
             M.eps4[t] = (float)(4.0 * eps);
             M.shift[t] = ctx->lj_shift ? (float)(4.0 * eps * (sc6 * sc6 - sc6)) : 0.f;
         }
+    // fixed-point unit of the half-shell reactions: a force scale Fu of the model (24 eps / sigma
+    // of the LJ pairs, q_a q_b / sigma_min^2 of the charges); resolution ~2^-34 Fu per term, range
+    // ~5e8 Fu (int64)
+    {
+        double Fu = 0.0, smin = 0.0;
+        for (int a = 0; a < lj_total; ++a)
+            for (int b = 0; b < lj_total; ++b) {
+                const double sg = 0.5 * (ljsig[a] + ljsig[b]);
+                Fu = std::max(Fu, 24.0 * std::sqrt(ljeps[a] * ljeps[b]) / sg);
+                smin = smin > 0 ? std::min(smin, sg) : sg;
+            }
+        if (!(smin > 0)) smin = ctx->rc / 8.0;
+        for (int c = 0; c < nc; ++c)
+            for (int k = 0; k < M.comp[c].n_q + M.comp[c].n_mu + M.comp[c].n_Q; ++k) {
+                const double q = M.comp[c].mom[M.comp[c].n_lj + k];
+                Fu = std::max(Fu, q * q / (smin * smin));
+            }
+        if (!(Fu > 0)) Fu = 1.0;
+        ctx->fscale = (float)std::ldexp(1.0, (int)std::floor(std::log2(std::ldexp(1.0, 34) / Fu)));
+        ctx->tscale = (float)std::ldexp(1.0, (int)std::floor(std::log2(std::ldexp(1.0, 34) / (Fu * smin))));
+    }
     // kernel choice
     if (!ctx->rigid && nc == 1) {
         ctx->kernel = KER_LJ1;
@@ -408,13 +435,27 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_gra
     a.eps24 = ctx->model.eps24[0];
     a.eps4 = ctx->model.eps4[0];
     a.shift = ctx->model.shift[0];
+    a.rfix = ctx->rfix;
+    a.fscale = ctx->fscale;
+    a.tscale = ctx->tscale;
     const int threads = 32 * ctx->force_warps_per_block;
+    // one domain: the Newton-3 half shell (Fig. 1) with fixed-point reactions; a rank of
+    // a decomposition keeps the full shell (no reverse exchange of halo reactions)
+    const bool half = ctx->nranks == 1;
     switch (ctx->shape) {
     case SHAPE_2CLJQ:
-        rig3::k_force_rigid3<2, 0, 0, 1><<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
+        if (half)
+            rig3::k_force_rigid3<2, 0, 0, 1, true>
+                <<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1, true>(), ctx->stream>>>(a);
+        else
+            rig3::k_force_rigid3<2, 0, 0, 1><<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
         break;
     case SHAPE_TIP4P:
-        rig3::k_force_rigid3<1, 3, 0, 0><<<ctx->force_grid, threads, rig3::smem_bytes<1, 3, 0, 0>(), ctx->stream>>>(a);
+        if (half)
+            rig3::k_force_rigid3<1, 3, 0, 0, true>
+                <<<ctx->force_grid, threads, rig3::smem_bytes<1, 3, 0, 0, true>(), ctx->stream>>>(a);
+        else
+            rig3::k_force_rigid3<1, 3, 0, 0><<<ctx->force_grid, threads, rig3::smem_bytes<1, 3, 0, 0>(), ctx->stream>>>(a);
         break;
     case SHAPE_GEN:
         k_force_rigid<4, 4, 2, 2, true, GEN_WARPS>
@@ -454,6 +495,11 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_gra
     }
     }
     ctx->launches += 1;
+    if (half && (ctx->shape == SHAPE_2CLJQ || ctx->shape == SHAPE_TIP4P)) {
+        rig3::k_merge_reactions<<<(int)((ctx->n + 255) / 256), 256, 0, ctx->stream>>>(
+            (int)ctx->n, ctx->force, ctx->torque, ctx->rfix, 1.f / ctx->fscale, 1.f / ctx->tscale);
+        ctx->launches += 1;
+    }
     return MARDYN_OK;
 }
 
@@ -647,6 +693,8 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
     int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ: {
+        CK(cudaFuncSetAttribute(rig3::k_force_rigid3<2, 0, 0, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                rig3::smem_bytes<2, 0, 0, 1, true>()));
         auto k = rig3::k_force_rigid3<2, 0, 0, 1>;
         const int sm = rig3::smem_bytes<2, 0, 0, 1>();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -654,6 +702,8 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
         break;
     }
     case SHAPE_TIP4P: {
+        CK(cudaFuncSetAttribute(rig3::k_force_rigid3<1, 3, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                rig3::smem_bytes<1, 3, 0, 0, true>()));
         auto k = rig3::k_force_rigid3<1, 3, 0, 0>;
         const int sm = rig3::smem_bytes<1, 3, 0, 0>();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -677,6 +727,7 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
         CK(cudaEventCreate(&ctx->ev_f0[b]));
         CK(cudaEventCreate(&ctx->ev_f1[b]));
     }
+    for (int k = 0; k < 4; ++k) CK(cudaEventCreate(&ctx->ev_r[k]));
     CK(cudaEventCreateWithFlags(&ctx->ev_s0, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ctx->ev_s1, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
@@ -730,6 +781,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         site = (float4*)take((size_t)16 * cap * std::max(1, ctx->nslots));
         tq = (float4*)take(16 * cap);
     }
+    unsigned long long* rfix = ctx->kernel == KER_RIGID ? (unsigned long long*)take(48 * (size_t)cap) : nullptr;
     float4* xs = (float4*)take(16 * cap);
     float4* force = (float4*)take(16 * cap);
     int* cell_of = (int*)take(4 * cap);
@@ -785,7 +837,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     if (assign) {
         ctx->pos[0] = pos0; ctx->pos[1] = pos1; ctx->vel[0] = vel0; ctx->vel[1] = vel1;
         ctx->quat[0] = q0; ctx->quat[1] = q1; ctx->angm[0] = j0; ctx->angm[1] = j1;
-        ctx->site = site; ctx->torque = tq; ctx->xs = xs; ctx->force = force;
+        ctx->site = site; ctx->torque = tq; ctx->xs = xs; ctx->force = force; ctx->rfix = rfix;
         ctx->cell_of = cell_of; ctx->rank = rank; ctx->keys = keys; ctx->oldidx = oldidx; ctx->count = count;
         ctx->start = start; ctx->scan_flags = scan_flags; ctx->fin_scratch = fin_scratch; ctx->fin_ticket = fin_ticket; ctx->fpart = fpart; ctx->kpart = kpart;
         ctx->nfw = nfw; ctx->nfpart = nfw + nbc; ctx->blk_ctr = blk_ctr;
@@ -831,6 +883,7 @@ int mardyn_set_workspace(mardyn_ctx* ctx, void* device_ptr, size_t bytes, int64_
     CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, ctx->stream));
     if (ctx->blk_ctr) CK(cudaMemsetAsync(ctx->blk_ctr, 0, sizeof(int), ctx->stream));
     CK(cudaMemsetAsync(ctx->hist, 0, sizeof(ObsRec) * MD_HISTORY, ctx->stream));
+    if (ctx->rfix) CK(cudaMemsetAsync(ctx->rfix, 0, 48 * (size_t)n_capacity, ctx->stream));
     if (ctx->nranks > 1 && !ctx->h_owner.empty()) {
         CK(cudaMemcpyAsync(ctx->owner, ctx->h_owner.data(), ctx->g.ncell, cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemcpyAsync(ctx->gmask, ctx->h_gmask.data(), 4 * (size_t)ctx->g.ncell, cudaMemcpyHostToDevice,
@@ -884,14 +937,18 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
             const int64_t need = (units + upb - 1) / upb;
             grid = (int)std::max<int64_t>(1, std::min<int64_t>(grid, need));
         }
+        const bool regraph = grid != ctx->force_grid || n != ctx->graph_n || ndof != ctx->graph_ndof;
         if (grid != ctx->force_grid) {
             ctx->force_grid = grid;
             CK(cudaMemsetAsync(ctx->fpart, 0, sizeof(ForcePartial) * ctx->nfpart, s));
         }
-        // the step graphs hold the launch shape, the molecule count n and N_dof: rebuilt after
-        // every reload (a graph of the previous n would scatter stale or too few molecules)
-        for (int b = 0; b < 2; ++b)
-            if (ctx->gexec[b]) { cudaGraphExecDestroy(ctx->gexec[b]); ctx->gexec[b] = nullptr; }
+        ctx->graph_n = n;
+        ctx->graph_ndof = ndof;
+        // the step graphs hold the launch shape, the molecule count n and N_dof: rebuilt when a
+        // reload changes them (a graph of another n would scatter stale or too few molecules)
+        if (regraph)
+            for (int b = 0; b < 2; ++b)
+                if (ctx->gexec[b]) { cudaGraphExecDestroy(ctx->gexec[b]); ctx->gexec[b] = nullptr; }
     }
     // host -> device (the caller's buffers; pinned ones are DMA'd directly)
     double* dr = (double*)ctx->stage;
@@ -1246,7 +1303,16 @@ int mardyn_last_step_timing(mardyn_ctx* ctx, double* total_ms, double* force_ms,
         cudaError_t e = cudaEventElapsedTime(&f, ctx->ev_f0[ctx->last_parity], ctx->ev_f1[ctx->last_parity]);
         if (e != cudaSuccess) { f = 0.f; cudaGetLastError(); }
     }
-    if (total_ms) *total_ms = 0.0;
+    double tot = 0.0;
+    if (ctx->rank_timed) {        // decomposed step: this rank's own kernels (begin + end halves)
+        float a = 0.f, b = 0.f;
+        if (cudaEventElapsedTime(&a, ctx->ev_r[0], ctx->ev_r[1]) == cudaSuccess &&
+            cudaEventElapsedTime(&b, ctx->ev_r[2], ctx->ev_r[3]) == cudaSuccess)
+            tot = (double)a + (double)b;
+        else
+            cudaGetLastError();
+    }
+    if (total_ms) *total_ms = tot;
     if (force_ms) *force_ms = f;
     if (force_launches) *force_launches = 1;
     return MARDYN_OK;
@@ -1312,6 +1378,8 @@ void mardyn_destroy(mardyn_ctx* ctx)
         if (ctx->ev_f1[b]) cudaEventDestroy(ctx->ev_f1[b]);
     }
     if (ctx->side_stream) cudaStreamDestroy(ctx->side_stream);
+    for (int k = 0; k < 4; ++k)
+        if (ctx->ev_r[k]) cudaEventDestroy(ctx->ev_r[k]);
     if (ctx->ev_s0) cudaEventDestroy(ctx->ev_s0);
     if (ctx->ev_s1) cudaEventDestroy(ctx->ev_s1);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);

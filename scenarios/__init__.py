@@ -376,6 +376,7 @@ def droplet(L=30.0, R=8.0, centre=(0.3, 0.55, 0.5), rho_l=0.73, rho_v=0.02, T=0.
     a = (4.0 / rho_l) ** (1.0 / 3.0)
     n = int(np.ceil(L / a))
     X = fcc(n, a)
+    X = X[(X < L).all(axis=1)]             # n a >= L: no duplicate points across the periodic seam
     c = np.asarray(centre) * L
     d = X - c
     d -= box * np.round(d / box)
