@@ -37,9 +37,6 @@ struct ForceArgs {
     int* flag;                   // error flags (2 = coincident molecule centres)
     const DevModel* model;
     float sig2, eps24, eps4, shift;   // single-site LJ fast path
-    // half-shell rigid kernel: fixed-point reactions on the partners (int64 per component)
-    unsigned long long* rfix;
-    float fscale, tscale;             // force / torque -> fixed point (powers of two)
 };
 
 // Row descriptor of the 27-cell neighbourhood: the 3 cells (dx = -1, 0, 1)

@@ -36,11 +36,7 @@ namespace rig3 {
 #ifndef MD_RIG3_WARPS
 #define MD_RIG3_WARPS 8
 #endif
-#ifndef MD_RIG3_CAPH
-#define MD_RIG3_CAPH 640
-#endif
-constexpr int CAP = MD_RIG3_CAP;      // staged molecules per chunk of the neighbourhood (27 cells)
-constexpr int CAPH = MD_RIG3_CAPH;    // the same for the half shell (14 cells)
+constexpr int CAP = MD_RIG3_CAP;      // staged molecules per chunk of the neighbourhood
 constexpr int WARPS = MD_RIG3_WARPS;
 constexpr int HCAP = 256;             // hit-list entries per group
 constexpr int NHMAX = 64;             // home molecules per batch (force/torque accumulators)
@@ -79,56 +75,21 @@ __device__ __forceinline__ void lj_noshift(V3 r, float sig2, float eps24, float 
     fh.x = fh.x - fr * r.x; fh.y = fh.y - fr * r.y; fh.z = fh.z - fr * r.z;
 }
 
-template <int NLJ, int NQ, int NMU, int NQQ, bool HALF = false>
+template <int NLJ, int NQ, int NMU, int NQQ>
 constexpr int smem_bytes()
 {
-    // COM pairs (CP/2 + 1 pairs x 24 B, +1: the far dummy pair), NSLOT x (CP + 1) site float4,
-    // hit lists, accumulators, row table; half shell: reaction accumulators (6 x int64 per
-    // staged molecule) and the staged molecules' sorted indices
-    constexpr int CP = HALF ? CAPH : CAP;
-    return (CP / 2 + 1) * 16 + ((CP / 2 + 2) & ~1) * 8 + (NLJ + NQ + 2 * NMU + 2 * NQQ) * (CP + 1) * 16 + WARPS * 2 * 2 * (HCAP + 2) * 2 +
-           NHMAX * 8 * 4 + WARPS * 2 * 8 * 4 + 16 * 8 * 4 + (HALF ? CP * (6 * 8 + 4) : 0);
+    // COM pairs (CAP/2 + 1 pairs x 24 B, +1: the far dummy pair), NSLOT x (CAP + 1) site float4,
+    // hit lists, accumulators, row table
+    return (CAP / 2 + 1) * 16 + ((CAP / 2 + 2) & ~1) * 8 + (NLJ + NQ + 2 * NMU + 2 * NQQ) * (CAP + 1) * 16 + WARPS * 2 * 2 * (HCAP + 2) * 2 +
+           NHMAX * 8 * 4 + WARPS * 2 * 8 * 4 + 16 * 8 * 4;
 }
 
-// Reaction of the Newton-3 half shell: the half-shell kernel adds the force and torque on the
-// partner of every pair in fixed point (int64, order-independent sums, so the result is bitwise
-// reproducible) to rfix; this folds them into the forces and clears rfix for the next step.
-__global__ void k_merge_reactions(int n, float4* __restrict__ force, float4* __restrict__ torque,
-                                  unsigned long long* __restrict__ rfix, float inv_f, float inv_t)
-{
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    unsigned long long* r = rfix + 6 * (size_t)i;
-    float4 F = force[i], T = torque[i];
-    F.x += (float)((double)(long long)r[0] * inv_f); F.y += (float)((double)(long long)r[1] * inv_f);
-    F.z += (float)((double)(long long)r[2] * inv_f);
-    T.x += (float)((double)(long long)r[3] * inv_t); T.y += (float)((double)(long long)r[4] * inv_t);
-    T.z += (float)((double)(long long)r[5] * inv_t);
-    force[i] = F;
-    torque[i] = T;
-#pragma unroll
-    for (int q = 0; q < 6; ++q) r[q] = 0ull;
-}
-
-// 64-bit add to shared memory as two native 32-bit atomics with the carry of the low word
-// propagated: the result is the exact sum mod 2^64 in any order (sm_100 has no native 64-bit
-// shared-memory add; the compiler's CAS loop is much slower)
-__device__ __forceinline__ void add64(unsigned long long* p, long long v)
-{
-    unsigned* w = reinterpret_cast<unsigned*>(p);
-    const unsigned lo = (unsigned)v, hi = (unsigned)((unsigned long long)v >> 32);
-    const unsigned old = atomicAdd(w, lo);
-    const unsigned carry = (old + lo) < old ? 1u : 0u;
-    if (hi + carry) atomicAdd(w + 1, hi + carry);
-}
-
-template <int NLJ, int NQ, int NMU, int NQQ, bool HALF = false>
+template <int NLJ, int NQ, int NMU, int NQQ>
 __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceArgs a)
 {
     using SH = Shape<NLJ, NQ, NMU, NQQ>;
     constexpr int NSLOT = SH::NSLOT;
     constexpr int NPOL = (NMU + NQQ) > 0 ? (NMU + NQQ) : 1;
-    constexpr int CAP = HALF ? CAPH : rig3::CAP;
     constexpr int STRIDE = CAP + 1;
     constexpr int DUMMY = CAP;                                 // far dummy element (pair CAP / 2)
     constexpr unsigned FULL = 0xffffffffu;
@@ -147,10 +108,6 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
     float* acc = reinterpret_cast<float*>(hls + 2 * WARPS * 2 * (HCAP + 2));         // [NHMAX][8]: F, tau
     float* tacc = acc + NHMAX * 8;                                         // [NG][8]: tail slices (F, tau)
     int* rinfo = reinterpret_cast<int*>(tacc + 2 * WARPS * 8);             // [9][8] row table + [72..]: totals
-    // half shell: reaction accumulators racc[q * CAP + e] (F, tau of staged molecule e, fixed point)
-    // and the sorted index of every staged molecule
-    long long* racc = reinterpret_cast<long long*>(rinfo + 16 * 8);
-    int* ssrc = reinterpret_cast<int*>(racc + (HALF ? 6 * CAP : 0));
     const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
     const int half = lane >> 4, gl = lane & 15;
     const int grp = 2 * wib + half, NG = 2 * WARPS;
@@ -171,8 +128,6 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
             sws[(4 * s + 3) * STRIDE + DUMMY] = 0.f;
         }
     }
-    if (HALF)
-        for (int k = threadIdx.x; k < 6 * CAP; k += WARPS * 32) racc[k] = 0;
     double Uw = 0.0, Ww = 0.0;             // per lane (fp32 per home molecule, then fp64)
     long long npw = 0, ncw = 0;
     int nrej = 0;                          // band entries found out of range
@@ -186,20 +141,13 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
         if (n_all == 0) continue;
         // row table: threads 0..26 read the 27 cells' start / count
         __syncthreads();                  // previous cell's consumers are done with smem
-        if (HALF && tid == 0) rinfo[74] = 0;
-        if (HALF) __syncthreads();
         if (tid < 27) {
             const int r = tid / 3, k = tid % 3;
             const int dy = r % 3 - 1, dz = r / 3 - 1;
             const int cc = wrapi(cx + k - 1, g.nc[0]) + g.nc[0] * (wrapi(cy + dy, g.nc[1]) + g.nc[1] * wrapi(cz + dz, g.nc[2]));
             const int st = __ldg(a.start + cc);
-            const int cn = __ldg(a.start + cc + 1) - st;
             rinfo[8 * r + k] = st;
-            // half shell (Fig. 1): the home cell and the 13 forward cells -- rows dz = +1, row
-            // (dy = +1, dz = 0), and cell dx = +1 of the home row; every pair once
-            const bool fwd = r >= 5 || (r == 4 && k >= 1);
-            rinfo[8 * r + 3 + k] = (!HALF || fwd) ? cn : 0;
-            if (HALF) atomicAdd(&rinfo[74], cn);          // the full-shell count (n_candidates)
+            rinfo[8 * r + 3 + k] = __ldg(a.start + cc + 1) - st;
         }
         __syncthreads();
         if (tid < 32) {                   // exclusive prefix of the row lengths -> rinfo[8 r + 6]
@@ -215,7 +163,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
         }
         __syncthreads();
         const int mtot = rinfo[72];
-        if (tid == 0) ncw += (long long)n_all * ((HALF ? rinfo[74] : mtot) - 1);
+        if (tid == 0) ncw += (long long)n_all * (mtot - 1);
         for (int ib = 0; ib < n_all; ib += NHMAX) {
             const int nb = min(NHMAX, n_all - ib);
             if (ib > 0) __syncthreads();          // previous batch written out
@@ -250,7 +198,6 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
 #pragma unroll
                     for (int s = 0; s < NSLOT; ++s) sv[s] = __ldg(a.site + (size_t)s * a.cap + src);
                     const int ph = k >> 1, od = k & 1;
-                    if (HALF) ssrc[k] = src;
                     cxf[4 * ph + od] = x.x + offx;
                     cxf[4 * ph + 2 + od] = x.y + offy;
                     czf[2 * ph + od] = x.z + offz;
@@ -341,10 +288,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                             const int h0 = hn0, h1 = hn1;
                             hn0 = e0 + 32 < cnt ? hl[e0 + 32] : DUMMY;
                             hn1 = e1 + 32 < cnt ? hl[e1 + 32] : DUMMY;
-                            // full shell: the molecule itself; half shell: every home-cell element up to
-                            // itself (the home cell is staged first: pair (i, j) with j > i only)
-                            const bool s0 = v0 && (HALF ? h0 <= self : h0 == self);
-                            const bool s1 = v1 && (HALF ? h1 <= self : h1 == self);
+                            const bool s0 = v0 && h0 == self, s1 = v1 && h1 == self;
                             int j0 = s0 ? DUMMY : h0, j1 = s1 ? DUMMY : h1;
                             auto com_of = [&](int j, float& X, float& Y, float& Z) {
                                 const int q = 4 * (j >> 1) + (j & 1);
@@ -376,7 +320,6 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                             }
                             nval += (j0 != DUMMY ? 1 : 0) + (j1 != DUMMY ? 1 : 0);
                             V3 fh = v3zero();
-                            V3 tj = v3zero();                    // half shell: torque on the partners
 #pragma unroll
                             for (int ia = 0; ia < NLJ; ++ia) {
                                 const V3 sa = bcast(si[ia]);
@@ -386,16 +329,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                                     const V3 sb = slot3(ibb, j0, j1);
                                     const V3 rv = V3{da.x + sb.x, da.y + sb.y, da.z + sb.z};
                                     const float4 pp = ljp[ia * NLJ + ibb];
-                                    if (HALF) {
-                                        V3 fp = v3zero();            // force on site a of this pair; on b: -fp
-                                        V3 fp2 = v3zero();
-                                        lj_noshift(rv, pp.x, pp.y, pp.z, uacc, fp, fp2);
-                                        fs[ia].x += fp.x; fs[ia].y += fp.y; fs[ia].z += fp.z;
-                                        fh.x += fp.x; fh.y += fp.y; fh.z += fp.z;
-                                        pk2::cross_acc(tj, fp, sb);  // s_b x (-fp)
-                                    } else {
-                                        lj_noshift(rv, pp.x, pp.y, pp.z, uacc, fs[ia], fh);
-                                    }
+                                    lj_noshift(rv, pp.x, pp.y, pp.z, uacc, fs[ia], fh);
                                 }
                             }
 #pragma unroll
@@ -407,15 +341,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                                 for (int ibb = 0; ibb < NQ; ++ibb) {
                                     const V3 sb = slot3(SH::SQ + ibb, j0, j1);
                                     const V3 rv = V3{da.x + sb.x, da.y + sb.y, da.z + sb.z};
-                                    if (HALF) {
-                                        V3 fp = v3zero(), fp2 = v3zero();
-                                        qq_nocrf(rv, sa4.w * slotw(SH::SQ + ibb, j0, j1), krf, uacc, fp, fp2);
-                                        fs[NLJ + ia].x += fp.x; fs[NLJ + ia].y += fp.y; fs[NLJ + ia].z += fp.z;
-                                        fh.x += fp.x; fh.y += fp.y; fh.z += fp.z;
-                                        pk2::cross_acc(tj, fp, sb);
-                                    } else {
-                                        qq_nocrf(rv, sa4.w * slotw(SH::SQ + ibb, j0, j1), krf, uacc, fs[NLJ + ia], fh);
-                                    }
+                                    qq_nocrf(rv, sa4.w * slotw(SH::SQ + ibb, j0, j1), krf, uacc, fs[NLJ + ia], fh);
                                 }
                             }
 #define RIG3_POLAR(KA, KB, NA, NB, SLA, SLB, FIDX, TIDX, STA, STB)                                          \
@@ -431,11 +357,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
             const V3 eb = (STB == 2) ? slot3((slb + 1) % NSLOT, j0, j1) : v3zero();                        \
             const V3 rv = V3{d.x + pb.x - pa.x, d.y + pb.y - pa.y, d.z + pb.z - pa.z};                     \
             V3 tdummy = v3zero();                                                                          \
-            V3 fbp = v3zero();                                                                             \
-            pk2::polar2<KA, KB, HALF>(rv, ea, eb, pa4.w * slotw(slb, j0, j1), kmm, uacc, fs[FIDX + ia],   \
-                                       (TIDX) >= 0 ? ts[((TIDX) >= 0 ? (TIDX) : 0) + ia] : tdummy, fh,     \
-                                       &fbp, &tj);                                                         \
-            if (HALF) pk2::cross_acc(tj, pb, fbp);                                                         \
+            pk2::polar2<KA, KB>(rv, ea, eb, pa4.w * slotw(slb, j0, j1), kmm, uacc, fs[FIDX + ia],         \
+                                 (TIDX) >= 0 ? ts[((TIDX) >= 0 ? (TIDX) : 0) + ia] : tdummy, fh);        \
         }                                                                                                  \
     }
                             if (NQ > 0 && NMU > 0) {
@@ -458,21 +381,6 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                             }
 #undef RIG3_POLAR
                             wacc -= dot(d, fh);      // molecular virial (A6): -r_ij . F_ij
-                            if (HALF) {
-                                // reaction on the partners (Newton 3): force -fh, torque tj; fixed
-                                // point so that the order of the shared-memory atomics is irrelevant
-                                auto radd = [&](int j, float fx, float fy, float fz, float tx, float ty, float tz) {
-                                    unsigned long long* r = reinterpret_cast<unsigned long long*>(racc) + j;
-                                    add64(r, __float2ll_rn(-fx * a.fscale));
-                                    add64(r + CAP, __float2ll_rn(-fy * a.fscale));
-                                    add64(r + 2 * CAP, __float2ll_rn(-fz * a.fscale));
-                                    add64(r + 3 * CAP, __float2ll_rn(tx * a.tscale));
-                                    add64(r + 4 * CAP, __float2ll_rn(ty * a.tscale));
-                                    add64(r + 5 * CAP, __float2ll_rn(tz * a.tscale));
-                                };
-                                if (j0 != DUMMY) radd(j0, fh.x.v.x, fh.y.v.x, fh.z.v.x, tj.x.v.x, tj.y.v.x, tj.z.v.x);
-                                if (j1 != DUMMY) radd(j1, fh.x.v.y, fh.y.v.y, fh.z.v.y, tj.x.v.y, tj.y.v.y, tj.z.v.y);
-                            }
                         }
                         // ---- molecule force and torque of this lane's share, group reduction
                         float F[3] = {0.f, 0.f, 0.f}, T[3] = {0.f, 0.f, 0.f};
@@ -577,21 +485,6 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                     flush(cntB, hlB, myB, xiB, selfB, tgtB, gB);
                     __syncwarp();
                 }
-                if (HALF) {
-                    // the chunk's reactions to the sorted molecules (global int64 adds: order-free)
-                    __syncthreads();
-                    for (int k = tid; k < mm; k += WARPS * 32) {
-                        unsigned long long* dst = a.rfix + 6 * (size_t)ssrc[k];
-#pragma unroll
-                        for (int q = 0; q < 6; ++q) {
-                            const long long v = racc[q * CAP + k];
-                            if (v) {
-                                atomicAdd(dst + q, (unsigned long long)v);
-                                racc[q * CAP + k] = 0;
-                            }
-                        }
-                    }
-                }
             }
             __syncthreads();
             for (int k = tid; k < nb; k += WARPS * 32) {
@@ -612,11 +505,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
     Ww = warp_sum_d(Ww);
     npw = warp_sum_ll(npw - nrej - nself);
     ncw = warp_sum_ll(ncw);
-    // full shell: every pair seen from both sides (halved here; k_finalize halves the pair
-    // count); half shell: once
-    if (lane == 0)
-        a.part[blockIdx.x * WARPS + wib] = HALF ? ForcePartial{Uw, Ww, 2 * npw, ncw, 0.0}
-                                                : ForcePartial{0.5 * Uw, 0.5 * Ww, npw, ncw, 0.0};
+    if (lane == 0) a.part[blockIdx.x * WARPS + wib] = ForcePartial{0.5 * Uw, 0.5 * Ww, npw, ncw, 0.0};
 }
 
 }  // namespace rig3

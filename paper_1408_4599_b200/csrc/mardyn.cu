@@ -102,8 +102,6 @@ struct mardyn_ctx {
     float4* site = nullptr;
     float4* force = nullptr;
     float4* torque = nullptr;
-    unsigned long long* rfix = nullptr;  // half-shell reactions, fixed point (6 x int64 per molecule)
-    float fscale = 1.f, tscale = 1.f;    // force / torque -> fixed point
     int* cell_of = nullptr;
     int* rank = nullptr;
     int* count = nullptr;
@@ -343,27 +341,6 @@ static int build_model(mardyn_ctx* ctx)
             M.eps4[t] = (float)(4.0 * eps);
             M.shift[t] = ctx->lj_shift ? (float)(4.0 * eps * (sc6 * sc6 - sc6)) : 0.f;
         }
-    // fixed-point unit of the half-shell reactions: a force scale Fu of the model (24 eps / sigma
-    // of the LJ pairs, q_a q_b / sigma_min^2 of the charges); resolution ~2^-34 Fu per term, range
-    // ~5e8 Fu (int64)
-    {
-        double Fu = 0.0, smin = 0.0;
-        for (int a = 0; a < lj_total; ++a)
-            for (int b = 0; b < lj_total; ++b) {
-                const double sg = 0.5 * (ljsig[a] + ljsig[b]);
-                Fu = std::max(Fu, 24.0 * std::sqrt(ljeps[a] * ljeps[b]) / sg);
-                smin = smin > 0 ? std::min(smin, sg) : sg;
-            }
-        if (!(smin > 0)) smin = ctx->rc / 8.0;
-        for (int c = 0; c < nc; ++c)
-            for (int k = 0; k < M.comp[c].n_q + M.comp[c].n_mu + M.comp[c].n_Q; ++k) {
-                const double q = M.comp[c].mom[M.comp[c].n_lj + k];
-                Fu = std::max(Fu, q * q / (smin * smin));
-            }
-        if (!(Fu > 0)) Fu = 1.0;
-        ctx->fscale = (float)std::ldexp(1.0, (int)std::floor(std::log2(std::ldexp(1.0, 34) / Fu)));
-        ctx->tscale = (float)std::ldexp(1.0, (int)std::floor(std::log2(std::ldexp(1.0, 34) / (Fu * smin))));
-    }
     // kernel choice
     if (!ctx->rigid && nc == 1) {
         ctx->kernel = KER_LJ1;
@@ -435,27 +412,13 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_gra
     a.eps24 = ctx->model.eps24[0];
     a.eps4 = ctx->model.eps4[0];
     a.shift = ctx->model.shift[0];
-    a.rfix = ctx->rfix;
-    a.fscale = ctx->fscale;
-    a.tscale = ctx->tscale;
     const int threads = 32 * ctx->force_warps_per_block;
-    // one domain: the Newton-3 half shell (Fig. 1) with fixed-point reactions; a rank of
-    // a decomposition keeps the full shell (no reverse exchange of halo reactions)
-    const bool half = ctx->nranks == 1;
     switch (ctx->shape) {
     case SHAPE_2CLJQ:
-        if (half)
-            rig3::k_force_rigid3<2, 0, 0, 1, true>
-                <<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1, true>(), ctx->stream>>>(a);
-        else
-            rig3::k_force_rigid3<2, 0, 0, 1><<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
+        rig3::k_force_rigid3<2, 0, 0, 1><<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
         break;
     case SHAPE_TIP4P:
-        if (half)
-            rig3::k_force_rigid3<1, 3, 0, 0, true>
-                <<<ctx->force_grid, threads, rig3::smem_bytes<1, 3, 0, 0, true>(), ctx->stream>>>(a);
-        else
-            rig3::k_force_rigid3<1, 3, 0, 0><<<ctx->force_grid, threads, rig3::smem_bytes<1, 3, 0, 0>(), ctx->stream>>>(a);
+        rig3::k_force_rigid3<1, 3, 0, 0><<<ctx->force_grid, threads, rig3::smem_bytes<1, 3, 0, 0>(), ctx->stream>>>(a);
         break;
     case SHAPE_GEN:
         k_force_rigid<4, 4, 2, 2, true, GEN_WARPS>
@@ -495,11 +458,6 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_gra
     }
     }
     ctx->launches += 1;
-    if (half && (ctx->shape == SHAPE_2CLJQ || ctx->shape == SHAPE_TIP4P)) {
-        rig3::k_merge_reactions<<<(int)((ctx->n + 255) / 256), 256, 0, ctx->stream>>>(
-            (int)ctx->n, ctx->force, ctx->torque, ctx->rfix, 1.f / ctx->fscale, 1.f / ctx->tscale);
-        ctx->launches += 1;
-    }
     return MARDYN_OK;
 }
 
@@ -693,8 +651,6 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
     int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ: {
-        CK(cudaFuncSetAttribute(rig3::k_force_rigid3<2, 0, 0, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                rig3::smem_bytes<2, 0, 0, 1, true>()));
         auto k = rig3::k_force_rigid3<2, 0, 0, 1>;
         const int sm = rig3::smem_bytes<2, 0, 0, 1>();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -702,8 +658,6 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
         break;
     }
     case SHAPE_TIP4P: {
-        CK(cudaFuncSetAttribute(rig3::k_force_rigid3<1, 3, 0, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                rig3::smem_bytes<1, 3, 0, 0, true>()));
         auto k = rig3::k_force_rigid3<1, 3, 0, 0>;
         const int sm = rig3::smem_bytes<1, 3, 0, 0>();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -781,7 +735,6 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         site = (float4*)take((size_t)16 * cap * std::max(1, ctx->nslots));
         tq = (float4*)take(16 * cap);
     }
-    unsigned long long* rfix = ctx->kernel == KER_RIGID ? (unsigned long long*)take(48 * (size_t)cap) : nullptr;
     float4* xs = (float4*)take(16 * cap);
     float4* force = (float4*)take(16 * cap);
     int* cell_of = (int*)take(4 * cap);
@@ -837,7 +790,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     if (assign) {
         ctx->pos[0] = pos0; ctx->pos[1] = pos1; ctx->vel[0] = vel0; ctx->vel[1] = vel1;
         ctx->quat[0] = q0; ctx->quat[1] = q1; ctx->angm[0] = j0; ctx->angm[1] = j1;
-        ctx->site = site; ctx->torque = tq; ctx->xs = xs; ctx->force = force; ctx->rfix = rfix;
+        ctx->site = site; ctx->torque = tq; ctx->xs = xs; ctx->force = force;
         ctx->cell_of = cell_of; ctx->rank = rank; ctx->keys = keys; ctx->oldidx = oldidx; ctx->count = count;
         ctx->start = start; ctx->scan_flags = scan_flags; ctx->fin_scratch = fin_scratch; ctx->fin_ticket = fin_ticket; ctx->fpart = fpart; ctx->kpart = kpart;
         ctx->nfw = nfw; ctx->nfpart = nfw + nbc; ctx->blk_ctr = blk_ctr;
@@ -883,7 +836,6 @@ int mardyn_set_workspace(mardyn_ctx* ctx, void* device_ptr, size_t bytes, int64_
     CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, ctx->stream));
     if (ctx->blk_ctr) CK(cudaMemsetAsync(ctx->blk_ctr, 0, sizeof(int), ctx->stream));
     CK(cudaMemsetAsync(ctx->hist, 0, sizeof(ObsRec) * MD_HISTORY, ctx->stream));
-    if (ctx->rfix) CK(cudaMemsetAsync(ctx->rfix, 0, 48 * (size_t)n_capacity, ctx->stream));
     if (ctx->nranks > 1 && !ctx->h_owner.empty()) {
         CK(cudaMemcpyAsync(ctx->owner, ctx->h_owner.data(), ctx->g.ncell, cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemcpyAsync(ctx->gmask, ctx->h_gmask.data(), 4 * (size_t)ctx->g.ncell, cudaMemcpyHostToDevice,

@@ -78,20 +78,8 @@ __device__ __forceinline__ void qq2(V3 r, P2 qq, float krf, float crf, P2& u, V3
 
 // point multipoles (A5), same closed forms and gradient recipe as
 // sitepair.cuh:pair_polar; p = m_a m_b (masked)
-// t += a x b (packed)
-__device__ __forceinline__ void cross_acc(V3& t, V3 a, V3 b)
-{
-    t.x = fma(a.y, b.z, t.x); t.x = fma(a.z * p2(-1.f), b.y, t.x);
-    t.y = fma(a.z, b.x, t.y); t.y = fma(a.x * p2(-1.f), b.z, t.y);
-    t.z = fma(a.x, b.y, t.z); t.z = fma(a.y * p2(-1.f), b.x, t.z);
-}
-
-// REACT (Newton-3 half shell): also the partner's side -- its site torque tb += tau_b
-// (tau_b = -e_b x du/de_b) and the site force on b (returned in fb: the force on a is du,
-// the force on b is -du)
-template <int KA, int KB, bool REACT = false>
-__device__ __forceinline__ void polar2(V3 r, V3 ea, V3 eb, P2 p, float kmm, P2& u, V3& fa, V3& ta, V3& fh,
-                                       V3* fb = nullptr, V3* tb = nullptr)
+template <int KA, int KB>
+__device__ __forceinline__ void polar2(V3 r, V3 ea, V3 eb, P2 p, float kmm, P2& u, V3& fa, V3& ta, V3& fh)
 {
     const P2 r2 = dot(r, r);
     const P2 ir = rsqrt2(r2);
@@ -159,16 +147,6 @@ __device__ __forceinline__ void polar2(V3 r, V3 ea, V3 eb, P2 p, float kmm, P2& 
         ta.x -= ea.y * gv.z - ea.z * gv.y;
         ta.y -= ea.z * gv.x - ea.x * gv.z;
         ta.z -= ea.x * gv.y - ea.y * gv.x;
-    }
-    if (REACT) {
-        *fb = V3{p2(-1.f) * du.x, p2(-1.f) * du.y, p2(-1.f) * du.z};
-        if (KB != MD_CHARGE) {
-            V3 gv = V3{ucb * rh.x, ucb * rh.y, ucb * rh.z};
-            if (KA != MD_CHARGE) { gv.x = fma(ucab, ea.x, gv.x); gv.y = fma(ucab, ea.y, gv.y); gv.z = fma(ucab, ea.z, gv.z); }
-            tb->x -= eb.y * gv.z - eb.z * gv.y;
-            tb->y -= eb.z * gv.x - eb.x * gv.z;
-            tb->z -= eb.x * gv.y - eb.y * gv.x;
-        }
     }
 }
 
