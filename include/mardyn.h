@@ -162,9 +162,10 @@ int mardyn_step(struct mardyn_ctx* ctx, int32_t n);
  * NVT by velocity rescaling ("kept constant by velocity rescaling";
  * reading A24 of DESIGN.md): after every interval-th step k the half-step
  * velocities and angular momenta are scaled by sqrt(T_target / T(t_k)).
- * T_target = 0 or interval = 0: NVE (default).  Errors: MARDYN_EINVAL for a
- * negative or non-finite T_target or a negative interval; MARDYN_ESTATE on a
- * decomposed context; a step with T(t_k) = 0 reports MARDYN_EUNSTABLE.
+ * T_target = 0 or interval = 0: NVE (default).  On a decomposed run T(t_k) is
+ * the global temperature.  Errors: MARDYN_EINVAL for a negative or non-finite
+ * T_target or a negative interval; a step with T(t_k) = 0 reports
+ * MARDYN_EUNSTABLE.
  */
 int mardyn_set_thermostat(struct mardyn_ctx* ctx, double T_target, int32_t interval);
 
@@ -278,7 +279,8 @@ int mardyn_kd_decompose(const double* cost, int32_t nx, int32_t ny, int32_t nz, 
  * of the ranks' partials; ncclAllGather) and are collective calls;
  * mardyn_get_molecules / get_forces / get_raw return the rank's owned
  * molecules (compacted, ordered by input index) with their ids.  NVT
- * rescaling is not available on decomposed contexts (MARDYN_ESTATE).
+ * rescaling uses the global temperature (an allreduce of the ranks' kinetic
+ * energies; set it on every rank, or on rank 0 of a loopback group).
  * world = 1 is allowed: a one-domain context whose observables travel
  * through the communicator.  Errors: MARDYN_ENCCL (NCCL missing or failed;
  * the context is poisoned), MARDYN_ECAPACITY (a rank's owned + halo +

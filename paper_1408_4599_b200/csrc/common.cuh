@@ -110,6 +110,10 @@ struct DDArgs {
                                  // (records); nullptr: uniform segments r * seg_cap of seg_cap records
     DDRec* const* put_rec = nullptr;   // direct puts: record k for rank r goes to put_rec[r][k] (this rank's
                                  // segment in r's receive buffer; peer memory), nullptr: own send buffer
+    int* const* put_cnt = nullptr;     // direct puts: where this rank's count for rank r goes (fused kernels:
+                                 // the last CTA to finish stores them)
+    int* done = nullptr;               // fused kernels: CTA completion ticket (zero between launches)
+    int* n_force = nullptr;            // fused kernels: the sorted count the forces were computed for
 };
 
 // Pack this lane's exchange records (spatial decomposition): one record for every rank in

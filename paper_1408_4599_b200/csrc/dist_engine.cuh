@@ -21,9 +21,11 @@ struct Group {
     int live = 0;                        // contexts not yet destroyed
     cudaStream_t stream = nullptr;       // loopback: the one stream every rank enqueues on
     bool own_stream = false;
+    std::vector<const ObsRec*> hist_tab; // loopback NVT: the ranks' observable rings (host staging)
 };
 
 static bool group_is_nccl(const Group* g) { return g && g->nccl; }
+static std::vector<mardyn_ctx*> group_members(mardyn_ctx* ctx) { return ctx->grp ? ctx->grp->m : std::vector<mardyn_ctx*>{ctx}; }
 
 #define NCK(call)                                                                                    \
     do {                                                                                             \
@@ -369,21 +371,20 @@ static int dd_begin_async(mardyn_ctx* ctx)
 {
     cudaStream_t s = ctx->stream;
     const int b = ctx->cur;
-    CK(cudaMemcpyAsync(ctx->n_aux + 1, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToDevice, s));
     DDArgs dd = dd_args(ctx, false);
     dd.n_dev = ctx->start + ctx->g.ncell;             // the sorted count of the last cell rebuild
     dd.put_rec = ctx->direct ? ctx->put_rec : nullptr;
-    CK(cudaMemsetAsync(ctx->send_cnt, 0, sizeof(int) * ctx->nranks, s));
+    // (send_cnt is zero here: the last import cleared it)
     if (ctx->kernel == KER_LJ1) {
         // single-site kernel with the leapfrog, binning and exchange packing fused in (the cell
-        // counts are zero: the last rebuild's scan cleared them)
+        // counts are zero: the last rebuild's scan cleared them); it also records its sorted
+        // count and, with direct puts, stores the record counts into the receivers
+        dd.n_force = ctx->n_aux + 1;
+        dd.put_cnt = ctx->direct ? ctx->put_cnt : nullptr;
+        dd.done = ctx->n_aux + 3;
         CK(cudaEventRecord(ctx->ev_f0[b], s));
-        launch_force(ctx, b, true, false, &dd);
+        launch_force(ctx, b, true, true, &dd);
         CK(cudaEventRecord(ctx->ev_f1[b], s));
-        if (ctx->direct) {
-            k_put_counts<<<1, 32, 0, s>>>(ctx->nranks, ctx->send_cnt, ctx->put_cnt);
-            ctx->launches += 1;
-        }
         // the step's observables on a side stream, concurrent with the exchange and the rebuild
         CK(cudaEventRecord(ctx->ev_s0, s));
         CK(cudaStreamWaitEvent(ctx->side_stream, ctx->ev_s0, 0));
@@ -397,6 +398,7 @@ static int dd_begin_async(mardyn_ctx* ctx)
         ctx->last_parity = b;
         return MARDYN_OK;
     }
+    CK(cudaMemcpyAsync(ctx->n_aux + 1, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToDevice, s));
     CK(cudaEventRecord(ctx->ev_f0[b], s));
     launch_force(ctx, b);
     CK(cudaEventRecord(ctx->ev_f1[b], s));
@@ -432,7 +434,7 @@ static int dd_end_async(mardyn_ctx* ctx)
         ctx->nranks, seg, ctx->peer_segs ? ctx->seg_tab + 2 * ctx->nranks : nullptr, ctx->recv_cnt,
         ctx->start + ctx->g.ncell, (int)ctx->cap, ctx->g, ctx->recvbuf, ctx->pos[b], ctx->vel[b],
         ctx->rigid ? ctx->quat[b] : nullptr, ctx->rigid ? ctx->angm[b] : nullptr, ctx->cell_of, ctx->rank,
-        ctx->count, ctx->n_aux, ctx->flag);
+        ctx->count, ctx->n_aux, ctx->flag, ctx->send_cnt);
     ctx->launches += 1;
     int rc = enqueue_sort(ctx, b, 1 - b, -1, ctx->n_aux);
     if (rc) return rc;
@@ -466,6 +468,7 @@ static int dd_set_segments(mardyn_ctx* ctx, const std::vector<int64_t>& sc, cons
     ctx->recv_caps = rcap;
     CK(cudaMemcpyAsync(ctx->seg_tab, tab.data(), sizeof(int) * tab.size(), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemsetAsync(ctx->recv_cnt, 0, sizeof(int) * p, ctx->stream));
+    CK(cudaMemsetAsync(ctx->send_cnt, 0, sizeof(int) * p, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->peer_segs = true;
     ctx->seg_cap = 0;
@@ -713,6 +716,46 @@ static int group_rebalance(Group* G)
     return MARDYN_OK;
 }
 
+// NVT (reading A24) on a decomposed run: after step k (k + 1 a multiple of the
+// interval) the global KE of t_k (rank-ordered sum of the ranks' partials: ncclAllReduce, or
+// read across the loopback ranks) sets lambda; every rank scales its molecules
+static int group_thermostat(Group* G, long long k)
+{
+    mardyn_ctx* c0 = G->m[0];
+    if (!(c0->T_target > 0) || c0->thermo_interval < 1 || (k + 1) % c0->thermo_interval != 0) return MARDYN_OK;
+    const int p = G->p;
+    std::vector<double*> ke;
+    if (G->nccl) {
+        mardyn_ctx* ctx = c0;
+        double* d = reinterpret_cast<double*>(c0->cmat);
+        k_ke_entry<<<1, 32, 0, c0->stream>>>(c0->hist, k, d);
+        NCK(mdn::api().AllReduce(d, d, 2, ncclDouble, ncclSum, G->comm, c0->stream));
+        c0->launches += 1;
+        ke.push_back(d);
+    } else {
+        mardyn_ctx* ctx = c0;
+        // the p history rings' addresses (after the two KE doubles of rank 0's scratch)
+        double* d = reinterpret_cast<double*>(c0->cmat);
+        const ObsRec** tab = reinterpret_cast<const ObsRec**>(c0->cmat + 2);
+        G->hist_tab.resize(p);
+        for (mardyn_ctx* c : G->m) G->hist_tab[c->dd_rank] = c->hist;
+        CK(cudaMemcpyAsync(tab, G->hist_tab.data(), sizeof(void*) * p, cudaMemcpyHostToDevice, c0->stream));
+        k_ke_sum<<<1, 32, 0, c0->stream>>>(p, tab, k, d);
+        c0->launches += 1;
+        for (int r = 0; r < p; ++r) ke.push_back(d);
+    }
+    for (size_t r = 0; r < G->m.size(); ++r) {
+        mardyn_ctx* c = G->m[r];
+        mardyn_ctx* ctx = c;
+        k_rescale_global<<<std::min(nblk(c->cap, 256), 8 * c->num_sms), 256, 0, c->stream>>>(
+            (int)c->cap, c->start + c->g.ncell, c->vel[c->cur], c->rigid ? c->angm[c->cur] : nullptr, ke[r],
+            c->ndof_global, c->T_target, c->flag);
+        c->launches += 1;
+        CK(cudaGetLastError());
+    }
+    return MARDYN_OK;
+}
+
 static int group_step(mardyn_ctx* ctx, int32_t nsteps)
 {
     Group* G = ctx->grp;
@@ -729,6 +772,7 @@ static int group_step(mardyn_ctx* ctx, int32_t nsteps)
         }
         int rc = ctx->seg_ready ? group_async_step(G) : group_sync_step(G);
         if (rc) return rc;
+        if ((rc = group_thermostat(G, st))) return rc;
     }
     for (mardyn_ctx* c : G->m) c->last_force_launches = nsteps;
     return MARDYN_OK;

@@ -671,6 +671,26 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
     if (STEP && pend_mi >= 0) a.rank[pend_mi] = __shfl_sync(pend_m, pend_b, __ffs(pend_m) - 1) + pend_r;
     ncw = warp_sum_ll(ncw);
     if (lane == 0) a.part[gw] = ForcePartial{0.0, 0.0, 0, ncw, 0.0};
+    if (DD) {
+        // the decomposed step's bookkeeping without extra launches: the sorted count of these
+        // forces, and (direct puts) this rank's record counts into the receivers' count arrays,
+        // stored by the last CTA to finish (all packing atomics are done by then)
+        if (blockIdx.x == 0 && threadIdx.x == 0 && a.dd.n_force) *a.dd.n_force = nsorted;
+        if (a.dd.put_cnt) {
+            __shared__ int last_cta;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                __threadfence();
+                last_cta = atomicAdd(a.dd.done, 1) == (int)gridDim.x - 1;
+            }
+            __syncthreads();
+            if (last_cta && threadIdx.x < a.dd.nranks) {
+                __threadfence();
+                *a.dd.put_cnt[threadIdx.x] = *(volatile int*)(a.dd.send_cnt + threadIdx.x);
+                if (threadIdx.x == 0) *a.dd.done = 0;
+            }
+        }
+    }
 }
 
 }  // namespace lj1

@@ -75,9 +75,11 @@ __global__ void k_iota64(int n, int64_t* __restrict__ a)
 }
 
 // ------------------------------------------------------------------------
-// exclusive scan of the per-cell counts (3 kernels: tile scan, scan of tile
-// totals, add).  Tiles of 4096 cells, 1024 threads x 4 cells.
-#define SCAN_TILE 4096
+// exclusive scan of the per-cell counts.  Tiles of 16384 cells, 1024 threads
+// x 16 consecutive cells (4 x int4): a 4.1 M-cell grid (c4) is 252 tiles, one
+// wave of the co-resident CTAs (4096-cell tiles took four waves, ~80 us)
+#define SCAN_PT 16
+#define SCAN_TILE (1024 * SCAN_PT)
 
 __device__ __forceinline__ int warp_incl_scan(int v)
 {
@@ -146,20 +148,20 @@ __global__ void __launch_bounds__(1024) k_scan(int ncell, int* __restrict__ coun
     const int tile = (int)(ticket_s % (unsigned)ntiles);
     const unsigned epoch = (ticket_s / (unsigned)ntiles + 1u) & 0x3fffffffu;
     if (tile == 0 && threadIdx.x == 0 && blk_ctr) *blk_ctr = 0;
-    const int base = tile * SCAN_TILE + threadIdx.x * 4;
-    int a[4];
-    if (base + 3 < ncell) {
-        const int4 c4 = *reinterpret_cast<const int4*>(count + base);
-        a[0] = c4.x; a[1] = c4.y; a[2] = c4.z; a[3] = c4.w;
-        *reinterpret_cast<int4*>(count + base) = make_int4(0, 0, 0, 0);
-    } else {
+    const int base = tile * SCAN_TILE + threadIdx.x * SCAN_PT;
+    int a[SCAN_PT];
+    // count is padded to whole tiles (ncell_pad), so the vector loads never leave it
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            a[k] = (base + k < ncell) ? count[base + k] : 0;
-            if (base + k < ncell) count[base + k] = 0;
-        }
+    for (int v = 0; v < SCAN_PT / 4; ++v) {
+        const int4 c4 = *reinterpret_cast<const int4*>(count + base + 4 * v);
+        a[4 * v] = c4.x; a[4 * v + 1] = c4.y; a[4 * v + 2] = c4.z; a[4 * v + 3] = c4.w;
     }
-    int ex = block_excl_scan(a[0] + a[1] + a[2] + a[3], &tot);
+#pragma unroll
+    for (int v = 0; v < SCAN_PT / 4; ++v) *reinterpret_cast<int4*>(count + base + 4 * v) = make_int4(0, 0, 0, 0);
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_PT; ++k) sum += a[k];
+    int ex = block_excl_scan(sum, &tot);
     if (threadIdx.x < 32) {                  // warp 0: publish, then look back 32 tiles at a time
         const int lane = threadIdx.x;
         const int agg = tot;
@@ -187,10 +189,23 @@ __global__ void __launch_bounds__(1024) k_scan(int ncell, int* __restrict__ coun
     }
     __syncthreads();
     ex += excl_s;
+    if (base + SCAN_PT <= ncell) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        if (base + k < ncell) start[base + k] = ex;
-        ex += a[k];
+        for (int v = 0; v < SCAN_PT / 4; ++v) {
+            int4 o;
+            o.x = ex; ex += a[4 * v];
+            o.y = ex; ex += a[4 * v + 1];
+            o.z = ex; ex += a[4 * v + 2];
+            o.w = ex; ex += a[4 * v + 3];
+            if ((((uintptr_t)(start + base)) & 15) == 0) *reinterpret_cast<int4*>(start + base + 4 * v) = o;
+            else { start[base + 4 * v] = o.x; start[base + 4 * v + 1] = o.y; start[base + 4 * v + 2] = o.z; start[base + 4 * v + 3] = o.w; }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < SCAN_PT; ++k) {
+            if (base + k < ncell) start[base + k] = ex;
+            ex += a[k];
+        }
     }
 }
 
@@ -462,10 +477,12 @@ __global__ void k_import_seg(int nranks, int seg_cap, const int* __restrict__ rt
                              const int* __restrict__ n_old_dev, int cap, GridP g, const DDRec* __restrict__ recv,
                              uint4* __restrict__ pos, float4* __restrict__ vel, float4* __restrict__ quat,
                              float4* __restrict__ angm, int* __restrict__ cell_of, int* __restrict__ rank,
-                             int* __restrict__ count, int* __restrict__ n_unsorted, int* __restrict__ flag)
+                             int* __restrict__ count, int* __restrict__ n_unsorted, int* __restrict__ flag,
+                             int* __restrict__ send_cnt = nullptr)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int n_old = *n_old_dev;
+    if (send_cnt && t < nranks) send_cnt[t] = 0;       // consumed by this step's exchange: ready for the next
     int r = nranks, k = 0, base = n_old, tot = n_old;
     for (int q = 0; q < nranks; ++q) {
         const int off = rtab ? rtab[q] : q * seg_cap, cq = rtab ? rtab[nranks + q] : seg_cap;
@@ -812,6 +829,53 @@ __global__ void k_rescale(int n, float4* __restrict__ vel, float4* __restrict__ 
         float4 j = angm[t];
         j.x *= lam; j.y *= lam; j.z *= lam;
         angm[t] = j;
+    }
+}
+
+// NVT on a decomposed run (reading A24 with the GLOBAL temperature): ke[0..1] = the
+// global KE_t, KE_r of step k (summed over the ranks); every molecule this rank holds
+// (owned + halo copies; the copies are refreshed by the next exchange anyway) is scaled
+// by lambda = sqrt(T_target / T(t_k)), T = 2 (KE_t + KE_r) / N_dof.
+__global__ void k_ke_entry(const ObsRec* __restrict__ hist, long long k, double* __restrict__ ke)
+{
+    if (threadIdx.x == 0) {
+        const ObsRec& o = hist[k % MD_HISTORY];
+        ke[0] = o.KEt;
+        ke[1] = o.KEr;
+    }
+}
+__global__ void k_ke_sum(int p, const ObsRec* const* __restrict__ hists, long long k, double* __restrict__ ke)
+{
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int r = 0; r < p; ++r) {              // rank order: deterministic
+            a += hists[r][k % MD_HISTORY].KEt;
+            b += hists[r][k % MD_HISTORY].KEr;
+        }
+        ke[0] = a;
+        ke[1] = b;
+    }
+}
+__global__ void k_rescale_global(int cap, const int* __restrict__ n_dev, float4* __restrict__ vel,
+                                 float4* __restrict__ angm, const double* __restrict__ ke, double ndof,
+                                 double T_target, int* __restrict__ flag)
+{
+    const double T = 2.0 * (ke[0] + ke[1]) / ndof;
+    if (!(T > 0.0)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(flag, 1);
+        return;
+    }
+    const float lam = (float)sqrt(T_target / T);
+    const int n = min(*n_dev, cap);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        float4 v = vel[t];
+        v.x *= lam; v.y *= lam; v.z *= lam;
+        vel[t] = v;
+        if (angm) {
+            float4 j = angm[t];
+            j.x *= lam; j.y *= lam; j.z *= lam;
+            angm[t] = j;
+        }
     }
 }
 

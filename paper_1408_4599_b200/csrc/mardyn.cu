@@ -67,6 +67,7 @@ static int group_step(mardyn_ctx* ctx, int32_t nsteps);
 static int group_compute_forces(mardyn_ctx* ctx);
 static void group_release(mardyn_ctx* ctx);
 static int compute_forces_local(mardyn_ctx* ctx);
+static std::vector<mardyn_ctx*> group_members(mardyn_ctx* ctx);
 
 struct mardyn_ctx {
     std::string err;
@@ -997,10 +998,10 @@ int mardyn_set_thermostat(mardyn_ctx* ctx, double T_target, int32_t interval)
     if (!ctx) return MARDYN_EINVAL;
     if (!(T_target >= 0) || !std::isfinite(T_target) || interval < 0)
         return fail(ctx, MARDYN_EINVAL, "T_target must be finite and >= 0, interval >= 0");
-    if (ctx->nranks > 1 && T_target > 0)
-        return fail(ctx, MARDYN_ESTATE, "NVT rescaling is not available on decomposed contexts");
     ctx->T_target = T_target;
     ctx->thermo_interval = interval;
+    if (ctx->grp && ctx->nranks > 1)      // a decomposed run rescales with the global T: every rank alike
+        for (mardyn_ctx* c : group_members(ctx)) { c->T_target = T_target; c->thermo_interval = interval; }
     for (int b = 0; b < 2; ++b)                       // the step graphs change
         if (ctx->gexec[b]) { cudaGraphExecDestroy(ctx->gexec[b]); ctx->gexec[b] = nullptr; }
     return MARDYN_OK;

@@ -30,14 +30,16 @@ def t_single(s):
     ctx.step(WARM)
     ctx.get_observables()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ms = []
+    ms, fms = [], []
     for _ in range(STEPS):
         e0.record(st)
         ctx.step(1)
         e1.record(st)
         st.synchronize()
         ms.append(e0.elapsed_time(e1))
+        fms.append(ctx.last_step_timing()["force_ms"])
     del ctx
+    print(json.dumps({"single_force_ms": float(np.median(fms))}), flush=True)
     return float(np.median(ms))
 
 
@@ -45,14 +47,18 @@ def t_ranks(s, p, boxes=None, rebalance=0):
     run = mardyn.DecomposedRun(s, p, transport="loopback", boxes=boxes, rebalance_interval=rebalance)
     run.step(WARM)
     run.observables()
-    per = []
+    per, fper = [], []
     for _ in range(STEPS):
         run.step(1)
         run.lead.stream.synchronize()
-        per.append([c.last_step_timing()["total_ms"] for c in run.ctxs])
+        tm = [c.last_step_timing() for c in run.ctxs]
+        per.append([t["total_ms"] for t in tm])
+        fper.append([t["force_ms"] for t in tm])
     per = np.array(per)
     med = np.median(per, axis=0)
+    fmed = np.median(np.array(fper), axis=0)
     out = {"rank_ms": [round(float(x), 4) for x in med], "slowest_ms": float(med.max()),
+           "force_ms": [round(float(x), 4) for x in fmed],
            "owned": run.owned_counts(), "boxes": np.asarray(run.boxes).reshape(p, 6).tolist()}
     del run
     return out
@@ -83,6 +89,21 @@ def main():
         name, p = sys.argv[2], int(sys.argv[3])
         r = t_ranks(S.config(name), p)
         print(json.dumps(r), flush=True)
+    elif mode == "static":                  # Fig. 7 direction on the slab: static z-slabs / octants vs k-d
+        name = sys.argv[2]
+        s = S.config(name)
+        n = np.floor(np.asarray(s["box"]) / s["rc"]).astype(int)
+        for p in [int(x) for x in sys.argv[3:]]:
+            zc = [round(k * n[2] / p) for k in range(p + 1)]
+            slabs = [[0, 0, zc[k], n[0], n[1], zc[k + 1]] for k in range(p)]
+            out = {"config": name, "p": p}
+            for lab, bx in (("zslab", slabs), ("octant", equal_volume(s, p)), ("kd", None)):
+                r = t_ranks(s, p, boxes=bx)
+                out[lab + "_slowest_ms"] = r["slowest_ms"]
+                out[lab + "_owned_max_over_mean"] = float(max(r["owned"]) / np.mean(r["owned"]))
+                out[lab + "_rank_ms"] = r["rank_ms"]
+            out["zslab_over_kd"] = out["zslab_slowest_ms"] / out["kd_slowest_ms"]
+            print(json.dumps(out), flush=True)
     elif mode == "droplet":
         t = time.time()
         s = S.droplet(L=160.0, R=42.0)          # R / L < 0.3: the lattice sphere does not wrap

@@ -131,3 +131,20 @@ def test_nccl_single_rank(md, oracle_mod):
     _, _, _, _, obs = o.run(s["dt"], s["comp"], o.quantize(s["r"]), s["v"], s["q"], s["j"], 10, mode="full")
     for key, ok in (("U_pot", "U"), ("virial", "W"), ("T", "T")):
         assert scaled_err([x[key] for x in h], obs[ok]).max() <= 1e-5
+
+
+def test_nvt_decomposed_vs_oracle(md, oracle_mod):
+    """NVT velocity rescaling (reading A24) on a decomposed run: the ranks' kinetic
+    energies are summed (rank order) before lambda = sqrt(T_target / T(t_k)) is applied,
+    so the run follows the oracle's one-domain NVT trajectory."""
+    s = S.config("c1s")
+    run = md.DecomposedRun(s, 3, transport="loopback")
+    run.lead.set_thermostat(1.1, 4)
+    run.step(16)
+    hist = run.observable_history(16)
+    o = oracle_mod.System(s)
+    _, _, _, _, obs = o.run(s["dt"], s["comp"], o.quantize(s["r"]), s["v"], s["q"], s["j"], 16, mode="full",
+                            T_target=1.1, thermostat_interval=4)
+    for key, ok in (("U_pot", "U"), ("virial", "W"), ("T", "T")):
+        assert scaled_err([h[key] for h in hist], obs[ok]).max() <= 1e-5, key
+    assert abs(hist[4]["T"] - 1.1) < 0.05              # rescaled after step 3
