@@ -337,6 +337,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                 continue;
             }
             if (total + 2 > CAPP || passes >= 2) {
+#ifdef MD_LJ1_STATS
+                if (lane == 0) atomicAdd((unsigned long long*)(a.flag + 22), (unsigned long long)__popc(todo));
+#endif
                 // sparse or over-full: per-lane path for the remaining lanes
                 Acc A;
                 acc_zero(A);
@@ -526,6 +529,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
             }
             sseg[32 * nseg + lane] = seg_make(total, total + 2);    // sentinel
             const int tmax = __reduce_max_sync(0xffffffffu, ttot);
+#ifdef MD_LJ1_STATS
+            {   // profiling build (profiles/tools/lj1_stats.py): lane balance of the main loop --
+                // useful pairs vs executed pair slots (32 x the longest list) -- and lanes per path
+                const int tsum = __reduce_add_sync(0xffffffffu, ttot);
+                if (lane == 0) {
+                    atomicAdd((unsigned long long*)(a.flag + 16), (unsigned long long)tsum);
+                    atomicAdd((unsigned long long*)(a.flag + 18), (unsigned long long)(32 * tmax));
+                    atomicAdd((unsigned long long*)(a.flag + 20), (unsigned long long)__popc(members));
+                }
+            }
+#endif
             __syncwarp();
             // ---------------- main loop: each lane walks its own segments, two candidates per pair;
             //                  the next segment is kept in registers so that the pair index never

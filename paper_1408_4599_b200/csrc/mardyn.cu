@@ -1324,6 +1324,14 @@ const char* mardyn_last_error(const mardyn_ctx* ctx) { return ctx ? ctx->err.c_s
 void mardyn_destroy(mardyn_ctx* ctx)
 {
     if (!ctx) return;
+#ifdef MD_LJ1_STATS
+    if (ctx->flag) {
+        unsigned long long st[4] = {0, 0, 0, 0};
+        cudaMemcpy(st, ctx->flag + 16, sizeof(st), cudaMemcpyDeviceToHost);
+        std::printf("LJ1_STATS useful_pairs %llu slot_pairs %llu balance %.4f subchunk_lanes %llu perlane_lanes %llu\n",
+                    st[0], st[1], st[1] ? (double)st[0] / (double)st[1] : 0.0, st[2], st[3]);
+    }
+#endif
     group_release(ctx);
     for (int b = 0; b < 2; ++b) {
         if (ctx->gexec[b]) cudaGraphExecDestroy(ctx->gexec[b]);
