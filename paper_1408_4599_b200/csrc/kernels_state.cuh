@@ -75,11 +75,13 @@ __global__ void k_iota64(int n, int64_t* __restrict__ a)
 }
 
 // ------------------------------------------------------------------------
-// exclusive scan of the per-cell counts.  Tiles of 16384 cells, 1024 threads
-// x 16 consecutive cells (4 x int4): a 4.1 M-cell grid (c4) is 252 tiles, one
-// wave of the co-resident CTAs (4096-cell tiles took four waves, ~80 us)
-#define SCAN_PT 16
-#define SCAN_TILE (1024 * SCAN_PT)
+// exclusive scan of the per-cell counts.  Tiles of 1024 threads x PT consecutive
+// cells: PT = 16 for large grids (a 4.1 M-cell grid (c4) is 252 tiles, one wave of
+// the co-resident CTAs; 4096-cell tiles took four waves, ~80 us), PT = 4 below
+// 2^20 cells (more tiles in flight: c1's 85 k cells are 21 tiles)
+#define SCAN_PT_MAX 16
+#define SCAN_TILE (1024 * SCAN_PT_MAX)          // padding unit of the count array
+#define SCAN_BIG_GRID (1 << 20)
 
 __device__ __forceinline__ int warp_incl_scan(int v)
 {
@@ -136,19 +138,21 @@ __device__ __forceinline__ unsigned long long scan_word(unsigned epoch, unsigned
     return ((unsigned long long)epoch << 34) | ((unsigned long long)status << 32) | (unsigned)value;
 }
 
+template <int SCAN_PT>
 __global__ void __launch_bounds__(1024) k_scan(int ncell, int* __restrict__ count, int* __restrict__ start,
                                                unsigned long long* __restrict__ flags,
                                                unsigned* __restrict__ tile_ctr, int* __restrict__ blk_ctr)
 {
     __shared__ int tot, excl_s;
     __shared__ unsigned ticket_s;
-    const int ntiles = (ncell + SCAN_TILE - 1) / SCAN_TILE;
+    constexpr int TILE = 1024 * SCAN_PT;
+    const int ntiles = (ncell + TILE - 1) / TILE;
     if (threadIdx.x == 0) ticket_s = atomicAdd(tile_ctr, 1u);
     __syncthreads();
     const int tile = (int)(ticket_s % (unsigned)ntiles);
     const unsigned epoch = (ticket_s / (unsigned)ntiles + 1u) & 0x3fffffffu;
     if (tile == 0 && threadIdx.x == 0 && blk_ctr) *blk_ctr = 0;
-    const int base = tile * SCAN_TILE + threadIdx.x * SCAN_PT;
+    const int base = tile * TILE + threadIdx.x * SCAN_PT;
     int a[SCAN_PT];
     // count is padded to whole tiles (ncell_pad), so the vector loads never leave it
 #pragma unroll
