@@ -25,7 +25,13 @@ struct Group {
 };
 
 static bool group_is_nccl(const Group* g) { return g && g->nccl; }
-static std::vector<mardyn_ctx*> group_members(mardyn_ctx* ctx) { return ctx->grp ? ctx->grp->m : std::vector<mardyn_ctx*>{ctx}; }
+static std::vector<mardyn_ctx*> group_members(mardyn_ctx* ctx)
+{
+    std::vector<mardyn_ctx*> out;
+    for (mardyn_ctx* c : ctx->grp ? ctx->grp->m : std::vector<mardyn_ctx*>{ctx})
+        if (c) out.push_back(c);
+    return out;
+}
 
 #define NCK(call)                                                                                    \
     do {                                                                                             \
@@ -41,6 +47,8 @@ static void group_release(mardyn_ctx* ctx)
     Group* G = ctx->grp;
     if (!G) return;
     ctx->grp = nullptr;
+    for (auto& c : G->m)                  // the remaining ranks see a destroyed rank (group_ok)
+        if (c == ctx) c = nullptr;
     if (--G->live > 0) return;
     if (G->comm) mdn::api().CommDestroy(G->comm);
     if (G->own_stream && G->stream) cudaStreamDestroy(G->stream);
@@ -756,10 +764,19 @@ static int group_thermostat(Group* G, long long k)
     return MARDYN_OK;
 }
 
+// every rank of the group still exists (a destroyed loopback rank leaves a hole)
+static bool group_ok(const Group* G)
+{
+    for (const mardyn_ctx* c : G->m)
+        if (!c) return false;
+    return true;
+}
+
 static int group_step(mardyn_ctx* ctx, int32_t nsteps)
 {
     Group* G = ctx->grp;
     if (!G) return fail(ctx, MARDYN_ESTATE, "decomposed context without a group");
+    if (!group_ok(G)) return fail(ctx, MARDYN_ESTATE, "a rank of the group was destroyed");
     if (!G->nccl && ctx != G->m[0]) return fail(ctx, MARDYN_ESTATE, "step a loopback group through its rank 0");
     for (mardyn_ctx* c : G->m) {
         if (c->poisoned) return fail(ctx, MARDYN_ECUDA, "a rank's context is poisoned");
@@ -781,6 +798,7 @@ static int group_step(mardyn_ctx* ctx, int32_t nsteps)
 static int group_compute_forces(mardyn_ctx* ctx)
 {
     Group* G = ctx->grp;
+    if (!group_ok(G)) return fail(ctx, MARDYN_ESTATE, "a rank of the group was destroyed");
     if (!G->nccl && ctx != G->m[0]) return fail(ctx, MARDYN_ESTATE, "compute_forces of a loopback group through rank 0");
     for (mardyn_ctx* c : G->m) {
         if (!c->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules on every rank first");
@@ -795,6 +813,7 @@ static int group_observables(mardyn_ctx* ctx, std::vector<ObsRec>& ring)
 {
     Group* G = ctx->grp;
     const int p = G->p;
+    if (!group_ok(G)) return fail(ctx, MARDYN_ESTATE, "a rank of the group was destroyed");
     ring.assign(MD_HISTORY, ObsRec{});
     std::vector<ObsRec> h(MD_HISTORY * (size_t)p);
     if (G->nccl) {
@@ -989,6 +1008,7 @@ int mardyn_rebalance(mardyn_ctx* ctx)
     if (!ctx) return MARDYN_EINVAL;
     if (ctx->nranks < 2 || !ctx->grp) return MARDYN_OK;
     Group* G = ctx->grp;
+    if (!group_ok(G)) return fail(ctx, MARDYN_ESTATE, "a rank of the group was destroyed");
     if (!G->nccl && ctx != G->m[0]) return fail(ctx, MARDYN_ESTATE, "rebalance a loopback group through its rank 0");
     for (mardyn_ctx* c : G->m)
         if (!c->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules on every rank first");
