@@ -22,7 +22,18 @@ struct Group {
     cudaStream_t stream = nullptr;       // loopback: the one stream every rank enqueues on
     bool own_stream = false;
     std::vector<const ObsRec*> hist_tab; // loopback NVT: the ranks' observable rings (host staging)
+    // the steady-state step of every local rank (begin halves, exchange, end halves) captured as
+    // one CUDA graph per buffer parity; rebuilt when the segment layout, the partition, the
+    // molecules or the profiling switch change
+    cudaGraphExec_t gx[2] = {nullptr, nullptr};
 };
+
+static void group_drop_graphs(Group* G)
+{
+    if (!G) return;
+    for (int b = 0; b < 2; ++b)
+        if (G->gx[b]) { cudaGraphExecDestroy(G->gx[b]); G->gx[b] = nullptr; }
+}
 
 static bool group_is_nccl(const Group* g) { return g && g->nccl; }
 static std::vector<mardyn_ctx*> group_members(mardyn_ctx* ctx)
@@ -47,6 +58,7 @@ static void group_release(mardyn_ctx* ctx)
     Group* G = ctx->grp;
     if (!G) return;
     ctx->grp = nullptr;
+    group_drop_graphs(G);                 // the graphs hold this rank's buffers
     for (auto& c : G->m)                  // the remaining ranks see a destroyed rank (group_ok)
         if (c == ctx) c = nullptr;
     if (--G->live > 0) return;
@@ -162,6 +174,7 @@ static int set_molecules_dd(mardyn_ctx* ctx, int64_t n, const int64_t* id, const
     ctx->ndof = ctx->ndof_global = ndof;      // T of the rank-local partials sums to the global T
     ctx->n_global = ctx->n_input = n;
     ctx->n_stale = false;
+    group_drop_graphs(ctx->grp);
     ctx->seg_ready = false;
     ctx->peer_segs = false;
     ctx->direct = false;
@@ -390,9 +403,9 @@ static int dd_begin_async(mardyn_ctx* ctx)
         dd.n_force = ctx->n_aux + 1;
         dd.put_cnt = ctx->direct ? ctx->put_cnt : nullptr;
         dd.done = ctx->n_aux + 3;
-        CK(cudaEventRecord(ctx->ev_f0[b], s));
+        CK(cudaEventRecordWithFlags(ctx->ev_f0[b], s, cudaEventRecordExternal));
         launch_force(ctx, b, true, true, &dd);
-        CK(cudaEventRecord(ctx->ev_f1[b], s));
+        CK(cudaEventRecordWithFlags(ctx->ev_f1[b], s, cudaEventRecordExternal));
         // the step's observables on a side stream, concurrent with the exchange and the rebuild
         CK(cudaEventRecord(ctx->ev_s0, s));
         CK(cudaStreamWaitEvent(ctx->side_stream, ctx->ev_s0, 0));
@@ -407,9 +420,9 @@ static int dd_begin_async(mardyn_ctx* ctx)
         return MARDYN_OK;
     }
     CK(cudaMemcpyAsync(ctx->n_aux + 1, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToDevice, s));
-    CK(cudaEventRecord(ctx->ev_f0[b], s));
-    launch_force(ctx, b);
-    CK(cudaEventRecord(ctx->ev_f1[b], s));
+    CK(cudaEventRecordWithFlags(ctx->ev_f0[b], s, cudaEventRecordExternal));
+    launch_force(ctx, b, false, true);
+    CK(cudaEventRecordWithFlags(ctx->ev_f1[b], s, cudaEventRecordExternal));
     CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
     const int nkb = ctx->nkblocks;
     if (ctx->rigid)
@@ -550,6 +563,7 @@ static int exchange_exact(Group* G, const std::vector<std::vector<int64_t>>& C, 
 static int group_sync_step(Group* G)
 {
     const int p = G->p;
+    group_drop_graphs(G);                 // the segment layout is about to change
     for (mardyn_ctx* c : G->m) c->rank_timed = false;
     std::vector<std::vector<int64_t>> C(p, std::vector<int64_t>(p, 0));
     for (mardyn_ctx* c : G->m) {
@@ -606,14 +620,15 @@ static int group_sync_step(Group* G)
 }
 
 // steady-state step: no host synchronisation.  NCCL: the fixed segments and their counts as
-// grouped send / recv on the context stream; loopback: the packing kernels already stored them
-static int group_async_step(Group* G)
+// grouped send / recv on the context stream; loopback: the packing kernels already stored them.
+// Enqueued once per buffer parity under stream capture and replayed as a CUDA graph.
+static int group_async_enqueue(Group* G)
 {
     for (mardyn_ctx* c : G->m) {
         mardyn_ctx* ctx = c;
-        if (c->profiling) CK(cudaEventRecord(c->ev_r[0], c->stream));
+        if (c->profiling) CK(cudaEventRecordWithFlags(c->ev_r[0], c->stream, cudaEventRecordExternal));
         if (int rc = dd_begin_async(c)) return rc;
-        if (c->profiling) CK(cudaEventRecord(c->ev_r[1], c->stream));
+        if (c->profiling) CK(cudaEventRecordWithFlags(c->ev_r[1], c->stream, cudaEventRecordExternal));
     }
     if (G->nccl) {
         mardyn_ctx* ctx = G->m[0];
@@ -631,11 +646,48 @@ static int group_async_step(Group* G)
     }
     for (mardyn_ctx* c : G->m) {
         mardyn_ctx* ctx = c;
-        if (c->profiling) CK(cudaEventRecord(c->ev_r[2], c->stream));
+        if (c->profiling) CK(cudaEventRecordWithFlags(c->ev_r[2], c->stream, cudaEventRecordExternal));
         if (int rc = dd_end_async(c)) return rc;
-        if (c->profiling) CK(cudaEventRecord(c->ev_r[3], c->stream));
+        if (c->profiling) CK(cudaEventRecordWithFlags(c->ev_r[3], c->stream, cudaEventRecordExternal));
         c->rank_timed = c->profiling;
     }
+    return MARDYN_OK;
+}
+
+static int group_async_step(Group* G)
+{
+    mardyn_ctx* ctx = G->m[0];
+    cudaStream_t s = ctx->stream;             // loopback: every rank's stream; NCCL: the one rank's
+    const int b = ctx->cur;
+    if (G->gx[b]) {
+        CK(cudaGraphLaunch(G->gx[b], s));
+        for (mardyn_ctx* c : G->m) {           // the host-side bookkeeping of begin / end
+            c->last_parity = c->cur;
+            c->cur = 1 - c->cur;
+            c->n_stale = true;
+            c->side_join = false;
+            c->host_step += 1;
+            c->last_obs = c->host_step - 1;
+            c->rank_timed = c->profiling;
+        }
+        for (mardyn_ctx* c : G->m) c->launches += c->dd_glaunch;
+        return MARDYN_OK;
+    }
+    // capture this parity's step (the capture pass performs the host bookkeeping itself)
+    std::vector<long long> l0;
+    for (mardyn_ctx* c : G->m) l0.push_back(c->launches);
+    cudaGraph_t graph;
+    CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    int rc = group_async_enqueue(G);
+    cudaError_t e = cudaStreamEndCapture(s, &graph);
+    if (rc) return rc;
+    CK(e);
+    cudaGraphExec_t gx = nullptr;
+    CK(cudaGraphInstantiate(&gx, graph, 0));
+    CK(cudaGraphDestroy(graph));
+    G->gx[b] = gx;
+    for (size_t r = 0; r < G->m.size(); ++r) G->m[r]->dd_glaunch = G->m[r]->launches - l0[r];
+    CK(cudaGraphLaunch(gx, s));
     return MARDYN_OK;
 }
 
@@ -645,6 +697,7 @@ static int group_async_step(Group* G)
 static int group_rebalance(Group* G)
 {
     const int p = G->p;
+    group_drop_graphs(G);
     mardyn_ctx* c0 = G->m[0];
     const int ncell = c0->g.ncell;
     std::vector<int32_t> counts((size_t)ncell, 0), tmp((size_t)ncell);
@@ -948,6 +1001,7 @@ int mardyn_set_partition(mardyn_ctx* ctx, const int32_t* boxes)
     if (!ctx || !boxes) return MARDYN_EINVAL;
     if (ctx->nranks < 2) return fail(ctx, MARDYN_ESTATE, "not a decomposed context");
     if (ctx->loaded) ctx->loaded = false;       // the molecules must be loaded again
+    group_drop_graphs(ctx->grp);
     return dd_set_maps(ctx, boxes);
 }
 

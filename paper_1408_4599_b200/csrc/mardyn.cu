@@ -68,6 +68,7 @@ static int group_compute_forces(mardyn_ctx* ctx);
 static void group_release(mardyn_ctx* ctx);
 static int compute_forces_local(mardyn_ctx* ctx);
 static std::vector<mardyn_ctx*> group_members(mardyn_ctx* ctx);
+static void group_drop_graphs(Group* G);
 
 struct mardyn_ctx {
     std::string err;
@@ -146,6 +147,7 @@ struct mardyn_ctx {
     cudaEvent_t ev_s0 = nullptr, ev_s1 = nullptr;      // fork / join of the graph's side branch
     cudaEvent_t ev_r[4] = {nullptr, nullptr, nullptr, nullptr};   // decomposed step: this rank's begin / end
     bool rank_timed = false;
+    long long dd_glaunch = 0;              // kernel launches of this rank per replay of the group's step graph
     cudaStream_t side_stream = nullptr;
     int last_parity = 0;
     bool profiling = true;
@@ -1282,6 +1284,7 @@ int mardyn_set_profiling(mardyn_ctx* ctx, int32_t on)
     if (!ctx) return MARDYN_EINVAL;
     if ((bool)on != ctx->profiling) {
         ctx->profiling = on != 0;
+        group_drop_graphs(ctx->grp);
         for (int b = 0; b < 2; ++b)
             if (ctx->gexec[b]) { cudaGraphExecDestroy(ctx->gexec[b]); ctx->gexec[b] = nullptr; }
     }
