@@ -64,9 +64,41 @@ struct GridP {
     float band_mid, band_hw;     // 0.5 (lo + hi), 0.5 (hi - lo) + 1e-6 hi (fp32, set with lo / hi)
     long long cut2_q;            // exact threshold in quanta^2: in range iff r2q < cut2_q
     float dt;
-    int hlo[3], hdim[3];         // home cells of this rank: box [hlo, hlo + hdim) (whole grid if 1 rank)
+    // Rank-local cell window (spatial decomposition): the cells a rank can hold -- its box plus
+    // one halo layer -- numbered locally, x fastest: local l_k = (c_k - wlo_k) mod nc_k in
+    // [0, wn_k); an axis the window covers entirely keeps wlo = 0, wn = nc (and its periodic wrap).
+    // count[] / start[] / cell_of[] use local indices (the scan runs over wncell cells), the
+    // owner / halo maps global ones.  One domain: wlo = 0, wn = nc (identity).
+    int wlo[3], wn[3];
+    int wncell;
+    int hlo[3], hdim[3];         // home cells of this rank, LOCAL: box [hlo, hlo + hdim) (whole grid if 1 rank)
     int nhome;
 };
+
+// local coordinate of global cell coordinate c on axis k (c inside the window)
+__host__ __device__ __forceinline__ int loc_axis(const GridP& g, int k, int c)
+{
+    int l = c - g.wlo[k];
+    if (l < 0) l += g.nc[k];
+    return l;
+}
+// global cell coordinate of local coordinate l on axis k
+__host__ __device__ __forceinline__ int glob_axis(const GridP& g, int k, int l)
+{
+    int c = g.wlo[k] + l;
+    if (c >= g.nc[k]) c -= g.nc[k];
+    return c;
+}
+// local linear index (count / start / cell_of) of a cell given by global coordinates
+__host__ __device__ __forceinline__ int cell_loc(const GridP& g, int cx, int cy, int cz)
+{
+    return loc_axis(g, 0, cx) + g.wn[0] * (loc_axis(g, 1, cy) + g.wn[1] * loc_axis(g, 2, cz));
+}
+// global linear index (owner / halo maps) of a cell given by global coordinates
+__host__ __device__ __forceinline__ int cell_glob(const GridP& g, int cx, int cy, int cz)
+{
+    return cx + g.nc[0] * (cy + g.nc[1] * cz);
+}
 
 // cell index along axis k of a fixed-point coordinate: floor(u / E_k) by a
 // multiply-high (exact for u < 2^32, E_k <= 2^23: the rounding excess of
@@ -76,13 +108,13 @@ __device__ __forceinline__ int cell_of_u(const GridP& g, int k, uint32_t u)
     return (int)__umul64hi((unsigned long long)u, g.Einv[k]);
 }
 
-// home cell t (0 <= t < nhome) of the rank's box, x fastest
+// home cell t (0 <= t < nhome) of the rank's box, x fastest: LOCAL coordinates and index
 __device__ __forceinline__ int home_cell(const GridP& g, int t, int& cx, int& cy, int& cz)
 {
     cx = g.hlo[0] + t % g.hdim[0];
     cy = g.hlo[1] + (t / g.hdim[0]) % g.hdim[1];
     cz = g.hlo[2] + t / (g.hdim[0] * g.hdim[1]);
-    return cx + g.nc[0] * (cy + g.nc[1] * cz);
+    return cx + g.wn[0] * (cy + g.wn[1] * cz);
 }
 
 // vel.w carries the component id (bits 0-7) and the ghost flag (bit 8) of

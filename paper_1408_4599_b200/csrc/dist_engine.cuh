@@ -120,7 +120,15 @@ static int dd_set_maps(mardyn_ctx* ctx, const int32_t* boxes)
     ctx->h_gmask.swap(gmask);
     const int32_t* b = boxes + 6 * ctx->dd_rank;
     GridP& g = ctx->g;
-    for (int k = 0; k < 3; ++k) { g.hlo[k] = b[k]; g.hdim[k] = b[3 + k] - b[k]; }
+    // the rank-local cell window: the box and one halo layer (the whole axis if that covers it)
+    g.wncell = 1;
+    for (int k = 0; k < 3; ++k) {
+        g.hdim[k] = b[3 + k] - b[k];
+        if (g.hdim[k] + 2 >= g.nc[k]) { g.wlo[k] = 0; g.wn[k] = g.nc[k]; }
+        else { g.wlo[k] = (b[k] - 1 + g.nc[k]) % g.nc[k]; g.wn[k] = g.hdim[k] + 2; }
+        g.hlo[k] = loc_axis(g, k, b[k]);
+        g.wncell *= g.wn[k];
+    }
     g.nhome = g.hdim[0] * g.hdim[1] * g.hdim[2];
     if (ctx->ws) {
         CK(cudaMemcpyAsync(ctx->owner, ctx->h_owner.data(), ctx->g.ncell, cudaMemcpyHostToDevice, ctx->stream));
@@ -374,7 +382,7 @@ static int dd_import_sort(mardyn_ctx* ctx, int64_t n_recv, bool advance)
     if (rc) return rc;
     CK(cudaGetLastError());
     int kept = 0;
-    CK(cudaMemcpyAsync(&kept, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&kept, ctx->start + ctx->g.wncell, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     ctx->n = kept;
     ctx->cur = 1 - b;
@@ -393,7 +401,7 @@ static int dd_begin_async(mardyn_ctx* ctx)
     cudaStream_t s = ctx->stream;
     const int b = ctx->cur;
     DDArgs dd = dd_args(ctx, false);
-    dd.n_dev = ctx->start + ctx->g.ncell;             // the sorted count of the last cell rebuild
+    dd.n_dev = ctx->start + ctx->g.wncell;             // the sorted count of the last cell rebuild
     dd.put_rec = ctx->direct ? ctx->put_rec : nullptr;
     // (send_cnt is zero here: the last import cleared it)
     if (ctx->kernel == KER_LJ1) {
@@ -419,7 +427,7 @@ static int dd_begin_async(mardyn_ctx* ctx)
         ctx->last_parity = b;
         return MARDYN_OK;
     }
-    CK(cudaMemcpyAsync(ctx->n_aux + 1, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(ctx->n_aux + 1, ctx->start + ctx->g.wncell, 4, cudaMemcpyDeviceToDevice, s));
     CK(cudaEventRecordWithFlags(ctx->ev_f0[b], s, cudaEventRecordExternal));
     launch_force(ctx, b, false, true);
     CK(cudaEventRecordWithFlags(ctx->ev_f1[b], s, cudaEventRecordExternal));
@@ -453,7 +461,7 @@ static int dd_end_async(mardyn_ctx* ctx)
     const int64_t span = ctx->peer_segs ? ctx->recv_span : (int64_t)seg * ctx->nranks;
     k_import_seg<<<nblk(span, 256), 256, 0, s>>>(
         ctx->nranks, seg, ctx->peer_segs ? ctx->seg_tab + 2 * ctx->nranks : nullptr, ctx->recv_cnt,
-        ctx->start + ctx->g.ncell, (int)ctx->cap, ctx->g, ctx->recvbuf, ctx->pos[b], ctx->vel[b],
+        ctx->start + ctx->g.wncell, (int)ctx->cap, ctx->g, ctx->recvbuf, ctx->pos[b], ctx->vel[b],
         ctx->rigid ? ctx->quat[b] : nullptr, ctx->rigid ? ctx->angm[b] : nullptr, ctx->cell_of, ctx->rank,
         ctx->count, ctx->n_aux, ctx->flag, ctx->send_cnt);
     ctx->launches += 1;
@@ -704,7 +712,8 @@ static int group_rebalance(Group* G)
     for (mardyn_ctx* c : G->m) {
         mardyn_ctx* ctx = c;
         if (int rc = refresh_n(c)) return rc;
-        k_owned_counts<<<nblk(ncell, 256), 256, 0, c->stream>>>(ncell, c->start, c->owner, c->dd_rank, c->gcount);
+        CK(cudaMemsetAsync(c->gcount, 0, 4 * (size_t)ncell, c->stream));
+        k_owned_counts<<<nblk(c->g.wncell, 256), 256, 0, c->stream>>>(c->g, c->start, c->owner, c->dd_rank, c->gcount);
         c->launches += 1;
         CK(cudaGetLastError());
     }
@@ -809,7 +818,7 @@ static int group_thermostat(Group* G, long long k)
         mardyn_ctx* c = G->m[r];
         mardyn_ctx* ctx = c;
         k_rescale_global<<<std::min(nblk(c->cap, 256), 8 * c->num_sms), 256, 0, c->stream>>>(
-            (int)c->cap, c->start + c->g.ncell, c->vel[c->cur], c->rigid ? c->angm[c->cur] : nullptr, ke[r],
+            (int)c->cap, c->start + c->g.wncell, c->vel[c->cur], c->rigid ? c->angm[c->cur] : nullptr, ke[r],
             c->ndof_global, c->T_target, c->flag);
         c->launches += 1;
         CK(cudaGetLastError());

@@ -49,10 +49,10 @@ __device__ __forceinline__ Row load_row(const int* __restrict__ start, const Gri
                                         int cz, int dy, int dz)
 {
     const int lane = threadIdx.x & 31;
-    int ry = wrapi(cy + dy, g.nc[1]), rz = wrapi(cz + dz, g.nc[2]);
+    int ry = wrapi(cy + dy, g.wn[1]), rz = wrapi(cz + dz, g.wn[2]);     // rank-local window
     int st = 0, cn = 0;
     if (lane < 3) {
-        int c = wrapi(cx + lane - 1, g.nc[0]) + g.nc[0] * (ry + g.nc[1] * rz);
+        int c = wrapi(cx + lane - 1, g.wn[0]) + g.wn[0] * (ry + g.wn[1] * rz);
         st = __ldg(start + c);
         cn = __ldg(start + c + 1) - st;
     }

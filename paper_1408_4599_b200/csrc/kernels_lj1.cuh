@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
 
     const GridP& g = a.g;
     const int gw = blockIdx.x * WARPS + wib, nw = gridDim.x * WARPS;
-    const int nx = g.nc[0], ny = g.nc[1], nz = g.nc[2];
+    // cell coordinates in the rank-local window (the whole grid for one domain)
+    const int nx = g.wn[0], ny = g.wn[1], nz = g.wn[2];
     const int kmax = min(KMAX, nx - 2);
     const float lo = g.cut2_lo, hi = g.cut2_hi;
     const float c6 = a.sig2 * a.sig2 * a.sig2, hc = 0.5f / c6;     // sigma^6, 1/(2 sigma^6)
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
 
     // n_candidates (27-cell full-shell count, reported observable): each home lane
     // adds sum_27 N_c' - 1 for its molecule (from the staged cell table or start[])
-    const int nsorted = __ldg(a.start + g.ncell);
+    const int nsorted = __ldg(a.start + g.wncell);
     const int nb32 = (nsorted + 31) >> 5;
     const int B1 = nb32 <= MD_LJ1_HALF * nw ? 0 : nb32;       // blocks of 32, or half blocks of 16
     const int nblocks = B1 + max(0, (nsorted - 32 * B1 + 15) >> 4);
@@ -282,7 +283,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
         bool valid = mi < nsorted;
         uint4 pi = valid ? a.pos[mi] : make_uint4(0, 0, 0, 0);
         const float4 vi = (STEP && valid) ? a.vel[mi] : make_float4(0.f, 0.f, 0.f, 0.f);   // in flight during the forces
-        const int cx = cell_of_u(g, 0, pi.x), cy = cell_of_u(g, 1, pi.y), cz = cell_of_u(g, 2, pi.z);
+        const int cx = loc_axis(g, 0, cell_of_u(g, 0, pi.x)), cy = loc_axis(g, 1, cell_of_u(g, 1, pi.y)),
+                  cz = loc_axis(g, 2, cell_of_u(g, 2, pi.z));
         const bool home = valid && cx >= g.hlo[0] && cx < g.hlo[0] + g.hdim[0] && cy >= g.hlo[1] &&
                           cy < g.hlo[1] + g.hdim[1] && cz >= g.hlo[2] && cz < g.hlo[2] + g.hdim[2];
         const int row = cy + ny * cz;
@@ -643,12 +645,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                 if (o.bad) atomicOr(a.flag, 1);
                 a.pos[mi] = o.p;
                 a.vel[mi] = o.v;
-                clb = o.c[0] + nx * (o.c[1] + ny * o.c[2]);
+                clb = cell_loc(g, o.c[0], o.c[1], o.c[2]);
                 if (DD) {
                     pn = o.p;
                     vn = o.v;
-                    own = a.dd.owner[clb];
-                    const uint32_t gm = a.dd.gmask[clb];
+                    const int clg = cell_glob(g, o.c[0], o.c[1], o.c[2]);
+                    own = a.dd.owner[clg];
+                    const uint32_t gm = a.dd.gmask[clg];
                     dmask = (gm & ~(1u << a.dd.rank)) | (own != a.dd.rank ? 1u << own : 0u);
                     if (own != a.dd.rank) {                // migrant: kept as a ghost if in my halo
                         if ((gm >> a.dd.rank) & 1u) a.vel[mi] = make_float4(vn.x, vn.y, vn.z, __int_as_float(md_comp(vn.w) | 256));

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
         if (tid < 27) {
             const int r = tid / 3, k = tid % 3;
             const int dy = r % 3 - 1, dz = r / 3 - 1;
-            const int cc = wrapi(cx + k - 1, g.nc[0]) + g.nc[0] * (wrapi(cy + dy, g.nc[1]) + g.nc[1] * wrapi(cz + dz, g.nc[2]));
+            const int cc = wrapi(cx + k - 1, g.wn[0]) + g.wn[0] * (wrapi(cy + dy, g.wn[1]) + g.wn[1] * wrapi(cz + dz, g.wn[2]));
             const int st = __ldg(a.start + cc);
             rinfo[8 * r + k] = st;
             rinfo[8 * r + 3 + k] = __ldg(a.start + cc + 1) - st;

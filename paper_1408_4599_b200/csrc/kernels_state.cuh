@@ -47,7 +47,7 @@ __global__ void k_ingest(int n, const double* __restrict__ r, const double* __re
         u[k] = (uint32_t)x;
         c[k] = cell_of_u(g, k, u[k]);
     }
-    const int cl0 = c[0] + g.nc[0] * (c[1] + g.nc[1] * c[2]);
+    const int cl0 = cell_glob(g, c[0], c[1], c[2]);
     int gflag = 0;
     if (owner) {                            // spatial decomposition: keep owned + halo molecules
         const bool ghost = (gmask[cl0] >> me) & 1u;
@@ -63,7 +63,7 @@ __global__ void k_ingest(int n, const double* __restrict__ r, const double* __re
         angm[i] = j ? make_float4((float)j[3 * i], (float)j[3 * i + 1], (float)j[3 * i + 2], 0.f)
                     : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    int cl = c[0] + g.nc[0] * (c[1] + g.nc[1] * c[2]);
+    int cl = cell_loc(g, c[0], c[1], c[2]);
     cell_of[i] = cl;
     rank[i] = atomicAdd(&count[cl], 1);
 }
@@ -262,16 +262,18 @@ __device__ __forceinline__ void canon_one(int t, int cap, const GridP& g, const 
     float4 v = vel_s[old];
     pos_d[dst] = p;
     vel_d[dst] = v;
-    int cx = c % g.nc[0];
-    int cy = (c / g.nc[0]) % g.nc[1];
-    int cz = c / (g.nc[0] * g.nc[1]);
+    // the slot's cell: local (window) coordinates, and the global ones of its origin
+    const int lx = c % g.wn[0];
+    const int ly = (c / g.wn[0]) % g.wn[1];
+    const int lz = c / (g.wn[0] * g.wn[1]);
+    const int cx = glob_axis(g, 0, lx), cy = glob_axis(g, 1, ly), cz = glob_axis(g, 2, lz);
     float4 x;
     x.x = (float)(int)(p.x - (uint32_t)cx * g.E[0]) * g.s;    // exact (A12)
     x.y = (float)(int)(p.y - (uint32_t)cy * g.E[1]) * g.s;
     x.z = (float)(int)(p.z - (uint32_t)cz * g.E[2]) * g.s;
-    // rigid kernels: component bits; single-site kernel: the cell's x index
+    // rigid kernels: component bits; single-site kernel: the cell's local x index
     // (it rebuilds sub-chunk-relative x = xs.x + (cx - c_origin) * edge exactly)
-    x.w = RIGID ? __int_as_float(md_comp(v.w)) : (float)cx;
+    x.w = RIGID ? __int_as_float(md_comp(v.w)) : (float)lx;
     xs[dst] = x;
     if (RIGID) {
         float4 q = quat_s[old];
@@ -307,7 +309,7 @@ __global__ void k_canon(int n, int cap, GridP g, const unsigned long long* __res
                         float4* __restrict__ xs, float4* __restrict__ site,
                         const DevModel* __restrict__ model)
 {
-    const int lim = min(n, start[g.ncell]);
+    const int lim = min(n, start[g.wncell]);
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < lim; t += gridDim.x * blockDim.x)
         canon_one<RIGID>(t, cap, g, keys, oldidx, slot_cell, start, pos_s, vel_s, quat_s, angm_s, pos_d, vel_d,
                          quat_d, angm_d, xs, site, model);
@@ -407,19 +409,20 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
             angm[t] = make_float4(jn.x, jn.y, jn.z, 0.f);
             if (!(isfinite(jn.x) && isfinite(jn.y) && isfinite(jn.z))) atomicOr(flag, 1);
         }
-        int cl = c[0] + g.nc[0] * (c[1] + g.nc[1] * c[2]);
+        const int clg = cell_glob(g, c[0], c[1], c[2]);     // owner / halo maps
+        int cl = cell_loc(g, c[0], c[1], c[2]);             // count / cell_of (rank-local window)
         if (DD) {
             pn = pos[t];
             vn = vel[t];
             qn = RIGID ? quat[t] : make_float4(1.f, 0.f, 0.f, 0.f);
             jn = RIGID ? angm[t] : make_float4(0.f, 0.f, 0.f, 0.f);
-            own = dd.owner[cl];
+            own = dd.owner[clg];
             // halo copies for the other ranks whose halo holds the new cell; the record for the
             // new owner (migrant) if that is another rank -- packed below, one atomic per warp
             // and destination
-            dmask = (dd.gmask[cl] & ~(1u << dd.rank)) | (own != dd.rank ? 1u << own : 0u);
+            dmask = (dd.gmask[clg] & ~(1u << dd.rank)) | (own != dd.rank ? 1u << own : 0u);
             if (own != dd.rank) {                          // migrant
-                if ((dd.gmask[cl] >> dd.rank) & 1u) {      // its new cell is in my halo: keep a copy
+                if ((dd.gmask[clg] >> dd.rank) & 1u) {     // its new cell is in my halo: keep a copy
                     vel[t] = make_float4(vn.x, vn.y, vn.z, __int_as_float(md_comp(vn.w) | 256));
                 } else {
                     cell_of[t] = -1;
@@ -458,7 +461,7 @@ __global__ void k_import(int n, int base, GridP g, const DDRec* __restrict__ rec
     pos[t] = r.pos;
     vel[t] = r.vel;
     if (quat) { quat[t] = r.quat; angm[t] = r.angm; }
-    const int cl = cell_of_u(g, 0, r.pos.x) + g.nc[0] * (cell_of_u(g, 1, r.pos.y) + g.nc[1] * cell_of_u(g, 2, r.pos.z));
+    const int cl = cell_loc(g, cell_of_u(g, 0, r.pos.x), cell_of_u(g, 1, r.pos.y), cell_of_u(g, 2, r.pos.z));
     cell_of[t] = cl;
     rank[t] = atomicAdd(&count[cl], 1);
 }
@@ -508,7 +511,7 @@ __global__ void k_import_seg(int nranks, int seg_cap, const int* __restrict__ rt
     pos[slot] = rec.pos;
     vel[slot] = rec.vel;
     if (quat) { quat[slot] = rec.quat; angm[slot] = rec.angm; }
-    const int cl = cell_of_u(g, 0, rec.pos.x) + g.nc[0] * (cell_of_u(g, 1, rec.pos.y) + g.nc[1] * cell_of_u(g, 2, rec.pos.z));
+    const int cl = cell_loc(g, cell_of_u(g, 0, rec.pos.x), cell_of_u(g, 1, rec.pos.y), cell_of_u(g, 2, rec.pos.z));
     cell_of[slot] = cl;
     rank[slot] = atomicAdd(&count[cl], 1);
 }
@@ -555,9 +558,10 @@ __global__ void k_ingest_dd(int m, int base, const double* __restrict__ r, const
                 u[k] = (uint32_t)x;
                 c[k] = cell_of_u(g, k, u[k]);
             }
-            cl = c[0] + g.nc[0] * (c[1] + g.nc[1] * c[2]);
-            ghost = (gmask[cl] >> me) & 1u;
-            keep = owner[cl] == me || ghost;
+            const int clg = cell_glob(g, c[0], c[1], c[2]);
+            ghost = (gmask[clg] >> me) & 1u;
+            keep = owner[clg] == me || ghost;
+            if (keep) cl = cell_loc(g, c[0], c[1], c[2]);
         }
     }
     const unsigned b = __ballot_sync(0xffffffffu, keep);
@@ -582,11 +586,15 @@ __global__ void k_ingest_dd(int m, int base, const double* __restrict__ r, const
 
 // per-cell molecule counts of the cells this rank owns (0 elsewhere) from the last cell
 // rebuild: the measured load of the rebalance (Eq. 6 input, reading A19)
-__global__ void k_owned_counts(int ncell, const int* __restrict__ start, const uint8_t* __restrict__ owner,
+__global__ void k_owned_counts(GridP g, const int* __restrict__ start, const uint8_t* __restrict__ owner,
                                int me, int* __restrict__ out)
 {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c < ncell) out[c] = owner[c] == me ? start[c + 1] - start[c] : 0;
+    // over the rank-local window (out[] is zero elsewhere), written per global cell
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= g.wncell) return;
+    const int lx = l % g.wn[0], ly = (l / g.wn[0]) % g.wn[1], lz = l / (g.wn[0] * g.wn[1]);
+    const int c = cell_glob(g, glob_axis(g, 0, lx), glob_axis(g, 1, ly), glob_axis(g, 2, lz));
+    if (owner[c] == me) out[c] = start[l + 1] - start[l];
 }
 
 // Rebalance: re-distribute the sorted state under the new cell
@@ -611,12 +619,14 @@ __global__ void k_repartition(int n, GridP g, DDArgs dd, const uint4* __restrict
         v = vel[t];
         if (!md_ghost(v.w)) {
             p = pos[t];
-            cl = cell_of_u(g, 0, p.x) + g.nc[0] * (cell_of_u(g, 1, p.y) + g.nc[1] * cell_of_u(g, 2, p.z));
-            own = dd.owner[cl];
-            const uint32_t gm = dd.gmask[cl];
+            const int gx = cell_of_u(g, 0, p.x), gy = cell_of_u(g, 1, p.y), gz = cell_of_u(g, 2, p.z);
+            const int clg = cell_glob(g, gx, gy, gz);
+            own = dd.owner[clg];
+            const uint32_t gm = dd.gmask[clg];
             dmask = (gm & ~(1u << dd.rank)) | (own != dd.rank ? 1u << own : 0u);
             if (quat) { qn = quat[t]; jn = angm[t]; }
             if (!COUNT) {
+                cl = cell_loc(g, gx, gy, gz);                // in the NEW window
                 if (own == dd.rank) {
                     vel[t] = make_float4(v.x, v.y, v.z, __int_as_float(md_comp(v.w)));
                 } else if ((gm >> dd.rank) & 1u) {

@@ -258,8 +258,9 @@ static int grid_setup(const double L[3], double rc, double dt, GridP& g, std::st
     g.band_hw = 0.5f * (g.cut2_hi - g.cut2_lo) + 1e-6f * g.cut2_hi;
     g.cut2_q = (long long)std::ceil(rc2 / (s * s));
     g.dt = (float)dt;
-    for (int k = 0; k < 3; ++k) { g.hlo[k] = 0; g.hdim[k] = g.nc[k]; }
+    for (int k = 0; k < 3; ++k) { g.hlo[k] = 0; g.hdim[k] = g.nc[k]; g.wlo[k] = 0; g.wn[k] = g.nc[k]; }
     g.nhome = g.ncell;
+    g.wncell = g.ncell;
     return MARDYN_OK;
 }
 
@@ -380,7 +381,7 @@ static int refresh_n(mardyn_ctx* ctx)
     }
     if (!ctx->n_stale) return MARDYN_OK;
     int kept = 0, nf = 0;
-    CK(cudaMemcpyAsync(&kept, ctx->start + ctx->g.ncell, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&kept, ctx->start + ctx->g.wncell, 4, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(&nf, ctx->n_aux + 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->n = kept;
@@ -472,7 +473,8 @@ static inline int nblk(int64_t n, int t) { return (int)((n + t - 1) / t); }
 // the grids then cover the capacity)
 static int enqueue_sort(mardyn_ctx* ctx, int src, int dst, int64_t n_unsorted = -1, const int* n_dev = nullptr)
 {
-    const int n = n_dev ? (int)ctx->cap : (int)(n_unsorted < 0 ? ctx->n : n_unsorted), ncell = ctx->g.ncell;
+    // the scan covers the rank-local cell window (the whole grid for one domain)
+    const int n = n_dev ? (int)ctx->cap : (int)(n_unsorted < 0 ? ctx->n : n_unsorted), ncell = ctx->g.wncell;
     // count known on the host: one thread per molecule; in device memory only: a grid-stride
     // grid of 8 blocks per SM (independent of the capacity)
     const int gb = n_dev ? std::min(nblk(n, 256), 8 * ctx->num_sms) : nblk(n, 256);
@@ -1248,9 +1250,16 @@ int mardyn_get_raw(mardyn_ctx* ctx, int64_t cap, uint32_t* pos_fixed, int32_t* c
     if (rc) return rc;
     if (cell_count) {
         // counts of the current sorted state = start differences
-        std::vector<int> st(ctx->g.ncell + 1);
-        CK(cudaMemcpy(st.data(), ctx->start, sizeof(int) * (ctx->g.ncell + 1), cudaMemcpyDeviceToHost));
-        for (int c = 0; c < ctx->g.ncell; ++c) cell_count[c] = st[c + 1] - st[c];
+        // counts of the current sorted state = start differences over the (rank-local) window,
+        // reported per global cell (0 outside the window)
+        const GridP& g = ctx->g;
+        std::vector<int> st(g.wncell + 1);
+        CK(cudaMemcpy(st.data(), ctx->start, sizeof(int) * (g.wncell + 1), cudaMemcpyDeviceToHost));
+        std::fill(cell_count, cell_count + g.ncell, 0);
+        for (int l = 0; l < g.wncell; ++l) {
+            const int lx = l % g.wn[0], ly = (l / g.wn[0]) % g.wn[1], lz = l / (g.wn[0] * g.wn[1]);
+            cell_count[cell_glob(g, glob_axis(g, 0, lx), glob_axis(g, 1, ly), glob_axis(g, 2, lz))] = st[l + 1] - st[l];
+        }
     }
     return MARDYN_OK;
 }
