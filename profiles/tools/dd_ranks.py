@@ -106,7 +106,7 @@ def main():
             print(json.dumps(out), flush=True)
     elif mode == "droplet":
         t = time.time()
-        s = S.droplet(L=160.0, R=42.0)          # R / L < 0.3: the lattice sphere does not wrap
+        s = S.droplet(L=320.0, R=85.0)          # ~2.5 M molecules; R / L < 0.3 keeps the sphere off the seam
         print(json.dumps({"droplet_n": len(s["r"]), "gen_s": time.time() - t}), flush=True)
         t1 = t_single(s)
         for p in [int(x) for x in sys.argv[2:]]:

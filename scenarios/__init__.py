@@ -389,15 +389,15 @@ def droplet(L=30.0, R=8.0, centre=(0.3, 0.55, 0.5), rho_l=0.73, rho_v=0.02, T=0.
         dc = cand - c
         dc -= box * np.round(dc / box)
         cand = cand[np.einsum("ij,ij->i", dc, dc) > (R + 1.0) ** 2]
-        for p in cand:
-            if len(acc) >= N_v:
-                break
-            if len(acc):
-                dd = acc - p
-                dd -= box * np.round(dd / box)
-                if np.min(np.einsum("ij,ij->i", dd, dd)) < 1.0:
-                    continue
-            acc = np.vstack([acc, p])
+        # sequential rejection in draw order (as config4): against the accepted vapour by a
+        # grid lookup, then conflicts inside the batch resolved in draw order
+        cand = cand[~_neighbours_within(acc, box, cand, 1.0)]
+        keep = np.ones(len(cand), dtype=bool)
+        for i_, j_ in _pairs_within(cand, box, 1.0):
+            if keep[i_]:
+                keep[j_] = False
+        cand = cand[keep]
+        acc = np.concatenate([acc, cand[: N_v - len(acc)]])
     X = np.concatenate([liq, acc]) % box
     V = maxwell_boltzmann(rng, len(X), 1.0, T)
     return _system("droplet", box, 2.5, 0.002, steps, T, [lj1_component()], X, V)
