@@ -28,6 +28,12 @@ struct Group {
     cudaGraphExec_t gx[2] = {nullptr, nullptr};
 };
 
+static bool nccl_graphs()
+{
+    static const bool on = [] { const char* e = std::getenv("MARDYN_NCCL_GRAPHS"); return e && e[0] == '1'; }();
+    return on;
+}
+
 static void group_drop_graphs(Group* G)
 {
     if (!G) return;
@@ -667,6 +673,9 @@ static int group_async_step(Group* G)
     mardyn_ctx* ctx = G->m[0];
     cudaStream_t s = ctx->stream;             // loopback: every rank's stream; NCCL: the one rank's
     const int b = ctx->cur;
+    // NCCL p2p under stream capture has not run on several GPUs here (one GPU this round): the
+    // NCCL step stays eager unless MARDYN_NCCL_GRAPHS=1
+    if (G->nccl && !nccl_graphs()) return group_async_enqueue(G);
     if (G->gx[b]) {
         CK(cudaGraphLaunch(G->gx[b], s));
         for (mardyn_ctx* c : G->m) {           // the host-side bookkeeping of begin / end
