@@ -314,6 +314,14 @@ int mardyn_set_partition(struct mardyn_ctx* ctx, const int32_t* boxes);
 int mardyn_get_partition(const struct mardyn_ctx* ctx, int32_t* boxes);
 int mardyn_dd_counts(struct mardyn_ctx* ctx, int64_t n, const double* r, int64_t* counts);
 
+/* Per-cell load the k-d tree balances (partition and rebalance; every rank of a group):
+ * 0 = Eq. 6 (the default: pair-interaction cost N_i/2 (N_i + sum_26 N_j)),
+ * 1 = the molecule count N_i.  On a B200 the step time per molecule varies by less than
+ * the pair count does (per-molecule work -- staging, window searches, integration, the
+ * rebuild -- dominates, and sparse cells take the slower per-lane path), so model 1 balances
+ * heterogeneous systems better.  Errors: MARDYN_EINVAL.             */
+int mardyn_set_cost_model(struct mardyn_ctx* ctx, int32_t model);
+
 /* Host-only (no context, no GPU): cells per axis of the A12 lattice for box and
  * cutoff (ncell[3]) and, if counts != NULL, the molecules per cell (x fastest) of
  * the n positions r (n*3); and the k-d partition of those positions into p boxes

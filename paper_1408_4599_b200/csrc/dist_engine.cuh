@@ -152,7 +152,10 @@ static int boxes_from_counts(mardyn_ctx* ctx, const int32_t* counts, std::vector
     const GridP& g = ctx->g;
     const int nx = g.nc[0], ny = g.nc[1], nz = g.nc[2], p = ctx->nranks;
     std::vector<double> cost((size_t)g.ncell);
-    mdd::cell_cost(counts, nx, ny, nz, cost.data());
+    if (ctx->cost_model == 1)             // linear: the molecules per cell (mardyn_set_cost_model)
+        for (size_t c = 0; c < cost.size(); ++c) cost[c] = (double)counts[c];
+    else
+        mdd::cell_cost(counts, nx, ny, nz, cost.data());
     std::vector<mdd::Box> leaves;
     mdd::Box all;
     all.lo[0] = all.lo[1] = all.lo[2] = 0;
@@ -1073,6 +1076,14 @@ int mardyn_kd_partition(const double box[3], double cutoff, int64_t n, const dou
     std::vector<double> cost(counts.size());
     mdd::cell_cost(counts.data(), nc[0], nc[1], nc[2], cost.data());
     return mardyn_kd_decompose(cost.data(), nc[0], nc[1], nc[2], p, boxes, loads);
+}
+
+int mardyn_set_cost_model(mardyn_ctx* ctx, int32_t model)
+{
+    if (!ctx) return MARDYN_EINVAL;
+    if (model != 0 && model != 1) return fail(ctx, MARDYN_EINVAL, "cost model: 0 = Eq. 6, 1 = molecule count");
+    for (mardyn_ctx* c : group_members(ctx)) c->cost_model = model;
+    return MARDYN_OK;
 }
 
 int mardyn_rebalance(mardyn_ctx* ctx)

@@ -159,6 +159,7 @@ struct mardyn_ctx {
     Group* grp = nullptr;                  // distributed / loopback group (nullptr: one domain)
     int dd_rank = 0, nranks = 1;
     int rebalance_interval = 0;            // steps between re-partitions (0: static)
+    int cost_model = 0;                    // per-cell load of the k-d tree: 0 = Eq. 6, 1 = molecule count
     long long last_rebalance = -1;         // host_step of the last re-partition
     bool seg_ready = false;                // exchange segments sized (else the next step is synchronous)
     bool n_stale = false;                  // asynchronous decomposed steps: host copy of n out of date

@@ -30,7 +30,7 @@ EXPORTS = ["mardyn_create", "mardyn_get_grid", "mardyn_workspace_bytes", "mardyn
            "mardyn_launch_count", "mardyn_cell_cost", "mardyn_kd_decompose",
            "mardyn_nccl_unique_id", "mardyn_create_distributed", "mardyn_create_loopback",
            "mardyn_partition", "mardyn_set_partition", "mardyn_get_partition", "mardyn_dd_counts",
-           "mardyn_rebalance", "mardyn_grid_counts", "mardyn_kd_partition",
+           "mardyn_rebalance", "mardyn_grid_counts", "mardyn_kd_partition", "mardyn_set_cost_model",
            "mardyn_set_thermostat", "mardyn_lj_tail", "mardyn_get_tail_corrections",
            "mardyn_last_error", "mardyn_destroy"]
 
@@ -115,6 +115,7 @@ def load_library():
     lib.mardyn_get_partition.argtypes = [vp, vp]
     lib.mardyn_dd_counts.argtypes = [vp, C.c_int64, vp, vp]
     lib.mardyn_rebalance.argtypes = [vp]
+    lib.mardyn_set_cost_model.argtypes = [vp, C.c_int32]
     lib.mardyn_grid_counts.argtypes = [P(C.c_double), C.c_double, C.c_int64, vp, vp, vp]
     lib.mardyn_kd_partition.argtypes = [P(C.c_double), C.c_double, C.c_int64, vp, C.c_int32, vp, vp]
     lib.mardyn_set_thermostat.argtypes = [vp, C.c_double, C.c_int32]
@@ -398,6 +399,10 @@ class Context:
     def rebalance(self):
         self._check(self.lib.mardyn_rebalance(self.h))
 
+    def set_cost_model(self, model):
+        """Per-cell load of the k-d tree: 0 = Eq. 6 (default), 1 = molecule count."""
+        self._check(self.lib.mardyn_set_cost_model(self.h, int(model)))
+
     def _n(self):
         n = C.c_int64()
         self._check(self.lib.mardyn_get_molecules(self.h, self.capacity, C.byref(n), None, None, None,
@@ -532,7 +537,7 @@ class DecomposedRun:
     the NCCL unique id travels by torch.distributed.broadcast_object_list)."""
 
     def __init__(self, system, nranks, transport="loopback", rank=None, eta=None, boxes=None, stream=None,
-                 rebalance_interval=0, headroom=1.5):
+                 rebalance_interval=0, headroom=1.5, cost_model=0):
         import torch
         self.torch = torch
         self.system, self.nranks, self.transport = system, int(nranks), transport
@@ -550,6 +555,7 @@ class DecomposedRun:
         self.lead = self.ctxs[0]
         self.stream = self.lead.stream
         r = system["r"]
+        self.lead.set_cost_model(cost_model)
         for c in self.ctxs:
             if boxes is None:
                 c.partition(r)

@@ -43,8 +43,9 @@ def t_single(s):
     return float(np.median(ms))
 
 
-def t_ranks(s, p, boxes=None, rebalance=0):
-    run = mardyn.DecomposedRun(s, p, transport="loopback", boxes=boxes, rebalance_interval=rebalance)
+def t_ranks(s, p, boxes=None, rebalance=0, cost_model=0):
+    run = mardyn.DecomposedRun(s, p, transport="loopback", boxes=boxes, rebalance_interval=rebalance,
+                               cost_model=cost_model)
     run.step(WARM)
     run.observables()
     per, fper = [], []
@@ -109,9 +110,19 @@ def main():
         s = S.droplet(L=320.0, R=85.0)          # ~2.5 M molecules; R / L < 0.3 keeps the sphere off the seam
         print(json.dumps({"droplet_n": len(s["r"]), "gen_s": time.time() - t}), flush=True)
         t1 = t_single(s)
+        counts = mardyn.grid_counts(s["box"], s["rc"], s["r"]).astype(np.float64)
         for p in [int(x) for x in sys.argv[2:]]:
             st = t_ranks(s, p, boxes=equal_volume(s, p))
             kd = t_ranks(s, p)
+            # the same tree on plain molecule counts (cost model 1) and on Eq. 6 + alpha N_i
+            kdn = t_ranks(s, p, cost_model=1)
+            eq6 = mardyn.cell_cost(counts.astype(np.int32))
+            alt = {}
+            for alpha in (100.0, 300.0):
+                bA, _ = mardyn.kd_decompose(eq6 + alpha * counts, p)
+                alt[alpha] = t_ranks(s, p, boxes=bA.reshape(p, 6))["slowest_ms"]
+            print(json.dumps({"p": p, "kd_counts_slowest_ms": kdn["slowest_ms"], "kd_counts_rank_ms": kdn["rank_ms"],
+                              "kd_eq6_alpha_slowest_ms": alt}), flush=True)
             print(json.dumps({"config": "droplet", "n": len(s["r"]), "p": p, "T1_ms": t1,
                               "static_slowest_ms": st["slowest_ms"], "kd_slowest_ms": kd["slowest_ms"],
                               "static_over_kd": st["slowest_ms"] / kd["slowest_ms"],

@@ -79,13 +79,15 @@ def equal_volume_boxes(s, p):
             for y0, y1 in zip(cuts[1], cuts[1][1:]) for x0, x1 in zip(cuts[0], cuts[0][1:])]
 
 
-def test_rebalance_droplet_vs_oracle(md, oracle_mod):
+@pytest.mark.parametrize("cost_model", [0, 1])
+def test_rebalance_droplet_vs_oracle(md, oracle_mod, cost_model):
     """Off-centre droplet on 4 ranks starting from equal-volume
-    boxes, re-partitioned every 5 steps from the measured cell loads: the owned-load
-    imbalance drops, the boxes change, and every step still matches the oracle."""
+    boxes, re-partitioned every 5 steps from the measured cell loads (Eq. 6 or the
+    molecule count): the owned-load imbalance drops, the boxes change, and every step
+    still matches the oracle."""
     s = S.config("droplet")
     static = equal_volume_boxes(s, 4)
-    run = md.DecomposedRun(s, 4, transport="loopback", boxes=static, rebalance_interval=5)
+    run = md.DecomposedRun(s, 4, transport="loopback", boxes=static, rebalance_interval=5, cost_model=cost_model)
     before = run.owned_counts()
     compare_run(md, oracle_mod, s, run, 12)
     after = run.owned_counts()
