@@ -1,7 +1,8 @@
 """Full-length trajectory parity: the CUDA path (through the C ABI) and the
 fp64 oracle evolve the same seeded initial state independently for every
 BASELINE config's own run length (c0 10 steps, c1 100 at full size, c1s /
-c2s / c3s 100, c4s 200; BASELINE.json configs, Eqs. 2-5).
+c2s / c3s 100, c4s 200; and c2, c3 at full size for 10 steps; BASELINE.json
+configs, Eqs. 2-5).
 
 Per step k (reading A23): U, W, T of t_k.  Error measure (reading A25,
 DESIGN.md §2): e_k = |X_gpu(k) - X_oracle(k)| / max_k' |X_oracle(k')| -- W
@@ -26,7 +27,11 @@ from parity_util import assert_forces_close, assert_rel, min_image
 
 pytestmark = pytest.mark.gpu
 
-RUNS = [("c0", 10), ("c1s", 100), ("c4s", 200), ("c2s", 100), ("c3s", 100), ("c1", 100)]
+RUNS = [("c0", 10), ("c1s", 100), ("c4s", 200), ("c2s", 100), ("c3s", 100), ("c1", 100),
+        # the rigid configs at FULL size (10^6 2CLJQ, 5 * 10^5 TIP4P) for their first 10 steps: the
+        # oracle takes ~5 s per step there; the first 10 steps are well-conditioned (env < 1.5e-6,
+        # tests/test_oracle_sensitivity.py), so the strict bar applies
+        ("c2", 10), ("c3", 10)]
 
 
 @pytest.fixture(scope="module")
@@ -68,11 +73,12 @@ def test_full_length_run(md, oracle_mod, name, nsteps):
     o = oracle_mod.System(s)
     u0 = o.quantize(s["r"])
     uo, vo, qo, jo, obs = o.run(s["dt"], s["comp"], u0, s["v"], s["q"], s["j"], nsteps, mode="full")
-    rigid = name in ("c2s", "c3s")
-    env = envelope(o, s, u0, obs, nsteps) if rigid else None
+    rigid = name in ("c2s", "c3s", "c2", "c3")
+    use_env = rigid and nsteps > 10
+    env = envelope(o, s, u0, obs, nsteps) if use_env else None
     for key, ok in (("U_pot", "U"), ("virial", "W"), ("T", "T")):
         e = scaled_err([h[key] for h in hist], obs[ok])
-        bar = np.maximum(1e-5, 4.0 * env[ok]) if rigid else np.full(nsteps, 1e-5)
+        bar = np.maximum(1e-5, 4.0 * env[ok]) if use_env else np.full(nsteps, 1e-5)
         bad = np.nonzero(e > bar)[0]
         assert bad.size == 0, f"{name} {key}: step {bad[0]} error {e[bad[0]]:.2e} > {bar[bad[0]]:.2e}"
     npg = np.array([h["n_pairs"] for h in hist])
