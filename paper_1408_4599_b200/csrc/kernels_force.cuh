@@ -37,6 +37,11 @@ struct ForceArgs {
     int* flag;                   // error flags (2 = coincident molecule centres)
     const DevModel* model;
     float sig2, eps24, eps4, shift;   // single-site LJ fast path
+    // one-component rigid kernels (rig3): LJ site pairs (ia, ib < 2) as (sigma^2, 24 eps, 4 eps,
+    // shift) and the reaction-field constants, as kernel parameters -- constant-bank operands
+    // instead of registers
+    float4 lj3[4];
+    float krf, crf, kmm;
 };
 
 // Row descriptor of the 27-cell neighbourhood: the 3 cells (dx = -1, 0, 1)

@@ -11,8 +11,9 @@
 // molecules one at a time.  For home molecule i a group
 //   1. tests every staged molecule j against the COM cutoff (reading A1; the
 //      guard band around rc^2 is decided exactly in integer quanta), two
-//      candidates per lane per step, and appends the hits to the group's list
-//      in shared memory by ballot compaction (deterministic order);
+//      candidates per lane per step, collects the hits as per-lane bits over
+//      four steps and appends them to the group's list in shared memory at
+//      once (a group prefix of the lanes' counts; deterministic order);
 //   2. evaluates the site pairs of its list 32 partners per round (two per
 //      lane, packed into the fp32x2 instructions FADD2/FMUL2/FFMA2 of sm_100);
 //   3. reduces the 16 lanes' force and torque (tau = sum_a s_a x f_a + tau_a)
@@ -35,6 +36,9 @@ namespace rig3 {
 #endif
 #ifndef MD_RIG3_WARPS
 #define MD_RIG3_WARPS 8
+#endif
+#ifndef MD_RIG3_BITS
+#define MD_RIG3_BITS 1
 #endif
 constexpr int CAP = MD_RIG3_CAP;      // staged molecules per chunk of the neighbourhood
 constexpr int WARPS = MD_RIG3_WARPS;
@@ -115,8 +119,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
     uint16_t* hlB = hlA + (HCAP + 2);
     const unsigned gmask = 0xffffu << (16 * half);
     const GridP& g = a.g;
-    const DevModel* __restrict__ M = a.model;
-    const float krf = M->krf, crf = M->crf, kmm = M->krf_mumu;
+    const float krf = a.krf, crf = a.crf, kmm = a.kmm;
     if (tid == 0) {                       // far dummy partner (padding): COM far away, sites at the COM
         cxy[CAP / 2] = make_float4(1.0e4f, 1.0e4f, 1.0e4f, 1.0e4f);
         pz[CAP / 2] = make_float2(1.0e4f, 1.0e4f);
@@ -249,15 +252,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                         float4 si[NSLOT];
 #pragma unroll
                         for (int s = 0; s < NSLOT; ++s) si[s] = __ldg(a.site + (size_t)s * a.cap + my);
-                        float4 ljp[NLJ > 0 ? NLJ * NLJ : 1];
-#pragma unroll
-                        for (int ia = 0; ia < NLJ; ++ia)
-#pragma unroll
-                            for (int ibb = 0; ibb < NLJ; ++ibb) {
-                                const int t = ia * MD_MAX_LJ_TOTAL + ibb;
-                                ljp[ia * NLJ + ibb] = make_float4(__ldg(M->sig2 + t), __ldg(M->eps24 + t),
-                                                                  __ldg(M->eps4 + t), __ldg(M->shift + t));
-                            }
+                        static_assert(NLJ <= 2, "rig3: at most two LJ sites (ForceArgs::lj3)");
+                        const float4* ljp = a.lj3;             // [2 ia + ib], kernel parameters
                         V3 fs[SH::NS];
                         V3 ts[NPOL];
 #pragma unroll
@@ -328,7 +324,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                                 for (int ibb = 0; ibb < NLJ; ++ibb) {
                                     const V3 sb = slot3(ibb, j0, j1);
                                     const V3 rv = V3{da.x + sb.x, da.y + sb.y, da.z + sb.z};
-                                    const float4 pp = ljp[ia * NLJ + ibb];
+                                    const float4 pp = ljp[2 * ia + ibb];
                                     lj_noshift(rv, pp.x, pp.y, pp.z, uacc, fs[ia], fh);
                                 }
                             }
@@ -416,7 +412,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                             }
                         float shsum = 0.f;                     // LJTS shifts of one molecule pair (A2)
 #pragma unroll
-                        for (int k = 0; k < NLJ * NLJ; ++k) shsum += ljp[k].w;
+                        for (int k = 0; k < NLJ * NLJ; ++k) shsum += ljp[2 * (k / NLJ) + k % NLJ].w;
                         float qtot = 0.f;                      // molecule charge (one component: partners alike)
 #pragma unroll
                         for (int k = 0; k < NQ; ++k) qtot += si[SH::SQ + k].w;
@@ -430,7 +426,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                     };
 
                     // ---- distance phase: candidate pair p = base + gl (elements 2p, 2p + 1) against A
-                    //      and B, ballot compaction into the two lists (fixed order)
+                    //      and B, compaction into the two lists (fixed order)
                     int cntA = 0, cntB = 0;
                     const float2 nxA = make_float2(-xiA.x, -xiA.x), nyA = make_float2(-xiA.y, -xiA.y),
                                  nzA = make_float2(-xiA.z, -xiA.z);
@@ -438,6 +434,72 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                                  nzB = make_float2(-xiB.z, -xiB.z);
                     const float hiA = gA ? g.cut2_hi : -1.f, hiB = gB ? g.cut2_hi : -1.f;   // idle: no hits
                     const int span = max(__shfl_sync(FULL, p1 - p0, 0), __shfl_sync(FULL, p1 - p0, 16));
+#if MD_RIG3_BITS
+                    // hits are collected as per-lane bits over up to 4 iterations (16 bits per list:
+                    // bit k = 4 it + 2 u + e for element e of pair p0 + b0 + 32 it + 16 u + gl), then
+                    // compacted at once: a group prefix of the lanes' counts (one packed scan for both
+                    // lists) and each lane writing its own entries -- lane-major order, fixed
+                    int base = 0;
+                    for (;;) {
+                        const int b0 = base;
+                        unsigned bA = 0u, bB = 0u;
+#pragma unroll
+                        for (int it = 0; it < 4; ++it) {
+                            if (base >= span) break;
+#pragma unroll
+                            for (int u = 0; u < 2; ++u) {
+                                const int p = p0 + base + 16 * u + gl;
+                                const int pp = p < p1 ? p : CAP / 2;
+                                const float4 xy = cxy[pp];
+                                const float2 zz = pz[pp];
+                                const float2 xx = make_float2(xy.x, xy.y), yy = make_float2(xy.z, xy.w);
+                                float2 dx = __fadd2_rn(xx, nxA), dy = __fadd2_rn(yy, nyA), dz = __fadd2_rn(zz, nzA);
+                                float2 r2 = __fmul2_rn(dx, dx);
+                                r2 = __ffma2_rn(dy, dy, r2);
+                                r2 = __ffma2_rn(dz, dz, r2);
+                                bA |= ((r2.x < hiA ? 1u : 0u) | (r2.y < hiA ? 2u : 0u)) << (4 * it + 2 * u);
+                                dx = __fadd2_rn(xx, nxB); dy = __fadd2_rn(yy, nyB); dz = __fadd2_rn(zz, nzB);
+                                r2 = __fmul2_rn(dx, dx);
+                                r2 = __ffma2_rn(dy, dy, r2);
+                                r2 = __ffma2_rn(dz, dz, r2);
+                                bB |= ((r2.x < hiB ? 1u : 0u) | (r2.y < hiB ? 2u : 0u)) << (4 * it + 2 * u);
+                            }
+                            base += 32;
+                        }
+                        // group prefix of (count A | count B << 16)
+                        const int nab = __popc(bA) | (__popc(bB) << 16);
+                        int incl = nab;
+#pragma unroll
+                        for (int o = 1; o < 16; o <<= 1) {
+                            const int v = __shfl_up_sync(FULL, incl, o, 16);
+                            if (gl >= o) incl += v;
+                        }
+                        const int tot = __shfl_sync(FULL, incl, 15, 16);
+                        const int totA = tot & 0xffff, totB = tot >> 16;
+                        if (__any_sync(FULL, cntA + totA > HCAP || cntB + totB > HCAP)) {
+                            __syncwarp();                           // a list would overflow: evaluate both now
+                            flush(cntA, hlA, myA, xiA, selfA, tgtA, gA);
+                            flush(cntB, hlB, myB, xiB, selfB, tgtB, gB);
+                            cntA = cntB = 0;
+                            __syncwarp();
+                        }
+                        const int e0 = 2 * (p0 + b0 + gl);
+                        int oA = cntA + ((incl - nab) & 0xffff), oB = cntB + ((incl - nab) >> 16);
+                        while (bA) {
+                            const int k = __ffs(bA) - 1;
+                            bA &= bA - 1u;
+                            hlA[oA++] = (uint16_t)(e0 + 16 * k - 15 * (k & 1));
+                        }
+                        while (bB) {
+                            const int k = __ffs(bB) - 1;
+                            bB &= bB - 1u;
+                            hlB[oB++] = (uint16_t)(e0 + 16 * k - 15 * (k & 1));
+                        }
+                        cntA += totA;
+                        cntB += totB;
+                        if (base >= span) break;
+                    }
+#else
                     unsigned below;
                     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(below));
                     auto append = [&](uint16_t* hl, int& cnt, bool h0, bool h1, int pp) {
@@ -480,6 +542,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                         cntA = cntB = 0;
                         __syncwarp();
                     }
+#endif
                     __syncwarp();
                     flush(cntA, hlA, myA, xiA, selfA, tgtA, gA);
                     flush(cntB, hlB, myB, xiB, selfB, tgtB, gB);

@@ -418,6 +418,15 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_gra
     a.eps24 = ctx->model.eps24[0];
     a.eps4 = ctx->model.eps4[0];
     a.shift = ctx->model.shift[0];
+    for (int ia = 0; ia < 2; ++ia)
+        for (int ib = 0; ib < 2; ++ib) {
+            const int t = ia * MD_MAX_LJ_TOTAL + ib;
+            a.lj3[2 * ia + ib] = make_float4(ctx->model.sig2[t], ctx->model.eps24[t], ctx->model.eps4[t],
+                                             ctx->model.shift[t]);
+        }
+    a.krf = ctx->model.krf;
+    a.crf = ctx->model.crf;
+    a.kmm = ctx->model.krf_mumu;
     const int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ:
