@@ -539,6 +539,7 @@ static int gather_counts(Group* G, std::vector<std::vector<int64_t>>& C)
 // contiguous in source order); returns per local rank the records received
 static int exchange_exact(Group* G, const std::vector<std::vector<int64_t>>& C, std::vector<int64_t>& nrecv)
 {
+    NvtxRange nvtx_range("dd_exchange");
     const int p = G->p;
     const size_t RB = sizeof(DDRec);
     nrecv.assign(p, 0);
@@ -579,6 +580,7 @@ static int exchange_exact(Group* G, const std::vector<std::vector<int64_t>>& C, 
 // neighbours send far more than edge or corner ones); loopback ranks get direct puts
 static int group_sync_step(Group* G)
 {
+    NvtxRange nvtx_range("dd_sync_step");
     const int p = G->p;
     group_drop_graphs(G);                 // the segment layout is about to change
     for (mardyn_ctx* c : G->m) c->rank_timed = false;
@@ -673,6 +675,7 @@ static int group_async_enqueue(Group* G)
 
 static int group_async_step(Group* G)
 {
+    NvtxRange nvtx_range("dd_async_step");
     mardyn_ctx* ctx = G->m[0];
     cudaStream_t s = ctx->stream;             // loopback: every rank's stream; NCCL: the one rank's
     const int b = ctx->cur;
@@ -716,6 +719,7 @@ static int group_async_step(Group* G)
 // rank re-distributes its owned molecules through exchange records
 static int group_rebalance(Group* G)
 {
+    NvtxRange nvtx_range("dd_rebalance");
     const int p = G->p;
     group_drop_graphs(G);
     mardyn_ctx* c0 = G->m[0];
@@ -885,6 +889,7 @@ static int group_compute_forces(mardyn_ctx* ctx)
 // counts; ranks count ordered pairs of their owned molecules) and T from the global N_dof
 static int group_observables(mardyn_ctx* ctx, std::vector<ObsRec>& ring)
 {
+    NvtxRange nvtx_range("dd_observables");
     Group* G = ctx->grp;
     const int p = G->p;
     if (!group_ok(G)) return fail(ctx, MARDYN_ESTATE, "a rank of the group was destroyed");

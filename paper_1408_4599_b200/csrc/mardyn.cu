@@ -11,6 +11,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/mardyn.h"
 #include "common.cuh"
 #include "decomp.hpp"
@@ -19,6 +21,15 @@
 #include "kernels_lj1.cuh"
 #include "kernels_rigid3.cuh"
 #include "kernels_state.cuh"
+
+// NVTX ranges around the library's host phases (visible in Nsight Systems / ncu --nvtx; a no-op
+// without a tool attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace {
 
@@ -872,6 +883,7 @@ int mardyn_set_workspace(mardyn_ctx* ctx, void* device_ptr, size_t bytes, int64_
 int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const int32_t* comp, const double* r,
                          const double* v, const double* q, const double* j, int32_t half_step)
 {
+    NvtxRange nvtx_range("mardyn_set_molecules");
     if (!ctx) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->ws) return fail(ctx, MARDYN_ESTATE, "set_workspace must precede set_molecules");
@@ -981,6 +993,7 @@ int mardyn_set_molecules(mardyn_ctx* ctx, int64_t n, const int64_t* id, const in
 
 int mardyn_compute_forces(mardyn_ctx* ctx)
 {
+    NvtxRange nvtx_range("mardyn_compute_forces");
     if (!ctx) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (ctx->grp && ctx->nranks > 1) return group_compute_forces(ctx);
@@ -1075,6 +1088,7 @@ int mardyn_get_tail_corrections(mardyn_ctx* ctx, double* U, double* W)
 
 int mardyn_step(mardyn_ctx* ctx, int32_t nsteps)
 {
+    NvtxRange nvtx_range("mardyn_step");
     if (!ctx) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
@@ -1212,6 +1226,7 @@ static int egress(mardyn_ctx* ctx, double* r, double* v, double* q, double* j, d
 int mardyn_get_molecules(mardyn_ctx* ctx, int64_t cap, int64_t* n, int64_t* id, int32_t* comp, double* r,
                          double* v, double* q, double* j)
 {
+    NvtxRange nvtx_range("mardyn_get_molecules");
     if (!ctx || !n) return MARDYN_EINVAL;
     if (ctx->poisoned) return fail(ctx, MARDYN_ECUDA, "context poisoned");
     if (!ctx->loaded) return fail(ctx, MARDYN_ESTATE, "set_molecules first");
