@@ -81,7 +81,12 @@ __global__ void k_iota64(int n, int64_t* __restrict__ a)
 // 2^20 cells (more tiles in flight: c1's 85 k cells are 21 tiles)
 #define SCAN_PT_MAX 16
 #define SCAN_TILE (1024 * SCAN_PT_MAX)          // padding unit of the count array
+#ifndef SCAN_PT_SMALL
+#define SCAN_PT_SMALL 4
+#endif
+#ifndef SCAN_BIG_GRID
 #define SCAN_BIG_GRID (1 << 20)
+#endif
 
 __device__ __forceinline__ int warp_incl_scan(int v)
 {
@@ -155,13 +160,20 @@ __global__ void __launch_bounds__(1024) k_scan(int ncell, int* __restrict__ coun
     const int base = tile * TILE + threadIdx.x * SCAN_PT;
     int a[SCAN_PT];
     // count is padded to whole tiles (ncell_pad), so the vector loads never leave it
+    if constexpr (SCAN_PT % 4 == 0) {
 #pragma unroll
-    for (int v = 0; v < SCAN_PT / 4; ++v) {
-        const int4 c4 = *reinterpret_cast<const int4*>(count + base + 4 * v);
-        a[4 * v] = c4.x; a[4 * v + 1] = c4.y; a[4 * v + 2] = c4.z; a[4 * v + 3] = c4.w;
+        for (int v = 0; v < SCAN_PT / 4; ++v) {
+            const int4 c4 = *reinterpret_cast<const int4*>(count + base + 4 * v);
+            a[4 * v] = c4.x; a[4 * v + 1] = c4.y; a[4 * v + 2] = c4.z; a[4 * v + 3] = c4.w;
+        }
+#pragma unroll
+        for (int v = 0; v < SCAN_PT / 4; ++v) *reinterpret_cast<int4*>(count + base + 4 * v) = make_int4(0, 0, 0, 0);
+    } else {
+#pragma unroll
+        for (int k = 0; k < SCAN_PT; ++k) a[k] = count[base + k];
+#pragma unroll
+        for (int k = 0; k < SCAN_PT; ++k) count[base + k] = 0;
     }
-#pragma unroll
-    for (int v = 0; v < SCAN_PT / 4; ++v) *reinterpret_cast<int4*>(count + base + 4 * v) = make_int4(0, 0, 0, 0);
     int sum = 0;
 #pragma unroll
     for (int k = 0; k < SCAN_PT; ++k) sum += a[k];
@@ -193,7 +205,7 @@ __global__ void __launch_bounds__(1024) k_scan(int ncell, int* __restrict__ coun
     }
     __syncthreads();
     ex += excl_s;
-    if (base + SCAN_PT <= ncell) {
+    if (SCAN_PT % 4 == 0 && base + SCAN_PT <= ncell) {
 #pragma unroll
         for (int v = 0; v < SCAN_PT / 4; ++v) {
             int4 o;

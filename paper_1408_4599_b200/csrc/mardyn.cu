@@ -507,7 +507,7 @@ static int enqueue_sort(mardyn_ctx* ctx, int src, int dst, int64_t n_unsorted = 
                                                            reinterpret_cast<unsigned*>(ctx->scan_flags + ctx->ntiles),
                                                            ctx->blk_ctr);
     else
-        k_scan<4><<<(ncell + 4095) / 4096, 1024, 0, s>>>(ncell, ctx->count, ctx->start, ctx->scan_flags,
+        k_scan<SCAN_PT_SMALL><<<(ncell + 1024 * SCAN_PT_SMALL - 1) / (1024 * SCAN_PT_SMALL), 1024, 0, s>>>(ncell, ctx->count, ctx->start, ctx->scan_flags,
                                                         reinterpret_cast<unsigned*>(ctx->scan_flags + ctx->ntiles),
                                                         ctx->blk_ctr);
     k_scatter<<<gb, 256, 0, s>>>(n, ctx->pos[src], ctx->cell_of, ctx->rank, ctx->start, ctx->keys,
@@ -751,7 +751,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     };
     const int ncell = ctx->g.ncell;
     const int ncell_pad = (int)align_up((size_t)ncell, SCAN_TILE);
-    const int ntiles = ncell_pad / 4096;        // look-back flags: enough for the smallest tiles
+    const int ntiles = ncell_pad / (1024 * SCAN_PT_SMALL);   // look-back flags: enough for the smallest tiles
     const int nk = std::max(1, nblk(cap, 256));
     const int nfw = std::max(1, ctx->force_blocks * ctx->force_warps_per_block);
     // single-site kernel: one partial per block -- blocks of 32, or (small systems) half blocks
