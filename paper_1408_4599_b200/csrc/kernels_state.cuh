@@ -77,15 +77,16 @@ __global__ void k_iota64(int n, int64_t* __restrict__ a)
 // ------------------------------------------------------------------------
 // exclusive scan of the per-cell counts.  Tiles of 1024 threads x PT consecutive
 // cells: PT = 16 for large grids (a 4.1 M-cell grid (c4) is 252 tiles, one wave of
-// the co-resident CTAs; 4096-cell tiles took four waves, ~80 us), PT = 4 below
-// 2^20 cells (more tiles in flight: c1's 85 k cells are 21 tiles)
+// the co-resident CTAs; 4096-cell tiles took four waves, ~80 us; the 0.55 M-cell window
+// of a c4 rank at p = 8 is 34 tiles: 3 us less than 134), PT = 4 below 2^18 cells (c1's
+// 85 k cells are 21 tiles; 16 k-cell tiles measured 3.5 us slower there)
 #define SCAN_PT_MAX 16
 #define SCAN_TILE (1024 * SCAN_PT_MAX)          // padding unit of the count array
 #ifndef SCAN_PT_SMALL
 #define SCAN_PT_SMALL 4
 #endif
 #ifndef SCAN_BIG_GRID
-#define SCAN_BIG_GRID (1 << 20)
+#define SCAN_BIG_GRID (1 << 18)
 #endif
 
 __device__ __forceinline__ int warp_incl_scan(int v)

@@ -21,6 +21,7 @@ from paper_1408_4599_b200 import mardyn  # noqa: E402
 import os  # noqa: E402
 
 STEPS, WARM = int(os.environ.get("DD_STEPS", 20)), int(os.environ.get("DD_WARM", 4))
+COST_MODEL = int(os.environ.get("DD_COST_MODEL", 0))      # 0: Eq. 6, 1: molecule counts (scale / one)
 
 
 def t_single(s):
@@ -83,8 +84,9 @@ def main():
         for p in ps:
             if p == 1:
                 continue
-            r = t_ranks(s, p)
-            r.update({"config": name, "p": p, "T1_over_p_ms": t1 / p, "ratio": r["slowest_ms"] / (t1 / p)})
+            r = t_ranks(s, p, cost_model=COST_MODEL)
+            r.update({"config": name, "p": p, "cost_model": COST_MODEL, "T1_over_p_ms": t1 / p,
+                      "ratio": r["slowest_ms"] / (t1 / p)})
             print(json.dumps(r), flush=True)
     elif mode == "one":                     # one configuration, p ranks only (profiling)
         name, p = sys.argv[2], int(sys.argv[3])
