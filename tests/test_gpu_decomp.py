@@ -96,6 +96,26 @@ def test_rebalance_droplet_vs_oracle(md, oracle_mod, cost_model):
     assert not np.array_equal(np.asarray(run.boxes), np.asarray(static))
 
 
+@pytest.mark.parametrize("name,p", [("c2s", 4), ("c3m", 2)])
+def test_rigid_rebalance_vs_oracle(md, oracle_mod, name, p):
+    """Rigid molecules (2CLJQ, water) through a rebalance: the run starts from boxes cut
+    along z (and y), the k-d tree of the rebalance cuts x first, so every rebalance (every
+    4 steps) redistributes molecules -- positions, velocities, quaternions and angular
+    momenta travel in the exchange records (k_repartition) -- and every step still
+    matches the oracle."""
+    s = S.config3(12) if name == "c3m" else S.config(name)
+    n = np.floor(np.asarray(s["box"]) / s["rc"]).astype(int)
+    if p == 2:
+        boxes = [[0, 0, 0, n[0], n[1], 2], [0, 0, 2, n[0], n[1], n[2]]]
+    else:
+        boxes = [[0, 0, 0, n[0], 2, 2], [0, 2, 0, n[0], n[1], 2], [0, 0, 2, n[0], 2, n[2]],
+                 [0, 2, 2, n[0], n[1], n[2]]]
+    run = md.DecomposedRun(s, p, transport="loopback", boxes=boxes, rebalance_interval=4)
+    compare_run(md, oracle_mod, s, run, 12)
+    assert not np.array_equal(np.asarray(run.boxes).reshape(p, 6), np.asarray(boxes))
+    assert sum(run.owned_counts()) == len(s["r"])
+
+
 def test_explicit_rebalance_vs_oracle(md, oracle_mod):
     """mardyn_rebalance mid-run (collective re-partition + redistribution through the
     exchange records) on the slab: the run continues in step with the oracle."""
