@@ -34,15 +34,15 @@ def scaled_err(a, b):
     return np.abs(np.asarray(a, float) - b) / np.abs(b).max()
 
 
-def compare_run(md, oracle_mod, s, run, nsteps, tol=1e-5):
+def compare_run(md, oracle_mod, s, run, nsteps, tol=1e-5, eta=None):
     """Step the decomposed run and the oracle independently from the same state."""
     F, tau, ids = run.forces()                         # F(t0), tau(t0): every molecule exactly once
     assert np.array_equal(ids, np.arange(len(s["r"])))
-    o = oracle_mod.System(s)
+    o = oracle_mod.System(s, eta=eta)
     u0 = o.quantize(s["r"])
     Fo, to, _ = o.forces(s["comp"], u0, s["q"], mode="full")
     assert_forces_close(F, Fo, "force(t0)")
-    if s["components"][0]["charges"] or s["components"][0]["quadrupoles"]:
+    if any(c["charges"] or c["dipoles"] or c["quadrupoles"] for c in s["components"]):
         assert_forces_close(tau, to, "torque(t0)")
     run.step(nsteps)
     hist = run.observable_history(nsteps)
@@ -94,6 +94,19 @@ def test_rebalance_droplet_vs_oracle(md, oracle_mod, cost_model):
     assert sum(after) == len(s["r"])
     assert max(after) / np.mean(after) < max(before) / np.mean(before) - 0.2
     assert not np.array_equal(np.asarray(run.boxes), np.asarray(static))
+
+
+def test_decomposed_mixture_vs_oracle(md, oracle_mod):
+    """Two species with every site kind (LJ, charges, dipoles, quadrupoles; reaction field)
+    and the binary parameter eta -- the generic force kernel -- on 2 ranks: the
+    component ids travel with the migrants and halo copies, and each rank's N_dof counts
+    its species' rotational degrees of freedom."""
+    comps = S.random_polar_components()
+    s = S.random_system(400, (11.0, 10.0, 12.0), comps, seed_k=101, rc=2.5, eps_rf=4.0)
+    eta = np.array([[1.0, 0.9], [0.9, 1.0]])
+    run = md.DecomposedRun(s, 2, transport="loopback", eta=eta)
+    assert run.lead.get_grid()["kernel"] == 2
+    compare_run(md, oracle_mod, s, run, 6, eta=eta)
 
 
 @pytest.mark.parametrize("name,p", [("c2s", 4), ("c3m", 2)])
