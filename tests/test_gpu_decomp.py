@@ -96,6 +96,24 @@ def test_rebalance_droplet_vs_oracle(md, oracle_mod, cost_model):
     assert not np.array_equal(np.asarray(run.boxes), np.asarray(static))
 
 
+def test_empty_rank_vs_oracle(md, oracle_mod):
+    """A rank that owns no molecule: a liquid slab filling x < 0.45 L next to vacuum, two
+    boxes cut at 4 of 7 cells -- rank 1 starts with an empty home box (only halo copies of
+    the slab's surface) and receives whatever evaporates into it."""
+    s0 = S.config("c1s")
+    L = s0["box"][0]
+    keep = np.nonzero(s0["r"][:, 0] < 0.45 * L)[0]
+    s = dict(s0, id=np.arange(len(keep), dtype=np.int64))
+    for k in ("r", "v", "q", "j", "comp"):
+        s[k] = np.ascontiguousarray(s0[k][keep])
+    n = np.floor(np.asarray(s["box"]) / s["rc"]).astype(int)
+    boxes = [[0, 0, 0, 4, n[1], n[2]], [4, 0, 0, n[0], n[1], n[2]]]
+    run = md.DecomposedRun(s, 2, transport="loopback", boxes=boxes)
+    assert run.owned_counts()[1] == 0
+    compare_run(md, oracle_mod, s, run, 20)
+    assert sum(run.owned_counts()) == len(s["r"])
+
+
 def test_decomposed_mixture_vs_oracle(md, oracle_mod):
     """Two species with every site kind (LJ, charges, dipoles, quadrupoles; reaction field)
     and the binary parameter eta -- the generic force kernel -- on 2 ranks: the
