@@ -91,3 +91,39 @@ def test_tiny_system(md, oracle_mod, name, n):
     ug, cg, ng = ctx.get_raw()
     co, no = o.cells(ug)
     assert np.array_equal(cg, co) and np.array_equal(ng, no)
+
+
+def test_cell_faces_and_box_edges(md, oracle_mod):
+    """Molecules exactly on cell faces (x = k edge), on the periodic boundary written as
+    L instead of 0, and a hair below L: the device ingest and the oracle quantise them to
+    the same fixed-point lattice (reading A12) and bin them into the same cells, and the
+    forces agree.  One molecule per cell corner (spacing = edge >= rc)."""
+    s0 = S.config("c1s")
+    L = s0["box"]
+    n = np.floor(L / s0["rc"]).astype(int)
+    edge = L / n
+    g = np.stack(np.meshgrid(*[np.arange(k) for k in n], indexing="ij"), -1).reshape(-1, 3).astype(float)
+    r = g * edge
+    r[r[:, 1] == 0.0, 0] += 0.3 * edge[0]            # break the cubic symmetry a little
+    sel = (g[:, 0] == 0) & (g[:, 2] == 1)
+    r[sel, 0] = L[0]                                  # x = L: the same point as x = 0
+    sel = (g[:, 1] == 0) & (g[:, 2] == 2)
+    r[sel, 1] = np.nextafter(L[1], 0.0)               # a hair below L
+    m = len(r)
+    rng = np.random.default_rng(7)
+    s = dict(s0, id=np.arange(m, dtype=np.int64), r=r, v=0.2 * rng.normal(size=(m, 3)),
+             q=np.tile([1.0, 0.0, 0.0, 0.0], (m, 1)), j=np.zeros((m, 3)), comp=np.zeros(m, np.int32))
+    ctx = md.from_system(s)
+    F, _ = ctx.get_forces()
+    ctx.compute_forces()
+    obs = ctx.get_observables()
+    ug, cg, ng = ctx.get_raw()
+    o = oracle_mod.System(s)
+    uo = o.quantize(s["r"])
+    co, no = o.cells(uo)
+    assert np.array_equal(ug, uo)
+    assert np.array_equal(cg, co) and np.array_equal(ng, no)
+    Fo, _, tot = o.forces(s["comp"], uo, s["q"], mode="full")
+    assert obs["n_pairs"] == tot["npairs"]
+    assert_forces_close(F, Fo, "force")
+    assert_rel(obs["U_pot"], tot["U"], "U_pot")
