@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
     const int grp = 2 * wib + half, NG = 2 * WARPS;
     uint16_t* hlA = hls + grp * 2 * (HCAP + 2);                            // two lists per group (+ spare slots)
     uint16_t* hlB = hlA + (HCAP + 2);
-    const unsigned gmask = 0xffffu << (16 * half);
+    [[maybe_unused]] const unsigned gmask = 0xffffu << (16 * half);   // the per-step ballots (MD_RIG3_BITS=0)
     const GridP& g = a.g;
     const float krf = a.krf, crf = a.crf, kmm = a.kmm;
     if (tid == 0) {                       // far dummy partner (padding): COM far away, sites at the COM
