@@ -37,6 +37,9 @@ namespace rig3 {
 #ifndef MD_RIG3_WARPS
 #define MD_RIG3_WARPS 8
 #endif
+#ifndef MD_RIG3_SU
+#define MD_RIG3_SU 4       // staging: elements per thread with their loads in flight together
+#endif
 #ifndef MD_RIG3_BITS
 #define MD_RIG3_BITS 1
 #endif
@@ -183,38 +186,51 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                 const int mm = min(CAP, mtot - k0);
                 __syncthreads();
                 // ---- stage elements k0 .. k0 + mm - 1 of the neighbourhood (rows in order)
-                for (int k = tid; k < mm; k += WARPS * 32) {
-                    const int kg = k0 + k;
-                    int r = 0;
+                // SU elements per thread per pass: all their loads are issued before any store,
+                // so a pass waits for one memory latency instead of SU
+                constexpr int SU = MD_RIG3_SU;
+                for (int kb = tid; kb < mm; kb += SU * WARPS * 32) {
+                    float4 xv[SU], sv[SU][NSLOT];
+                    float ox[SU], oy[SU], oz[SU];
 #pragma unroll
-                    for (int q = 1; q < 9; ++q) r += kg >= rinfo[8 * q + 6] ? 1 : 0;
-                    const int* ri = rinfo + 8 * r;
-                    int kk = kg - ri[6];
-                    int src;
-                    float offx;
-                    if (kk < ri[3]) { src = ri[0] + kk; offx = -g.edge[0]; }
-                    else if (kk < ri[3] + ri[4]) { src = ri[1] + kk - ri[3]; offx = 0.f; }
-                    else { src = ri[2] + kk - ri[3] - ri[4]; offx = g.edge[0]; }
-                    const float offy = (float)(r % 3 - 1) * g.edge[1], offz = (float)(r / 3 - 1) * g.edge[2];
-                    const float4 x = __ldg(a.xs + src);
-                    float4 sv[NSLOT];
+                    for (int u = 0; u < SU; ++u) {
+                        const int k = kb + u * WARPS * 32;
+                        const int kg = k0 + min(k, mm - 1);
+                        int r = 0;
 #pragma unroll
-                    for (int s = 0; s < NSLOT; ++s) sv[s] = __ldg(a.site + (size_t)s * a.cap + src);
-                    const int ph = k >> 1, od = k & 1;
-                    cxf[4 * ph + od] = x.x + offx;
-                    cxf[4 * ph + 2 + od] = x.y + offy;
-                    czf[2 * ph + od] = x.z + offz;
-                    if (k == mm - 1 && !od) {                   // odd chunk: far pad element
-                        cxf[4 * ph + 1] = 1.0e4f;
-                        cxf[4 * ph + 3] = 1.0e4f;
-                        czf[2 * ph + 1] = 1.0e4f;
+                        for (int q = 1; q < 9; ++q) r += kg >= rinfo[8 * q + 6] ? 1 : 0;
+                        const int* ri = rinfo + 8 * r;
+                        const int kk = kg - ri[6];
+                        int src;
+                        if (kk < ri[3]) { src = ri[0] + kk; ox[u] = -g.edge[0]; }
+                        else if (kk < ri[3] + ri[4]) { src = ri[1] + kk - ri[3]; ox[u] = 0.f; }
+                        else { src = ri[2] + kk - ri[3] - ri[4]; ox[u] = g.edge[0]; }
+                        oy[u] = (float)(r % 3 - 1) * g.edge[1];
+                        oz[u] = (float)(r / 3 - 1) * g.edge[2];
+                        xv[u] = __ldg(a.xs + src);
+#pragma unroll
+                        for (int s = 0; s < NSLOT; ++s) sv[u][s] = __ldg(a.site + (size_t)s * a.cap + src);
                     }
 #pragma unroll
-                    for (int s = 0; s < NSLOT; ++s) {
-                        sws[(4 * s + 0) * STRIDE + k] = sv[s].x;
-                        sws[(4 * s + 1) * STRIDE + k] = sv[s].y;
-                        sws[(4 * s + 2) * STRIDE + k] = sv[s].z;
-                        sws[(4 * s + 3) * STRIDE + k] = sv[s].w;
+                    for (int u = 0; u < SU; ++u) {
+                        const int k = kb + u * WARPS * 32;
+                        if (k >= mm) break;
+                        const int ph = k >> 1, od = k & 1;
+                        cxf[4 * ph + od] = xv[u].x + ox[u];
+                        cxf[4 * ph + 2 + od] = xv[u].y + oy[u];
+                        czf[2 * ph + od] = xv[u].z + oz[u];
+                        if (k == mm - 1 && !od) {                   // odd chunk: far pad element
+                            cxf[4 * ph + 1] = 1.0e4f;
+                            cxf[4 * ph + 3] = 1.0e4f;
+                            czf[2 * ph + 1] = 1.0e4f;
+                        }
+#pragma unroll
+                        for (int s = 0; s < NSLOT; ++s) {
+                            sws[(4 * s + 0) * STRIDE + k] = sv[u][s].x;
+                            sws[(4 * s + 1) * STRIDE + k] = sv[u][s].y;
+                            sws[(4 * s + 2) * STRIDE + k] = sv[u][s].z;
+                            sws[(4 * s + 3) * STRIDE + k] = sv[u][s].w;
+                        }
                     }
                 }
                 __syncthreads();
