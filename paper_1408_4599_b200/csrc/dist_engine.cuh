@@ -516,6 +516,27 @@ static int dd_set_segments(mardyn_ctx* ctx, const std::vector<int64_t>& sc, cons
 
 // ---- the group's steps
 
+// A rank that fails before a collective and returns would leave its peers waiting in that
+// collective.  Before each collective of the host-synchronous paths (first step, rebalance,
+// observables) the ranks therefore agree on the outcome: a one-word ncclAllReduce(max) of
+// "this rank failed"; every rank then returns an error.  (A poisoned context cannot enqueue
+// anything; its peers stop at their next NCCL call.)
+static int group_agree(Group* G, int rc)
+{
+    if (!G || !G->nccl || G->p < 2) return rc;
+    mardyn_ctx* ctx = G->m[0];
+    if (ctx->poisoned || !ctx->cmat) return rc;
+    int32_t* d = reinterpret_cast<int32_t*>(ctx->cmat + (size_t)G->p * (G->p + 1));
+    int32_t h = rc != MARDYN_OK ? 1 : 0;
+    CK(cudaMemcpyAsync(d, &h, 4, cudaMemcpyHostToDevice, ctx->stream));
+    NCK(mdn::api().AllReduce(d, d, 1, ncclInt32, ncclMax, G->comm, ctx->stream));
+    CK(cudaMemcpyAsync(&h, d, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (rc != MARDYN_OK) return rc;
+    if (h) return fail(ctx, MARDYN_ESTATE, "another rank of the decomposition failed");
+    return MARDYN_OK;
+}
+
 // the record-count matrix C[src][dst] of every rank (allgather over NCCL, or read across the
 // loopback ranks); rows = this process's ranks' counts
 static int gather_counts(Group* G, std::vector<std::vector<int64_t>>& C)
@@ -586,7 +607,7 @@ static int group_sync_step(Group* G)
     for (mardyn_ctx* c : G->m) c->rank_timed = false;
     std::vector<std::vector<int64_t>> C(p, std::vector<int64_t>(p, 0));
     for (mardyn_ctx* c : G->m) {
-        if (int rc = dd_begin_sync(c, C[c->dd_rank].data())) return rc;
+        if (int rc = group_agree(G, dd_begin_sync(c, C[c->dd_rank].data()))) return rc;
         c->send_off.assign(p, 0);
         for (int d = 0; d < p; ++d) c->send_off[d] = (int64_t)d * c->seg_max;   // uniform segments
     }
@@ -594,7 +615,7 @@ static int group_sync_step(Group* G)
     std::vector<int64_t> nrecv;
     if (int rc = exchange_exact(G, C, nrecv)) return rc;
     for (mardyn_ctx* c : G->m)
-        if (int rc = dd_import_sort(c, nrecv[c->dd_rank], true)) return rc;
+        if (int rc = group_agree(G, dd_import_sort(c, nrecv[c->dd_rank], true))) return rc;
     // segment capacities from the global count matrix (the same decision on every rank)
     auto capof = [](int64_t c) { return ((2 * c + 1024 + 255) / 256) * 256; };
     bool fits = true;
@@ -727,7 +748,7 @@ static int group_rebalance(Group* G)
     std::vector<int32_t> counts((size_t)ncell, 0), tmp((size_t)ncell);
     for (mardyn_ctx* c : G->m) {
         mardyn_ctx* ctx = c;
-        if (int rc = refresh_n(c)) return rc;
+        if (int rc = group_agree(G, refresh_n(c))) return rc;
         CK(cudaMemsetAsync(c->gcount, 0, 4 * (size_t)ncell, c->stream));
         k_owned_counts<<<nblk(c->g.wncell, 256), 256, 0, c->stream>>>(c->g, c->start, c->owner, c->dd_rank, c->gcount);
         c->launches += 1;
@@ -896,7 +917,7 @@ static int group_observables(mardyn_ctx* ctx, std::vector<ObsRec>& ring)
     ring.assign(MD_HISTORY, ObsRec{});
     std::vector<ObsRec> h(MD_HISTORY * (size_t)p);
     if (G->nccl) {
-        int rc = sync_check(ctx);
+        int rc = group_agree(G, sync_check(ctx));
         if (rc) return rc;
         NCK(mdn::api().AllGather(ctx->hist, ctx->obs_all, sizeof(ObsRec) * MD_HISTORY, ncclChar, G->comm, ctx->stream));
         CK(cudaMemcpyAsync(h.data(), ctx->obs_all, sizeof(ObsRec) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));

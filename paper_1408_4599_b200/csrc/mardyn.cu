@@ -808,7 +808,7 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         owner = (uint8_t*)take((size_t)ncell);
         gmask = (uint32_t*)take(4 * (size_t)ncell);
         gcount = (int*)take(4 * (size_t)ncell);
-        cmat = (int64_t*)take(8 * (size_t)ctx->nranks * (ctx->nranks + 1));
+        cmat = (int64_t*)take(8 * ((size_t)ctx->nranks * (ctx->nranks + 1) + 2));   // + group_agree's flag
         sendbuf = (DDRec*)take(sizeof(DDRec) * (size_t)seg_cap * ctx->nranks);
         recvbuf = (DDRec*)take(sizeof(DDRec) * (size_t)recv_cap);
         send_cnt = (int*)take(4 * (size_t)ctx->nranks);
