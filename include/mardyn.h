@@ -285,6 +285,10 @@ int mardyn_kd_decompose(const double* cost, int32_t nx, int32_t ny, int32_t nz, 
  * through the communicator.  Errors: MARDYN_ENCCL (NCCL missing or failed;
  * the context is poisoned), MARDYN_ECAPACITY (a rank's owned + halo +
  * received molecules exceed its capacity, or an exchange segment overflows).
+ * Before the collectives of the first step after a load or rebalance, of the
+ * rebalance and of get_observables the ranks agree on failure: when one rank
+ * fails there, it returns its own error and every other rank returns
+ * MARDYN_ESTATE ("another rank of the decomposition failed").
  */
 int mardyn_nccl_unique_id(void* out128);
 int mardyn_create_distributed(const double box[3], double cutoff, const mardyn_component* comps,
