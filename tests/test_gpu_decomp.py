@@ -96,6 +96,16 @@ def test_rebalance_droplet_vs_oracle(md, oracle_mod, cost_model):
     assert not np.array_equal(np.asarray(run.boxes), np.asarray(static))
 
 
+def test_decomposed_fullsize_c1_vs_oracle(md, oracle_mod):
+    """The N > 1 bench workload at full size: c1 (1 048 576 molecules, BASELINE configs[1]) on
+    8 ranks -- k-d boxes, halo exchange and migration every step -- for its full 100-step run
+    against the oracle's one-domain run (F(t0) per molecule, per-step global U, W, T and
+    n_pairs, ids, final positions)."""
+    s = S.config("c1")
+    run = md.DecomposedRun(s, 8, transport="loopback")
+    compare_run(md, oracle_mod, s, run, 100)
+
+
 def test_empty_rank_vs_oracle(md, oracle_mod):
     """A rank that owns no molecule: a liquid slab filling x < 0.45 L next to vacuum, two
     boxes cut at 4 of 7 cells -- rank 1 starts with an empty home box (only halo copies of
