@@ -106,6 +106,16 @@ def test_decomposed_fullsize_c1_vs_oracle(md, oracle_mod):
     compare_run(md, oracle_mod, s, run, 100)
 
 
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_decomposed_fullsize_rigid_vs_oracle(md, oracle_mod, name):
+    """The rigid path of the decomposition at full size: c2 (10^6 2CLJQ molecules) and c3
+    (5 x 10^5 water molecules) on 4 ranks, their first 10 steps against the oracle (the
+    well-conditioned stretch of these runs, tests/test_oracle_sensitivity.py)."""
+    s = S.config(name)
+    run = md.DecomposedRun(s, 4, transport="loopback")
+    compare_run(md, oracle_mod, s, run, 10)
+
+
 def test_empty_rank_vs_oracle(md, oracle_mod):
     """A rank that owns no molecule: a liquid slab filling x < 0.45 L next to vacuum, two
     boxes cut at 4 of 7 cells -- rank 1 starts with an empty home box (only halo copies of
