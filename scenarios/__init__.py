@@ -403,9 +403,14 @@ def droplet(L=30.0, R=8.0, centre=(0.3, 0.55, 0.5), rho_l=0.73, rho_v=0.02, T=0.
     return _system("droplet", box, 2.5, 0.002, steps, T, [lj1_component()], X, V)
 
 
+_CACHE = {}
+
+
 def config(name):
     """Config by name: 'c0'..'c4' at full size, or scaled parity variants
-    'c1s', 'c2s', 'c3s', 'c4s'; 'droplet' (heterogeneous, off-centre)."""
+    'c1s', 'c2s', 'c3s', 'c4s'; 'droplet' (heterogeneous, off-centre).  The full-size
+    c4 (its vapour takes ~1 min of sequential rejection) is generated once per process
+    and handed out as copies."""
     table = {
         "c0": config0,
         "c1": config1, "c1s": lambda: config1(10),
@@ -414,7 +419,11 @@ def config(name):
         "c4": config4, "c4s": lambda: config4(16),
         "droplet": droplet,
     }
-    return table[name]()
+    if name != "c4":
+        return table[name]()
+    if name not in _CACHE:
+        _CACHE[name] = table[name]()
+    return {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in _CACHE[name].items()}
 
 
 # ----------------------------------------------------------------------------

@@ -106,6 +106,14 @@ def test_decomposed_fullsize_c1_vs_oracle(md, oracle_mod):
     compare_run(md, oracle_mod, s, run, 100)
 
 
+def test_decomposed_fullsize_c4_vs_oracle(md, oracle_mod):
+    """The slab at full size: c4 (16.8 M molecules, liquid and vapour, BASELINE configs[4]) on
+    8 ranks for 5 steps against the oracle's one-domain run."""
+    s = S.config("c4")
+    run = md.DecomposedRun(s, 8, transport="loopback")
+    compare_run(md, oracle_mod, s, run, 5)
+
+
 @pytest.mark.parametrize("name", ["c2", "c3"])
 def test_decomposed_fullsize_rigid_vs_oracle(md, oracle_mod, name):
     """The rigid path of the decomposition at full size: c2 (10^6 2CLJQ molecules) and c3
