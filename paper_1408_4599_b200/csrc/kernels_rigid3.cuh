@@ -145,19 +145,24 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
         const int s_i = __ldg(a.start + c);
         const int n_all = __ldg(a.start + c + 1) - s_i;
         if (n_all == 0) continue;
-        // row table: threads 0..26 read the 27 cells' start / count
+        // row table, built by warp 0 alone: lanes 0..26 read the 27 cells' start / count, lanes
+        // 0..8 form the row lengths and their exclusive prefix (rinfo[8 r + 6]) by shuffles
         __syncthreads();                  // previous cell's consumers are done with smem
-        if (tid < 27) {
-            const int r = tid / 3, k = tid % 3;
-            const int dy = r % 3 - 1, dz = r / 3 - 1;
-            const int cc = wrapi(cx + k - 1, g.wn[0]) + g.wn[0] * (wrapi(cy + dy, g.wn[1]) + g.wn[1] * wrapi(cz + dz, g.wn[2]));
-            const int st = __ldg(a.start + cc);
-            rinfo[8 * r + k] = st;
-            rinfo[8 * r + 3 + k] = __ldg(a.start + cc + 1) - st;
-        }
-        __syncthreads();
-        if (tid < 32) {                   // exclusive prefix of the row lengths -> rinfo[8 r + 6]
-            const int len = lane < 9 ? rinfo[8 * lane + 3] + rinfo[8 * lane + 4] + rinfo[8 * lane + 5] : 0;
+        if (tid < 32) {
+            int st = 0, cnt = 0;
+            if (lane < 27) {
+                const int r = lane / 3, k = lane % 3;
+                const int dy = r % 3 - 1, dz = r / 3 - 1;
+                const int cc = wrapi(cx + k - 1, g.wn[0]) + g.wn[0] * (wrapi(cy + dy, g.wn[1]) + g.wn[1] * wrapi(cz + dz, g.wn[2]));
+                st = __ldg(a.start + cc);
+                cnt = __ldg(a.start + cc + 1) - st;
+                rinfo[8 * r + k] = st;
+                rinfo[8 * r + 3 + k] = cnt;
+            }
+            const int r3 = min(3 * lane, 30);
+            const int c0 = __shfl_sync(FULL, cnt, r3), c1 = __shfl_sync(FULL, cnt, r3 + 1),
+                      c2 = __shfl_sync(FULL, cnt, r3 + 2);
+            const int len = lane < 9 ? c0 + c1 + c2 : 0;
             int incl = len;
 #pragma unroll
             for (int o = 1; o < 16; o <<= 1) {
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
             const int nrounds = npr + (rem > 0 ? 1 : 0);
             for (int k0 = 0; k0 < mtot; k0 += CAP) {
                 const int mm = min(CAP, mtot - k0);
-                __syncthreads();
+                if (k0 > 0) __syncthreads();      // the previous chunk's rounds are done with it
                 // ---- stage elements k0 .. k0 + mm - 1 of the neighbourhood (rows in order)
                 // SU elements per thread per pass: all their loads are issued before any store,
                 // so a pass waits for one memory latency instead of SU
