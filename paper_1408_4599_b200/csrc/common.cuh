@@ -13,6 +13,16 @@
 //   site  float4 [n_slots][cap]              world-frame site offsets / axes
 //   force float4 (F, 0), torque float4 (tau, 0)
 #pragma once
+
+// debug builds (-DMD_DEBUG_CHECKS, profiles/tools/debug_checks.sh): device-side bounds checks of the
+// shared-memory lists and slabs and of the sorted-slot indices; a failed check aborts the kernel
+// (cudaErrorAssert -> MARDYN_ECUDA).  compute-sanitizer is not available on the GPU pool.
+#ifdef MD_DEBUG_CHECKS
+#include <cassert>
+#define MD_CHECK(c) assert(c)
+#else
+#define MD_CHECK(c) ((void)0)
+#endif
 #include <cstdint>
 #include <cuda_runtime.h>
 

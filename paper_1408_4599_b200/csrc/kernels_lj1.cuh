@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                                     Y[h] = real ? w.y + offy : FAR;
                                     Z[h] = real ? w.z + offz : FAR;
                                 }
+                                MD_CHECK(base + q < CAPP);
                                 sxy[base + q] = make_float4(X[0], X[1], Y[0], Y[1]);
                                 sz[base + q] = make_float2(Z[0], Z[1]);
                             }
@@ -519,12 +520,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
                     if (r == 4 && act && own_lane) {
                         if (pself > pa) {
                             const int qa = pa - ((pself - pa) & 1);
+                            MD_CHECK(nseg < NSEG - 1);
                             sseg[32 * nseg + lane] = seg_make(qa, pself); ++nseg; ttot += pself - qa;
                         }
                         pa = pself + 1;
                     }
                     if (pb > pa) {
                         const int qb = pb + ((pb - pa) & 1);
+                        MD_CHECK(nseg < NSEG - 1 && qb <= total);
                         sseg[32 * nseg + lane] = seg_make(pa, qb); ++nseg; ttot += qb - pa;
                     }
                 }

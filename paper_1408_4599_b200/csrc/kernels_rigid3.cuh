@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                         const int k = kb + u * WARPS * 32;
                         if (k >= mm) break;
                         const int ph = k >> 1, od = k & 1;
+                        MD_CHECK(k < CAP);
                         cxf[4 * ph + od] = xv[u].x + ox[u];
                         cxf[4 * ph + 2 + od] = xv[u].y + oy[u];
                         czf[2 * ph + od] = xv[u].z + oz[u];
@@ -509,11 +510,13 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                         while (bA) {
                             const int k = __ffs(bA) - 1;
                             bA &= bA - 1u;
+                            MD_CHECK(oA < HCAP + 2 && e0 + 16 * k - 15 * (k & 1) < CAP);
                             hlA[oA++] = (uint16_t)(e0 + 16 * k - 15 * (k & 1));
                         }
                         while (bB) {
                             const int k = __ffs(bB) - 1;
                             bB &= bB - 1u;
+                            MD_CHECK(oB < HCAP + 2 && e0 + 16 * k - 15 * (k & 1) < CAP);
                             hlB[oB++] = (uint16_t)(e0 + 16 * k - 15 * (k & 1));
                         }
                         cntA += totA;

@@ -271,6 +271,7 @@ __device__ __forceinline__ void canon_one(int t, int cap, const GridP& g, const 
     int r = 0;
     for (int m = s0; m < s1; ++m) r += keys[m] < key;
     int dst = s0 + r;
+    MD_CHECK(dst >= 0 && dst < cap && old >= 0 && old < cap && r < s1 - s0);
     uint4 p = pos_s[old];
     float4 v = vel_s[old];
     pos_d[dst] = p;
