@@ -23,6 +23,7 @@ in the body frame relative to the centre of mass.
 """
 from __future__ import annotations
 
+import copy
 import math
 
 import numpy as np
@@ -423,7 +424,7 @@ def config(name):
         return table[name]()
     if name not in _CACHE:
         _CACHE[name] = table[name]()
-    return {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in _CACHE[name].items()}
+    return copy.deepcopy(_CACHE[name])
 
 
 # ----------------------------------------------------------------------------
