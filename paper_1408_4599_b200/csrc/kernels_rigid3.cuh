@@ -58,28 +58,51 @@ using pk2::dot;
 
 // charge-charge with reaction field (A4) without the constant c_rf, which the caller
 // subtracts per partner as c_rf (sum_a q_a)(sum_b q_b) -- zero for neutral molecules
-__device__ __forceinline__ void qq_nocrf(V3 r, P2 qq, float krf, P2& u, V3& fa, V3& fh)
+// SV (site virial, molecules without charges): the site force -fr r is accumulated with one
+// FFMA2 per component from nfr = -fr (the _rn packed intrinsics are never contracted, so
+// fa - fr * r is an FMUL2 and an FADD2), and there is no partner-pair force fh; the virial is
+// summed per site pair as -r_ab . f_ab = fr r^2 and corrected per home molecule by
+// -2 sum_a s_a . F_a at the flush (see the flush below: over the full shell the two
+// give the same total as -sum_j d_j . F_ij, reading A6)
+template <bool SV>
+__device__ __forceinline__ void qq_nocrf(V3 r, P2 qq, float krf, P2& u, V3& fa, V3& fh, P2& w)
 {
     const P2 r2 = dot(r, r);
     const P2 ir = pk2::rsqrt2(r2);
     const P2 ir2 = ir * ir;
     u = fma(qq, fma(p2(krf), r2, ir), u);
-    const P2 fr = qq * fma(ir, ir2, p2(-2.f * krf));
-    fa.x = fa.x - fr * r.x; fa.y = fa.y - fr * r.y; fa.z = fa.z - fr * r.z;
-    fh.x = fh.x - fr * r.x; fh.y = fh.y - fr * r.y; fh.z = fh.z - fr * r.z;
+    if (SV) {
+        const P2 nfr = pk2::neg(qq) * fma(ir, ir2, p2(-2.f * krf));
+        fa.x = fma(nfr, r.x, fa.x); fa.y = fma(nfr, r.y, fa.y); fa.z = fma(nfr, r.z, fa.z);
+        w = fma(pk2::neg(nfr), r2, w);
+    } else {
+        // with charges the molecular force and virial are small differences of the site terms
+        // (neutral molecules): the product is rounded once and subtracted from both sums, the
+        // rounding the parity tolerances were established with
+        const P2 fr = qq * fma(ir, ir2, p2(-2.f * krf));
+        fa.x = fa.x - fr * r.x; fa.y = fa.y - fr * r.y; fa.z = fa.z - fr * r.z;
+        fh.x = fh.x - fr * r.x; fh.y = fh.y - fr * r.y; fh.z = fh.z - fr * r.z;
+    }
 }
 
 // LJ 12-6 of a site pair without the LJTS shift (added per partner by the caller), r = x_b - x_a
-__device__ __forceinline__ void lj_noshift(V3 r, float sig2, float eps24, float eps4, P2& u, V3& fa, V3& fh)
+template <bool SV>
+__device__ __forceinline__ void lj_noshift(V3 r, float sig2, float eps24, float eps4, P2& u, V3& fa, V3& fh, P2& w)
 {
     const P2 r2 = dot(r, r);
     const P2 ir2 = pk2::rcp2(r2);
     const P2 s2 = sig2 * ir2;
     const P2 s6 = s2 * s2 * s2;
-    const P2 fr = (eps24 * ir2) * s6 * fma(p2(2.f), s6, p2(-1.f));
     u = fma(eps4 * s6, s6 - p2(1.f), u);
-    fa.x = fa.x - fr * r.x; fa.y = fa.y - fr * r.y; fa.z = fa.z - fr * r.z;
-    fh.x = fh.x - fr * r.x; fh.y = fh.y - fr * r.y; fh.z = fh.z - fr * r.z;
+    if (SV) {
+        const P2 nfr = (-eps24 * ir2) * s6 * fma(p2(2.f), s6, p2(-1.f));
+        fa.x = fma(nfr, r.x, fa.x); fa.y = fma(nfr, r.y, fa.y); fa.z = fma(nfr, r.z, fa.z);
+        w = fma(pk2::neg(nfr), r2, w);
+    } else {
+        const P2 fr = (eps24 * ir2) * s6 * fma(p2(2.f), s6, p2(-1.f));
+        fa.x = fa.x - fr * r.x; fa.y = fa.y - fr * r.y; fa.z = fa.z - fr * r.z;
+        fh.x = fh.x - fr * r.x; fh.y = fh.y - fr * r.y; fh.z = fh.z - fr * r.z;
+    }
 }
 
 template <int NLJ, int NQ, int NMU, int NQQ>
@@ -96,6 +119,12 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
 {
     using SH = Shape<NLJ, NQ, NMU, NQQ>;
     constexpr int NSLOT = SH::NSLOT;
+    // site-pair virial (no charges: the site terms of point charges cancel strongly within a
+    // neutral molecule, and fp32 sums of them lose the molecular virial's digits)
+#ifndef MD_RIG3_SV
+#define MD_RIG3_SV 1       // 0: never, 1: molecules without charges, 2: always
+#endif
+    constexpr bool SV = MD_RIG3_SV == 2 || (MD_RIG3_SV == 1 && NQ == 0);
     constexpr int NPOL = (NMU + NQQ) > 0 ? (NMU + NQQ) : 1;
     constexpr int STRIDE = CAP + 1;
     constexpr int DUMMY = CAP;                                 // far dummy element (pair CAP / 2)
@@ -347,7 +376,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                                     const V3 sb = slot3(ibb, j0, j1);
                                     const V3 rv = V3{da.x + sb.x, da.y + sb.y, da.z + sb.z};
                                     const float4 pp = ljp[2 * ia + ibb];
-                                    lj_noshift(rv, pp.x, pp.y, pp.z, uacc, fs[ia], fh);
+                                    lj_noshift<SV>(rv, pp.x, pp.y, pp.z, uacc, fs[ia], fh, wacc);
                                 }
                             }
 #pragma unroll
@@ -359,7 +388,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                                 for (int ibb = 0; ibb < NQ; ++ibb) {
                                     const V3 sb = slot3(SH::SQ + ibb, j0, j1);
                                     const V3 rv = V3{da.x + sb.x, da.y + sb.y, da.z + sb.z};
-                                    qq_nocrf(rv, sa4.w * slotw(SH::SQ + ibb, j0, j1), krf, uacc, fs[NLJ + ia], fh);
+                                    qq_nocrf<SV>(rv, sa4.w * slotw(SH::SQ + ibb, j0, j1), krf, uacc, fs[NLJ + ia], fh, wacc);
                                 }
                             }
 #define RIG3_POLAR(KA, KB, NA, NB, SLA, SLB, FIDX, TIDX, STA, STB)                                          \
@@ -375,8 +404,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
             const V3 eb = (STB == 2) ? slot3((slb + 1) % NSLOT, j0, j1) : v3zero();                        \
             const V3 rv = V3{d.x + pb.x - pa.x, d.y + pb.y - pa.y, d.z + pb.z - pa.z};                     \
             V3 tdummy = v3zero();                                                                          \
-            pk2::polar2<KA, KB>(rv, ea, eb, pa4.w * slotw(slb, j0, j1), kmm, uacc, fs[FIDX + ia],         \
-                                 (TIDX) >= 0 ? ts[((TIDX) >= 0 ? (TIDX) : 0) + ia] : tdummy, fh);        \
+            pk2::polar2<KA, KB, SV>(rv, ea, eb, pa4.w * slotw(slb, j0, j1), kmm, uacc, fs[FIDX + ia],     \
+                                 (TIDX) >= 0 ? ts[((TIDX) >= 0 ? (TIDX) : 0) + ia] : tdummy, fh, wacc);  \
         }                                                                                                  \
     }
                             if (NQ > 0 && NMU > 0) {
@@ -398,10 +427,11 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                                 RIG3_POLAR(MD_QUAD, MD_QUAD, NQQ, NQQ, SH::SQQ, SH::SQQ, NLJ + NQ + NMU, NMU, 2, 2)
                             }
 #undef RIG3_POLAR
-                            wacc -= dot(d, fh);      // molecular virial (A6): -r_ij . F_ij
+                            if (!SV) wacc -= dot(d, fh);      // molecular virial (A6): -r_ij . F_ij
                         }
                         // ---- molecule force and torque of this lane's share, group reduction
                         float F[3] = {0.f, 0.f, 0.f}, T[3] = {0.f, 0.f, 0.f};
+                        float sdf = 0.f;                       // SV: sum_a s_a . (this lane's F_a)
 #pragma unroll
                         for (int k = 0; k < SH::NS; ++k) {
                             int slot;
@@ -413,6 +443,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                             const float fx = fs[k].x.v.x + fs[k].x.v.y, fy = fs[k].y.v.x + fs[k].y.v.y,
                                         fz = fs[k].z.v.x + fs[k].z.v.y;
                             F[0] += fx; F[1] += fy; F[2] += fz;
+                            if (SV) sdf += sp.x * fx + sp.y * fy + sp.z * fz;
                             T[0] += sp.y * fz - sp.z * fy;
                             T[1] += sp.z * fx - sp.x * fz;
                             T[2] += sp.x * fy - sp.y * fx;
@@ -439,7 +470,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
 #pragma unroll
                         for (int k = 0; k < NQ; ++k) qtot += si[SH::SQ + k].w;
                         Uw += (double)uacc.v.x + (double)uacc.v.y - ((double)shsum + (double)crf * qtot * qtot) * nval;
-                        Ww += (double)wacc.v.x + (double)wacc.v.y;
+                        Ww += (double)wacc.v.x + (double)wacc.v.y - (SV ? 2.0 * (double)sdf : 0.0);
                         npw += gl == 0 ? cnt : 0;
                         if (gact && gl == 0) {
                             tgt[0] += F[0]; tgt[1] += F[1]; tgt[2] += F[2];

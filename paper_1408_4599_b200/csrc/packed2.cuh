@@ -20,6 +20,7 @@ __device__ __forceinline__ P2 operator-(P2 a, P2 b) { return P2{__fadd2_rn(a.v, 
 __device__ __forceinline__ P2 operator*(P2 a, P2 b) { return P2{__fmul2_rn(a.v, b.v)}; }
 __device__ __forceinline__ P2 operator*(float a, P2 b) { return P2{__fmul2_rn(make_float2(a, a), b.v)}; }
 __device__ __forceinline__ P2 fma(P2 a, P2 b, P2 c) { return P2{__ffma2_rn(a.v, b.v, c.v)}; }
+__device__ __forceinline__ P2 neg(P2 a) { return P2{make_float2(-a.v.x, -a.v.y)}; }   // folded into the operand
 __device__ __forceinline__ P2& operator+=(P2& a, P2 b) { a = a + b; return a; }
 __device__ __forceinline__ P2& operator-=(P2& a, P2 b) { a = a - b; return a; }
 
@@ -78,8 +79,10 @@ __device__ __forceinline__ void qq2(V3 r, P2 qq, float krf, float crf, P2& u, V3
 
 // point multipoles (A5), same closed forms and gradient recipe as
 // sitepair.cuh:pair_polar; p = m_a m_b (masked)
-template <int KA, int KB>
-__device__ __forceinline__ void polar2(V3 r, V3 ea, V3 eb, P2 p, float kmm, P2& u, V3& fa, V3& ta, V3& fh)
+// SV: no partner-pair force fh; the site virial -r . f_a = -|r| u_r is summed into w instead
+// (r . du = |r| u_r exactly: the angular terms are orthogonal to r after the k0 correction)
+template <int KA, int KB, bool SV = false>
+__device__ __forceinline__ void polar2(V3 r, V3 ea, V3 eb, P2 p, float kmm, P2& u, V3& fa, V3& ta, V3& fh, P2& w)
 {
     const P2 r2 = dot(r, r);
     const P2 ir = rsqrt2(r2);
@@ -140,7 +143,11 @@ __device__ __forceinline__ void polar2(V3 r, V3 ea, V3 eb, P2 p, float kmm, P2& 
         du.x = fma(c, eb.x, du.x); du.y = fma(c, eb.y, du.y); du.z = fma(c, eb.z, du.z);
     }
     fa.x += du.x; fa.y += du.y; fa.z += du.z;
-    fh.x += du.x; fh.y += du.y; fh.z += du.z;
+    if (SV) {
+        w = fma(neg(r2 * ir), ur, w);
+    } else {
+        fh.x += du.x; fh.y += du.y; fh.z += du.z;
+    }
     if (KA != MD_CHARGE) {
         V3 gv = V3{uca * rh.x, uca * rh.y, uca * rh.z};
         if (KB != MD_CHARGE) { gv.x = fma(ucab, eb.x, gv.x); gv.y = fma(ucab, eb.y, gv.y); gv.z = fma(ucab, eb.z, gv.z); }
