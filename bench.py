@@ -270,7 +270,7 @@ def measure_e2e(args, system, ctx, run, world, dist, flush):
             e_ms.append(dt * 1e3)
     ms = float(np.mean(e_ms))
     if dist:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([ms], device="cpu" if dist.get_backend() == "gloo" else "cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     h2d = N * (3 * 8 + 3 * 8 + 4 + 8 + (7 * 8 if rigid else 0))
@@ -292,6 +292,12 @@ def main():
         return run_reference(args, system, rank, world)
 
     import torch
+    # MARDYN_BENCH_ONE_DEVICE=1 (tests only, never the driver): every rank on cuda:0 with a
+    # gloo process group, the library's transport through MARDYN_NCCL_LIB (the one-GPU NCCL
+    # stand-in of tests/nccl_shim.c) -- exercises this N > 1 path on a one-GPU box
+    one_dev = os.environ.get("MARDYN_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -299,7 +305,10 @@ def main():
         # the halo exchange, migration, rebalance and observable reductions run on the
         # library's own communicator (include/mardyn.h)
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1408_4599_b200 import build as b
     from paper_1408_4599_b200 import mardyn
     if rank == 0 or world == 1:
@@ -352,7 +361,7 @@ def main():
     obs = run.observables() if run is not None else ctx.get_observables()
     tot_ms = float(sum(step_ms))
     if dist:
-        t = torch.tensor([tot_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([tot_ms], device="cpu" if dist.get_backend() == "gloo" else "cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
         dist.barrier()

@@ -263,7 +263,10 @@ int mardyn_kd_decompose(const double* cost, int32_t nx, int32_t ny, int32_t nz, 
  *
  * The library owns the NCCL communicator (NCCL is loaded at run time,
  * dlopen("libnccl.so.2"): the copy a host process already loaded, else the
- * system one).  Each step: forces on the rank's home box (its k-d box; the
+ * system one; the environment variable MARDYN_NCCL_LIB names another library
+ * with NCCL's entry points instead -- the tests run several ranks on one GPU
+ * through a host-staged stand-in, tests/nccl_shim.c, since NCCL refuses two
+ * ranks of a communicator on one device).  Each step: forces on the rank's home box (its k-d box; the
  * halo holds copies of every molecule within one cell layer of edge >= rc,
  * P:220-221), kick / drift / rotation of the owned molecules, then every
  * molecule whose new cell lies in another rank's box (migrant) or halo

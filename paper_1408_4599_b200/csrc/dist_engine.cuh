@@ -42,6 +42,18 @@ static void group_drop_graphs(Group* G)
 }
 
 static bool group_is_nccl(const Group* g) { return g && g->nccl; }
+
+// timing events of the decomposed step: recorded as external event nodes when the step is
+// being captured into a graph (loopback, MARDYN_NCCL_GRAPHS=1), as plain records when it is
+// enqueued eagerly (the NCCL step): cudaEventRecordExternal outside a capture is an error
+static cudaError_t ev_record(cudaEvent_t e, cudaStream_t s)
+{
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    const cudaError_t q = cudaStreamIsCapturing(s, &cs);
+    if (q != cudaSuccess) return q;
+    return cudaEventRecordWithFlags(e, s, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal
+                                                                             : cudaEventRecordDefault);
+}
 static std::vector<mardyn_ctx*> group_members(mardyn_ctx* ctx)
 {
     std::vector<mardyn_ctx*> out;
@@ -420,9 +432,9 @@ static int dd_begin_async(mardyn_ctx* ctx)
         dd.n_force = ctx->n_aux + 1;
         dd.put_cnt = ctx->direct ? ctx->put_cnt : nullptr;
         dd.done = ctx->n_aux + 3;
-        CK(cudaEventRecordWithFlags(ctx->ev_f0[b], s, cudaEventRecordExternal));
+        CK(ev_record(ctx->ev_f0[b], s));
         launch_force(ctx, b, true, true, &dd);
-        CK(cudaEventRecordWithFlags(ctx->ev_f1[b], s, cudaEventRecordExternal));
+        CK(ev_record(ctx->ev_f1[b], s));
         // the step's observables on a side stream, concurrent with the exchange and the rebuild
         CK(cudaEventRecord(ctx->ev_s0, s));
         CK(cudaStreamWaitEvent(ctx->side_stream, ctx->ev_s0, 0));
@@ -437,9 +449,9 @@ static int dd_begin_async(mardyn_ctx* ctx)
         return MARDYN_OK;
     }
     CK(cudaMemcpyAsync(ctx->n_aux + 1, ctx->start + ctx->g.wncell, 4, cudaMemcpyDeviceToDevice, s));
-    CK(cudaEventRecordWithFlags(ctx->ev_f0[b], s, cudaEventRecordExternal));
+    CK(ev_record(ctx->ev_f0[b], s));
     launch_force(ctx, b, false, true);
-    CK(cudaEventRecordWithFlags(ctx->ev_f1[b], s, cudaEventRecordExternal));
+    CK(ev_record(ctx->ev_f1[b], s));
     CK(cudaMemsetAsync(ctx->count, 0, sizeof(int) * ctx->ncell_pad, s));
     const int nkb = ctx->nkblocks;
     if (ctx->rigid)
@@ -666,9 +678,9 @@ static int group_async_enqueue(Group* G)
 {
     for (mardyn_ctx* c : G->m) {
         mardyn_ctx* ctx = c;
-        if (c->profiling) CK(cudaEventRecordWithFlags(c->ev_r[0], c->stream, cudaEventRecordExternal));
+        if (c->profiling) CK(ev_record(c->ev_r[0], c->stream));
         if (int rc = dd_begin_async(c)) return rc;
-        if (c->profiling) CK(cudaEventRecordWithFlags(c->ev_r[1], c->stream, cudaEventRecordExternal));
+        if (c->profiling) CK(ev_record(c->ev_r[1], c->stream));
     }
     if (G->nccl) {
         mardyn_ctx* ctx = G->m[0];
@@ -686,9 +698,9 @@ static int group_async_enqueue(Group* G)
     }
     for (mardyn_ctx* c : G->m) {
         mardyn_ctx* ctx = c;
-        if (c->profiling) CK(cudaEventRecordWithFlags(c->ev_r[2], c->stream, cudaEventRecordExternal));
+        if (c->profiling) CK(ev_record(c->ev_r[2], c->stream));
         if (int rc = dd_end_async(c)) return rc;
-        if (c->profiling) CK(cudaEventRecordWithFlags(c->ev_r[3], c->stream, cudaEventRecordExternal));
+        if (c->profiling) CK(ev_record(c->ev_r[3], c->stream));
         c->rank_timed = c->profiling;
     }
     return MARDYN_OK;

@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -35,7 +36,16 @@ inline Api& api()
     static Api a;
     static std::once_flag once;
     std::call_once(once, [] {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        // MARDYN_NCCL_LIB: another library with NCCL's entry points (the tests load a
+        // host-staged stand-in, tests/nccl_shim.c, to run several ranks on one GPU, which
+        // NCCL itself refuses); its own symbols are taken, not a loaded NCCL's
+        const char* alt = std::getenv("MARDYN_NCCL_LIB");
+        void* h = (alt && alt[0]) ? dlopen(alt, RTLD_NOW | RTLD_LOCAL | RTLD_DEEPBIND) : nullptr;
+        if (alt && alt[0] && !h) {
+            a.err = std::string("cannot load MARDYN_NCCL_LIB: ") + dlerror();
+            return;
+        }
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
         if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
         if (!h) {
             a.err = std::string("cannot load libnccl.so.2: ") + dlerror();
