@@ -271,9 +271,13 @@ int mardyn_kd_decompose(const double* cost, int32_t nx, int32_t ny, int32_t nz, 
  * P:220-221), kick / drift / rotation of the owned molecules, then every
  * molecule whose new cell lies in another rank's box (migrant) or halo
  * (halo copy) is packed as a 64-byte record (position, v, q, j) by the same
- * kernel, the records move by NCCL send / recv over NVLink (fixed per-peer
- * segments with device-side counts: no host synchronisation after the first
- * step), and the receiver imports them and rebuilds its cells.  Every
+ * kernel and stored straight into the receiving rank's memory (CUDA IPC
+ * mappings of the peers' receive areas, opened after the first step; one
+ * one-word ncclAllReduce per step orders the stores before the imports), or,
+ * when a rank cannot export or open them or MARDYN_IPC_PUTS=0, moved by NCCL
+ * send / recv (fixed per-peer segments with device-side counts); no host
+ * synchronisation after the first step.  The receiver imports them and
+ * rebuilds its cells.  Every
  * rebalance_interval steps the measured per-cell loads of the last cell
  * rebuild are summed over the ranks (ncclAllReduce), the Eq. 6 cost and the
  * k-d tree are recomputed on every rank (identical host code), and the

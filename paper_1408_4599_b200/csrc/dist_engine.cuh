@@ -22,6 +22,7 @@ struct Group {
     cudaStream_t stream = nullptr;       // loopback: the one stream every rank enqueues on
     bool own_stream = false;
     std::vector<const ObsRec*> hist_tab; // loopback NVT: the ranks' observable rings (host staging)
+    std::vector<std::pair<std::string, void*>> ipc_open;   // NCCL: peers' receive allocations opened (CUDA IPC)
     // the steady-state step of every local rank (begin halves, exchange, end halves) captured as
     // one CUDA graph per buffer parity; rebuilt when the segment layout, the partition, the
     // molecules or the profiling switch change
@@ -80,6 +81,7 @@ static void group_release(mardyn_ctx* ctx)
     for (auto& c : G->m)                  // the remaining ranks see a destroyed rank (group_ok)
         if (c == ctx) c = nullptr;
     if (--G->live > 0) return;
+    for (auto& kv : G->ipc_open) cudaIpcCloseMemHandle(kv.second);
     if (G->comm) mdn::api().CommDestroy(G->comm);
     if (G->own_stream && G->stream) cudaStreamDestroy(G->stream);
     delete G;
@@ -608,6 +610,128 @@ static int exchange_exact(Group* G, const std::vector<std::vector<int64_t>>& C, 
     return MARDYN_OK;
 }
 
+// NCCL groups: this step's receive area, count array and put tables (parity = cur: every rank
+// flips cur once per step, so the ranks agree on it)
+static void nccl_parity(Group* G)
+{
+    if (!G || !G->nccl || G->p < 2) return;
+    for (mardyn_ctx* c : G->m) {
+        const int b = c->cur & 1;
+        c->recvbuf = c->recv_area[b];
+        c->recv_cnt = c->rcnt_area[b];
+        c->put_rec = c->put_rec_area[b];
+        c->put_cnt = c->put_cnt_area[b];
+    }
+}
+
+static bool ipc_puts_enabled()
+{
+    static const bool on = [] { const char* e = std::getenv("MARDYN_IPC_PUTS"); return !(e && e[0] == '0'); }();
+    return on;
+}
+
+// Direct puts across processes (GPUs): every rank exports the allocation holding its two
+// receive areas as a CUDA IPC handle, the handles, offsets and receive-segment layouts are
+// all-gathered over the communicator, and every rank opens its peers' allocations (over
+// NVLink peer mappings on a multi-GPU node).  The packing kernels then store each record
+// straight into its receiver's area of this step's parity, and the count of records into the
+// receiver's count array, while the force + leapfrog kernel produces them -- the transfer
+// overlaps the computation -- and one stream-ordered one-word all-reduce per step orders
+// every rank's stores before every rank's import.  Two areas per rank: a peer that has
+// passed step k's all-reduce stores step k + 1's records into the other area while this rank
+// still imports step k's.  Taken only when every rank could export and open (agreed by an
+// all-reduce); otherwise, or with MARDYN_IPC_PUTS=0, the records move by grouped send / recv.
+static int nccl_ipc_setup(Group* G)
+{
+    mardyn_ctx* ctx = G->m[0];
+    const int p = G->p, me = ctx->dd_rank;
+    ctx->direct = false;
+    if (!G->nccl || p < 2 || !ipc_puts_enabled() || !ctx->ipc_blob || !ctx->ipc_word) return MARDYN_OK;
+    cudaStream_t s = ctx->stream;
+    const size_t B = ipc_blob_bytes(p);
+    std::vector<char> mine(B, 0), all(B * (size_t)p);
+    typedef int (*AddrRange)(unsigned long long*, size_t*, unsigned long long);
+    static const AddrRange range = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            f = nullptr;
+        }
+        return reinterpret_cast<AddrRange>(f);
+    }();
+    unsigned long long base = 0;
+    size_t asize = 0;
+    int64_t ok = 0;
+    cudaIpcMemHandle_t h;
+    if (range && range(&base, &asize, (unsigned long long)(uintptr_t)ctx->recv_area[0]) == 0 &&
+        cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base) == cudaSuccess) {
+        ok = 1;
+        std::memcpy(mine.data(), &h, 64);
+    } else {
+        cudaGetLastError();
+    }
+    int64_t* w = reinterpret_cast<int64_t*>(mine.data() + 64);
+    w[0] = ok;
+    w[1] = (int64_t)((uintptr_t)ctx->recv_area[0] - base);
+    w[2] = (int64_t)((uintptr_t)ctx->recv_area[1] - base);
+    w[3] = (int64_t)((uintptr_t)ctx->rcnt_area[0] - base);
+    w[4] = (int64_t)((uintptr_t)ctx->rcnt_area[1] - base);
+    for (int r = 0; r < p; ++r) w[5 + r] = ctx->recv_off[r];
+    char* slot = ctx->ipc_blob + (size_t)me * B;
+    CK(cudaMemcpyAsync(slot, mine.data(), B, cudaMemcpyHostToDevice, s));
+    NCK(mdn::api().AllGather(slot, ctx->ipc_blob, B, ncclChar, G->comm, s));
+    CK(cudaMemcpyAsync(all.data(), ctx->ipc_blob, B * (size_t)p, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<uint64_t> tab(4 * (size_t)p);          // [q][dst] record base, [q][dst] count word
+    int32_t good = 1;
+    for (int d = 0; d < p && good; ++d) {
+        const char* e = all.data() + (size_t)d * B;
+        const int64_t* v = reinterpret_cast<const int64_t*>(e + 64);
+        if (!v[0]) { good = 0; break; }
+        char* pb = nullptr;
+        if (d == me) {
+            pb = (char*)(uintptr_t)base;
+        } else {
+            const std::string key(e, 64);
+            for (auto& kv : G->ipc_open)
+                if (kv.first == key) pb = (char*)kv.second;
+            if (!pb) {
+                cudaIpcMemHandle_t hd;
+                std::memcpy(&hd, e, 64);
+                void* ptr = nullptr;
+                if (cudaIpcOpenMemHandle(&ptr, hd, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    cudaGetLastError();
+                    good = 0;
+                    break;
+                }
+                G->ipc_open.emplace_back(key, ptr);
+                pb = (char*)ptr;
+            }
+        }
+        for (int q = 0; q < 2; ++q) {
+            tab[(size_t)q * 2 * p + d] = (uint64_t)(uintptr_t)(pb + v[1 + q]) + sizeof(DDRec) * (uint64_t)v[5 + me];
+            tab[(size_t)q * 2 * p + p + d] = (uint64_t)(uintptr_t)(pb + v[3 + q]) + 4 * (uint64_t)me;
+        }
+    }
+    // every rank takes the direct path, or none does
+    CK(cudaMemcpyAsync(ctx->ipc_word, &good, 4, cudaMemcpyHostToDevice, s));
+    NCK(mdn::api().AllReduce(ctx->ipc_word, ctx->ipc_word, 1, ncclInt32, ncclMin, G->comm, s));
+    CK(cudaMemcpyAsync(&good, ctx->ipc_word, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!good) return MARDYN_OK;
+    for (int q = 0; q < 2; ++q) {
+        CK(cudaMemcpyAsync(ctx->put_rec_area[q], tab.data() + (size_t)q * 2 * p, 8 * (size_t)p,
+                           cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->put_cnt_area[q], tab.data() + (size_t)q * 2 * p + p, 8 * (size_t)p,
+                           cudaMemcpyHostToDevice, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    ctx->direct = true;
+    return MARDYN_OK;
+}
+
 // first step after a load or a rebalance: record counts to the host, exact exchange, then the
 // per-peer segments of the asynchronous steps (twice the count + 1024 records: face
 // neighbours send far more than edge or corner ones); loopback ranks get direct puts
@@ -616,6 +740,7 @@ static int group_sync_step(Group* G)
     NvtxRange nvtx_range("dd_sync_step");
     const int p = G->p;
     group_drop_graphs(G);                 // the segment layout is about to change
+    nccl_parity(G);
     for (mardyn_ctx* c : G->m) c->rank_timed = false;
     std::vector<std::vector<int64_t>> C(p, std::vector<int64_t>(p, 0));
     for (mardyn_ctx* c : G->m) {
@@ -667,6 +792,8 @@ static int group_sync_step(Group* G)
             CK(cudaStreamSynchronize(src->stream));
             src->direct = true;
         }
+    } else if (int rc = nccl_ipc_setup(G)) {
+        return rc;
     }
     return MARDYN_OK;
 }
@@ -676,6 +803,7 @@ static int group_sync_step(Group* G)
 // Enqueued once per buffer parity under stream capture and replayed as a CUDA graph.
 static int group_async_enqueue(Group* G)
 {
+    nccl_parity(G);
     for (mardyn_ctx* c : G->m) {
         mardyn_ctx* ctx = c;
         if (c->profiling) CK(ev_record(c->ev_r[0], c->stream));
@@ -686,6 +814,12 @@ static int group_async_enqueue(Group* G)
         mardyn_ctx* ctx = G->m[0];
         const int p = G->p, me = ctx->dd_rank;
         const size_t RB = sizeof(DDRec);
+        if (ctx->direct) {
+            // records and counts are already in the receivers' areas (IPC puts): this one-word
+            // all-reduce, stream-ordered after every rank's packing kernels, orders them
+            // before every rank's import
+            NCK(mdn::api().AllReduce(ctx->ipc_word, ctx->ipc_word, 1, ncclInt32, ncclSum, G->comm, ctx->stream));
+        } else {
         NCK(mdn::api().GroupStart());
         for (int d = 0; d < p; ++d) {
             if (d == me) continue;
@@ -695,6 +829,7 @@ static int group_async_enqueue(Group* G)
             NCK(mdn::api().Recv(ctx->recv_cnt + d, 1, ncclInt32, d, G->comm, ctx->stream));
         }
         NCK(mdn::api().GroupEnd());
+        }
     }
     for (mardyn_ctx* c : G->m) {
         mardyn_ctx* ctx = c;
@@ -755,6 +890,7 @@ static int group_rebalance(Group* G)
     NvtxRange nvtx_range("dd_rebalance");
     const int p = G->p;
     group_drop_graphs(G);
+    nccl_parity(G);
     mardyn_ctx* c0 = G->m[0];
     const int ncell = c0->g.ncell;
     std::vector<int32_t> counts((size_t)ncell, 0), tmp((size_t)ncell);

@@ -699,13 +699,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
         if (a.dd.put_cnt) {
             __shared__ int last_cta;
             __syncthreads();
+            // system scope: the receivers may be other GPUs (IPC puts of a NCCL group)
             if (threadIdx.x == 0) {
-                __threadfence();
+                __threadfence_system();
                 last_cta = atomicAdd(a.dd.done, 1) == (int)gridDim.x - 1;
             }
             __syncthreads();
             if (last_cta && threadIdx.x < a.dd.nranks) {
-                __threadfence();
+                __threadfence_system();
                 *a.dd.put_cnt[threadIdx.x] = *(volatile int*)(a.dd.send_cnt + threadIdx.x);
                 if (threadIdx.x == 0) *a.dd.done = 0;
             }

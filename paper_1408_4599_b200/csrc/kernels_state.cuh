@@ -491,6 +491,7 @@ __global__ void k_import(int n, int base, GridP g, const DDRec* __restrict__ rec
 __global__ void k_put_counts(int nranks, const int* __restrict__ send_cnt, int* const* __restrict__ put_cnt)
 {
     const int r = threadIdx.x;
+    __threadfence_system();                     // receivers on other GPUs (IPC puts)
     if (r < nranks) *put_cnt[r] = send_cnt[r];
 }
 

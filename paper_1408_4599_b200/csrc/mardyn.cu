@@ -69,6 +69,10 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Group;                            // ranks that step together (dist_engine.cuh)
 struct mardyn_ctx;
 static bool group_is_nccl(const Group* g);
+// one rank's entry of the IPC handle all-gather (dist_engine.cuh: nccl_ipc_setup): the
+// 64-byte handle of the allocation holding its receive areas, their offsets, the receive
+// capacity, a success word and its per-source receive-segment offsets
+static size_t ipc_blob_bytes(int p) { return 64 + 5 * 8 + 8 * (size_t)p; }
 static int set_molecules_dd(mardyn_ctx* ctx, int64_t n, const int64_t* id, const int32_t* comp, const double* r,
                             const double* v, const double* q, const double* j, int32_t half_step);
 static int egress_dd(mardyn_ctx* ctx, double* r, double* v, double* q, double* j, double* F, double* tau,
@@ -179,6 +183,15 @@ struct mardyn_ctx {
     DDRec** put_rec = nullptr;             // direct puts: per destination rank, where this rank's records go
     int** put_cnt = nullptr;               //   and where its record count goes (device arrays of addresses)
     bool direct = false;
+    // NCCL groups: two receive areas (and count arrays, put tables) used by alternate steps
+    // (parity = cur), so that a peer storing the next step's records never overwrites the
+    // records this rank is still importing; direct puts across processes through CUDA IPC
+    DDRec* recv_area[2] = {nullptr, nullptr};
+    int* rcnt_area[2] = {nullptr, nullptr};
+    DDRec** put_rec_area[2] = {nullptr, nullptr};
+    int** put_cnt_area[2] = {nullptr, nullptr};
+    char* ipc_blob = nullptr;              // device staging of the handle all-gather
+    int* ipc_word = nullptr;               // the one-word all-reduce that orders puts before imports
     int* n_aux = nullptr;                  // [0] unsorted count after the import, [1] n at force time, [2] egress counter
     int64_t seg_max = 0;                   // send segment stride of the workspace layout
     int* seg_tab = nullptr;                // per-peer segments (device): send offsets, send caps, recv offsets, recv caps
@@ -802,6 +815,10 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
     int* seg_tab = nullptr;
     DDRec** put_rec = nullptr;
     int** put_cnt = nullptr;
+    char* ipc_blob = nullptr;
+    int* ipc_word = nullptr;
+    const bool two_areas = ctx->nranks > 1 && ctx->grp && group_is_nccl(ctx->grp);
+    const int nar = two_areas ? 2 : 1;
     const int64_t seg_cap = ctx->nranks > 1 ? cap / ctx->nranks + 4096 : 0;
     const int64_t recv_cap = ctx->nranks > 1 ? cap : 0;
     if (ctx->nranks > 1) {
@@ -810,13 +827,17 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         gcount = (int*)take(4 * (size_t)ncell);
         cmat = (int64_t*)take(8 * ((size_t)ctx->nranks * (ctx->nranks + 1) + 2));   // + group_agree's flag
         sendbuf = (DDRec*)take(sizeof(DDRec) * (size_t)seg_cap * ctx->nranks);
-        recvbuf = (DDRec*)take(sizeof(DDRec) * (size_t)recv_cap);
+        recvbuf = (DDRec*)take(sizeof(DDRec) * (size_t)recv_cap * nar);
         send_cnt = (int*)take(4 * (size_t)ctx->nranks);
-        recv_cnt = (int*)take(4 * (size_t)ctx->nranks);
+        recv_cnt = (int*)take(4 * (size_t)ctx->nranks * nar);
         n_aux = (int*)take(16);                    // [0] unsorted count after import, [1] n at force time, [2] egress
         seg_tab = (int*)take(16 * (size_t)ctx->nranks);
-        put_rec = (DDRec**)take(sizeof(void*) * (size_t)ctx->nranks);
-        put_cnt = (int**)take(sizeof(void*) * (size_t)ctx->nranks);
+        put_rec = (DDRec**)take(sizeof(void*) * (size_t)ctx->nranks * nar);
+        put_cnt = (int**)take(sizeof(void*) * (size_t)ctx->nranks * nar);
+        if (two_areas) {
+            ipc_blob = take(ipc_blob_bytes(ctx->nranks) * (size_t)ctx->nranks);
+            ipc_word = (int*)take(4);
+        }
     }
     if (ctx->grp && group_is_nccl(ctx->grp))
         obs_all = (ObsRec*)take(sizeof(ObsRec) * MD_HISTORY * (size_t)ctx->nranks);
@@ -837,6 +858,14 @@ static size_t layout(mardyn_ctx* ctx, int64_t cap, bool assign)
         ctx->seg_ready = false;
         ctx->seg_tab = seg_tab; ctx->peer_segs = false;
         ctx->put_rec = put_rec; ctx->put_cnt = put_cnt; ctx->direct = false;
+        for (int q = 0; q < 2; ++q) {
+            const int a = q < nar ? q : 0;
+            ctx->recv_area[q] = recvbuf ? recvbuf + (size_t)a * recv_cap : nullptr;
+            ctx->rcnt_area[q] = recv_cnt ? recv_cnt + (size_t)a * ctx->nranks : nullptr;
+            ctx->put_rec_area[q] = put_rec ? put_rec + (size_t)a * ctx->nranks : nullptr;
+            ctx->put_cnt_area[q] = put_cnt ? put_cnt + (size_t)a * ctx->nranks : nullptr;
+        }
+        ctx->ipc_blob = ipc_blob; ctx->ipc_word = ipc_word;
         ctx->ncell_pad = ncell_pad; ctx->ntiles = ntiles; ctx->nkblocks = nk;
     }
     return off;

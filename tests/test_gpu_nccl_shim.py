@@ -32,9 +32,9 @@ def system(cfg):
     return S.config3(12) if cfg == "c3m" else S.config(cfg)      # c3m: water, 6 912 molecules, 5^3 cells
 
 
-def _rank_main(rank, world, port, shim, outdir, cfg, nsteps, rebalance, boxes):
+def _rank_main(rank, world, port, shim, outdir, cfg, nsteps, rebalance, boxes, ipc):
     os.environ.update(MARDYN_NCCL_LIB=shim, MDSHIM_DIR=outdir, MDSHIM_LOG=outdir, MDSHIM_TIMEOUT_S="120",
-                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+                      MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), MARDYN_IPC_PUTS="1" if ipc else "0")
     import torch
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=world)    # launches ranks, carries the unique id
@@ -59,17 +59,29 @@ def _rank_main(rank, world, port, shim, outdir, cfg, nsteps, rebalance, boxes):
     dist.destroy_process_group()
 
 
-def run_ranks(tmp_path, world, cfg, nsteps, rebalance=0, boxes=None):
+def run_ranks(tmp_path, world, cfg, nsteps, rebalance=0, boxes=None, ipc=True):
     import socket
     import torch.multiprocessing as tmp
     shim = build_shim(tmp_path)
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
         port = so.getsockname()[1]
-    tmp.start_processes(_rank_main, args=(world, port, shim, str(tmp_path), cfg, nsteps, rebalance, boxes),
+    tmp.start_processes(_rank_main, args=(world, port, shim, str(tmp_path), cfg, nsteps, rebalance, boxes, ipc),
                         nprocs=world, join=True, start_method="spawn")
     res = [json.load(open(tmp_path / f"rank{r}.json")) for r in range(world)]
+    for r in res:        # point-to-point messages this rank sent through the stand-in
+        r["p2p_sends"] = sum(1 for l in open(tmp_path / f"shim_rank{r['rank']}.log") if l.startswith("send "))
     return res
+
+
+def check_transport(res, world, nsteps, ipc, sync_steps=1):
+    """IPC puts: point-to-point messages only in the synchronous steps (the exact exchange of
+    the first step and of each rebalance); send / recv: four per peer in every other step."""
+    for r in res:
+        if ipc:
+            assert r["p2p_sends"] <= 2 * (world - 1) * sync_steps, r["p2p_sends"]
+        else:
+            assert r["p2p_sends"] >= 2 * (world - 1) * (nsteps - sync_steps), r["p2p_sends"]
 
 
 def shim_logs(tmp_path, n=12):
@@ -127,22 +139,28 @@ def built():
     return True
 
 
-def test_nccl_two_processes_lj(built, oracle_mod, tmp_path):
-    """c1s (single-site LJ) on two processes: halo exchange and migration every step."""
-    res = run_ranks(tmp_path, 2, "c1s", 12)
+@pytest.mark.parametrize("ipc", [True, False])
+def test_nccl_two_processes_lj(built, oracle_mod, tmp_path, ipc):
+    """c1s (single-site LJ) on two processes: halo exchange and migration every step, the
+    records stored by the fused force + leapfrog kernel straight into the peer's receive area
+    (IPC puts), or moved by grouped send / recv (MARDYN_IPC_PUTS=0)."""
+    res = run_ranks(tmp_path, 2, "c1s", 12, ipc=ipc)
     check_against_oracle(oracle_mod, tmp_path, res, "c1s", 12)
+    check_transport(res, 2, 12, ipc)
     assert all(min(r["owned"]) > 0 for r in res)
 
 
-def test_nccl_three_processes_water_rebalance(built, oracle_mod, tmp_path):
+@pytest.mark.parametrize("ipc", [True, False])
+def test_nccl_three_processes_water_rebalance(built, oracle_mod, tmp_path, ipc):
     """Water (four sites, reaction field) on three processes from unequal boxes (a z slab and two halves of the rest),
     re-partitioned from the measured cell loads every 4 steps (all-reduce of the loads,
     redistribution through the exchange records)."""
     s = system("c3m")
     n = np.floor(np.asarray(s["box"]) / s["rc"]).astype(int)
     boxes = [[0, 0, 0, n[0], n[1], 2], [0, 0, 2, n[0], 2, n[2]], [0, 2, 2, n[0], n[1], n[2]]]
-    res = run_ranks(tmp_path, 3, "c3m", 10, rebalance=4, boxes=boxes)
+    res = run_ranks(tmp_path, 3, "c3m", 10, rebalance=4, boxes=boxes, ipc=ipc)
     check_against_oracle(oracle_mod, tmp_path, res, "c3m", 10)
+    check_transport(res, 3, 10, ipc, sync_steps=3)           # the first step, after rebalances at 4 and 8
     assert res[0]["boxes1"] == res[1]["boxes1"] == res[2]["boxes1"]
     assert np.asarray(res[0]["boxes1"]).reshape(3, 6).tolist() != boxes          # re-partitioned
 
@@ -151,6 +169,7 @@ def test_nccl_four_processes_slab_rebalance(built, oracle_mod, tmp_path):
     """c4s (vapour-liquid slab) on four processes with rebalances every 3 steps."""
     res = run_ranks(tmp_path, 4, "c4s", 9, rebalance=3)
     check_against_oracle(oracle_mod, tmp_path, res, "c4s", 9)
+    check_transport(res, 4, 9, True, sync_steps=3)
 
 
 def test_bench_two_ranks_one_device(built, tmp_path):
