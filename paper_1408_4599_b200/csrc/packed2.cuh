@@ -1,7 +1,7 @@
 // packed2.cuh -- packed fp32x2 arithmetic (one FADD2 / FMUL2 / FFMA2 per
-// operation on sm_100) and the packed site-pair kernels of the rigid force
-// kernel (kernels_rigid3.cuh): LJTS (reading A2), charge-charge with reaction
-// field (A4) and the point multipoles (A5) for two molecule pairs at a time.
+// operation on sm_100) and the packed point-multipole site pairs (reading A5)
+// of the rigid force kernel (kernels_rigid3.cuh, which holds the packed LJ and
+// charge-charge terms), for two molecule pairs at a time.
 #pragma once
 #include "common.cuh"
 #include "kernels_force.cuh"
@@ -50,31 +50,6 @@ __device__ __forceinline__ P2 rsqrt2(P2 x)
     const P2 y = p2(a, b);
     const P2 e = fma(P2{make_float2(-x.v.x, -x.v.y)} * y, y, p2(1.f));
     return fma(p2(0.5f) * y, e, y);
-}
-
-// LJ 12-6, energy shifted (LJTS, A2), r = x_b - x_a; m = mask (0 for padding)
-__device__ __forceinline__ void lj2(V3 r, float sig2, P2 eps24m, P2 eps4m, P2 shiftm, P2& u, V3& fa, V3& fh)
-{
-    const P2 r2 = dot(r, r);
-    const P2 ir2 = rcp2(r2);
-    const P2 s2 = sig2 * ir2;
-    const P2 s6 = s2 * s2 * s2;
-    const P2 fr = eps24m * ir2 * s6 * fma(p2(2.f), s6, p2(-1.f));
-    u = fma(eps4m * s6, s6 - p2(1.f), u) - shiftm;
-    fa.x = fa.x - fr * r.x; fa.y = fa.y - fr * r.y; fa.z = fa.z - fr * r.z;
-    fh.x = fh.x - fr * r.x; fh.y = fh.y - fr * r.y; fh.z = fh.z - fr * r.z;
-}
-
-// charge-charge with reaction field (A4)
-__device__ __forceinline__ void qq2(V3 r, P2 qq, float krf, float crf, P2& u, V3& fa, V3& fh)
-{
-    const P2 r2 = dot(r, r);
-    const P2 ir = rsqrt2(r2);
-    const P2 ir2 = ir * ir;
-    u = fma(qq, fma(p2(krf), r2, ir) - p2(crf), u);
-    const P2 fr = qq * fma(ir, ir2, p2(-2.f * krf));
-    fa.x = fa.x - fr * r.x; fa.y = fa.y - fr * r.y; fa.z = fa.z - fr * r.z;
-    fh.x = fh.x - fr * r.x; fh.y = fh.y - fr * r.y; fh.z = fh.z - fr * r.z;
 }
 
 // point multipoles (A5), same closed forms and gradient recipe as
