@@ -114,7 +114,10 @@ constexpr int smem_bytes()
            NHMAX * 8 * 4 + WARPS * 2 * 8 * 4 + 16 * 8 * 4;
 }
 
-template <int NLJ, int NQ, int NMU, int NQQ>
+// PC: every dipole / quadrupole site sits at the centre of mass (2CLJQ, c2): its site-pair
+// separation is the COM separation itself, so the partner's polar site position is not loaded
+// (bitwise the same result: d + 0 - 0 = d)
+template <int NLJ, int NQ, int NMU, int NQQ, bool PC = false>
 __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceArgs a)
 {
     using SH = Shape<NLJ, NQ, NMU, NQQ>;
@@ -400,9 +403,10 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
         _Pragma("unroll") for (int ibb = 0; ibb < NB; ++ibb)                                               \
         {                                                                                                  \
             const int slb = (SLB) + ibb * STB;                                                             \
-            const V3 pb = slot3(slb, j0, j1);                                                              \
+            const bool pcab = PC && KA != MD_CHARGE && KB != MD_CHARGE;                                   \
+            const V3 pb = pcab ? v3zero() : slot3(slb, j0, j1);                                            \
             const V3 eb = (STB == 2) ? slot3((slb + 1) % NSLOT, j0, j1) : v3zero();                        \
-            const V3 rv = V3{d.x + pb.x - pa.x, d.y + pb.y - pa.y, d.z + pb.z - pa.z};                     \
+            const V3 rv = pcab ? d : V3{d.x + pb.x - pa.x, d.y + pb.y - pa.y, d.z + pb.z - pa.z};          \
             V3 tdummy = v3zero();                                                                          \
             pk2::polar2<KA, KB, SV>(rv, ea, eb, pa4.w * slotw(slb, j0, j1), kmm, uacc, fs[FIDX + ia],     \
                                  (TIDX) >= 0 ? ts[((TIDX) >= 0 ? (TIDX) : 0) + ia] : tdummy, fh, wacc);  \

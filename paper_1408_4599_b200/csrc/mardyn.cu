@@ -183,6 +183,7 @@ struct mardyn_ctx {
     DDRec** put_rec = nullptr;             // direct puts: per destination rank, where this rank's records go
     int** put_cnt = nullptr;               //   and where its record count goes (device arrays of addresses)
     bool direct = false;
+    bool polar_com = false;                // 2CLJQ with the quadrupole at the centre of mass
     // NCCL groups: two receive areas (and count arrays, put tables) used by alternate steps
     // (parity = cur), so that a peer storing the next step's records never overwrites the
     // records this rank is still importing; direct puts across processes through CUDA IPC
@@ -378,6 +379,8 @@ static int build_model(mardyn_ctx* ctx)
         ctx->force_warps_per_block = LJ1_WARPS;
     } else if (nc == 1 && M.comp[0].n_lj == 2 && M.comp[0].n_q == 0 && M.comp[0].n_mu == 0 && M.comp[0].n_Q == 1) {
         ctx->kernel = KER_RIGID; ctx->shape = SHAPE_2CLJQ; ctx->force_warps_per_block = RIG_WARPS;
+        const float* qp = M.comp[0].bpos[M.comp[0].n_lj + M.comp[0].n_q + M.comp[0].n_mu];   // the Q site
+        ctx->polar_com = qp[0] == 0.f && qp[1] == 0.f && qp[2] == 0.f && !std::getenv("MARDYN_NO_POLAR_COM");
     } else if (nc == 1 && M.comp[0].n_lj == 1 && M.comp[0].n_q == 3 && M.comp[0].n_mu == 0 && M.comp[0].n_Q == 0) {
         ctx->kernel = KER_RIGID; ctx->shape = SHAPE_TIP4P; ctx->force_warps_per_block = RIG_WARPS;
     } else {
@@ -454,7 +457,10 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_gra
     const int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ:
-        rig3::k_force_rigid3<2, 0, 0, 1><<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
+        if (ctx->polar_com)
+            rig3::k_force_rigid3<2, 0, 0, 1, true><<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
+        else
+            rig3::k_force_rigid3<2, 0, 0, 1><<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
         break;
     case SHAPE_TIP4P:
         rig3::k_force_rigid3<1, 3, 0, 0><<<ctx->force_grid, threads, rig3::smem_bytes<1, 3, 0, 0>(), ctx->stream>>>(a);
@@ -697,7 +703,7 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
     int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ: {
-        auto k = rig3::k_force_rigid3<2, 0, 0, 1>;
+        auto k = ctx->polar_com ? rig3::k_force_rigid3<2, 0, 0, 1, true> : rig3::k_force_rigid3<2, 0, 0, 1>;
         const int sm = rig3::smem_bytes<2, 0, 0, 1>();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         ctx->force_blocks = occupancy_grid(ctx, k, threads, sm);
