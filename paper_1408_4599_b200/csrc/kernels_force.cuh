@@ -42,6 +42,7 @@ struct ForceArgs {
     // instead of registers
     float4 lj3[4];
     float krf, crf, kmm;
+    float hsym[2];               // rig3 SYM: the LJ sites' positions along the molecular axis
 };
 
 // Row descriptor of the 27-cell neighbourhood: the 3 cells (dx = -1, 0, 1)

@@ -117,7 +117,10 @@ constexpr int smem_bytes()
 // PC: every dipole / quadrupole site sits at the centre of mass (2CLJQ, c2): its site-pair
 // separation is the COM separation itself, so the partner's polar site position is not loaded
 // (bitwise the same result: d + 0 - 0 = d)
-template <int NLJ, int NQ, int NMU, int NQQ, bool PC = false>
+// SYM (with PC): a linear molecule whose LJ sites sit at h_b e along the quadrupole axis e
+// (2CLJQ): the partner's LJ site offsets are h_b times its staged axis and its quadrupole
+// moment is the component's, so a partner costs its COM and axis instead of four site slots
+template <int NLJ, int NQ, int NMU, int NQQ, bool PC = false, bool SYM = false>
 __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceArgs a)
 {
     using SH = Shape<NLJ, NQ, NMU, NQQ>;
@@ -370,13 +373,24 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                             }
                             nval += (j0 != DUMMY ? 1 : 0) + (j1 != DUMMY ? 1 : 0);
                             V3 fh = v3zero();
+                            static_assert(!SYM || (PC && NQQ == 1 && NQ == 0 && NMU == 0), "rig3: SYM");
+                            // SYM: the partners' axes (also the quadrupole axes), and the moment
+                            // product m^2 for real partners (0 for the far dummy)
+                            V3 eBs = v3zero();
+                            P2 mm2 = p2(0.f);
+                            if (SYM) {
+                                eBs = slot3(SH::SQQ + 1, j0, j1);
+                                const float m = si[SH::SQQ].w;
+                                mm2 = p2(j0 != DUMMY ? m * m : 0.f, j1 != DUMMY ? m * m : 0.f);
+                            }
 #pragma unroll
                             for (int ia = 0; ia < NLJ; ++ia) {
                                 const V3 sa = bcast(si[ia]);
                                 const V3 da = V3{d.x - sa.x, d.y - sa.y, d.z - sa.z};
 #pragma unroll
                                 for (int ibb = 0; ibb < NLJ; ++ibb) {
-                                    const V3 sb = slot3(ibb, j0, j1);
+                                    const V3 sb = SYM ? V3{a.hsym[ibb] * eBs.x, a.hsym[ibb] * eBs.y, a.hsym[ibb] * eBs.z}
+                                                      : slot3(ibb, j0, j1);
                                     const V3 rv = V3{da.x + sb.x, da.y + sb.y, da.z + sb.z};
                                     const float4 pp = ljp[2 * ia + ibb];
                                     lj_noshift<SV>(rv, pp.x, pp.y, pp.z, uacc, fs[ia], fh, wacc);
@@ -405,10 +419,11 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
             const int slb = (SLB) + ibb * STB;                                                             \
             const bool pcab = PC && KA != MD_CHARGE && KB != MD_CHARGE;                                   \
             const V3 pb = pcab ? v3zero() : slot3(slb, j0, j1);                                            \
-            const V3 eb = (STB == 2) ? slot3((slb + 1) % NSLOT, j0, j1) : v3zero();                        \
+            const V3 eb = SYM ? eBs : (STB == 2) ? slot3((slb + 1) % NSLOT, j0, j1) : v3zero();           \
             const V3 rv = pcab ? d : V3{d.x + pb.x - pa.x, d.y + pb.y - pa.y, d.z + pb.z - pa.z};          \
             V3 tdummy = v3zero();                                                                          \
-            pk2::polar2<KA, KB, SV>(rv, ea, eb, pa4.w * slotw(slb, j0, j1), kmm, uacc, fs[FIDX + ia],     \
+            pk2::polar2<KA, KB, SV>(rv, ea, eb, SYM ? mm2 : pa4.w * slotw(slb, j0, j1), kmm, uacc,         \
+                                     fs[FIDX + ia],                                                        \
                                  (TIDX) >= 0 ? ts[((TIDX) >= 0 ? (TIDX) : 0) + ia] : tdummy, fh, wacc);  \
         }                                                                                                  \
     }

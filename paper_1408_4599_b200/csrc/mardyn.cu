@@ -184,6 +184,8 @@ struct mardyn_ctx {
     int** put_cnt = nullptr;               //   and where its record count goes (device arrays of addresses)
     bool direct = false;
     bool polar_com = false;                // 2CLJQ with the quadrupole at the centre of mass
+    bool sym_linear = false;               //   and both LJ sites on its axis (rig3 SYM)
+    float hsym[2] = {0.f, 0.f};
     // NCCL groups: two receive areas (and count arrays, put tables) used by alternate steps
     // (parity = cur), so that a peer storing the next step's records never overwrites the
     // records this rank is still importing; direct puts across processes through CUDA IPC
@@ -381,6 +383,17 @@ static int build_model(mardyn_ctx* ctx)
         ctx->kernel = KER_RIGID; ctx->shape = SHAPE_2CLJQ; ctx->force_warps_per_block = RIG_WARPS;
         const float* qp = M.comp[0].bpos[M.comp[0].n_lj + M.comp[0].n_q + M.comp[0].n_mu];   // the Q site
         ctx->polar_com = qp[0] == 0.f && qp[1] == 0.f && qp[2] == 0.f && !std::getenv("MARDYN_NO_POLAR_COM");
+        // linear: both LJ sites on the quadrupole axis (body positions h_b * axis exactly)
+        const DevComp& C = M.comp[0];
+        const int iq = C.n_lj + C.n_q + C.n_mu;
+        const float* ax = C.baxis[iq];
+        bool lin = ctx->polar_com && !std::getenv("MARDYN_NO_SYM");
+        for (int b = 0; b < 2 && lin; ++b) {
+            const float h = C.bpos[b][0] * ax[0] + C.bpos[b][1] * ax[1] + C.bpos[b][2] * ax[2];
+            for (int k = 0; k < 3; ++k) lin = lin && C.bpos[b][k] == h * ax[k];
+            ctx->hsym[b] = h;
+        }
+        ctx->sym_linear = lin;
     } else if (nc == 1 && M.comp[0].n_lj == 1 && M.comp[0].n_q == 3 && M.comp[0].n_mu == 0 && M.comp[0].n_Q == 0) {
         ctx->kernel = KER_RIGID; ctx->shape = SHAPE_TIP4P; ctx->force_warps_per_block = RIG_WARPS;
     } else {
@@ -454,10 +467,14 @@ static int launch_force(mardyn_ctx* ctx, int buf, bool step = false, bool in_gra
     a.krf = ctx->model.krf;
     a.crf = ctx->model.crf;
     a.kmm = ctx->model.krf_mumu;
+    a.hsym[0] = ctx->hsym[0];
+    a.hsym[1] = ctx->hsym[1];
     const int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ:
-        if (ctx->polar_com)
+        if (ctx->sym_linear)
+            rig3::k_force_rigid3<2, 0, 0, 1, true, true><<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
+        else if (ctx->polar_com)
             rig3::k_force_rigid3<2, 0, 0, 1, true><<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
         else
             rig3::k_force_rigid3<2, 0, 0, 1><<<ctx->force_grid, threads, rig3::smem_bytes<2, 0, 0, 1>(), ctx->stream>>>(a);
@@ -703,7 +720,8 @@ int mardyn_create(const double box[3], double cutoff, const mardyn_component* co
     int threads = 32 * ctx->force_warps_per_block;
     switch (ctx->shape) {
     case SHAPE_2CLJQ: {
-        auto k = ctx->polar_com ? rig3::k_force_rigid3<2, 0, 0, 1, true> : rig3::k_force_rigid3<2, 0, 0, 1>;
+        auto k = ctx->sym_linear ? rig3::k_force_rigid3<2, 0, 0, 1, true, true>
+                 : ctx->polar_com ? rig3::k_force_rigid3<2, 0, 0, 1, true> : rig3::k_force_rigid3<2, 0, 0, 1>;
         const int sm = rig3::smem_bytes<2, 0, 0, 1>();
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         ctx->force_blocks = occupancy_grid(ctx, k, threads, sm);
