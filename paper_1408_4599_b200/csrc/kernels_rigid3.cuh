@@ -131,6 +131,9 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
 #define MD_RIG3_SV 1       // 0: never, 1: molecules without charges, 2: always
 #endif
     constexpr bool SV = MD_RIG3_SV == 2 || (MD_RIG3_SV == 1 && NQ == 0);
+    // slots the partner rounds read: SYM reads only the quadrupole axis, the others are not
+    // staged (PC still reads the polar moments, kept in the position slots' w)
+    auto staged_slot = [](int s) { return !SYM || s == SH::SQQ + 1; };
     constexpr int NPOL = (NMU + NQQ) > 0 ? (NMU + NQQ) : 1;
     constexpr int STRIDE = CAP + 1;
     constexpr int DUMMY = CAP;                                 // far dummy element (pair CAP / 2)
@@ -249,7 +252,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                         oz[u] = (float)(r / 3 - 1) * g.edge[2];
                         xv[u] = __ldg(a.xs + src);
 #pragma unroll
-                        for (int s = 0; s < NSLOT; ++s) sv[u][s] = __ldg(a.site + (size_t)s * a.cap + src);
+                        for (int s = 0; s < NSLOT; ++s)
+                            if (staged_slot(s)) sv[u][s] = __ldg(a.site + (size_t)s * a.cap + src);
                     }
 #pragma unroll
                     for (int u = 0; u < SU; ++u) {
@@ -267,6 +271,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16 / WARPS) k_force_rigid3(ForceAr
                         }
 #pragma unroll
                         for (int s = 0; s < NSLOT; ++s) {
+                            if (!staged_slot(s)) continue;
                             sws[(4 * s + 0) * STRIDE + k] = sv[u][s].x;
                             sws[(4 * s + 1) * STRIDE + k] = sv[u][s].y;
                             sws[(4 * s + 2) * STRIDE + k] = sv[u][s].z;
