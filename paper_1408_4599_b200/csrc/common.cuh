@@ -156,6 +156,8 @@ struct DDArgs {
                                  // the last CTA to finish stores them)
     int* done = nullptr;               // fused kernels: CTA completion ticket (zero between launches)
     int* n_force = nullptr;            // fused kernels: the sorted count the forces were computed for
+    bool peer_puts = false;            // put_rec points into other devices (CUDA IPC): a system-scope
+                                       // fence orders each thread's record stores before it exits
 };
 
 // Pack this lane's exchange records (spatial decomposition): one record for every rank in

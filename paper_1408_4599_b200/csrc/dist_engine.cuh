@@ -426,6 +426,7 @@ static int dd_begin_async(mardyn_ctx* ctx)
     DDArgs dd = dd_args(ctx, false);
     dd.n_dev = ctx->start + ctx->g.wncell;             // the sorted count of the last cell rebuild
     dd.put_rec = ctx->direct ? ctx->put_rec : nullptr;
+    dd.peer_puts = ctx->direct && ctx->grp && ctx->grp->nccl;    // IPC puts into other processes / GPUs
     // (send_cnt is zero here: the last import cleared it)
     if (ctx->kernel == KER_LJ1) {
         // single-site kernel with the leapfrog, binning and exchange packing fused in (the cell

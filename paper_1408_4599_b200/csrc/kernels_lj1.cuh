@@ -666,7 +666,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) k_force_lj1(Args a)
             } else if (DD && valid && own_lane) {
                 a.cell_of[mi] = -1;                        // last step's halo copies are dropped
             }
-            if (DD) dd_pack_warp(a.dd, dmask, own, pn, vn, make_float4(1.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f));
+            if (DD) {
+                dd_pack_warp(a.dd, dmask, own, pn, vn, make_float4(1.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f));
+                if (a.dd.peer_puts) __threadfence_system();   // receivers on other GPUs (IPC puts)
+            }
             // arrival ranks: one atomic per distinct cell; the rank store waits for the
             // atomic's reply, so it is deferred to after the next block's forces
             if (pend_mi >= 0) a.rank[pend_mi] = __shfl_sync(pend_m, pend_b, __ffs(pend_m) - 1) + pend_r;

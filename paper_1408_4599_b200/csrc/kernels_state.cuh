@@ -447,7 +447,10 @@ __global__ void __launch_bounds__(256) k_integrate(int n, GridP g, const DevMode
         if (cl >= 0) cell_of[t] = cl;
         cl_bin = cl;
     }
-    if (DD) dd_pack_warp(dd, dmask, own, pn, vn, qn, jn);   // warp-aggregated (one atomic per destination)
+    if (DD) {
+        dd_pack_warp(dd, dmask, own, pn, vn, qn, jn);   // warp-aggregated (one atomic per destination)
+        if (dd.peer_puts) __threadfence_system();       // receivers on other GPUs (IPC puts)
+    }
     // next step's cell histogram + arrival rank: molecules are in cell order, so
     // the lanes of a warp share few cells; one atomic per distinct cell (the arrival
     // order only places molecules before the canonical in-cell ordering)
