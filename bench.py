@@ -383,6 +383,11 @@ def main():
         traffic = prof.get(args.config)
     except Exception:
         pass
+    l1 = None                      # the force kernel's L1 / shared data-pipe utilisation (ncu, committed)
+    try:
+        l1 = json.load(open(os.path.join(ROOT, "profiles", "l1_pipe.json"))).get(args.config)
+    except Exception:
+        pass
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": {0: "k_force_lj1", 1: "k_force_rigid3"}.get(ctx.get_grid()["kernel"], "k_force_rigid"),
@@ -390,7 +395,10 @@ def main():
                 "algorithmic_gflop_per_launch": flops / world / 1e9,
                 "flop_model": "8 x half-shell COM candidates + per unique in-range pair: sum over site pairs of "
                               "(8 separation + kernel: LJ 20, q-q RF 23, Q-Q 110) (SURVEY 8(d)); single-site LJ: 20",
-                "peak_note": "FP32 CUDA cores: SMs x 128 x 2 x sm_max_mhz (MEASURED_PEAKS.json), derived"}
+                "peak_note": "FP32 CUDA cores: SMs x 128 x 2 x sm_max_mhz (MEASURED_PEAKS.json), derived",
+                "l1_data_pipe_frac": l1,
+                "l1_note": "fraction of the L1/shared data pipe's peak the force kernel used under ncu "
+                           "(profiles/l1_pipe.json): the single-site kernel's main loop is bound by it"}
     # ---- end to end through the C ABI with pinned host buffers: every step uploads the
     #      molecules (set_molecules from pinned host arrays, exact resume) and reads back the
     #      observables and the molecules (get_molecules into pinned host arrays); at N > 1 each
