@@ -172,6 +172,41 @@ def test_trajectory(md, oracle_mod, name, nsteps):
         assert dq.max() < 1e-4
 
 
+@pytest.mark.parametrize("variant", ["sym", "sym_pc_only", "generic", "sym_unequal_h", "pc_off_axis_lj",
+                                     "generic_off_centre_q"])
+def test_2cljq_kernel_instances(md, oracle_mod, monkeypatch, variant):
+    """The three instances of the 2CLJQ force kernel against the oracle: the
+    linear-molecule one (c2's molecule, and LJ sites at unequal distances on the axis), the
+    polar-at-COM one (MARDYN_NO_SYM=1, or an LJ site off the axis), and the generic one
+    (MARDYN_NO_POLAR_COM=1, or the quadrupole off the centre of mass).  F(t0), tau(t0), U, W,
+    cells bit-exact, then 8 steps of U, W, T, positions and orientations."""
+    s = dict(S.config("c2s"))
+    c = dict(s["components"][0])
+    qm = c["quadrupoles"][0][2]
+    if variant == "sym_pc_only":
+        monkeypatch.setenv("MARDYN_NO_SYM", "1")
+    elif variant == "generic":
+        monkeypatch.setenv("MARDYN_NO_POLAR_COM", "1")
+    elif variant == "sym_unequal_h":
+        c["lj"] = [((0.0, 0.0, 0.3), 1.0, 1.0), ((0.0, 0.0, -0.2), 1.0, 1.0)]
+    elif variant == "pc_off_axis_lj":
+        c["lj"] = [((0.05, 0.0, 0.25), 1.0, 1.0), ((0.0, 0.0, -0.25), 1.0, 1.0)]
+    elif variant == "generic_off_centre_q":
+        c["quadrupoles"] = [((0.0, 0.0, 0.1), (0.0, 0.0, 1.0), qm)]
+    s["components"] = [c]
+    check_step0(md, oracle_mod, s)
+    nsteps = 8
+    ctx, hist, mol, o, u, v, q, j, obs = run_both(md, oracle_mod, s, nsteps)
+    for k in range(nsteps):
+        assert hist[k]["n_pairs"] == obs["npairs"][k]
+        assert_rel(hist[k]["U_pot"], obs["U"][k], f"U[{k}]")
+        assert_rel(hist[k]["virial"], obs["W"][k], f"W[{k}]")
+        assert_rel(hist[k]["T"], obs["T"][k], f"T[{k}]")
+    assert np.abs(min_image(mol["r"] - u * o.quantum, o.box)).max() <= 1e-4
+    dq = np.minimum(np.abs(mol["q"] - q).max(1), np.abs(mol["q"] + q).max(1))
+    assert dq.max() < 1e-4
+
+
 @pytest.mark.parametrize("name,nsteps", [("c2s", 60), ("c3s", 60)])
 def test_rigid_long_run(md, oracle_mod, name, nsteps):
     """Longer rigid-body runs (Fincham rotation, reading A7).  Independent fp32 and
